@@ -1,0 +1,100 @@
+"""ctypes front end of O-1 (oracle/o1_naive.c). TEST INFRASTRUCTURE ONLY.
+
+O-1 evaluates y = A z by plain quadrature loops with no sum factorization
+(the "plain, slow" oracle BASELINE.json's north_star asks for). See the C
+file's header for the formulas and PAPER.md citations.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "o1_naive.c")
+_LIB = os.path.join(_HERE, "libo1_naive.so")
+
+VOLUME, INTERIOR, BOUNDARY, ALL = 1, 2, 4, 7
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [("nc", ctypes.c_int64 * 3), ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
+                ("k", ctypes.c_int), ("D", ctypes.c_double * 9), ("b", ctypes.c_double * 3),
+                ("c", ctypes.c_double), ("sigma", ctypes.c_double)]
+
+
+def build(force=False):
+    """Compile the C oracle with gcc (-O3, OpenMP, portable x86-64 code)."""
+    if not force and os.path.exists(_LIB) and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC):
+        return _LIB
+    tmp = _LIB + ".tmp%d" % os.getpid()
+    subprocess.check_call(["gcc", "-O3", "-fopenmp", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+    os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        _lib.o1_apply.restype = ctypes.c_int
+        _lib.o1_apply.argtypes = [ctypes.POINTER(_Problem), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint,
+                                  ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int]
+        _lib.o1_tables.restype = ctypes.c_int
+        _lib.o1_tables.argtypes = [ctypes.c_int] + [ctypes.c_void_p] * 8
+    return _lib
+
+
+def _problem(ncells, lo, hi, k, D, b, c, sigma):
+    P = _Problem()
+    for q in range(3):
+        P.nc[q] = int(ncells[q])
+        P.lo[q] = float(lo[q])
+        P.hi[q] = float(hi[q])
+        P.b[q] = float(b[q])
+    Dm = np.asarray(D, dtype=np.float64).reshape(3, 3)
+    for i in range(9):
+        P.D[i] = float(Dm.flat[i])
+    P.k = int(k)
+    P.c = float(c)
+    P.sigma = float(sigma)
+    return P
+
+
+def tables(k):
+    """The oracle's own 1D tables: (xi, w, theta[i,j], dtheta[i,j], th0, th1, dth0, dth1)."""
+    n = k + 1
+    arrs = [np.zeros(n), np.zeros(n), np.zeros((n, n)), np.zeros((n, n))] + [np.zeros(n) for _ in range(4)]
+    rc = lib().o1_tables(k, *[a.ctypes.data for a in arrs])
+    if rc != 0:
+        raise ValueError("o1_tables: bad degree %d" % k)
+    return arrs
+
+
+def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL, cells=None, nthreads=0):
+    """y = A z (mask selects volume / interior-face / boundary-face terms).
+
+    cells=None: full vector. cells=int64 array: returns the compact blocks of
+    those cells only, shape (len(cells), n^3) (sampled mode). Returns (y, threads)."""
+    n3 = (k + 1) ** 3
+    ncell_total = int(ncells[0]) * int(ncells[1]) * int(ncells[2])
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    if z.size != ncell_total * n3:
+        raise ValueError("z has %d entries, expected %d" % (z.size, ncell_total * n3))
+    P = _problem(ncells, lo, hi, k, D, b, c, sigma)
+    if cells is None:
+        y = np.zeros(ncell_total * n3)
+        used = lib().o1_apply(ctypes.byref(P), z.ctypes.data, y.ctypes.data, mask, None, 0, 0, nthreads)
+    else:
+        cells = np.ascontiguousarray(cells, dtype=np.int64)
+        if cells.size and (cells.min() < 0 or cells.max() >= ncell_total):
+            raise ValueError("cell index out of range")
+        y = np.zeros((cells.size, n3))
+        used = lib().o1_apply(ctypes.byref(P), z.ctypes.data, y.ctypes.data, mask, cells.ctypes.data,
+                              cells.size, 1, nthreads)
+    if used < 0:
+        raise ValueError("o1_apply failed (%d)" % used)
+    return y, used

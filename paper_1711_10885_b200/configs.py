@@ -1,0 +1,111 @@
+"""The five BASELINE.json configurations as data (mesh, degree, coefficients,
+penalty, seed). No method arithmetic. Readings C-10, C-11, C-12, C-20 of
+DESIGN.md fix what BASELINE.json leaves open (all-Dirichlet boundaries,
+sigma = 3k(k+2)/h_min, the weak-scaling domain, the C4 meshes)."""
+from dataclasses import dataclass, field
+from typing import Tuple
+
+import numpy as np
+
+
+@dataclass
+class Config:
+    name: str
+    ncells: Tuple[int, int, int]
+    lo: Tuple[float, float, float]
+    hi: Tuple[float, float, float]
+    k: int
+    D: Tuple[float, ...]
+    b: Tuple[float, float, float]
+    c: float
+    sigma: float
+    seed: int
+    parts: Tuple[int, int, int] = (1, 1, 1)
+
+    @property
+    def n3(self):
+        return (self.k + 1) ** 3
+
+    @property
+    def ncell(self):
+        return self.ncells[0] * self.ncells[1] * self.ncells[2]
+
+    @property
+    def ndofs(self):
+        return self.ncell * self.n3
+
+    @property
+    def h(self):
+        return tuple((self.hi[q] - self.lo[q]) / self.ncells[q] for q in range(3))
+
+    def args(self):
+        """Positional (ncells, lo, hi, k, D, b, c, sigma) as used by the oracle functions."""
+        return (self.ncells, self.lo, self.hi, self.k, self.D, self.b, self.c, self.sigma)
+
+
+I3 = (1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
+B_A = (1.0, 0.5, 0.25)
+
+
+def sigma_for(k, h_min):
+    """sigma = 3 k (k+2) / h_min (BASELINE.json configs; alpha = 3, reading C-4/C-11)."""
+    return 3.0 * k * (k + 2) / h_min
+
+
+def c1():
+    return Config("C1", (4, 4, 4), (0, 0, 0), (1, 1, 1), 2, I3, B_A, 1.0, sigma_for(2, 0.25), 0)
+
+
+def c2():
+    D = (1.0, 0, 0, 0, 2.0, 0, 0, 0, 0.5)
+    return Config("C2", (32, 32, 32), (0, 0, 0), (1, 1, 1), 3, D, (1.0, -1.0, 0.5), 0.1,
+                  sigma_for(3, 1.0 / 32), 1)
+
+
+def c3():
+    return Config("C3", (128, 64, 64), (0, 0, 0), (2, 1, 1), 7, I3, B_A, 1.0, sigma_for(7, 1.0 / 64), 2)
+
+
+def c4(k):
+    N = int(round(464.16 / (k + 1)))
+    return Config("C4-k%d" % k, (N, N, N), (0, 0, 0), (1, 1, 1), k, I3, B_A, 1.0, sigma_for(k, 1.0 / N), 3)
+
+
+def c5_strong(parts=(1, 1, 1)):
+    return Config("C5-strong", (256, 128, 128), (0, 0, 0), (1, 1, 1), 7, I3, B_A, 1.0,
+                  sigma_for(7, 1.0 / 256), 4, parts)
+
+
+_WEAK_GRID = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+
+
+def c5_weak(P=1):
+    """128x128x64 cells per GPU at h = 1/128 (reading C-12)."""
+    px, py, pz = _WEAK_GRID[P]
+    nc = (128 * px, 128 * py, 64 * pz)
+    return Config("C5-weak-P%d" % P, nc, (0, 0, 0), tuple(v / 128.0 for v in nc), 7, I3, B_A, 1.0,
+                  sigma_for(7, 1.0 / 128), 4, (px, py, pz))
+
+
+def c3_weak(P=1):
+    """C3's per-GPU block (128x64x64 cells, h = 1/64, k = 7) replicated over a Px x Py x Pz grid."""
+    px, py, pz = _WEAK_GRID[P]
+    nc = (128 * px, 64 * py, 64 * pz)
+    return Config("C3-weak-P%d" % P, nc, (0, 0, 0), tuple(v / 64.0 for v in nc), 7, I3, B_A, 1.0,
+                  sigma_for(7, 1.0 / 64), 2, (px, py, pz))
+
+
+def by_name(name):
+    name = name.lower()
+    table = {"c1": c1, "c2": c2, "c3": c3, "c5strong": c5_strong, "c5weak": c5_weak}
+    if name.startswith("c4-k"):
+        return c4(int(name[4:]))
+    return table[name]()
+
+
+def small(k, ncells=(3, 2, 2), lo=(0, 0, 0), hi=(1.5, 1.0, 0.5), D=(1, 0, 0, 0, 2, 0, 0, 0, 0.5),
+          b=(1.0, -0.5, 0.25), c=0.3, seed=7):
+    """Survey test mesh (SURVEY.md 8(c) 'Verification'): anisotropic cells."""
+    h = [(hi[q] - lo[q]) / ncells[q] for q in range(3)]
+    return Config("small-k%d" % k, tuple(ncells), tuple(lo), tuple(hi), k, tuple(float(v) for v in D),
+                  tuple(b), c, sigma_for(k, min(h)), seed)

@@ -1,0 +1,49 @@
+"""Seeded synthetic inputs shared by the CUDA path's tests/bench and the oracle
+tests. Holds none of the method's arithmetic (no basis, quadrature or flux).
+
+z is i.i.d. uniform[-1,1] FP64 drawn by a counter-based splitmix64 over the
+GLOBAL cell-major DOF index g (reading C-13), all arithmetic mod 2^64:
+
+    x = (seed << 40) + g + 0x9E3779B97F4A7C15
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EB
+    x ^= x >> 31
+    z = (x >> 11) * 2^-53 * 2 - 1
+
+The same generator exists as a CUDA kernel in the library (dg_fill_uniform,
+paper_1711_10885_b200/csrc/dg_inputs.cu) so multi-GB inputs can be produced in
+HBM; tests check the two bit for bit. It is exact in FP64 and independent of
+the partition, so a rank can generate its own block from global indices.
+"""
+import numpy as np
+
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def uniform_from_index(g, seed):
+    """Values for an array of global indices g (uint64-convertible)."""
+    with np.errstate(over="ignore"):
+        x = np.asarray(g, dtype=np.uint64) + (np.uint64(seed) << np.uint64(40)) + _GOLDEN
+        x = (x ^ (x >> np.uint64(30))) * _M1
+        x = (x ^ (x >> np.uint64(27))) * _M2
+        x = x ^ (x >> np.uint64(31))
+    return (x >> np.uint64(11)).astype(np.float64) * (2.0 ** -53) * 2.0 - 1.0
+
+
+def uniform(count, seed, offset=0, chunk=1 << 24, out=None):
+    """z[0:count] for global indices offset .. offset+count-1."""
+    if out is None:
+        out = np.empty(count, dtype=np.float64)
+    for s in range(0, count, chunk):
+        e = min(count, s + chunk)
+        out[s:e] = uniform_from_index(np.arange(offset + s, offset + e, dtype=np.uint64), seed)
+    return out
+
+
+def uniform_cells(cells, n3, seed, ncells_global=None):
+    """z blocks for an explicit list of global cell indices (shape (len(cells), n3))."""
+    cells = np.asarray(cells, dtype=np.uint64)
+    g = cells[:, None] * np.uint64(n3) + np.arange(n3, dtype=np.uint64)[None, :]
+    return uniform_from_index(g, seed)

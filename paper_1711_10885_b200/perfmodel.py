@@ -1,0 +1,50 @@
+"""The paper's closed-form cost and roofline model
+used to normalise measurements (model GFLOP/s = FLOPDOF x DOFs/s), plus the
+B200 FP64 peak derivation used by bench.py's roofline object."""
+
+
+def C(d, rho):
+    """C_{d,rho} = sum_{q=1}^d rho^q."""
+    return sum(rho ** q for q in range(1, d + 1))
+
+
+def cost_vol(d, m, rho=1.0):
+    return 2.0 * C(d, rho) * m ** (d + 1)            # eq:cost_volume_sumfact
+
+
+def cost_face(d, m, rho=1.0):
+    return 2.0 * C(d, rho) * m ** d                  # eq:cost_face_sumfact
+
+
+def flopdof_vol(d, p):
+    return 4.0 * (d + 1) * d * (p + 1) + 2 * d * d + 5 * d + 3
+
+
+def flopdof_face(d, p):
+    return 8.0 * (d + 1) * d * d + d * (2 * d * d + 8 * d + 18) / (p + 1.0)
+
+
+def flopdof(d, p):
+    return flopdof_vol(d, p) + flopdof_face(d, p)
+
+
+BDOF_VOL = 16.0
+
+
+def bdof_face(d):
+    return 32.0 * d
+
+
+def roofline(I, pi, beta):
+    return min(pi, beta * I)
+
+
+# B200 FP64 (non-tensor) arithmetic peak, derived from unit counts and clocks
+# (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz; 64 FP64 FMA lanes per SM
+# per clock = 4 SMSPs x 16): 148 * 64 * 2 flop * 1.965e9 = 37.2 TFLOP/s.
+B200_SMS = 148
+FP64_FMA_PER_CLK_PER_SM = 64
+
+
+def fp64_peak_tflops(sm_mhz=1965.0):
+    return B200_SMS * FP64_FMA_PER_CLK_PER_SM * 2 * sm_mhz * 1e6 / 1e12
