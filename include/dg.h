@@ -1,0 +1,134 @@
+/*
+ * dg.h -- C ABI of the B200-native (sm_100a, FP64) matrix-free SIPG/WSIPG
+ * operator of arXiv 1711.10885.
+ *
+ * The operation: for the convection-diffusion-reaction problem
+ *     -div(D grad u) + div(b u) + c u = f          (eq:modelproblem, stationary)
+ * discretized by the weighted symmetric interior penalty DG method with
+ * tensor-product orthonormal Legendre bases of degree k and (k+1)^3 Gauss
+ * points, the library computes
+ *     y = A z,   (A)_ij = a_h(phi_j, phi_i)           (eq:blf)
+ * matrix-free by sum factorization, and the residual
+ *     r = f - A z.
+ *
+ * Readings of the paper the ABI fixes:
+ *   - reference cell [0,1]^3, theta_j(x) = sqrt(2j+1) P_j(2x-1)        (C-2)
+ *   - DOF order: cell e = ix + Nx(iy + Ny iz) (of THIS RANK's local box),
+ *     local j = jx + n(jy + n jz), n = k+1; block e occupies
+ *     [e n^3, (e+1) n^3) of every vector                               (C-3)
+ *   - weighted average {v}_w = w- v- + w+ v+ (PAPER.md:271 garbled)   (C-1)
+ *   - penalty gamma_F = <delta-, delta+> * sigma, delta = nu^T D nu;
+ *     on the boundary gamma = delta * sigma                            (C-4, C-6)
+ *   - all six box sides weak Dirichlet with g = 0 inside A             (C-9, C-10)
+ *
+ * Vectors are caller-owned DEVICE pointers to FP64 arrays of dg_local_layout()
+ * ndofs entries (unless stated otherwise). The library never allocates or
+ * frees them. z must not alias y, r or f. y / r are fully overwritten.
+ *
+ * Every call returns an int status (DG_OK = 0 or a negative DG_E* code); no
+ * C++ exception crosses the ABI. dg_apply* / dg_residual are enqueued on the
+ * caller's CUDA stream and return immediately; device faults surface at
+ * dg_sync or dg_destroy. With nranks > 1 every apply is collective (all ranks
+ * call it in the same order). A context is not thread-safe; distinct contexts
+ * are independent.
+ */
+#ifndef DG_B200_H
+#define DG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dg_ctx dg_ctx;  /* opaque: tables, halo buffers, NCCL communicator, streams */
+
+typedef struct {
+    int64_t ncells[3];   /* GLOBAL structured box mesh: cells per direction (>= 1) */
+    double  lo[3], hi[3];/* box corners, hi > lo; uniform cuboid cells h_q = (hi-lo)/ncells */
+    int     bc[6];       /* per side (x-,x+,y-,y+,z-,z+): DG_BC_DIRICHLET only (periodic: later) */
+    int     parts[3];    /* rank grid Px,Py,Pz; product == nranks; each must divide ncells */
+} dg_mesh_desc;
+
+enum { DG_OK = 0, DG_EINVAL = -1, DG_ENOMEM = -2, DG_ECUDA = -3, DG_ENCCL = -4, DG_EUNSUPPORTED = -5 };
+
+/* Term masks (PAPER.md:342-347 split a_h into volume, interior-face, boundary-face parts). */
+enum { DG_VOLUME = 1, DG_INTERIOR_FACES = 2, DG_BOUNDARY_FACES = 4, DG_ALL = 7,
+       /* halo already placed in the receive buffers by the caller (dg_halo_buffer);
+          skip the pack + NCCL exchange. Used by single-process loopback tests. */
+       DG_HALO_EXTERNAL = 0x100 };
+
+enum { DG_BC_DIRICHLET = 0 };
+
+/*
+ * Create a context on CUDA device `device` for rank `rank` of `nranks`.
+ *   k      polynomial degree, 1 <= k <= 10 (n = k+1 basis functions and Gauss points per direction)
+ *   D      3x3 row-major diffusion tensor, symmetric positive semi-definite
+ *          (D = 0 is accepted: the mass-matrix invariant); off-diagonal D -> DG_EUNSUPPORTED (v1)
+ *   b      constant velocity (div b = 0), c reaction coefficient, sigma >= 0 penalty factor
+ *   nccl_unique_id  128-byte ncclUniqueId broadcast by the caller; NULL iff nranks == 1
+ *                   or iff the caller drives the halo itself (DG_HALO_EXTERNAL)
+ * Errors: DG_EINVAL (k, mesh, D not symmetric / negative diagonal, sigma < 0, parts),
+ *         DG_EUNSUPPORTED (bc != Dirichlet, off-diagonal D), DG_ECUDA, DG_ENCCL, DG_ENOMEM.
+ * Not timed; uploads tables and allocates the halo buffers.
+ */
+int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const double D[9], const double b[3],
+             double c, double sigma, int device, int rank, int nranks, const void* nccl_unique_id);
+
+/* This rank's cell box (global cell offset and counts) and its vector length. */
+int dg_local_layout(const dg_ctx* ctx, int64_t cell_lo[3], int64_t cell_cnt[3], int64_t* ndofs);
+
+/* y = A z on stream (a cudaStream_t; NULL = legacy default stream). */
+int dg_apply(dg_ctx* ctx, const double* z, double* y, void* stream);
+
+/* y = (the parts of A selected by `terms`) z; terms = OR of DG_VOLUME / DG_INTERIOR_FACES /
+   DG_BOUNDARY_FACES, optionally | DG_HALO_EXTERNAL. */
+int dg_apply_ex(dg_ctx* ctx, const double* z, double* y, unsigned terms, void* stream);
+
+/* r = f - A z, fused into the final store (f: assembled l_h(phi_i)). */
+int dg_residual(dg_ctx* ctx, const double* z, const double* f, double* r, void* stream);
+
+/* End-to-end variant with HOST buffers: z_host, y_host are host pointers (pinned for speed)
+   of ndofs doubles; copies in, applies, copies out on an internal stream; synchronous. */
+int dg_apply_host(dg_ctx* ctx, const double* z_host, double* y_host);
+
+/* Wait for all work of the context; surfaces asynchronous CUDA / NCCL errors. */
+int dg_sync(dg_ctx* ctx);
+int dg_destroy(dg_ctx* ctx);
+const char* dg_strerror(int code);
+
+/* ---- halo plumbing (multi-rank; also used by the single-process loopback test) ----
+ * face f = 2q + s (q = direction, s = 0 low / 1 high side of this rank's box).
+ * neighbor_rank = -1 when the face lies on the domain boundary. count = doubles in the
+ * layer (cells of the face layer x n^3). */
+int dg_halo_info(const dg_ctx* ctx, int face, int* neighbor_rank, int64_t* count);
+/* which = 0: send buffer (this rank's own boundary layer, filled by dg_halo_pack),
+   which = 1: receive buffer (the neighbour's layer adjacent to this face, read by the kernel). */
+int dg_halo_buffer(dg_ctx* ctx, int face, int which, double** ptr);
+int dg_halo_pack(dg_ctx* ctx, const double* z, void* stream);
+
+/* ---- seeded inputs (reading C-13; identical to paper_1711_10885_b200/inputs.py) ----
+ * dst[i] = U(seed, offset + i), i < count, on device memory. */
+int dg_fill_uniform(double* dst, int64_t count, uint64_t seed, int64_t offset, void* stream);
+/* Fill this rank's local vector with the values of the GLOBAL DOF indices it owns. */
+int dg_fill_uniform_local(dg_ctx* ctx, double* dst, uint64_t seed, void* stream);
+
+/* Create a 128-byte ncclUniqueId (rank 0 calls this and broadcasts it). */
+int dg_nccl_unique_id(void* out128);
+
+/* Library / kernel facts for the harness: kernel launches per dg_apply, threads and
+   cells per CTA, dynamic shared memory per CTA, registers per thread. */
+typedef struct {
+    int launches_per_apply;
+    int cells_per_cta;
+    int threads_per_cta;
+    int smem_bytes;
+    int regs_per_thread;
+    int ctas_per_sm;
+} dg_kernel_info;
+int dg_get_kernel_info(const dg_ctx* ctx, dg_kernel_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DG_B200_H */

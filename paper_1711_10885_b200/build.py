@@ -1,0 +1,85 @@
+"""Build libdg_b200.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
+
+    python -m paper_1711_10885_b200.build [--force] [-v]
+
+One object per basis size n = k+1 (dg_cell_inst.cu with -DDG_N=n) plus the host ABI,
+tables, dispatch, NCCL loader and auxiliary kernels; objects compile in parallel.
+"""
+import argparse
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(ROOT, "build", "obj")
+LIB = os.path.join(HERE, "libdg_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+NS = list(range(2, 12))
+
+
+def _sources():
+    jobs = []
+    for n in NS:
+        jobs.append((os.path.join(CSRC, "dg_cell_inst.cu"), os.path.join(OBJ, "dg_cell_n%d.o" % n), ["-DDG_N=%d" % n]))
+    for name in ("dg_aux.cu", "dg_abi.cpp", "dg_dispatch.cpp", "dg_nccl.cpp", "tables.cpp"):
+        base = os.path.splitext(name)[0]
+        extra = ["-x", "cu"] if name.endswith(".cpp") else []
+        jobs.append((os.path.join(CSRC, name), os.path.join(OBJ, base + ".o"), extra))
+    return jobs
+
+
+def _deps():
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "dg.h")]
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force=False, verbose=False, ptxas_v=False):
+    os.makedirs(OBJ, exist_ok=True)
+    deps = _deps()
+    jobs = _sources()
+
+    def compile_one(job):
+        src, obj, extra = job
+        if not force and not _stale(obj, deps):
+            return obj, ""
+        cmd = [NVCC] + ARCH + FLAGS + extra + (["-Xptxas", "-v"] if ptxas_v else []) + ["-c", src, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed for %s:\n%s\n%s" % (" ".join(cmd), r.stdout, r.stderr))
+        return obj, r.stderr
+
+    with cf.ThreadPoolExecutor(max_workers=max(2, os.cpu_count() or 2)) as ex:
+        results = list(ex.map(compile_one, jobs))
+    if verbose:
+        for obj, log in results:
+            if log:
+                print(os.path.basename(obj), log, file=sys.stderr)
+    objs = [o for o, _ in results]
+    if force or _stale(LIB, objs):
+        tmp = LIB + ".tmp%d" % os.getpid()
+        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("link failed:\n%s\n%s" % (r.stdout, r.stderr))
+        os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--ptxas", action="store_true", help="print -Xptxas -v (registers, spills)")
+    a = ap.parse_args()
+    print(build(force=a.force or a.ptxas, verbose=a.verbose or a.ptxas, ptxas_v=a.ptxas))

@@ -1,0 +1,416 @@
+// C ABI of libdg_b200.so (declared and documented in include/dg.h).
+#include "../../include/dg.h"
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "dg_internal.h"
+#include "dg_nccl.h"
+
+using namespace dg;
+
+struct dg_ctx {
+    int device = 0, rank = 0, nranks = 1, k = 1, n = 2, n3 = 8;
+    int parts[3] = {1, 1, 1}, pc[3] = {0, 0, 0};
+    int64_t nloc[3] = {0, 0, 0}, gofs[3] = {0, 0, 0}, gcells[3] = {0, 0, 0};
+    int64_t ndofs = 0;
+    int nbr[6] = {-1, -1, -1, -1, -1, -1};
+    int64_t halo_count[6] = {0, 0, 0, 0, 0, 0};
+    double* sendbuf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    double* recvbuf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool partitioned = false;        // some face has a neighbour rank
+    int64_t inner_lo[3] = {0, 0, 0}, inner_cnt[3] = {0, 0, 0};   // cells needing no remote data
+    int64_t* shell = nullptr;        // device list of the partition-layer cells
+    int64_t nshell = 0;
+    cudaStream_t comm_stream = nullptr, host_stream = nullptr;
+    cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
+    ncclComm_t comm = nullptr;
+    double* hz = nullptr;            // device staging for dg_apply_host
+    double* hy = nullptr;
+    KParams base;
+};
+
+static std::mutex g_tab_mu;
+static bool g_tab_done[64][KMAX + 1];
+
+static int cuda_rc(cudaError_t e) { return e == cudaSuccess ? DG_OK : DG_ECUDA; }
+
+#define DG_CUDA(x)                                   \
+    do {                                             \
+        cudaError_t e__ = (x);                       \
+        if (e__ != cudaSuccess) return DG_ECUDA;     \
+    } while (0)
+
+extern "C" const char* dg_strerror(int code)
+{
+    switch (code) {
+    case DG_OK: return "ok";
+    case DG_EINVAL: return "invalid argument";
+    case DG_ENOMEM: return "out of device memory";
+    case DG_ECUDA: return "CUDA error";
+    case DG_ENCCL: return "NCCL error (or NCCL unavailable)";
+    case DG_EUNSUPPORTED: return "unsupported configuration";
+    default: return "unknown error";
+    }
+}
+
+static void free_ctx(dg_ctx* c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (int f = 0; f < 6; ++f) {
+        if (c->sendbuf[f]) cudaFree(c->sendbuf[f]);
+        if (c->recvbuf[f]) cudaFree(c->recvbuf[f]);
+    }
+    if (c->shell) cudaFree(c->shell);
+    if (c->hz) cudaFree(c->hz);
+    if (c->hy) cudaFree(c->hy);
+    if (c->comm) {
+        const NcclApi* api = nccl_api();
+        if (api) api->ncclCommDestroy(c->comm);
+    }
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->host_stream) cudaStreamDestroy(c->host_stream);
+    if (c->ev_packed) cudaEventDestroy(c->ev_packed);
+    if (c->ev_recv) cudaEventDestroy(c->ev_recv);
+    delete c;
+}
+
+extern "C" int dg_nccl_unique_id(void* out128)
+{
+    if (!out128) return DG_EINVAL;
+    const NcclApi* api = nccl_api();
+    if (!api) return DG_ENCCL;
+    ncclUniqueId id;
+    if (api->ncclGetUniqueId(&id) != 0) return DG_ENCCL;
+    std::memcpy(out128, &id, sizeof(id));
+    return DG_OK;
+}
+
+extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const double D[9], const double b[3],
+                        double c, double sigma, int device, int rank, int nranks, const void* nccl_unique_id)
+{
+    if (!out || !mesh || !D || !b) return DG_EINVAL;
+    *out = nullptr;
+    if (k < 1 || k > KMAX) return DG_EINVAL;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return DG_EINVAL;
+    for (int q = 0; q < 3; ++q) {
+        if (mesh->ncells[q] < 1 || !(mesh->hi[q] > mesh->lo[q])) return DG_EINVAL;
+        if (!std::isfinite(mesh->lo[q]) || !std::isfinite(mesh->hi[q])) return DG_EINVAL;
+        if (mesh->parts[q] < 1 || mesh->ncells[q] % mesh->parts[q] != 0) return DG_EINVAL;
+    }
+    if ((int64_t)mesh->parts[0] * mesh->parts[1] * mesh->parts[2] != nranks) return DG_EINVAL;
+    for (int i = 0; i < 9; ++i)
+        if (!std::isfinite(D[i])) return DG_EINVAL;
+    for (int r = 0; r < 3; ++r) {
+        if (D[4 * r] < 0.0) return DG_EINVAL;                  // PSD => nonnegative diagonal
+        for (int s = 0; s < 3; ++s)
+            if (D[3 * r + s] != D[3 * s + r]) return DG_EINVAL;    // symmetric
+        if (!std::isfinite(b[r])) return DG_EINVAL;
+    }
+    if (!std::isfinite(c) || !std::isfinite(sigma) || sigma < 0.0) return DG_EINVAL;
+    for (int f = 0; f < 6; ++f)
+        if (mesh->bc[f] != DG_BC_DIRICHLET) return DG_EUNSUPPORTED;
+    for (int r = 0; r < 3; ++r)
+        for (int s = 0; s < 3; ++s)
+            if (r != s && D[3 * r + s] != 0.0) return DG_EUNSUPPORTED;   // full D: not in v1
+
+    dg_ctx* ctx = new (std::nothrow) dg_ctx();
+    if (!ctx) return DG_ENOMEM;
+    ctx->device = device;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    ctx->k = k;
+    ctx->n = k + 1;
+    ctx->n3 = ctx->n * ctx->n * ctx->n;
+    if (cudaSetDevice(device) != cudaSuccess) { free_ctx(ctx); return DG_ECUDA; }
+
+    // tables -> this device's constant bank (once per device and degree)
+    {
+        std::lock_guard<std::mutex> lk(g_tab_mu);
+        if (device < 0 || device >= 64) { free_ctx(ctx); return DG_EINVAL; }
+        if (!g_tab_done[device][k]) {
+            HostTables t;
+            if (build_tables(k, &t) != 0) { free_ctx(ctx); return DG_EINVAL; }
+            if (upload_tables(k, t) != 0) { free_ctx(ctx); return DG_ECUDA; }
+            g_tab_done[device][k] = true;
+        }
+    }
+
+    // block partition: rank = px + Px (py + Py pz)
+    for (int q = 0; q < 3; ++q) ctx->parts[q] = mesh->parts[q];
+    ctx->pc[0] = rank % ctx->parts[0];
+    ctx->pc[1] = (rank / ctx->parts[0]) % ctx->parts[1];
+    ctx->pc[2] = rank / (ctx->parts[0] * ctx->parts[1]);
+    for (int q = 0; q < 3; ++q) {
+        ctx->gcells[q] = mesh->ncells[q];
+        ctx->nloc[q] = mesh->ncells[q] / ctx->parts[q];
+        ctx->gofs[q] = ctx->nloc[q] * ctx->pc[q];
+    }
+    ctx->ndofs = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2] * (int64_t)ctx->n3;
+    for (int q = 0; q < 3; ++q)
+        for (int s = 0; s < 2; ++s) {
+            int pcn[3] = {ctx->pc[0], ctx->pc[1], ctx->pc[2]};
+            pcn[q] += s ? 1 : -1;
+            const int f = 2 * q + s;
+            if (pcn[q] >= 0 && pcn[q] < ctx->parts[q]) {
+                ctx->nbr[f] = pcn[0] + ctx->parts[0] * (pcn[1] + ctx->parts[1] * pcn[2]);
+                ctx->partitioned = true;
+            }
+            const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+            ctx->halo_count[f] = ctx->nloc[t1] * ctx->nloc[t2] * ctx->n3;
+        }
+
+    // kernel constants (eq:gauss_points; penalty reading C-4)
+    KParams& p = ctx->base;
+    std::memset(&p, 0, sizeof(p));
+    double h[3];
+    for (int q = 0; q < 3; ++q) {
+        h[q] = (mesh->hi[q] - mesh->lo[q]) / (double)mesh->ncells[q];
+        p.hinv[q] = 1.0 / h[q];
+        p.nloc[q] = ctx->nloc[q];
+        p.gofs[q] = ctx->gofs[q];
+        p.gcells[q] = ctx->gcells[q];
+        p.kb[q] = b[q] / h[q];
+        p.bq[q] = b[q];
+        p.Dqq_h[q] = D[4 * q] / h[q];
+        p.gam[q] = D[4 * q] * sigma;     // <delta, delta> = delta for constant D
+    }
+    for (int r = 0; r < 3; ++r)
+        for (int s = 0; s < 3; ++s) p.Dhat[3 * r + s] = D[3 * r + s] / (h[r] * h[s]);
+    p.c = c;
+    p.dT = h[0] * h[1] * h[2];
+    for (int q = 0; q < 3; ++q) p.dF[q] = p.dT / h[q];
+
+    if (ctx->partitioned) {
+        for (int f = 0; f < 6; ++f) {
+            if (ctx->nbr[f] < 0) continue;
+            const size_t bytes = (size_t)ctx->halo_count[f] * sizeof(double);
+            if (cudaMalloc(&ctx->sendbuf[f], bytes) != cudaSuccess || cudaMalloc(&ctx->recvbuf[f], bytes) != cudaSuccess) {
+                free_ctx(ctx);
+                return DG_ENOMEM;
+            }
+            cudaMemset(ctx->recvbuf[f], 0, bytes);
+        }
+        // interior box: cells whose faces touch no partition face
+        std::vector<int64_t> shell;
+        for (int q = 0; q < 3; ++q) {
+            const int64_t lo = ctx->nbr[2 * q] >= 0 ? 1 : 0;
+            const int64_t hi = ctx->nloc[q] - (ctx->nbr[2 * q + 1] >= 0 ? 1 : 0);
+            ctx->inner_lo[q] = lo;
+            ctx->inner_cnt[q] = hi > lo ? hi - lo : 0;
+        }
+        for (int64_t z = 0; z < ctx->nloc[2]; ++z)
+            for (int64_t y = 0; y < ctx->nloc[1]; ++y)
+                for (int64_t x = 0; x < ctx->nloc[0]; ++x) {
+                    const int64_t l[3] = {x, y, z};
+                    bool inner = true;
+                    for (int q = 0; q < 3; ++q)
+                        if (l[q] < ctx->inner_lo[q] || l[q] >= ctx->inner_lo[q] + ctx->inner_cnt[q]) inner = false;
+                    if (!inner) shell.push_back(x + ctx->nloc[0] * (y + ctx->nloc[1] * z));
+                }
+        ctx->nshell = (int64_t)shell.size();
+        if (ctx->nshell) {
+            if (cudaMalloc(&ctx->shell, shell.size() * sizeof(int64_t)) != cudaSuccess) { free_ctx(ctx); return DG_ENOMEM; }
+            if (cudaMemcpy(ctx->shell, shell.data(), shell.size() * sizeof(int64_t), cudaMemcpyHostToDevice) !=
+                cudaSuccess) { free_ctx(ctx); return DG_ECUDA; }
+        }
+        if (cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_recv, cudaEventDisableTiming) != cudaSuccess) {
+            free_ctx(ctx);
+            return DG_ECUDA;
+        }
+        if (nccl_unique_id) {
+            const NcclApi* api = nccl_api();
+            if (!api) { free_ctx(ctx); return DG_ENCCL; }
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_unique_id, sizeof(id));
+            if (api->ncclCommInitRank(&ctx->comm, nranks, id, rank) != 0) { ctx->comm = nullptr; free_ctx(ctx); return DG_ENCCL; }
+        }
+    } else {
+        for (int q = 0; q < 3; ++q) { ctx->inner_lo[q] = 0; ctx->inner_cnt[q] = ctx->nloc[q]; }
+    }
+    for (int f = 0; f < 6; ++f) p.ghost[f] = ctx->recvbuf[f];
+    *out = ctx;
+    return DG_OK;
+}
+
+extern "C" int dg_local_layout(const dg_ctx* ctx, int64_t cell_lo[3], int64_t cell_cnt[3], int64_t* ndofs)
+{
+    if (!ctx) return DG_EINVAL;
+    for (int q = 0; q < 3; ++q) {
+        if (cell_lo) cell_lo[q] = ctx->gofs[q];
+        if (cell_cnt) cell_cnt[q] = ctx->nloc[q];
+    }
+    if (ndofs) *ndofs = ctx->ndofs;
+    return DG_OK;
+}
+
+static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, unsigned terms, cudaStream_t s)
+{
+    if (!ctx || !z || !y) return DG_EINVAL;
+    if ((const double*)y == z || (f && f == z)) return DG_EINVAL;
+    if (terms & ~(unsigned)(DG_ALL | DG_HALO_EXTERNAL)) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    KParams p = ctx->base;
+    p.z = z;
+    p.y = y;
+    p.f = f;
+    p.mask = terms & DG_ALL;
+    const bool external = (terms & DG_HALO_EXTERNAL) != 0;
+    if (!ctx->partitioned) {
+        p.task_list = nullptr;
+        for (int q = 0; q < 3; ++q) { p.task_lo[q] = 0; p.task_cnt[q] = ctx->nloc[q]; }
+        p.ntasks = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2];
+        return cuda_rc(launch_cell(ctx->k, p, s));
+    }
+    // (iv) of SURVEY.md 3: pack partition layers, exchange on the comm stream, overlap with inner cells
+    const bool need_comm = !external && (p.mask & DG_INTERIOR_FACES);
+    if (need_comm) {
+        if (!ctx->comm) return DG_ENCCL;
+        const NcclApi* api = nccl_api();
+        if (!api) return DG_ENCCL;
+        for (int fc = 0; fc < 6; ++fc)
+            if (ctx->nbr[fc] >= 0) DG_CUDA(launch_pack(z, ctx->sendbuf[fc], ctx->n3, ctx->nloc, fc, s));
+        DG_CUDA(cudaEventRecord(ctx->ev_packed, s));
+        DG_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
+        if (api->ncclGroupStart() != 0) return DG_ENCCL;
+        for (int fc = 0; fc < 6; ++fc) {
+            if (ctx->nbr[fc] < 0) continue;
+            if (api->ncclSend(ctx->sendbuf[fc], (size_t)ctx->halo_count[fc], dgNcclFloat64, ctx->nbr[fc], ctx->comm,
+                              ctx->comm_stream) != 0 ||
+                api->ncclRecv(ctx->recvbuf[fc], (size_t)ctx->halo_count[fc], dgNcclFloat64, ctx->nbr[fc], ctx->comm,
+                              ctx->comm_stream) != 0) {
+                api->ncclGroupEnd();
+                return DG_ENCCL;
+            }
+        }
+        if (api->ncclGroupEnd() != 0) return DG_ENCCL;
+        DG_CUDA(cudaEventRecord(ctx->ev_recv, ctx->comm_stream));
+    }
+    // inner cells: no remote data
+    p.task_list = nullptr;
+    for (int q = 0; q < 3; ++q) { p.task_lo[q] = ctx->inner_lo[q]; p.task_cnt[q] = ctx->inner_cnt[q]; }
+    p.ntasks = ctx->inner_cnt[0] * ctx->inner_cnt[1] * ctx->inner_cnt[2];
+    DG_CUDA(launch_cell(ctx->k, p, s));
+    if (need_comm) DG_CUDA(cudaStreamWaitEvent(s, ctx->ev_recv, 0));
+    p.task_list = ctx->shell;
+    p.ntasks = ctx->nshell;
+    return cuda_rc(launch_cell(ctx->k, p, s));
+}
+
+extern "C" int dg_apply(dg_ctx* ctx, const double* z, double* y, void* stream)
+{
+    return apply_impl(ctx, z, nullptr, y, DG_ALL, (cudaStream_t)stream);
+}
+
+extern "C" int dg_apply_ex(dg_ctx* ctx, const double* z, double* y, unsigned terms, void* stream)
+{
+    return apply_impl(ctx, z, nullptr, y, terms, (cudaStream_t)stream);
+}
+
+extern "C" int dg_residual(dg_ctx* ctx, const double* z, const double* f, double* r, void* stream)
+{
+    if (!f || f == r) return DG_EINVAL;
+    return apply_impl(ctx, z, f, r, DG_ALL, (cudaStream_t)stream);
+}
+
+extern "C" int dg_apply_host(dg_ctx* ctx, const double* z_host, double* y_host)
+{
+    if (!ctx || !z_host || !y_host) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    const size_t bytes = (size_t)ctx->ndofs * sizeof(double);
+    if (!ctx->host_stream && cudaStreamCreateWithFlags(&ctx->host_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return DG_ECUDA;
+    if (!ctx->hz) {
+        if (cudaMalloc(&ctx->hz, bytes) != cudaSuccess) return DG_ENOMEM;
+        if (cudaMalloc(&ctx->hy, bytes) != cudaSuccess) { cudaFree(ctx->hz); ctx->hz = nullptr; return DG_ENOMEM; }
+    }
+    DG_CUDA(cudaMemcpyAsync(ctx->hz, z_host, bytes, cudaMemcpyHostToDevice, ctx->host_stream));
+    int rc = apply_impl(ctx, ctx->hz, nullptr, ctx->hy, DG_ALL, ctx->host_stream);
+    if (rc != DG_OK) return rc;
+    DG_CUDA(cudaMemcpyAsync(y_host, ctx->hy, bytes, cudaMemcpyDeviceToHost, ctx->host_stream));
+    DG_CUDA(cudaStreamSynchronize(ctx->host_stream));
+    return DG_OK;
+}
+
+extern "C" int dg_sync(dg_ctx* ctx)
+{
+    if (!ctx) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    DG_CUDA(cudaDeviceSynchronize());
+    if (ctx->comm) {
+        const NcclApi* api = nccl_api();
+        ncclResult_t r = 0;
+        if (api && api->ncclCommGetAsyncError && api->ncclCommGetAsyncError(ctx->comm, &r) == 0 && r != 0)
+            return DG_ENCCL;
+    }
+    return DG_OK;
+}
+
+extern "C" int dg_destroy(dg_ctx* ctx)
+{
+    if (!ctx) return DG_EINVAL;
+    int rc = DG_OK;
+    cudaSetDevice(ctx->device);
+    if (cudaDeviceSynchronize() != cudaSuccess) rc = DG_ECUDA;
+    free_ctx(ctx);
+    return rc;
+}
+
+extern "C" int dg_halo_info(const dg_ctx* ctx, int face, int* neighbor_rank, int64_t* count)
+{
+    if (!ctx || face < 0 || face > 5) return DG_EINVAL;
+    if (neighbor_rank) *neighbor_rank = ctx->nbr[face];
+    if (count) *count = ctx->halo_count[face];
+    return DG_OK;
+}
+
+extern "C" int dg_halo_buffer(dg_ctx* ctx, int face, int which, double** ptr)
+{
+    if (!ctx || face < 0 || face > 5 || (which != 0 && which != 1) || !ptr) return DG_EINVAL;
+    *ptr = which ? ctx->recvbuf[face] : ctx->sendbuf[face];
+    return DG_OK;
+}
+
+extern "C" int dg_halo_pack(dg_ctx* ctx, const double* z, void* stream)
+{
+    if (!ctx || !z) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    for (int fc = 0; fc < 6; ++fc)
+        if (ctx->nbr[fc] >= 0) DG_CUDA(launch_pack(z, ctx->sendbuf[fc], ctx->n3, ctx->nloc, fc, (cudaStream_t)stream));
+    return DG_OK;
+}
+
+extern "C" int dg_fill_uniform(double* dst, int64_t count, uint64_t seed, int64_t offset, void* stream)
+{
+    if ((!dst && count > 0) || count < 0 || offset < 0) return DG_EINVAL;
+    return cuda_rc(launch_fill_uniform(dst, count, seed, offset, (cudaStream_t)stream));
+}
+
+extern "C" int dg_fill_uniform_local(dg_ctx* ctx, double* dst, uint64_t seed, void* stream)
+{
+    if (!ctx || !dst) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    return cuda_rc(launch_fill_uniform_local(dst, ctx->n3, ctx->nloc, ctx->gofs, ctx->gcells, seed, (cudaStream_t)stream));
+}
+
+extern "C" int dg_get_kernel_info(const dg_ctx* ctx, dg_kernel_info* info)
+{
+    if (!ctx || !info) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    LaunchInfo li;
+    if (cell_launch_info(ctx->k, &li) != 0) return DG_ECUDA;
+    info->launches_per_apply = ctx->partitioned ? 2 : 1;
+    info->cells_per_cta = li.cells_per_cta;
+    info->threads_per_cta = li.threads;
+    info->smem_bytes = li.smem;
+    info->regs_per_thread = li.regs;
+    info->ctas_per_sm = li.ctas_per_sm;
+    return DG_OK;
+}

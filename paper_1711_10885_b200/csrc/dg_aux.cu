@@ -1,0 +1,80 @@
+// Auxiliary kernels: halo packing (partition-layer cells -> contiguous send buffer)
+// and the counter-based input generator (reading C-13; identical to inputs.py).
+#include "dg_internal.h"
+
+namespace dg {
+
+// face f = 2q + s: the layer lc[q] = (s ? nloc[q]-1 : 0); cells ordered by the two
+// tangential local coordinates (t1 fastest), t1 < t2, each a contiguous n^3 block.
+__global__ void pack_kernel(const double* __restrict__ z, double* __restrict__ dst, int n3, int64_t n0, int64_t n1,
+                            int64_t n2, int q, int s, int64_t total)
+{
+    const int64_t nl[3] = {n0, n1, n2};
+    const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cellk = i / n3, j = i - cellk * n3;
+        int64_t lc[3];
+        lc[t1] = cellk % nl[t1];
+        lc[t2] = cellk / nl[t1];
+        lc[q] = s ? nl[q] - 1 : 0;
+        const int64_t e = lc[0] + n0 * (lc[1] + n1 * lc[2]);
+        dst[i] = z[e * n3 + j];
+    }
+}
+
+cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc[3], int face, cudaStream_t s)
+{
+    const int q = face >> 1, sd = face & 1;
+    const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+    const int64_t total = nloc[t1] * nloc[t2] * n3;
+    if (total == 0) return cudaSuccess;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    pack_kernel<<<(unsigned)blocks, 256, 0, s>>>(z, dst, n3, nloc[0], nloc[1], nloc[2], q, sd, total);
+    return cudaGetLastError();
+}
+
+__device__ __forceinline__ double splitmix_uniform(uint64_t g, uint64_t seed)
+{
+    uint64_t x = (seed << 40) + g + 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return (double)(x >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+}
+
+__global__ void fill_kernel(double* dst, int64_t count, uint64_t seed, int64_t offset)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = splitmix_uniform((uint64_t)(offset + i), seed);
+}
+
+cudaError_t launch_fill_uniform(double* dst, int64_t count, uint64_t seed, int64_t offset, cudaStream_t s)
+{
+    if (count <= 0) return cudaSuccess;
+    fill_kernel<<<148 * 8, 256, 0, s>>>(dst, count, seed, offset);
+    return cudaGetLastError();
+}
+
+__global__ void fill_local_kernel(double* dst, int n3, int64_t n0, int64_t n1, int64_t n2, int64_t o0, int64_t o1,
+                                  int64_t o2, int64_t g0, int64_t g1, uint64_t seed, int64_t total)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = i / n3, j = i - e * n3;
+        const int64_t lx = e % n0, ly = (e / n0) % n1, lz = e / (n0 * n1);
+        const int64_t ge = (o0 + lx) + g0 * ((o1 + ly) + g1 * (o2 + lz));
+        dst[i] = splitmix_uniform((uint64_t)(ge * n3 + j), seed);
+    }
+}
+
+cudaError_t launch_fill_uniform_local(double* dst, int n3, const int64_t nloc[3], const int64_t gofs[3],
+                                      const int64_t gcells[3], uint64_t seed, cudaStream_t s)
+{
+    const int64_t total = nloc[0] * nloc[1] * nloc[2] * n3;
+    if (total <= 0) return cudaSuccess;
+    fill_local_kernel<<<148 * 8, 256, 0, s>>>(dst, n3, nloc[0], nloc[1], nloc[2], gofs[0], gofs[1], gofs[2],
+                                              gcells[0], gcells[1], seed, total);
+    return cudaGetLastError();
+}
+
+}  // namespace dg

@@ -1,0 +1,80 @@
+// One translation unit per basis size n = k+1 (compiled with -DDG_N=n): the
+// fused cell kernel instantiation, its __constant__ table upload and launcher.
+#include "dg_cell.cuh"
+
+#include <cstring>
+
+#define DG_CAT2(a, b) a##b
+#define DG_CAT(a, b) DG_CAT2(a, b)
+
+namespace dg {
+
+int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
+{
+    constexpr int N = DG_N;
+    if (t.n != N) return -1;
+    Tab<N> h;
+    for (int i = 0; i < N; ++i) {
+        for (int j = 0; j < N; ++j) {
+            h.V[i][j] = t.V[i][j];
+            h.Dc[i][j] = t.Dc[i][j];
+        }
+        h.w[i] = t.w[i];
+        h.L0[i] = t.L0[i];
+        h.L1[i] = t.L1[i];
+        h.LD0[i] = t.LD0[i];
+        h.LD1[i] = t.LD1[i];
+        h.th0[i] = t.th0[i];
+        h.th1[i] = t.th1[i];
+        h.dth0[i] = t.dth0[i];
+        h.dth1[i] = t.dth1[i];
+    }
+    return cudaMemcpyToSymbol(g_tab, &h, sizeof(h)) == cudaSuccess ? 0 : -3;
+}
+
+static int g_attr_done[64];
+
+cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
+{
+    constexpr int N = DG_N;
+    constexpr int C = Cfg<N>::C;
+    if (p.ntasks <= 0) return cudaSuccess;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !g_attr_done[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(dg_cell_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Smem<N>::BYTES);
+        if (e != cudaSuccess) return e;
+        g_attr_done[dev] = 1;
+    }
+    const int64_t grid = (p.ntasks + C - 1) / C;
+    dg_cell_kernel<N><<<(unsigned)grid, C * N * N, Smem<N>::BYTES, s>>>(p);
+    return cudaGetLastError();
+}
+
+int DG_CAT(cell_info_n, DG_N)(LaunchInfo* info)
+{
+    constexpr int N = DG_N;
+    info->cells_per_cta = Cfg<N>::C;
+    info->threads = Cfg<N>::C * N * N;
+    info->smem = Smem<N>::BYTES;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, dg_cell_kernel<N>) != cudaSuccess) return -3;
+    info->regs = fa.numRegs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !g_attr_done[dev]) {
+        if (cudaFuncSetAttribute(dg_cell_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<N>::BYTES) !=
+            cudaSuccess)
+            return -3;
+        g_attr_done[dev] = 1;
+    }
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_cell_kernel<N>, info->threads, Smem<N>::BYTES) !=
+        cudaSuccess)
+        return -3;
+    info->ctas_per_sm = blocks;
+    return 0;
+}
+
+}  // namespace dg

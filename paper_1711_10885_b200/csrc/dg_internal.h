@@ -1,0 +1,64 @@
+// Internal declarations shared by the CUDA translation units of libdg_b200.so.
+// (Product path only; nothing here is shared with oracle/.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dg {
+
+constexpr int KMAX = 10;
+constexpr int NMAX = KMAX + 1;
+
+// 1D tables for one degree (host side, double). Built by tables.cpp.
+struct HostTables {
+    int n;
+    double xi[NMAX], w[NMAX];
+    double V[NMAX][NMAX];    // V[i][j]  = theta_j(xi_i)                    (A^(q) of eq:evalfe)
+    double Dc[NMAX][NMAX];   // Dc[i][l] = L'_l(xi_i): collocation derivative at the Gauss points
+    double L0[NMAX], L1[NMAX];    // L_l(0), L_l(1): Lagrange basis at the Gauss points, at the endpoints
+    double LD0[NMAX], LD1[NMAX];  // L'_l(0), L'_l(1)
+    double th0[NMAX], th1[NMAX];  // theta_j(0), theta_j(1)       (B^(d) of PAPER.md:528-545)
+    double dth0[NMAX], dth1[NMAX];// theta'_j(0), theta'_j(1)
+};
+int build_tables(int k, HostTables* t);
+
+// Per-launch parameters (passed by value; lands in the kernel parameter constant bank).
+struct KParams {
+    const double* z;
+    double* y;
+    const double* f;          // residual mode: y = f - A z (nullptr -> y = A z)
+    const double* ghost[6];   // neighbour-rank boundary layers per face 2q+s (nullptr: none)
+    const int64_t* task_list; // local linear cell ids (nullptr -> task box)
+    int64_t ntasks;
+    int64_t task_lo[3], task_cnt[3];
+    int64_t nloc[3];          // local cell counts
+    int64_t gofs[3];          // global index of local cell (0,0,0)
+    int64_t gcells[3];        // global cell counts
+    double hinv[3];
+    double Dhat[9];           // D_rs / (h_r h_s)
+    double kb[3];             // b_r / h_r
+    double c;
+    double dT;                // Delta_T = h1 h2 h3
+    double dF[3];             // Delta_F,q = prod_{r != q} h_r
+    double Dqq_h[3];          // D_qq / h_q   (normal flux scale)
+    double gam[3];            // gamma = <D_qq, D_qq> sigma = D_qq sigma
+    double bq[3];             // b_q
+    unsigned mask;
+};
+
+struct LaunchInfo {
+    int cells_per_cta, threads, smem, regs, ctas_per_sm;
+};
+
+// Per-degree launchers (one translation unit per n, dg_cell_n<N>.cu).
+int upload_tables(int k, const HostTables& t);          // to this device's __constant__ bank
+cudaError_t launch_cell(int k, const KParams& p, cudaStream_t s);
+int cell_launch_info(int k, LaunchInfo* info);
+
+// Halo / inputs kernels (dg_aux.cu).
+cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc[3], int face, cudaStream_t s);
+cudaError_t launch_fill_uniform(double* dst, int64_t count, uint64_t seed, int64_t offset, cudaStream_t s);
+cudaError_t launch_fill_uniform_local(double* dst, int n3, const int64_t nloc[3], const int64_t gofs[3],
+                                      const int64_t gcells[3], uint64_t seed, cudaStream_t s);
+
+}  // namespace dg

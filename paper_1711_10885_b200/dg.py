@@ -1,0 +1,227 @@
+"""Thin Python binding of libdg_b200.so (include/dg.h): argument marshalling only.
+
+Every step of y = A z runs in the library's CUDA kernels; there is no CPU or
+PyTorch fallback. If the shared library is missing this module raises at import
+of the library handle (DGError), loudly.
+
+Device vectors are torch CUDA float64 tensors (torch provides memory, streams and
+process groups only); host vectors for apply_host are numpy float64 arrays.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdg_b200.so")
+
+DG_OK, DG_EINVAL, DG_ENOMEM, DG_ECUDA, DG_ENCCL, DG_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
+VOLUME, INTERIOR_FACES, BOUNDARY_FACES, ALL, HALO_EXTERNAL = 1, 2, 4, 7, 0x100
+BC_DIRICHLET = 0
+
+EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residual", "dg_apply_host",
+            "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
+            "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info"]
+
+
+class DGError(RuntimeError):
+    def __init__(self, code, what=""):
+        self.code = code
+        msg = _lib.dg_strerror(code).decode() if _lib is not None else str(code)
+        super().__init__("%s: %s (%d)" % (what, msg, code))
+
+
+class MeshDesc(ctypes.Structure):
+    _fields_ = [("ncells", ctypes.c_int64 * 3), ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
+                ("bc", ctypes.c_int * 6), ("parts", ctypes.c_int * 3)]
+
+
+class KernelInfo(ctypes.Structure):
+    _fields_ = [("launches_per_apply", ctypes.c_int), ("cells_per_cta", ctypes.c_int),
+                ("threads_per_cta", ctypes.c_int), ("smem_bytes", ctypes.c_int),
+                ("regs_per_thread", ctypes.c_int), ("ctas_per_sm", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError("libdg_b200.so not built: run `python -m paper_1711_10885_b200.build` "
+                               "(there is no fallback path)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64
+        L.dg_setup.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(MeshDesc), ctypes.c_int, vp, vp, ctypes.c_double,
+                               ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
+        L.dg_local_layout.argtypes = [vp, vp, vp, vp]
+        L.dg_apply.argtypes = [vp, vp, vp, vp]
+        L.dg_apply_ex.argtypes = [vp, vp, vp, ctypes.c_uint, vp]
+        L.dg_residual.argtypes = [vp, vp, vp, vp, vp]
+        L.dg_apply_host.argtypes = [vp, vp, vp]
+        L.dg_sync.argtypes = [vp]
+        L.dg_destroy.argtypes = [vp]
+        L.dg_strerror.argtypes = [ctypes.c_int]
+        L.dg_strerror.restype = ctypes.c_char_p
+        L.dg_halo_info.argtypes = [vp, ctypes.c_int, vp, vp]
+        L.dg_halo_buffer.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]
+        L.dg_halo_pack.argtypes = [vp, vp, vp]
+        L.dg_fill_uniform.argtypes = [vp, i64, u64, i64, vp]
+        L.dg_fill_uniform_local.argtypes = [vp, vp, u64, vp]
+        L.dg_nccl_unique_id.argtypes = [vp]
+        L.dg_get_kernel_info.argtypes = [vp, ctypes.POINTER(KernelInfo)]
+        for name in EXPORTED:
+            if name != "dg_strerror":
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc, what):
+    if rc != DG_OK:
+        raise DGError(rc, what)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_vec(t, n, name):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TypeError("%s must be a contiguous CUDA float64 tensor" % name)
+    if t.numel() != n:
+        raise ValueError("%s has %d entries, expected %d" % (name, t.numel(), n))
+
+
+def nccl_unique_id():
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib().dg_nccl_unique_id(buf), "dg_nccl_unique_id")
+    return bytes(buf)
+
+
+def fill_uniform(t, seed, offset=0, stream=None):
+    """t[i] = U(seed, offset + i) on the device (reading C-13)."""
+    _check(lib().dg_fill_uniform(_ptr(t), t.numel(), seed, offset, _stream(stream)), "dg_fill_uniform")
+
+
+class Operator:
+    """One dg_ctx: the SIPG operator on this rank's block of a structured box mesh."""
+
+    def __init__(self, ncells, lo, hi, k, D, b, c, sigma, device=0, rank=0, nranks=1, parts=(1, 1, 1),
+                 nccl_id=None, bc=(BC_DIRICHLET,) * 6):
+        L = lib()
+        m = MeshDesc()
+        for q in range(3):
+            m.ncells[q] = int(ncells[q])
+            m.lo[q] = float(lo[q])
+            m.hi[q] = float(hi[q])
+            m.parts[q] = int(parts[q])
+        for f in range(6):
+            m.bc[f] = int(bc[f])
+        Dm = (ctypes.c_double * 9)(*[float(v) for v in np.asarray(D, dtype=np.float64).ravel()])
+        bv = (ctypes.c_double * 3)(*[float(v) for v in b])
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = (ctypes.c_ubyte * 128).from_buffer_copy(bytes(nccl_id))
+        h = ctypes.c_void_p()
+        _check(L.dg_setup(ctypes.byref(h), ctypes.byref(m), int(k), Dm, bv, float(c), float(sigma), int(device),
+                          int(rank), int(nranks), idbuf), "dg_setup")
+        self._h = h
+        self.k = k
+        self.n3 = (k + 1) ** 3
+        self.device = device
+        lo_ = (ctypes.c_int64 * 3)()
+        cnt = (ctypes.c_int64 * 3)()
+        nd = ctypes.c_int64()
+        _check(L.dg_local_layout(h, lo_, cnt, ctypes.byref(nd)), "dg_local_layout")
+        self.cell_lo = tuple(lo_)
+        self.cell_cnt = tuple(cnt)
+        self.ndofs = nd.value
+
+    # -- compute ------------------------------------------------------------------------------------
+    def apply(self, z, y, terms=ALL, stream=None):
+        _dev_vec(z, self.ndofs, "z")
+        _dev_vec(y, self.ndofs, "y")
+        _check(lib().dg_apply_ex(self._h, _ptr(z), _ptr(y), terms, _stream(stream)), "dg_apply_ex")
+        return y
+
+    def residual(self, z, f, r, stream=None):
+        for t, nm in ((z, "z"), (f, "f"), (r, "r")):
+            _dev_vec(t, self.ndofs, nm)
+        _check(lib().dg_residual(self._h, _ptr(z), _ptr(f), _ptr(r), _stream(stream)), "dg_residual")
+        return r
+
+    def apply_host(self, z_host, y_host):
+        """End-to-end: host arrays in, host array out (copies inside the call)."""
+        for a in (z_host, y_host):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+                    and a.size == self.ndofs):
+                raise TypeError("host vectors must be contiguous float64 numpy arrays of ndofs entries")
+        _check(lib().dg_apply_host(self._h, a_ptr(z_host), a_ptr(y_host)), "dg_apply_host")
+        return y_host
+
+    def fill_uniform_local(self, t, seed, stream=None):
+        _dev_vec(t, self.ndofs, "t")
+        _check(lib().dg_fill_uniform_local(self._h, _ptr(t), seed, _stream(stream)), "dg_fill_uniform_local")
+
+    # -- halo ---------------------------------------------------------------------------------------
+    def halo_info(self, face):
+        r = ctypes.c_int()
+        c = ctypes.c_int64()
+        _check(lib().dg_halo_info(self._h, face, ctypes.byref(r), ctypes.byref(c)), "dg_halo_info")
+        return r.value, c.value
+
+    def halo_buffer_ptr(self, face, which):
+        p = ctypes.c_void_p()
+        _check(lib().dg_halo_buffer(self._h, face, which, ctypes.byref(p)), "dg_halo_buffer")
+        return p.value
+
+    def halo_pack(self, z, stream=None):
+        _check(lib().dg_halo_pack(self._h, _ptr(z), _stream(stream)), "dg_halo_pack")
+
+    # -- info / lifetime ----------------------------------------------------------------------------
+    def kernel_info(self):
+        ki = KernelInfo()
+        _check(lib().dg_get_kernel_info(self._h, ctypes.byref(ki)), "dg_get_kernel_info")
+        return {f: getattr(ki, f) for f, _ in KernelInfo._fields_}
+
+    def sync(self):
+        _check(lib().dg_sync(self._h), "dg_sync")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            rc = lib().dg_destroy(self._h)
+            self._h = None
+            _check(rc, "dg_destroy")
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def a_ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def from_config(cfg, **kw):
+    return Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, **kw)

@@ -1,0 +1,73 @@
+"""C-ABI checks that need no GPU: the library loads, exports every entry point
+include/dg.h declares, and validates arguments before touching the device."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1711_10885_b200 import dg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "dg.h")).read()
+    return sorted(set(re.findall(r"\b(dg_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    L = dg.lib()
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(dg.EXPORTED) == set(syms)
+
+
+def test_strerror():
+    L = dg.lib()
+    assert L.dg_strerror(0) == b"ok"
+    assert b"invalid" in L.dg_strerror(-1)
+    assert L.dg_strerror(-99) == b"unknown error"
+
+
+def setup_rc(k=2, ncells=(2, 2, 2), lo=(0, 0, 0), hi=(1, 1, 1), D=(1, 0, 0, 0, 1, 0, 0, 0, 1), b=(1, 0, 0),
+             c=1.0, sigma=1.0, parts=(1, 1, 1), nranks=1, rank=0, bc=(0,) * 6):
+    L = dg.lib()
+    m = dg.MeshDesc()
+    for q in range(3):
+        m.ncells[q], m.lo[q], m.hi[q], m.parts[q] = ncells[q], lo[q], hi[q], parts[q]
+    for f in range(6):
+        m.bc[f] = bc[f]
+    h = ctypes.c_void_p()
+    Dm = (ctypes.c_double * 9)(*D)
+    bv = (ctypes.c_double * 3)(*b)
+    return L.dg_setup(ctypes.byref(h), ctypes.byref(m), k, Dm, bv, c, sigma, 0, rank, nranks, None)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(k=0), dg.DG_EINVAL), (dict(k=11), dg.DG_EINVAL),
+    (dict(ncells=(0, 2, 2)), dg.DG_EINVAL), (dict(hi=(1, 0, 1)), dg.DG_EINVAL),
+    (dict(D=(1, 0.5, 0, 0, 1, 0, 0, 0, 1)), dg.DG_EINVAL),          # not symmetric
+    (dict(D=(-1, 0, 0, 0, 1, 0, 0, 0, 1)), dg.DG_EINVAL),           # not PSD
+    (dict(sigma=-1.0), dg.DG_EINVAL), (dict(c=float("nan")), dg.DG_EINVAL),
+    (dict(parts=(2, 1, 1)), dg.DG_EINVAL),                          # product != nranks
+    (dict(parts=(3, 1, 1), nranks=3), dg.DG_EINVAL),                # does not divide ncells
+    (dict(nranks=1, rank=1), dg.DG_EINVAL),
+    (dict(bc=(1, 0, 0, 0, 0, 0)), dg.DG_EUNSUPPORTED),              # periodic: later
+    (dict(D=(1, 0.5, 0, 0.5, 1, 0, 0, 0, 1)), dg.DG_EUNSUPPORTED),  # full D: later
+])
+def test_setup_validation(kw, code):
+    assert setup_rc(**kw) == code
+
+
+def test_null_arguments():
+    L = dg.lib()
+    assert L.dg_apply(None, None, None, None) == dg.DG_EINVAL
+    assert L.dg_local_layout(None, None, None, None) == dg.DG_EINVAL
+    assert L.dg_destroy(None) == dg.DG_EINVAL
+    assert L.dg_sync(None) == dg.DG_EINVAL
+    assert L.dg_fill_uniform(None, 5, 0, 0, None) == dg.DG_EINVAL
+    assert L.dg_nccl_unique_id(None) == dg.DG_EINVAL
