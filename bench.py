@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the matrix-free SIPG operator y = A z (arXiv 1711.10885) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+One step = one dg_apply (the whole hot path: volume, interior-face and
+boundary-face terms, plus the halo exchange when N > 1) over the workload's
+synthetic seeded input already resident in HBM. At N = 1 the workload is
+BASELINE.json configs[2] ("C3": 128x64x64 cells, k = 7, 268M DOFs). For N > 1
+(launched by torchrun, one rank per GPU, NCCL) each GPU keeps C3's block
+(weak scaling, reading C-12'), block-partitioned 2x1x1 / 2x2x1 / 2x2x2.
+
+Rank 0 prints ONE JSON line. `value` is whole-job DOFs/s (max-over-ranks device
+time of K steps, CUDA events, barrier + synchronize on both sides); `e2e` is the
+same metric through the C ABI with pinned HOST buffers (dg_apply_host: H2D of z,
+apply, D2H of y inside the timed region); `roofline` is the cell kernel's
+model-flop rate against the derived B200 FP64 peak; `cpu_baseline` is the oracle
+O-1 timed on the host cores on a bounded sample of cells (N = 1, rank 0).
+`--impl reference` times that oracle as the reference arm.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1711_10885_b200 import configs, inputs, perfmodel  # noqa: E402
+
+METRIC = "DOFs/s & FP64 GFLOP/s of matrix-free DG apply (k=7), % of roofline, 1/2/4/8 GPU"
+UNIT = "DOF/s"
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def workload(name, world):
+    if name in (None, "", "default"):
+        return configs.c3() if world == 1 else configs.c3_weak(world)
+    name = name.lower()
+    if name == "c3weak":
+        return configs.c3_weak(world)
+    if name == "c5weak":
+        return configs.c5_weak(world)
+    if name == "c5strong":
+        grid = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}[world]
+        return configs.c5_strong(grid)
+    cfg = configs.by_name(name)
+    if world != 1:
+        raise SystemExit("workload %s is single-GPU" % name)
+    return cfg
+
+
+def workload_desc(cfg, world):
+    return {"workload": "%s: %dx%dx%d cells, k=%d, %d DOFs, box %s-%s, D=%s, b=%s, c=%g, sigma=%g, Dirichlet, seed %d"
+                        % (cfg.name, cfg.ncells[0], cfg.ncells[1], cfg.ncells[2], cfg.k, cfg.ndofs,
+                           list(cfg.lo), list(cfg.hi), list(cfg.D), list(cfg.b), cfg.c, cfg.sigma, cfg.seed),
+            "k": cfg.k, "ncells": list(cfg.ncells), "ndofs": cfg.ndofs, "parts": list(cfg.parts),
+            "parallelism": "block %dx%dx%d" % tuple(cfg.parts) if world > 1 else "1 GPU",
+            "l2": "no flush: z and y are %.2f GB each per GPU (> 126 MB L2)" % (cfg.ndofs / world * 8 / 1e9)}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def sample_cells(cfg, count, seed=0):
+    """Seeded random cells plus every boundary type (corners, edges, faces, interior)."""
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = cfg.ncells
+    special = [x + nx * (y + ny * z) for x in (0, nx // 2, nx - 1) for y in (0, ny // 2, ny - 1)
+               for z in (0, nz // 2, nz - 1)]
+    extra = rng.integers(0, cfg.ncell, max(0, count - len(special)))
+    return np.unique(np.r_[special, extra]).astype(np.int64)[:max(count, 1)]
+
+
+def cpu_oracle_rate(cfg, z_host, budget_s, seed=0):
+    """O-1 (oracle, as it stands) on a bounded sample of cells; returns (DOF/s, cores, sample text, seconds)."""
+    from oracle import o1   # only bench.py's cpu_baseline / reference legs may touch oracle/
+    probe = sample_cells(cfg, 16, seed)
+    t0 = time.perf_counter()
+    _, cores = o1.apply(*cfg.args(), z_host, cells=probe)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    per_cell = dt / probe.size
+    count = int(min(max(budget_s / per_cell, 16), cfg.ncell))
+    cells = sample_cells(cfg, count, seed + 1)
+    t0 = time.perf_counter()
+    _, cores = o1.apply(*cfg.args(), z_host, cells=cells)
+    dt = time.perf_counter() - t0
+    rate = cells.size * cfg.n3 / dt
+    text = ("O-1 naive quadrature (C/OpenMP, -O3) on %d of %d cells of %s (seeded random + all boundary types); "
+            "%.1f s on %d threads" % (cells.size, cfg.ncell, cfg.name, dt, cores))
+    return rate, cores, text, dt
+
+
+def load_traffic(cfg):
+    """dram bytes per launch of the cell kernel from the committed ncu --set full summary (or None)."""
+    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        ent = d.get(cfg.name)
+        if ent and ent.get("ndofs") == cfg.ndofs // max(1, cfg.parts[0] * cfg.parts[1] * cfg.parts[2]):
+            return ent.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------------------ reference
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import o1
+    cfg = workload(args.workload, world)
+    if world > 1:
+        # the oracle is a single-host program: time one GPU-share (rank 0's block) of the workload
+        pass
+    o1.build()
+    z = inputs.uniform(cfg.ndofs, cfg.seed)
+    budget = args.ref_seconds / max(1, args.steps + args.warmup)
+    probe = sample_cells(cfg, 8, 0)
+    t0 = time.perf_counter()
+    o1.apply(*cfg.args(), z, cells=probe)
+    per_cell = max(time.perf_counter() - t0, 1e-6) / probe.size
+    count = int(min(max(budget / per_cell, 8), cfg.ncell))
+    cells = sample_cells(cfg, count, 1)
+    cores = 0
+    for _ in range(args.warmup):
+        _, cores = o1.apply(*cfg.args(), z, cells=cells)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, cores = o1.apply(*cfg.args(), z, cells=cells)
+    dt = time.perf_counter() - t0
+    rate = args.steps * cells.size * cfg.n3 / dt
+    sample = ("each step: O-1 naive quadrature (C/OpenMP) on %d of %d cells of %s (seeded random + all boundary "
+              "types)" % (cells.size, cfg.ncell, cfg.name))
+    out = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64, C-13)",
+           "config": workload_desc(cfg, world),
+           "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------ ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1711_10885_b200 import dg
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workload(args.workload, world)
+    nccl_id = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.tensor(list(dg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().tolist())
+    op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, device=local_rank, rank=rank,
+                     nranks=world, parts=cfg.parts, nccl_id=nccl_id)
+    info = op.kernel_info()
+    z = torch.empty(op.ndofs, dtype=torch.float64, device=dev)
+    y = torch.empty_like(z)
+    op.fill_uniform_local(z, cfg.seed)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        op.apply(z, y)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.2)
+    # ---- timed region: K steps, device time by CUDA events on the launching stream
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        op.apply(z, y)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_local = e0.elapsed_time(e1) * 1e-3
+    # kernel-only time (no halo exchange; identical to the step at N = 1)
+    if world > 1:
+        k0 = torch.cuda.Event(enable_timing=True)
+        k1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        k0.record(stream)
+        for _ in range(args.steps):
+            op.apply(z, y, terms=dg.ALL | dg.HALO_EXTERNAL)
+        k1.record(stream)
+        torch.cuda.synchronize()
+        tk_local = k0.elapsed_time(k1) * 1e-3
+    else:
+        tk_local = t_local
+    clk = clocks.stop()
+    t = t_local
+    tk = tk_local
+    if world > 1:
+        tt = torch.tensor([t_local, tk_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t, tk = float(tt[0]), float(tt[1])
+    total_dofs = cfg.ndofs   # whole job (all ranks)
+    value = total_dofs * args.steps / t
+    ms_per_step = t / args.steps * 1e3
+
+    # ---- roofline of the dominant kernel (the fused cell kernel)
+    per_dof = perfmodel.flopdof(3, cfg.k)
+    flops_launch_rank = per_dof * op.ndofs
+    kern_t = tk / args.steps   # one cell-kernel pass over all local cells per apply (2 launches at N > 1)
+    achieved = flops_launch_rank / kern_t / 1e12
+    peak = perfmodel.fp64_peak_tflops(clk["sm_max_mhz"] or 1965.0)
+    traffic = load_traffic(cfg)
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic,
+            "kernel": "dg_cell_kernel<%d> (FP64 DFMA pipe)" % (cfg.k + 1),
+            "flops_basis": "paper model FLOPDOF_vol+FLOPDOF_face(3,%d) = %.1f flop/DOF x %d DOFs per launch "
+                           "(PAPER.md:675-676); the kernel executes fewer (collocation variant, DESIGN.md)"
+                           % (cfg.k, per_dof, op.ndofs),
+            "peak_basis": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x %.0f MHz (B200_PROFILING.md SM count/clock; "
+                          "MEASURED_PEAKS.json has no FP64 entry)" % (clk["sm_max_mhz"] or 1965.0),
+            "kernel_ms": kern_t * 1e3}
+
+    # ---- end to end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        zh = z.cpu().pin_memory().numpy()
+        yh = torch.empty(op.ndofs, dtype=torch.float64).pin_memory().numpy()
+        op.apply_host(zh, yh)   # warm (allocates the device staging once)
+        ke = max(2, min(args.steps, args.e2e_steps))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            op.apply_host(zh, yh)
+        te = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt[0])
+        e2e = {"value": total_dofs * ke / te, "unit": UNIT, "h2d_bytes_per_step": op.ndofs * 8 * world,
+               "d2h_bytes_per_step": op.ndofs * 8 * world, "steps": ke,
+               "path": "dg_apply_host (pinned host z -> H2D -> fused kernel -> D2H y), wall clock, max over ranks"}
+
+    # ---- CPU baseline: the oracle on the host cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        zn = z.cpu().numpy()
+        rate, cores, text, _ = cpu_oracle_rate(cfg, zn, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": text}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based uniform[-1,1] z, C-13)",
+               "config": workload_desc(cfg, world),
+               "gflops_model": per_dof * value / 1e9,
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+               "gpu_launches": args.steps * (info["launches_per_apply"] if world == 1 else
+                                             (2 + sum(1 for f in range(6) if op.halo_info(f)[0] >= 0))),
+               "kernel_info": info}
+        print(json.dumps(out), flush=True)
+    op.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default=None,
+                    help="default: C3 (N=1) / C3-per-GPU weak (N>1); also c1, c2, c4-kK, c5weak, c5strong")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline sample budget")
+    ap.add_argument("--ref-seconds", type=float, default=120.0, help="reference arm total budget")
+    args = ap.parse_args()
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus %d needs torchrun (one process per GPU)" % args.gpus)
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -75,6 +75,12 @@ enum { DG_BC_DIRICHLET = 0 };
 int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const double D[9], const double b[3],
              double c, double sigma, int device, int rank, int nranks, const void* nccl_unique_id);
 
+/* Host-only block partition (no device access): rank = px + Px (py + Py pz); this rank's
+   global cell offset / counts and the neighbour rank across each face 2q+s (-1: domain
+   boundary). dg_setup uses the same rule. */
+int dg_partition(const dg_mesh_desc* mesh, int rank, int nranks, int64_t cell_lo[3], int64_t cell_cnt[3],
+                 int nbr[6]);
+
 /* This rank's cell box (global cell offset and counts) and its vector length. */
 int dg_local_layout(const dg_ctx* ctx, int64_t cell_lo[3], int64_t cell_cnt[3], int64_t* ndofs);
 

@@ -240,6 +240,31 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
     return DG_OK;
 }
 
+extern "C" int dg_partition(const dg_mesh_desc* mesh, int rank, int nranks, int64_t cell_lo[3], int64_t cell_cnt[3],
+                            int nbr[6])
+{
+    if (!mesh || nranks < 1 || rank < 0 || rank >= nranks) return DG_EINVAL;
+    for (int q = 0; q < 3; ++q)
+        if (mesh->ncells[q] < 1 || mesh->parts[q] < 1 || mesh->ncells[q] % mesh->parts[q] != 0) return DG_EINVAL;
+    if ((int64_t)mesh->parts[0] * mesh->parts[1] * mesh->parts[2] != nranks) return DG_EINVAL;
+    int pc[3];
+    pc[0] = rank % mesh->parts[0];
+    pc[1] = (rank / mesh->parts[0]) % mesh->parts[1];
+    pc[2] = rank / (mesh->parts[0] * mesh->parts[1]);
+    for (int q = 0; q < 3; ++q) {
+        const int64_t nl = mesh->ncells[q] / mesh->parts[q];
+        if (cell_lo) cell_lo[q] = nl * pc[q];
+        if (cell_cnt) cell_cnt[q] = nl;
+        for (int s = 0; s < 2; ++s) {
+            int pn[3] = {pc[0], pc[1], pc[2]};
+            pn[q] += s ? 1 : -1;
+            if (nbr) nbr[2 * q + s] = (pn[q] >= 0 && pn[q] < mesh->parts[q])
+                                          ? pn[0] + mesh->parts[0] * (pn[1] + mesh->parts[1] * pn[2]) : -1;
+        }
+    }
+    return DG_OK;
+}
+
 extern "C" int dg_local_layout(const dg_ctx* ctx, int64_t cell_lo[3], int64_t cell_cnt[3], int64_t* ndofs)
 {
     if (!ctx) return DG_EINVAL;

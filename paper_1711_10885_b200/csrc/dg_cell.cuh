@@ -25,10 +25,12 @@ namespace dg {
 
 template <int N>
 struct Tab {
-    double V[N][N];
-    double Dc[N][N];
+    // One copy of V / Dc per use site: distinct constant addresses keep the compiler from
+    // hoisting a whole 1D matrix into registers across stages (it reloads per stage instead).
+    double V[8][N][N];
+    double Dc[6][N][N];
     double w[N];
-    double L0[N], L1[N], LD0[N], LD1[N];
+    double L[6][4][N];   // per use site: L_l(0), L_l(1), L'_l(0), L'_l(1)
     double th0[N], th1[N], dth0[N], dth1[N];
 };
 
@@ -40,16 +42,16 @@ __constant__ Tab<DG_N> g_tab;
 
 // Cells per CTA for each n (threads = C n^2; 2 CTAs per SM for n = 8).
 template <int N> struct Cfg;
-template <> struct Cfg<2>  { static constexpr int C = 32; };
-template <> struct Cfg<3>  { static constexpr int C = 14; };
-template <> struct Cfg<4>  { static constexpr int C = 8; };
-template <> struct Cfg<5>  { static constexpr int C = 10; };
-template <> struct Cfg<6>  { static constexpr int C = 7; };
-template <> struct Cfg<7>  { static constexpr int C = 5; };
-template <> struct Cfg<8>  { static constexpr int C = 4; };
-template <> struct Cfg<9>  { static constexpr int C = 3; };
-template <> struct Cfg<10> { static constexpr int C = 2; };
-template <> struct Cfg<11> { static constexpr int C = 2; };
+template <> struct Cfg<2> { static constexpr int C = 32; static constexpr int MINB = 4; };
+template <> struct Cfg<3> { static constexpr int C = 14; static constexpr int MINB = 4; };
+template <> struct Cfg<4> { static constexpr int C = 8; static constexpr int MINB = 4; };
+template <> struct Cfg<5> { static constexpr int C = 10; static constexpr int MINB = 2; };
+template <> struct Cfg<6> { static constexpr int C = 7; static constexpr int MINB = 2; };
+template <> struct Cfg<7> { static constexpr int C = 5; static constexpr int MINB = 2; };
+template <> struct Cfg<8> { static constexpr int C = 4; static constexpr int MINB = 2; };
+template <> struct Cfg<9> { static constexpr int C = 3; static constexpr int MINB = 2; };
+template <> struct Cfg<10> { static constexpr int C = 2; static constexpr int MINB = 2; };
+template <> struct Cfg<11> { static constexpr int C = 2; static constexpr int MINB = 2; };
 
 // Shared-memory layout of one n^3 cell array, chosen so that x-, y- and z-pencil
 // accesses of a warp are (nearly) bank-conflict free (searched offline; n = 8 uses an
@@ -153,8 +155,43 @@ __device__ __forceinline__ FaceOut flux_boundary(const KParams& p, int q, int s,
     return o;
 }
 
+// Face coefficients of the two faces of one direction at one face point, from the own
+// pencil of u at the Gauss points (normal direction q) and the neighbour traces in NT.
 template <int N>
-__global__ void __launch_bounds__(Cfg<N>::C * N * N)
+__device__ __forceinline__ void face_pair(const KParams& p, const Tab<N>& T, const double* NT, unsigned nbmask,
+                                          bool do_int, bool do_bnd, int q, double W, int pt, const double* u,
+                                          FaceOut* fo, const double (&Ls)[4][N])
+{
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const double uo = dot<N>(Ls[s], u);          // own trace: u(x_q = s)
+        const double dref = dot<N>(Ls[2 + s], u);    // own d u / d x_hat_q at x_q = s
+        const int f = 2 * q + s;
+        fo[s].cv = 0.0;
+        fo[s].cg = 0.0;
+        if ((nbmask >> f) & 1u) {
+            if (do_int) {
+                const double un = NT[FLay<N>::ARR * (2 * f) + pt];
+                const double sn = p.Dqq_h[q] * NT[FLay<N>::ARR * (2 * f + 1) + pt];
+                fo[s] = flux_interior(p, q, s, W, uo, dref, un, sn);
+            }
+        } else if (do_bnd) {
+            fo[s] = flux_boundary(p, q, s, W, uo, dref);
+        }
+    }
+}
+
+// t[e] += lifts of the two faces of one direction along the normal pencil (normal LAST).
+template <int N>
+__device__ __forceinline__ void add_lift(const double (&Ls)[4][N], const FaceOut* fo, double* t)
+{
+#pragma unroll
+    for (int e = 0; e < N; ++e)
+        t[e] += fo[0].cv * Ls[0][e] + fo[0].cg * Ls[2][e] + fo[1].cv * Ls[1][e] + fo[1].cg * Ls[3][e];
+}
+
+template <int N>
+__global__ void __launch_bounds__(Cfg<N>::C * N * N, Cfg<N>::MINB)
 dg_cell_kernel(const KParams p)
 {
     constexpr int C = Cfg<N>::C;
@@ -178,7 +215,7 @@ dg_cell_kernel(const KParams p)
     if (!valid) task = p.ntasks - 1;
     int64_t lc[3];
     if (p.task_list) {
-        int64_t e = p.task_list[task];
+        const int64_t e = p.task_list[task];
         lc[0] = e % p.nloc[0];
         lc[1] = (e / p.nloc[0]) % p.nloc[1];
         lc[2] = e / (p.nloc[0] * p.nloc[1]);
@@ -192,253 +229,188 @@ dg_cell_kernel(const KParams p)
     const double* zc = p.z + cell * n3;
     const bool do_int = (p.mask & 2u) != 0, do_bnd = (p.mask & 4u) != 0, do_vol = (p.mask & 1u) != 0;
 
-    // ---------------------------------------------------------------- neighbour traces
-    // For face f = 2q + s the neighbour lies at lc[q] + (s ? 1 : -1); its face is x_q = 1 - s.
-    // Step A (normal direction first): thread (a, bb) contracts the neighbour's line through
-    // tangential modal indices (j_t1 = a, j_t2 = bb) with theta(1-s) and theta'(1-s).
+    double r[N], t[N];
+
+    // ---------------------------------------------------------------- own cell: x-pencil stage
+    // x-pencil (y = a, z = bb): coefficients along x straight from global memory
+#pragma unroll
+    for (int e = 0; e < N; ++e) r[e] = __ldg(zc + e + N * (a + N * bb));
+
+    // ---------------------------------------------------------------- neighbour traces, step A
+    // Face f = 2q + s: the neighbour lies at lc[q] + (s ? 1 : -1) and its face is x_q = 1 - s.
+    // Normal direction FIRST: thread (a, bb) contracts the neighbour's line
+    // through tangential modal indices (j_t1 = a, j_t2 = bb) with theta(1-s) and theta'(1-s).
     unsigned nbmask = 0;   // bit f: face f has a neighbour cell (local or on another rank)
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const int f = 2 * q + s;
-            const int64_t g = p.gofs[q] + lc[q] + (s ? 1 : -1);
-            int kind = 0;
-            if (g >= 0 && g < p.gcells[q]) {
-                const int64_t l = lc[q] + (s ? 1 : -1);
-                kind = (l >= 0 && l < p.nloc[q]) ? 1 : 2;
-            }
-            if (kind) nbmask |= 1u << f;
-            const bool need = kind != 0 && do_int;
-            if (need) {
-                const double* zn;
-                if (kind == 1) {
-                    const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
-                    zn = zc + (s ? st : -st) * n3;
-                } else {
-                    // ghost layer indexed by the two tangential local coordinates
-                    const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
-                    zn = p.ghost[f] + (lc[t1] + p.nloc[t1] * lc[t2]) * n3;
-                }
-                const double* thv = s ? T.th0 : T.th1;    // neighbour face is at x_q = 1 - s
-                const double* dthv = s ? T.dth0 : T.dth1;
-                double su = 0.0, sd = 0.0;
-#pragma unroll
-                for (int e = 0; e < N; ++e) {
-                    int ix, iy, iz;
-                    if (q == 0) { ix = e; iy = a; iz = bb; }
-                    else if (q == 1) { ix = a; iy = e; iz = bb; }
-                    else { ix = a; iy = bb; iz = e; }
-                    const double v = __ldg(zn + ix + N * (iy + N * iz));
-                    su = fma(thv[e], v, su);
-                    sd = fma(dthv[e], v, sd);
-                }
-                NT[FLay<N>::at(2 * f, a, bb)] = su;
-                NT[FLay<N>::at(2 * f + 1, a, bb)] = sd;
-            }
+#pragma unroll 1
+    for (int f = 0; f < 6; ++f) {
+        const int q = f >> 1, s = f & 1;
+        const int64_t g = p.gofs[q] + lc[q] + (s ? 1 : -1);
+        if (g < 0 || g >= p.gcells[q]) continue;
+        nbmask |= 1u << f;
+        if (!do_int) continue;
+        const int64_t l = lc[q] + (s ? 1 : -1);
+        const double* zn;
+        if (l >= 0 && l < p.nloc[q]) {
+            const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
+            zn = zc + (s ? st : -st) * n3;
+        } else {
+            // ghost layer (other rank), indexed by the two tangential local coordinates
+            const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+            zn = p.ghost[f] + (lc[t1] + p.nloc[t1] * lc[t2]) * n3;
         }
+        // element (j_q = e) of the line: offset a*sa + bb*sb + e*se
+        const int se = (q == 0) ? 1 : (q == 1) ? N : NN;
+        const int base = (q == 0) ? N * a + NN * bb : (q == 1) ? a + NN * bb : a + N * bb;
+        const double* thv = s ? T.th0 : T.th1;
+        const double* dthv = s ? T.dth0 : T.dth1;
+        double su = 0.0, sd = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            const double v = __ldg(zn + base + e * se);
+            su = fma(thv[e], v, su);
+            sd = fma(dthv[e], v, sd);
+        }
+        NT[FLay<N>::at(2 * f, a, bb)] = su;
+        NT[FLay<N>::at(2 * f + 1, a, bb)] = sd;
     }
 
     // ---------------------------------------------------------------- (1) evaluate
-    double r[N], t[N];
-    // x-pencil (y = a, z = bb): coefficients along x from global memory
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = __ldg(zc + e + N * (a + N * bb));
-    mv<N>(T.V, r, t);
+    mv<N>(T.V[0], r, t);
 #pragma unroll
     for (int e = 0; e < N; ++e) A0[Lay<N>::at(e, a, bb)] = t[e];
     __syncthreads();
 
-    // neighbour traces, steps B/C: V along t1 then t2 for the 12 arrays (tasks: 12 arrays x N lines)
-    {
-        constexpr int NTASK = 12 * N;
-        for (int task2 = pi; task2 < NTASK; task2 += NN) {
-            const int arr = task2 / N, line = task2 % N;
-            if (do_int && ((nbmask >> (arr >> 1)) & 1u)) {
+    // neighbour traces, step B: V along the first tangential index (12 arrays x N lines)
+    for (int task2 = pi; task2 < 12 * N; task2 += NN) {
+        const int arr = task2 / N, line = task2 - arr * N;
+        if (do_int && ((nbmask >> (arr >> 1)) & 1u)) {
 #pragma unroll
-                for (int e = 0; e < N; ++e) r[e] = NT[FLay<N>::at(arr, e, line)];
-                mv<N>(T.V, r, t);
+            for (int e = 0; e < N; ++e) r[e] = NT[FLay<N>::at(arr, e, line)];
+            mv<N>(T.V[1], r, t);
 #pragma unroll
-                for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, e, line)] = t[e];
-            }
+            for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, e, line)] = t[e];
         }
     }
 
     // y-pencil (x = a, z = bb)
 #pragma unroll
     for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, e, bb)];
-    mv<N>(T.V, r, t);
+    mv<N>(T.V[2], r, t);
 #pragma unroll
     for (int e = 0; e < N; ++e) A1[Lay<N>::at(a, e, bb)] = t[e];
     __syncthreads();
 
-    {
-        constexpr int NTASK = 12 * N;
-        for (int task2 = pi; task2 < NTASK; task2 += NN) {
-            const int arr = task2 / N, line = task2 % N;
-            if (do_int && ((nbmask >> (arr >> 1)) & 1u)) {
+    // neighbour traces, step C: V along the second tangential index
+    for (int task2 = pi; task2 < 12 * N; task2 += NN) {
+        const int arr = task2 / N, line = task2 - arr * N;
+        if (do_int && ((nbmask >> (arr >> 1)) & 1u)) {
 #pragma unroll
-                for (int e = 0; e < N; ++e) r[e] = NT[FLay<N>::at(arr, line, e)];
-                mv<N>(T.V, r, t);
+            for (int e = 0; e < N; ++e) r[e] = NT[FLay<N>::at(arr, line, e)];
+            mv<N>(T.V[3], r, t);
 #pragma unroll
-                for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, line, e)] = t[e];
-            }
+            for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, line, e)] = t[e];
         }
     }
 
-    // z-pencil (x = a, y = bb): u at the Gauss points along z, and d/dz
-    double uz[N], dz[N];
+    // z-pencil (x = a, y = bb): u at the Gauss points
 #pragma unroll
     for (int e = 0; e < N; ++e) r[e] = A1[Lay<N>::at(a, bb, e)];
-    mv<N>(T.V, r, uz);
-    mv<N>(T.Dc, uz, dz);
+    mv<N>(T.V[4], r, t);
 #pragma unroll
-    for (int e = 0; e < N; ++e) A0[Lay<N>::at(a, bb, e)] = uz[e];
+    for (int e = 0; e < N; ++e) A0[Lay<N>::at(a, bb, e)] = t[e];
     __syncthreads();
 
-    // ---------------------------------------------------------------- faces: own traces + flux
-    // wq: tangential quadrature weight product at this thread's face point (a, bb)
-    const double wab = T.w[a] * T.w[bb];
+    // ---------------------------------------------------------------- faces + gradients
+    const double wab = T.w[a] * T.w[bb];          // tangential weights at this face point
+    const int pt = a + FLay<N>::RS * bb;          // face point (a, bb) in the NT arrays
     FaceOut fz[2], fx[2], fy[2];
-    {
-        // z faces at point (x = a, y = bb): traces from uz
-        const double W = p.dF[2] * wab;
+    // z-pencil: z-face traces and fluxes
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const double uo = dot<N>(s ? T.L1 : T.L0, uz);
-            const double dref = dot<N>(s ? T.LD1 : T.LD0, uz);
-            const int f = 4 + s;
-            fz[s].cv = 0.0; fz[s].cg = 0.0;
-            if ((nbmask >> f) & 1u) {
-                if (do_int) {
-                    const double un = NT[FLay<N>::at(2 * f, a, bb)];
-                    const double sn = p.Dqq_h[2] * NT[FLay<N>::at(2 * f + 1, a, bb)];
-                    fz[s] = flux_interior(p, 2, s, W, uo, dref, un, sn);
-                }
-            } else if (do_bnd) {
-                fz[s] = flux_boundary(p, 2, s, W, uo, dref);
-            }
-        }
-    }
-    // x-pencil (y = a, z = bb): d/dx and the x-face traces
+    for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, bb, e)];
+    face_pair<N>(p, T, NT, nbmask, do_int, do_bnd, 2, p.dF[2] * wab, pt, r, fz, T.L[0]);
+    // x-pencil: d/dx_hat (collocation) and x-face traces / fluxes
 #pragma unroll
     for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(e, a, bb)];
-    mv<N>(T.Dc, r, t);
+    mv<N>(T.Dc[0], r, t);
 #pragma unroll
     for (int e = 0; e < N; ++e) A1[Lay<N>::at(e, a, bb)] = t[e];
-    {
-        const double W = p.dF[0] * wab;
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const double uo = dot<N>(s ? T.L1 : T.L0, r);
-            const double dref = dot<N>(s ? T.LD1 : T.LD0, r);
-            const int f = s;
-            fx[s].cv = 0.0; fx[s].cg = 0.0;
-            if ((nbmask >> f) & 1u) {
-                if (do_int) {
-                    const double un = NT[FLay<N>::at(2 * f, a, bb)];
-                    const double sn = p.Dqq_h[0] * NT[FLay<N>::at(2 * f + 1, a, bb)];
-                    fx[s] = flux_interior(p, 0, s, W, uo, dref, un, sn);
-                }
-            } else if (do_bnd) {
-                fx[s] = flux_boundary(p, 0, s, W, uo, dref);
-            }
-        }
-    }
-    // y-pencil (x = a, z = bb): d/dy and the y-face traces
+    face_pair<N>(p, T, NT, nbmask, do_int, do_bnd, 0, p.dF[0] * wab, pt, r, fx, T.L[1]);
+    // y-pencil: d/dy_hat and y-face traces / fluxes
 #pragma unroll
     for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, e, bb)];
-    mv<N>(T.Dc, r, t);
+    mv<N>(T.Dc[1], r, t);
 #pragma unroll
     for (int e = 0; e < N; ++e) A2[Lay<N>::at(a, e, bb)] = t[e];
-    {
-        const double W = p.dF[1] * wab;
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const double uo = dot<N>(s ? T.L1 : T.L0, r);
-            const double dref = dot<N>(s ? T.LD1 : T.LD0, r);
-            const int f = 2 + s;
-            fy[s].cv = 0.0; fy[s].cg = 0.0;
-            if ((nbmask >> f) & 1u) {
-                if (do_int) {
-                    const double un = NT[FLay<N>::at(2 * f, a, bb)];
-                    const double sn = p.Dqq_h[1] * NT[FLay<N>::at(2 * f + 1, a, bb)];
-                    fy[s] = flux_interior(p, 1, s, W, uo, dref, un, sn);
-                }
-            } else if (do_bnd) {
-                fy[s] = flux_boundary(p, 1, s, W, uo, dref);
-            }
-        }
-    }
+    face_pair<N>(p, T, NT, nbmask, do_int, do_bnd, 1, p.dF[1] * wab, pt, r, fy, T.L[2]);
     __syncthreads();
 
     // ---------------------------------------------------------------- (2) quadrature-point data
-    // z-pencil (x = a, y = bb): x^(1..3) as coefficients of the REFERENCE test derivatives,
-    // x^(0) = W c u; X = x^(0) + Dc^T x^(3) + z-face lifts stays in registers.
+    // z-pencil (x = a, y = bb): u and d/dz_hat along z; x^(1), x^(2) back to A1, A2 in place,
+    // X = x^(0) + Dc^T x^(3) + z-face lifts in registers.
     double X[N];
     {
-        const double wxy = p.dT * wab;
-        double x1[N], x2[N], x3[N];
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, bb, e)];
+        double dz[N];
+        mv<N>(T.Dc[2], r, dz);
+        const double wxy = do_vol ? p.dT * wab : 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) {
-            const double gx = A1[Lay<N>::at(a, bb, e)];
-            const double gy = A2[Lay<N>::at(a, bb, e)];
+            const int ie = Lay<N>::at(a, bb, e);
+            const double gx = A1[ie];
+            const double gy = A2[ie];
             const double gz = dz[e];
-            const double u = uz[e];
-            const double W = do_vol ? wxy * T.w[e] : 0.0;
-            // x^(r) / h_r = W (sum_s D_rs/(h_r h_s) d_s u_hat - b_r/h_r u)     (eq:gauss_points)
-            x1[e] = W * (p.Dhat[0] * gx + p.Dhat[1] * gy + p.Dhat[2] * gz - p.kb[0] * u);
-            x2[e] = W * (p.Dhat[3] * gx + p.Dhat[4] * gy + p.Dhat[5] * gz - p.kb[1] * u);
-            x3[e] = W * (p.Dhat[6] * gx + p.Dhat[7] * gy + p.Dhat[8] * gz - p.kb[2] * u);
+            const double u = r[e];
+            const double W = wxy * T.w[e];
+            // x^(r) / h_r = W (sum_s D_rs/(h_r h_s) d_s u_hat - b_r/h_r u)   (eq:gauss_points)
+            A1[ie] = W * (p.Dhat[0] * gx + p.Dhat[1] * gy + p.Dhat[2] * gz - p.kb[0] * u);
+            A2[ie] = W * (p.Dhat[3] * gx + p.Dhat[4] * gy + p.Dhat[5] * gz - p.kb[1] * u);
+            t[e] = W * (p.Dhat[6] * gx + p.Dhat[7] * gy + p.Dhat[8] * gz - p.kb[2] * u);
             X[e] = W * p.c * u;
         }
+        double s3[N];
+        mtv<N>(T.Dc[3], t, s3);
 #pragma unroll
-        for (int e = 0; e < N; ++e) {
-            A1[Lay<N>::at(a, bb, e)] = x1[e];
-            A2[Lay<N>::at(a, bb, e)] = x2[e];
-        }
-        mtv<N>(T.Dc, x3, t);
-#pragma unroll
-        for (int e = 0; e < N; ++e)
-            X[e] += t[e] + fz[0].cv * T.L0[e] + fz[0].cg * T.LD0[e] + fz[1].cv * T.L1[e] + fz[1].cg * T.LD1[e];
+        for (int e = 0; e < N; ++e) X[e] += s3[e];
+        add_lift<N>(T.L[3], fz, X);
     }
     __syncthreads();
 
     // x-pencil: Dc^T x^(1) + x-face lifts (in place in A1)
 #pragma unroll
     for (int e = 0; e < N; ++e) r[e] = A1[Lay<N>::at(e, a, bb)];
-    mtv<N>(T.Dc, r, t);
+    mtv<N>(T.Dc[4], r, t);
+    add_lift<N>(T.L[4], fx, t);
 #pragma unroll
-    for (int e = 0; e < N; ++e)
-        A1[Lay<N>::at(e, a, bb)] = t[e] + fx[0].cv * T.L0[e] + fx[0].cg * T.LD0[e] + fx[1].cv * T.L1[e] + fx[1].cg * T.LD1[e];
+    for (int e = 0; e < N; ++e) A1[Lay<N>::at(e, a, bb)] = t[e];
     // y-pencil: Dc^T x^(2) + y-face lifts (in place in A2)
 #pragma unroll
     for (int e = 0; e < N; ++e) r[e] = A2[Lay<N>::at(a, e, bb)];
-    mtv<N>(T.Dc, r, t);
+    mtv<N>(T.Dc[5], r, t);
+    add_lift<N>(T.L[5], fy, t);
 #pragma unroll
-    for (int e = 0; e < N; ++e)
-        A2[Lay<N>::at(a, e, bb)] = t[e] + fy[0].cv * T.L0[e] + fy[0].cg * T.LD0[e] + fy[1].cv * T.L1[e] + fy[1].cg * T.LD1[e];
+    for (int e = 0; e < N; ++e) A2[Lay<N>::at(a, e, bb)] = t[e];
     __syncthreads();
 
     // ---------------------------------------------------------------- (3) integrate
     // z-pencil: gather, V^T along z
 #pragma unroll
     for (int e = 0; e < N; ++e) X[e] += A1[Lay<N>::at(a, bb, e)] + A2[Lay<N>::at(a, bb, e)];
-    mtv<N>(T.V, X, t);
+    mtv<N>(T.V[5], X, t);
 #pragma unroll
     for (int e = 0; e < N; ++e) A0[Lay<N>::at(a, bb, e)] = t[e];
     __syncthreads();
     // y-pencil: V^T along y
 #pragma unroll
     for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, e, bb)];
-    mtv<N>(T.V, r, t);
+    mtv<N>(T.V[6], r, t);
 #pragma unroll
     for (int e = 0; e < N; ++e) A1[Lay<N>::at(a, e, bb)] = t[e];
     __syncthreads();
     // x-pencil: V^T along x, then the single store of y (or f - y)
 #pragma unroll
     for (int e = 0; e < N; ++e) r[e] = A1[Lay<N>::at(e, a, bb)];
-    mtv<N>(T.V, r, t);
+    mtv<N>(T.V[7], r, t);
     if (valid) {
         double* yc = p.y + cell * n3 + N * (a + N * bb);
         if (p.f) {

@@ -16,14 +16,16 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
     Tab<N> h;
     for (int i = 0; i < N; ++i) {
         for (int j = 0; j < N; ++j) {
-            h.V[i][j] = t.V[i][j];
-            h.Dc[i][j] = t.Dc[i][j];
+            for (int c = 0; c < 8; ++c) h.V[c][i][j] = t.V[i][j];
+            for (int c = 0; c < 6; ++c) h.Dc[c][i][j] = t.Dc[i][j];
         }
         h.w[i] = t.w[i];
-        h.L0[i] = t.L0[i];
-        h.L1[i] = t.L1[i];
-        h.LD0[i] = t.LD0[i];
-        h.LD1[i] = t.LD1[i];
+        for (int c = 0; c < 6; ++c) {
+            h.L[c][0][i] = t.L0[i];
+            h.L[c][1][i] = t.L1[i];
+            h.L[c][2][i] = t.LD0[i];
+            h.L[c][3][i] = t.LD1[i];
+        }
         h.th0[i] = t.th0[i];
         h.th1[i] = t.th1[i];
         h.dth0[i] = t.dth0[i];

@@ -21,7 +21,7 @@ BC_DIRICHLET = 0
 
 EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residual", "dg_apply_host",
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
-            "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info"]
+            "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition"]
 
 
 class DGError(RuntimeError):
@@ -72,6 +72,7 @@ def lib():
         L.dg_fill_uniform_local.argtypes = [vp, vp, u64, vp]
         L.dg_nccl_unique_id.argtypes = [vp]
         L.dg_get_kernel_info.argtypes = [vp, ctypes.POINTER(KernelInfo)]
+        L.dg_partition.argtypes = [ctypes.POINTER(MeshDesc), ctypes.c_int, ctypes.c_int, vp, vp, vp]
         for name in EXPORTED:
             if name != "dg_strerror":
                 getattr(L, name).restype = ctypes.c_int
@@ -111,6 +112,29 @@ def nccl_unique_id():
     return bytes(buf)
 
 
+def mesh_desc(ncells, lo, hi, parts=(1, 1, 1), bc=(BC_DIRICHLET,) * 6):
+    m = MeshDesc()
+    for q in range(3):
+        m.ncells[q] = int(ncells[q])
+        m.lo[q] = float(lo[q])
+        m.hi[q] = float(hi[q])
+        m.parts[q] = int(parts[q])
+    for f in range(6):
+        m.bc[f] = int(bc[f])
+    return m
+
+
+def partition(ncells, parts, rank):
+    """Host-only block partition (dg_partition): (cell_lo, cell_cnt, neighbour rank per face)."""
+    m = mesh_desc(ncells, (0, 0, 0), (1, 1, 1), parts)
+    lo = (ctypes.c_int64 * 3)()
+    cnt = (ctypes.c_int64 * 3)()
+    nb = (ctypes.c_int * 6)()
+    nr = int(parts[0]) * int(parts[1]) * int(parts[2])
+    _check(lib().dg_partition(ctypes.byref(m), int(rank), nr, lo, cnt, nb), "dg_partition")
+    return tuple(lo), tuple(cnt), tuple(nb)
+
+
 def fill_uniform(t, seed, offset=0, stream=None):
     """t[i] = U(seed, offset + i) on the device (reading C-13)."""
     _check(lib().dg_fill_uniform(_ptr(t), t.numel(), seed, offset, _stream(stream)), "dg_fill_uniform")
@@ -122,14 +146,7 @@ class Operator:
     def __init__(self, ncells, lo, hi, k, D, b, c, sigma, device=0, rank=0, nranks=1, parts=(1, 1, 1),
                  nccl_id=None, bc=(BC_DIRICHLET,) * 6):
         L = lib()
-        m = MeshDesc()
-        for q in range(3):
-            m.ncells[q] = int(ncells[q])
-            m.lo[q] = float(lo[q])
-            m.hi[q] = float(hi[q])
-            m.parts[q] = int(parts[q])
-        for f in range(6):
-            m.bc[f] = int(bc[f])
+        m = mesh_desc(ncells, lo, hi, parts, bc)
         Dm = (ctypes.c_double * 9)(*[float(v) for v in np.asarray(D, dtype=np.float64).ravel()])
         bv = (ctypes.c_double * 3)(*[float(v) for v in b])
         idbuf = None
