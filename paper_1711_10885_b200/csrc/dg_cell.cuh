@@ -1,61 +1,75 @@
 // Fused cell kernel: y = A z for the SIPG/WSIPG operator of arXiv 1711.10885,
-// FP64, sm_100a. One CTA processes C cells; each cell is worked on by n^2
-// threads, each thread owning one "pencil" (a line of n points along one
-// direction) in each of three roles (x-, y- and z-pencil).
+// FP64, sm_100a.
+//
+// Work decomposition: a cell is processed by TPC threads (one warp for n = 7..9, a
+// fraction of a warp for small n, two warps for n >= 10); each thread owns P
+// "pencils" (lines of n points along one direction) in each of the three roles
+// (x-, y- and z-pencil), so one uniform-register load of a 1D matrix entry feeds P
+// DFMAs and the cell's phases synchronise with __syncwarp only (no CTA barrier for
+// TPC <= 32). The 1D matrices live in __constant__ memory (one copy per use site so
+// the compiler reloads per stage instead of hoisting whole matrices into registers).
 //
 // Per cell (Algorithm 1, reorganised owner-computes):
-//   (1) evaluate u at the n^3 Gauss points by sum factorization
-//       u_q = (V x V x V) z              (eq:evalfe; kernel eq:sum_fact_kernel :590-595)
-//       and the reference gradient by collocation derivatives along each pencil
-//       (Dc = G V^{-1}, exact since u in Q_k: DESIGN.md "What differs")
-//   (2) quadrature-point data x^(r) (eq:gauss_points) and x^(0) = c u W
-//   (3) integrate: y = (V^T x V^T x V^T)(x^(0) + sum_r Dc_r^T x^(r) + face lifts)   (eq:evalblf, :425-444)
-//   (4-10) faces: own traces (u, normal derivative) are 1D extrapolations of u_q along the
-//       normal (L_l(s), L'_l(s)); neighbour traces are the paper's face sum factorization
-//       with the normal direction FIRST: theta(s) / theta'(s) contraction of the
-//       neighbour's coefficients, then V along the two tangential directions. The SIPG
-//       consistency, symmetry, penalty and upwind terms (eq:blf :301-315, Phi :334-341) are
-//       evaluated pointwise and lifted back with the normal direction LAST, into the
-//       quadrature-space array before the transposed V stages. Each cell writes only its
-//       own y block: no atomics, no races, y stored once.
+//   (1) u at the n^3 Gauss points by sum factorization u_q = (V x V x V) z
+//       (eq:evalfe; kernel eq:sum_fact_kernel :590-595), each stage
+//       by the even-odd decomposition of V (V_{n-1-i,j} = (-1)^j V_ij); the reference
+//       gradient by collocation derivatives Dc = G V^{-1} along each pencil (exact on
+//       Q_k; Dc is centro-antisymmetric, also applied even-odd)
+//   (2) quadrature-point data x^(r) (eq:gauss_points), x^(0) = c u W
+//   (3) y = (V^T x V^T x V^T)(x^(0) + sum_r Dc_r^T x^(r) + face lifts)   (eq:evalblf :425-444)
+//   (4-10) faces: own traces are 1D extrapolations of u_q along the normal (L_l(s), L'_l(s));
+//       neighbour traces are the paper's face sum factorization with the normal direction
+//       FIRST: theta(s)/theta'(s) contraction of the neighbour's
+//       coefficients, then V along the two tangential directions. Consistency, symmetry,
+//       penalty and upwind terms (eq:blf :301-315, Phi :334-341) are evaluated pointwise
+//       and lifted with the normal direction LAST into the quadrature-space array before
+//       the transposed stages. Each cell writes only its own y block once: no atomics.
 #pragma once
 #include "dg_internal.h"
 
 namespace dg {
 
 template <int N>
+struct EO {                        // even-odd form of a centro-antisymmetric matrix A
+    static constexpr int H = N / 2;
+    double p[H > 0 ? H : 1][H > 0 ? H : 1];   // (A_ij + A_i,N-1-j) / 2
+    double m[H > 0 ? H : 1][H > 0 ? H : 1];   // (A_ij - A_i,N-1-j) / 2
+    double col[H > 0 ? H : 1];                // A_iH            (odd N)
+    double row[H > 0 ? H : 1];                // A_Hj            (odd N)
+};
+
+template <int N>
 struct Tab {
-    // One copy of V / Dc per use site: distinct constant addresses keep the compiler from
-    // hoisting a whole 1D matrix into registers across stages (it reloads per stage instead).
-    double V[8][N][N];
-    double Dc[6][N][N];
+    static constexpr int HC = (N + 1) / 2;
+    double Vh[10][HC][N];    // V_ij = theta_j(xi_i), rows i < ceil(n/2); one copy per use site
+    EO<N> Dc[6];             // collocation derivative Dc_il (row = point, col = value)
+    EO<N> DcT[6];            // its transpose
     double w[N];
-    double L[6][4][N];   // per use site: L_l(0), L_l(1), L'_l(0), L'_l(1)
+    double L[6][4][N];       // per use site: L_l(0), L_l(1), L'_l(0), L'_l(1)
     double th0[N], th1[N], dth0[N], dth1[N];
 };
 
 #ifndef DG_N
 #error "dg_cell.cuh is compiled once per degree with -DDG_N=<k+1>"
 #endif
-// The 1D tables of this translation unit's degree (uploaded by upload_tables).
 __constant__ Tab<DG_N> g_tab;
 
-// Cells per CTA for each n (threads = C n^2; 2 CTAs per SM for n = 8).
+// TPC threads per cell, P pencils per thread (TPC * P >= n^2), C cells per CTA.
 template <int N> struct Cfg;
-template <> struct Cfg<2> { static constexpr int C = 32; static constexpr int MINB = 4; };
-template <> struct Cfg<3> { static constexpr int C = 14; static constexpr int MINB = 4; };
-template <> struct Cfg<4> { static constexpr int C = 8; static constexpr int MINB = 4; };
-template <> struct Cfg<5> { static constexpr int C = 10; static constexpr int MINB = 2; };
-template <> struct Cfg<6> { static constexpr int C = 7; static constexpr int MINB = 2; };
-template <> struct Cfg<7> { static constexpr int C = 5; static constexpr int MINB = 2; };
-template <> struct Cfg<8> { static constexpr int C = 4; static constexpr int MINB = 2; };
-template <> struct Cfg<9> { static constexpr int C = 3; static constexpr int MINB = 2; };
-template <> struct Cfg<10> { static constexpr int C = 2; static constexpr int MINB = 2; };
-template <> struct Cfg<11> { static constexpr int C = 2; static constexpr int MINB = 2; };
+template <> struct Cfg<2>  { static constexpr int TPC = 4,  P = 1, C = 32, MINB = 8; };
+template <> struct Cfg<3>  { static constexpr int TPC = 8,  P = 2, C = 16, MINB = 8; };
+template <> struct Cfg<4>  { static constexpr int TPC = 8,  P = 2, C = 16, MINB = 6; };
+template <> struct Cfg<5>  { static constexpr int TPC = 16, P = 2, C = 8,  MINB = 4; };
+template <> struct Cfg<6>  { static constexpr int TPC = 16, P = 3, C = 4,  MINB = 8; };
+template <> struct Cfg<7>  { static constexpr int TPC = 32, P = 2, C = 1,  MINB = 16; };
+template <> struct Cfg<8>  { static constexpr int TPC = 32, P = 2, C = 1,  MINB = 16; };
+template <> struct Cfg<9>  { static constexpr int TPC = 32, P = 3, C = 1,  MINB = 12; };
+template <> struct Cfg<10> { static constexpr int TPC = 64, P = 2, C = 1,  MINB = 8; };
+template <> struct Cfg<11> { static constexpr int TPC = 64, P = 2, C = 1,  MINB = 8; };
 
-// Shared-memory layout of one n^3 cell array, chosen so that x-, y- and z-pencil
-// accesses of a warp are (nearly) bank-conflict free (searched offline; n = 8 uses an
-// XOR swizzle that is conflict free for all three access patterns).
+// Shared-memory layout of one n^3 cell array: x-, y- and z-pencil accesses of a warp are
+// (nearly) bank-conflict free (searched offline; n = 8 uses an XOR swizzle that is conflict
+// free for all three access patterns).
 template <int N> struct Lay {
     static constexpr int SY = (N == 6) ? 9 : (N == 10 ? 11 : N);
     static constexpr int SZ = (N == 2) ? 5 : (N == 3) ? 9 : (N == 4) ? 18 : (N == 5) ? 25 : (N == 6) ? 54
@@ -72,45 +86,129 @@ template <> struct Lay<8> {
     }
 };
 
-// Face-trace arrays: 6 faces x 2 quantities x n^2 points, row padded.
+// Face arrays: 6 faces x 2 quantities x n^2 points, row padded. Slot 2f holds the
+// neighbour trace u+, then the lift coefficient cv; slot 2f+1 the neighbour normal
+// derivative, then cg.
 template <int N> struct FLay {
-    static constexpr int RS = N + 1;              // row stride
-    static constexpr int ARR = N * RS + 1;        // one n x n array
+    static constexpr int RS = N + 1;
+    static constexpr int ARR = N * RS + 1;
     static constexpr int SLOT = 12 * ARR;
     __device__ __forceinline__ static int at(int arr, int i1, int i2) { return arr * ARR + i1 + RS * i2; }
 };
 
 template <int N>
 struct Smem {
-    static constexpr int C = Cfg<N>::C;
     static constexpr int PER_CELL = 3 * Lay<N>::SLOT + FLay<N>::SLOT;
-    static constexpr int BYTES = C * PER_CELL * 8;
+    static constexpr int BYTES = Cfg<N>::C * PER_CELL * 8;
 };
 
-// out[i] = sum_j M[i][j] in[j]
-template <int N>
-__device__ __forceinline__ void mv(const double (&M)[N][N], const double* in, double* out)
+// ---------------------------------------------------------------------------------- 1D stages
+// t[k][i] = sum_j V_ij r[k][j]  (even-odd: V_{n-1-i,j} = (-1)^j V_ij)
+template <int N, int P>
+__device__ __forceinline__ void v_fwd(const double (&Vh)[(N + 1) / 2][N], const double (&r)[P][N], double (&t)[P][N])
 {
+    constexpr int H = N / 2;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-        double s = 0.0;
+    for (int i = 0; i < H; ++i) {
+        double E[P], O[P];
 #pragma unroll
-        for (int j = 0; j < N; ++j) s = fma(M[i][j], in[j], s);
-        out[i] = s;
+        for (int k = 0; k < P; ++k) { E[k] = 0.0; O[k] = 0.0; }
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                if (j & 1) O[k] = fma(Vh[i][j], r[k][j], O[k]);
+                else E[k] = fma(Vh[i][j], r[k][j], E[k]);
+            }
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            t[k][i] = E[k] + O[k];
+            t[k][N - 1 - i] = E[k] - O[k];
+        }
+    }
+    if (N & 1) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            double E = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; j += 2) E = fma(Vh[H][j], r[k][j], E);
+            t[k][H] = E;
+        }
     }
 }
-// out[j] = sum_i M[i][j] in[i]
-template <int N>
-__device__ __forceinline__ void mtv(const double (&M)[N][N], const double* in, double* out)
+
+// t[k][j] = sum_i V_ij r[k][i]
+template <int N, int P>
+__device__ __forceinline__ void v_bwd(const double (&Vh)[(N + 1) / 2][N], const double (&r)[P][N], double (&t)[P][N])
 {
+    constexpr int H = N / 2;
+    double s[P][H > 0 ? H : 1], d[P][H > 0 ? H : 1];
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            s[k][i] = r[k][i] + r[k][N - 1 - i];
+            d[k][i] = r[k][i] - r[k][N - 1 - i];
+        }
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-        double s = 0.0;
+        double acc[P];
 #pragma unroll
-        for (int i = 0; i < N; ++i) s = fma(M[i][j], in[i], s);
-        out[j] = s;
+        for (int k = 0; k < P; ++k) acc[k] = ((N & 1) && !(j & 1)) ? Vh[H][j] * r[k][H] : 0.0;
+#pragma unroll
+        for (int i = 0; i < H; ++i)
+#pragma unroll
+            for (int k = 0; k < P; ++k) acc[k] = fma(Vh[i][j], (j & 1) ? d[k][i] : s[k][i], acc[k]);
+#pragma unroll
+        for (int k = 0; k < P; ++k) t[k][j] = acc[k];
     }
 }
+
+// t[k] = A r[k] for a centro-antisymmetric A (A_{n-1-i,n-1-j} = -A_ij) in even-odd form
+template <int N, int P>
+__device__ __forceinline__ void c_apply(const EO<N>& A, const double (&r)[P][N], double (&t)[P][N])
+{
+    constexpr int H = N / 2;
+    double s[P][H > 0 ? H : 1], d[P][H > 0 ? H : 1];
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            s[k][j] = r[k][j] + r[k][N - 1 - j];
+            d[k][j] = r[k][j] - r[k][N - 1 - j];
+        }
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        double Pp[P], Q[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            Pp[k] = (N & 1) ? A.col[i] * r[k][H] : 0.0;
+            Q[k] = 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < H; ++j)
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                Pp[k] = fma(A.p[i][j], s[k][j], Pp[k]);
+                Q[k] = fma(A.m[i][j], d[k][j], Q[k]);
+            }
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            t[k][i] = Pp[k] + Q[k];
+            t[k][N - 1 - i] = Q[k] - Pp[k];
+        }
+    }
+    if (N & 1) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < H; ++j) acc = fma(A.row[j], d[k][j], acc);
+            t[k][H] = acc;
+        }
+    }
+}
+
 template <int N>
 __device__ __forceinline__ double dot(const double* a, const double* v)
 {
@@ -120,27 +218,26 @@ __device__ __forceinline__ double dot(const double* a, const double* v)
     return s;
 }
 
-// Face coefficient pair (cv, cgref) at one face point for a cell face in direction q,
-// own side s (s = 1: face x_q = 1, this cell is T-; s = 0: face x_q = 0, this cell is T+).
-//   uo, dref : own trace and reference normal derivative (d/dx_hat_q)
-//   un, sn   : neighbour trace and physical normal flux D_qq d u/dx_q (nu = +e_q)
-// Returns the contribution cv * phi_i + cg_phys * d_q phi_i as (cv, cgref = cg_phys / h_q).
+// ---------------------------------------------------------------------------------- face terms
+// Contribution cv * phi_i + cg_phys * d_q phi_i of one face point, returned as
+// (cv, cg = cg_phys / h_q, the coefficient of the REFERENCE normal derivative).
+// own side s: s = 1 -> face x_q = 1, this cell is T- ; s = 0 -> face x_q = 0, this cell is T+.
 struct FaceOut { double cv, cg; };
 
 __device__ __forceinline__ FaceOut flux_interior(const KParams& p, int q, int s, double W, double uo, double dref,
                                                  double un, double sn)
 {
-    const double so = p.Dqq_h[q] * dref;           // D_qq du/dx_q
+    const double so = p.Dqq_h[q] * dref;                      // D_qq du/dx_q (own)
     const double um = s ? uo : un, up = s ? un : uo;
     const double sm = s ? so : sn, sp = s ? sn : so;
     const double bn = p.bq[q];
     const double Phi = (bn >= 0.0) ? bn * um : bn * up;       // upwind flux
     const double J = um - up;                                 // [[u]] = u- - u+
-    const double Avg = 0.5 * (sm + sp);                       // {D grad u}_w . nu, w = 1/2 (constant D), C-1
+    const double Avg = 0.5 * (sm + sp);                       // nu.{D grad u}_w, w = 1/2 (constant D), C-1
     const double com = Phi - Avg + p.gam[q] * J;
     FaceOut o;
     o.cv = s ? W * com : -W * com;                            // [[phi]] = +phi on T-, -phi on T+
-    o.cg = -W * 0.5 * J * p.Dqq_h[q];                         // -(nu.{D grad phi}_w, [[u]]): w = 1/2, / h_q
+    o.cg = -W * 0.5 * J * p.Dqq_h[q];                         // -(nu.{D grad phi}_w, [[u]])
     return o;
 }
 __device__ __forceinline__ FaceOut flux_boundary(const KParams& p, int q, int s, double W, double uo, double dref)
@@ -155,60 +252,31 @@ __device__ __forceinline__ FaceOut flux_boundary(const KParams& p, int q, int s,
     return o;
 }
 
-// Face coefficients of the two faces of one direction at one face point, from the own
-// pencil of u at the Gauss points (normal direction q) and the neighbour traces in NT.
+// ---------------------------------------------------------------------------------- kernel
 template <int N>
-__device__ __forceinline__ void face_pair(const KParams& p, const Tab<N>& T, const double* NT, unsigned nbmask,
-                                          bool do_int, bool do_bnd, int q, double W, int pt, const double* u,
-                                          FaceOut* fo, const double (&Ls)[4][N])
-{
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        const double uo = dot<N>(Ls[s], u);          // own trace: u(x_q = s)
-        const double dref = dot<N>(Ls[2 + s], u);    // own d u / d x_hat_q at x_q = s
-        const int f = 2 * q + s;
-        fo[s].cv = 0.0;
-        fo[s].cg = 0.0;
-        if ((nbmask >> f) & 1u) {
-            if (do_int) {
-                const double un = NT[FLay<N>::ARR * (2 * f) + pt];
-                const double sn = p.Dqq_h[q] * NT[FLay<N>::ARR * (2 * f + 1) + pt];
-                fo[s] = flux_interior(p, q, s, W, uo, dref, un, sn);
-            }
-        } else if (do_bnd) {
-            fo[s] = flux_boundary(p, q, s, W, uo, dref);
-        }
-    }
-}
-
-// t[e] += lifts of the two faces of one direction along the normal pencil (normal LAST).
-template <int N>
-__device__ __forceinline__ void add_lift(const double (&Ls)[4][N], const FaceOut* fo, double* t)
-{
-#pragma unroll
-    for (int e = 0; e < N; ++e)
-        t[e] += fo[0].cv * Ls[0][e] + fo[0].cg * Ls[2][e] + fo[1].cv * Ls[1][e] + fo[1].cg * Ls[3][e];
-}
-
-template <int N>
-__global__ void __launch_bounds__(Cfg<N>::C * N * N, Cfg<N>::MINB)
+__global__ void __launch_bounds__(Cfg<N>::C * Cfg<N>::TPC, Cfg<N>::MINB)
 dg_cell_kernel(const KParams p)
 {
-    constexpr int C = Cfg<N>::C;
+    constexpr int TPC = Cfg<N>::TPC, P = Cfg<N>::P, C = Cfg<N>::C;
     constexpr int NN = N * N;
-    extern __shared__ double smem[];
     static_assert(N == DG_N, "one degree per translation unit");
+    static_assert(TPC * P >= NN, "pencil slots");
+    static_assert(TPC <= 32 || C == 1, "multi-warp cells use CTA barriers: one cell per CTA");
+    extern __shared__ double smem[];
     const Tab<N>& T = g_tab;
 
     const int tid = threadIdx.x;
-    const int slot = tid / NN;
-    const int pi = tid - slot * NN;
-    const int a = pi % N, bb = pi / N;
+    const int slot = tid / TPC;
+    const int lane = tid - slot * TPC;
 
     double* A0 = smem + slot * Smem<N>::PER_CELL;
     double* A1 = A0 + Lay<N>::SLOT;
     double* A2 = A1 + Lay<N>::SLOT;
     double* NT = A2 + Lay<N>::SLOT;
+
+    auto csync = [&]() {
+        if (TPC <= 32) __syncwarp(); else __syncthreads();
+    };
 
     int64_t task = (int64_t)blockIdx.x * C + slot;
     const bool valid = task < p.ntasks;
@@ -229,197 +297,360 @@ dg_cell_kernel(const KParams p)
     const double* zc = p.z + cell * n3;
     const bool do_int = (p.mask & 2u) != 0, do_bnd = (p.mask & 4u) != 0, do_vol = (p.mask & 1u) != 0;
 
-    double r[N], t[N];
-
-    // ---------------------------------------------------------------- own cell: x-pencil stage
-    // x-pencil (y = a, z = bb): coefficients along x straight from global memory
+    // this thread's pencils: pencil index pc = lane + k TPC = a + N bb
+    int pa[P], pb[P];
+    bool act[P];
 #pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = __ldg(zc + e + N * (a + N * bb));
+    for (int k = 0; k < P; ++k) {
+        const int pc = lane + k * TPC;
+        act[k] = pc < NN;
+        const int pcc = act[k] ? pc : 0;
+        pa[k] = pcc % N;
+        pb[k] = pcc / N;
+    }
+
+    double r[P][N], t[P][N];
 
     // ---------------------------------------------------------------- neighbour traces, step A
     // Face f = 2q + s: the neighbour lies at lc[q] + (s ? 1 : -1) and its face is x_q = 1 - s.
-    // Normal direction FIRST: thread (a, bb) contracts the neighbour's line
-    // through tangential modal indices (j_t1 = a, j_t2 = bb) with theta(1-s) and theta'(1-s).
-    unsigned nbmask = 0;   // bit f: face f has a neighbour cell (local or on another rank)
-#pragma unroll 1
+    // Normal direction FIRST: contract the neighbour's line through tangential modal indices
+    // (j_t1, j_t2) = (a, bb) with theta(1-s) and theta'(1-s).
+    unsigned nbmask = 0;
+#pragma unroll
     for (int f = 0; f < 6; ++f) {
         const int q = f >> 1, s = f & 1;
         const int64_t g = p.gofs[q] + lc[q] + (s ? 1 : -1);
-        if (g < 0 || g >= p.gcells[q]) continue;
-        nbmask |= 1u << f;
-        if (!do_int) continue;
-        const int64_t l = lc[q] + (s ? 1 : -1);
-        const double* zn;
-        if (l >= 0 && l < p.nloc[q]) {
-            const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
-            zn = zc + (s ? st : -st) * n3;
-        } else {
-            // ghost layer (other rank), indexed by the two tangential local coordinates
-            const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
-            zn = p.ghost[f] + (lc[t1] + p.nloc[t1] * lc[t2]) * n3;
-        }
-        // element (j_q = e) of the line: offset a*sa + bb*sb + e*se
-        const int se = (q == 0) ? 1 : (q == 1) ? N : NN;
-        const int base = (q == 0) ? N * a + NN * bb : (q == 1) ? a + NN * bb : a + N * bb;
-        const double* thv = s ? T.th0 : T.th1;
-        const double* dthv = s ? T.dth0 : T.dth1;
-        double su = 0.0, sd = 0.0;
+        if (g >= 0 && g < p.gcells[q]) nbmask |= 1u << f;
+    }
+    if (do_int) {
+#pragma unroll 1
+        for (int f = 0; f < 6; ++f) {
+            if (!((nbmask >> f) & 1u)) continue;
+            const int q = f >> 1, s = f & 1;
+            const int64_t l = lc[q] + (s ? 1 : -1);
+            const double* zn;
+            if (l >= 0 && l < p.nloc[q]) {
+                const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
+                zn = zc + (s ? st : -st) * n3;
+            } else {
+                const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+                zn = p.ghost[f] + (lc[t1] + p.nloc[t1] * lc[t2]) * n3;
+            }
+            const int se = (q == 0) ? 1 : (q == 1) ? N : NN;
+            const double* thv = s ? T.th0 : T.th1;
+            const double* dthv = s ? T.dth0 : T.dth1;
 #pragma unroll
-        for (int e = 0; e < N; ++e) {
-            const double v = __ldg(zn + base + e * se);
-            su = fma(thv[e], v, su);
-            sd = fma(dthv[e], v, sd);
+            for (int k = 0; k < P; ++k) {
+                const int base = (q == 0) ? N * pa[k] + NN * pb[k] : (q == 1) ? pa[k] + NN * pb[k] : pa[k] + N * pb[k];
+#pragma unroll
+                for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(zn + base + e * se) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                double su = 0.0, sd = 0.0;
+#pragma unroll
+                for (int e = 0; e < N; ++e) {
+                    su = fma(thv[e], r[k][e], su);
+                    sd = fma(dthv[e], r[k][e], sd);
+                }
+                if (act[k]) {
+                    NT[FLay<N>::at(2 * f, pa[k], pb[k])] = su;
+                    NT[FLay<N>::at(2 * f + 1, pa[k], pb[k])] = sd;
+                }
+            }
         }
-        NT[FLay<N>::at(2 * f, a, bb)] = su;
-        NT[FLay<N>::at(2 * f + 1, a, bb)] = sd;
     }
 
     // ---------------------------------------------------------------- (1) evaluate
-    mv<N>(T.V[0], r, t);
+    // x-pencils (y = a, z = bb) straight from global memory, V along x
 #pragma unroll
-    for (int e = 0; e < N; ++e) A0[Lay<N>::at(e, a, bb)] = t[e];
-    __syncthreads();
-
-    // neighbour traces, step B: V along the first tangential index (12 arrays x N lines)
-    for (int task2 = pi; task2 < 12 * N; task2 += NN) {
-        const int arr = task2 / N, line = task2 - arr * N;
-        if (do_int && ((nbmask >> (arr >> 1)) & 1u)) {
+    for (int k = 0; k < P; ++k) {
+        const double* src = zc + N * (pa[k] + N * pb[k]);
+        if (N % 2 == 0) {
 #pragma unroll
-            for (int e = 0; e < N; ++e) r[e] = NT[FLay<N>::at(arr, e, line)];
-            mv<N>(T.V[1], r, t);
-#pragma unroll
-            for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, e, line)] = t[e];
-        }
-    }
-
-    // y-pencil (x = a, z = bb)
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, e, bb)];
-    mv<N>(T.V[2], r, t);
-#pragma unroll
-    for (int e = 0; e < N; ++e) A1[Lay<N>::at(a, e, bb)] = t[e];
-    __syncthreads();
-
-    // neighbour traces, step C: V along the second tangential index
-    for (int task2 = pi; task2 < 12 * N; task2 += NN) {
-        const int arr = task2 / N, line = task2 - arr * N;
-        if (do_int && ((nbmask >> (arr >> 1)) & 1u)) {
-#pragma unroll
-            for (int e = 0; e < N; ++e) r[e] = NT[FLay<N>::at(arr, line, e)];
-            mv<N>(T.V[3], r, t);
-#pragma unroll
-            for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, line, e)] = t[e];
-        }
-    }
-
-    // z-pencil (x = a, y = bb): u at the Gauss points
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = A1[Lay<N>::at(a, bb, e)];
-    mv<N>(T.V[4], r, t);
-#pragma unroll
-    for (int e = 0; e < N; ++e) A0[Lay<N>::at(a, bb, e)] = t[e];
-    __syncthreads();
-
-    // ---------------------------------------------------------------- faces + gradients
-    const double wab = T.w[a] * T.w[bb];          // tangential weights at this face point
-    const int pt = a + FLay<N>::RS * bb;          // face point (a, bb) in the NT arrays
-    FaceOut fz[2], fx[2], fy[2];
-    // z-pencil: z-face traces and fluxes
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, bb, e)];
-    face_pair<N>(p, T, NT, nbmask, do_int, do_bnd, 2, p.dF[2] * wab, pt, r, fz, T.L[0]);
-    // x-pencil: d/dx_hat (collocation) and x-face traces / fluxes
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(e, a, bb)];
-    mv<N>(T.Dc[0], r, t);
-#pragma unroll
-    for (int e = 0; e < N; ++e) A1[Lay<N>::at(e, a, bb)] = t[e];
-    face_pair<N>(p, T, NT, nbmask, do_int, do_bnd, 0, p.dF[0] * wab, pt, r, fx, T.L[1]);
-    // y-pencil: d/dy_hat and y-face traces / fluxes
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, e, bb)];
-    mv<N>(T.Dc[1], r, t);
-#pragma unroll
-    for (int e = 0; e < N; ++e) A2[Lay<N>::at(a, e, bb)] = t[e];
-    face_pair<N>(p, T, NT, nbmask, do_int, do_bnd, 1, p.dF[1] * wab, pt, r, fy, T.L[2]);
-    __syncthreads();
-
-    // ---------------------------------------------------------------- (2) quadrature-point data
-    // z-pencil (x = a, y = bb): u and d/dz_hat along z; x^(1), x^(2) back to A1, A2 in place,
-    // X = x^(0) + Dc^T x^(3) + z-face lifts in registers.
-    double X[N];
-    {
-#pragma unroll
-        for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, bb, e)];
-        double dz[N];
-        mv<N>(T.Dc[2], r, dz);
-        const double wxy = do_vol ? p.dT * wab : 0.0;
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-            const int ie = Lay<N>::at(a, bb, e);
-            const double gx = A1[ie];
-            const double gy = A2[ie];
-            const double gz = dz[e];
-            const double u = r[e];
-            const double W = wxy * T.w[e];
-            // x^(r) / h_r = W (sum_s D_rs/(h_r h_s) d_s u_hat - b_r/h_r u)   (eq:gauss_points)
-            A1[ie] = W * (p.Dhat[0] * gx + p.Dhat[1] * gy + p.Dhat[2] * gz - p.kb[0] * u);
-            A2[ie] = W * (p.Dhat[3] * gx + p.Dhat[4] * gy + p.Dhat[5] * gz - p.kb[1] * u);
-            t[e] = W * (p.Dhat[6] * gx + p.Dhat[7] * gy + p.Dhat[8] * gz - p.kb[2] * u);
-            X[e] = W * p.c * u;
-        }
-        double s3[N];
-        mtv<N>(T.Dc[3], t, s3);
-#pragma unroll
-        for (int e = 0; e < N; ++e) X[e] += s3[e];
-        add_lift<N>(T.L[3], fz, X);
-    }
-    __syncthreads();
-
-    // x-pencil: Dc^T x^(1) + x-face lifts (in place in A1)
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = A1[Lay<N>::at(e, a, bb)];
-    mtv<N>(T.Dc[4], r, t);
-    add_lift<N>(T.L[4], fx, t);
-#pragma unroll
-    for (int e = 0; e < N; ++e) A1[Lay<N>::at(e, a, bb)] = t[e];
-    // y-pencil: Dc^T x^(2) + y-face lifts (in place in A2)
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = A2[Lay<N>::at(a, e, bb)];
-    mtv<N>(T.Dc[5], r, t);
-    add_lift<N>(T.L[5], fy, t);
-#pragma unroll
-    for (int e = 0; e < N; ++e) A2[Lay<N>::at(a, e, bb)] = t[e];
-    __syncthreads();
-
-    // ---------------------------------------------------------------- (3) integrate
-    // z-pencil: gather, V^T along z
-#pragma unroll
-    for (int e = 0; e < N; ++e) X[e] += A1[Lay<N>::at(a, bb, e)] + A2[Lay<N>::at(a, bb, e)];
-    mtv<N>(T.V[5], X, t);
-#pragma unroll
-    for (int e = 0; e < N; ++e) A0[Lay<N>::at(a, bb, e)] = t[e];
-    __syncthreads();
-    // y-pencil: V^T along y
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = A0[Lay<N>::at(a, e, bb)];
-    mtv<N>(T.V[6], r, t);
-#pragma unroll
-    for (int e = 0; e < N; ++e) A1[Lay<N>::at(a, e, bb)] = t[e];
-    __syncthreads();
-    // x-pencil: V^T along x, then the single store of y (or f - y)
-#pragma unroll
-    for (int e = 0; e < N; ++e) r[e] = A1[Lay<N>::at(e, a, bb)];
-    mtv<N>(T.V[7], r, t);
-    if (valid) {
-        double* yc = p.y + cell * n3 + N * (a + N * bb);
-        if (p.f) {
-            const double* fc = p.f + cell * n3 + N * (a + N * bb);
-#pragma unroll
-            for (int e = 0; e < N; ++e) yc[e] = __ldg(fc + e) - t[e];
+            for (int e = 0; e < N; e += 2) {
+                const double2 v = act[k] ? __ldg(reinterpret_cast<const double2*>(src + e)) : make_double2(0.0, 0.0);
+                r[k][e] = v.x;
+                r[k][e + 1] = v.y;
+            }
         } else {
 #pragma unroll
-            for (int e = 0; e < N; ++e) yc[e] = t[e];
+            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
+        }
+    }
+    v_fwd<N, P>(T.Vh[0], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e) A0[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
+    csync();
+
+    // neighbour traces, step B: V along the first tangential index (12 arrays x N lines)
+    if (do_int) {
+        for (int tk = lane; tk < 12 * N; tk += TPC) {
+            const int arr = tk / N, line = tk - arr * N;
+            if ((nbmask >> (arr >> 1)) & 1u) {
+                double rr[1][N], tt[1][N];
+#pragma unroll
+                for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(arr, e, line)];
+                v_fwd<N, 1>(T.Vh[1], rr, tt);
+#pragma unroll
+                for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, e, line)] = tt[0][e];
+            }
+        }
+    }
+    // y-pencils (x = a, z = bb): V along y
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
+    v_fwd<N, P>(T.Vh[2], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e) A1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
+    csync();
+
+    // neighbour traces, step C: V along the second tangential index
+    if (do_int) {
+        for (int tk = lane; tk < 12 * N; tk += TPC) {
+            const int arr = tk / N, line = tk - arr * N;
+            if ((nbmask >> (arr >> 1)) & 1u) {
+                double rr[1][N], tt[1][N];
+#pragma unroll
+                for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(arr, line, e)];
+                v_fwd<N, 1>(T.Vh[3], rr, tt);
+#pragma unroll
+                for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, line, e)] = tt[0][e];
+            }
+        }
+    }
+    // z-pencils (x = a, y = bb): u at the Gauss points -> A0
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
+    v_fwd<N, P>(T.Vh[4], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
+    csync();   // step C results visible before the z-face fluxes read NT
+
+    // z faces: traces from this z-pencil of u, fluxes -> NT slots (in place, own point)
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const double W = p.dF[2] * T.w[pa[k]] * T.w[pb[k]];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int f = 4 + s;
+            const double uo = dot<N>(T.L[0][s], t[k]);
+            const double dref = dot<N>(T.L[0][2 + s], t[k]);
+            FaceOut fo = {0.0, 0.0};
+            const int i0 = FLay<N>::at(2 * f, pa[k], pb[k]), i1 = FLay<N>::at(2 * f + 1, pa[k], pb[k]);
+            if ((nbmask >> f) & 1u) {
+                if (do_int) fo = flux_interior(p, 2, s, W, uo, dref, NT[i0], p.Dqq_h[2] * NT[i1]);
+            } else if (do_bnd) {
+                fo = flux_boundary(p, 2, s, W, uo, dref);
+            }
+            if (act[k]) { NT[i0] = fo.cv; NT[i1] = fo.cg; }
+        }
+    }
+
+    // ---------------------------------------------------------------- gradients + x/y faces
+    // x-pencils (y = a, z = bb): d/dx_hat -> A1; x-face traces / fluxes
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
+    c_apply<N, P>(T.Dc[0], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e) A1[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const double W = p.dF[0] * T.w[pa[k]] * T.w[pb[k]];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int f = s;
+            const double uo = dot<N>(T.L[1][s], r[k]);
+            const double dref = dot<N>(T.L[1][2 + s], r[k]);
+            FaceOut fo = {0.0, 0.0};
+            const int i0 = FLay<N>::at(2 * f, pa[k], pb[k]), i1 = FLay<N>::at(2 * f + 1, pa[k], pb[k]);
+            if ((nbmask >> f) & 1u) {
+                if (do_int) fo = flux_interior(p, 0, s, W, uo, dref, NT[i0], p.Dqq_h[0] * NT[i1]);
+            } else if (do_bnd) {
+                fo = flux_boundary(p, 0, s, W, uo, dref);
+            }
+            if (act[k]) { NT[i0] = fo.cv; NT[i1] = fo.cg; }
+        }
+    }
+    // y-pencils (x = a, z = bb): d/dy_hat -> A2; y-face traces / fluxes
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
+    c_apply<N, P>(T.Dc[1], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e) A2[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const double W = p.dF[1] * T.w[pa[k]] * T.w[pb[k]];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int f = 2 + s;
+            const double uo = dot<N>(T.L[2][s], r[k]);
+            const double dref = dot<N>(T.L[2][2 + s], r[k]);
+            FaceOut fo = {0.0, 0.0};
+            const int i0 = FLay<N>::at(2 * f, pa[k], pb[k]), i1 = FLay<N>::at(2 * f + 1, pa[k], pb[k]);
+            if ((nbmask >> f) & 1u) {
+                if (do_int) fo = flux_interior(p, 1, s, W, uo, dref, NT[i0], p.Dqq_h[1] * NT[i1]);
+            } else if (do_bnd) {
+                fo = flux_boundary(p, 1, s, W, uo, dref);
+            }
+            if (act[k]) { NT[i0] = fo.cv; NT[i1] = fo.cg; }
+        }
+    }
+    csync();
+
+    // ---------------------------------------------------------------- (2) quadrature-point data
+    // z-pencils (x = a, y = bb): u, d/dz_hat; x^(1) -> A1, x^(2) -> A2 (in place);
+    // X = x^(0) + Dc^T x^(3) + z-face lifts -> A0 (in place over u)
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
+    c_apply<N, P>(T.Dc[2], r, t);   // t = d u / dz_hat
+    {
+        double x3[P][N];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const double wxy = do_vol ? p.dT * T.w[pa[k]] * T.w[pb[k]] : 0.0;
+#pragma unroll
+            for (int e = 0; e < N; ++e) {
+                const int ie = Lay<N>::at(pa[k], pb[k], e);
+                const double gx = act[k] ? A1[ie] : 0.0;
+                const double gy = act[k] ? A2[ie] : 0.0;
+                const double gz = t[k][e];
+                const double u = r[k][e];
+                const double W = wxy * T.w[e];
+                // x^(r) / h_r = W (sum_s D_rs/(h_r h_s) d_s u_hat - b_r/h_r u)   (eq:gauss_points)
+                const double x1 = W * (p.Dhat[0] * gx + p.Dhat[1] * gy + p.Dhat[2] * gz - p.kb[0] * u);
+                const double x2 = W * (p.Dhat[3] * gx + p.Dhat[4] * gy + p.Dhat[5] * gz - p.kb[1] * u);
+                x3[k][e] = W * (p.Dhat[6] * gx + p.Dhat[7] * gy + p.Dhat[8] * gz - p.kb[2] * u);
+                r[k][e] = W * p.c * u;                               // x^(0)
+                if (act[k]) { A1[ie] = x1; A2[ie] = x2; }
+            }
+        }
+        c_apply<N, P>(T.DcT[0], x3, t);
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const double cv0 = NT[FLay<N>::at(8, pa[k], pb[k])], cg0 = NT[FLay<N>::at(9, pa[k], pb[k])];
+            const double cv1 = NT[FLay<N>::at(10, pa[k], pb[k])], cg1 = NT[FLay<N>::at(11, pa[k], pb[k])];
+            if (act[k])
+#pragma unroll
+                for (int e = 0; e < N; ++e)
+                    A0[Lay<N>::at(pa[k], pb[k], e)] = r[k][e] + t[k][e] + cv0 * T.L[3][0][e] + cg0 * T.L[3][2][e] +
+                                                      cv1 * T.L[3][1][e] + cg1 * T.L[3][3][e];
+        }
+    }
+    csync();
+
+    // x-pencils: Dc^T x^(1) + x-face lifts (in place in A1)
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A1[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
+    c_apply<N, P>(T.DcT[1], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const double cv0 = NT[FLay<N>::at(0, pa[k], pb[k])], cg0 = NT[FLay<N>::at(1, pa[k], pb[k])];
+        const double cv1 = NT[FLay<N>::at(2, pa[k], pb[k])], cg1 = NT[FLay<N>::at(3, pa[k], pb[k])];
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e)
+                A1[Lay<N>::at(e, pa[k], pb[k])] = t[k][e] + cv0 * T.L[4][0][e] + cg0 * T.L[4][2][e] +
+                                                  cv1 * T.L[4][1][e] + cg1 * T.L[4][3][e];
+    }
+    // y-pencils: Dc^T x^(2) + y-face lifts (in place in A2)
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A2[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
+    c_apply<N, P>(T.DcT[2], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const double cv0 = NT[FLay<N>::at(4, pa[k], pb[k])], cg0 = NT[FLay<N>::at(5, pa[k], pb[k])];
+        const double cv1 = NT[FLay<N>::at(6, pa[k], pb[k])], cg1 = NT[FLay<N>::at(7, pa[k], pb[k])];
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e)
+                A2[Lay<N>::at(pa[k], e, pb[k])] = t[k][e] + cv0 * T.L[5][0][e] + cg0 * T.L[5][2][e] +
+                                                  cv1 * T.L[5][1][e] + cg1 * T.L[5][3][e];
+    }
+    csync();
+
+    // ---------------------------------------------------------------- (3) integrate
+    // z-pencils: X = A0 + A1 + A2, V^T along z -> A0
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            const int ie = Lay<N>::at(pa[k], pb[k], e);
+            r[k][e] = act[k] ? A0[ie] + A1[ie] + A2[ie] : 0.0;
+        }
+    v_bwd<N, P>(T.Vh[5], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
+    csync();
+    // y-pencils: V^T along y (in place)
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
+    v_bwd<N, P>(T.Vh[6], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
+    csync();
+    // x-pencils: V^T along x, then the single store of y (or f - y)
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
+    v_bwd<N, P>(T.Vh[7], r, t);
+    if (valid) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            if (!act[k]) continue;
+            const int64_t off = cell * n3 + N * (pa[k] + N * pb[k]);
+            double* yc = p.y + off;
+            if (p.f) {
+                const double* fc = p.f + off;
+#pragma unroll
+                for (int e = 0; e < N; ++e) t[k][e] = __ldg(fc + e) - t[k][e];
+            }
+            if (N % 2 == 0) {
+#pragma unroll
+                for (int e = 0; e < N; e += 2)
+                    *reinterpret_cast<double2*>(yc + e) = make_double2(t[k][e], t[k][e + 1]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < N; ++e) yc[e] = t[k][e];
+            }
         }
     }
 }

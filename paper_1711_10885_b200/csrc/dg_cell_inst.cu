@@ -9,16 +9,35 @@
 
 namespace dg {
 
+template <int N>
+static void fill_eo(EO<N>& o, const double (&A)[NMAX][NMAX], bool transpose)
+{
+    constexpr int H = N / 2;
+    auto a = [&](int i, int j) { return transpose ? A[j][i] : A[i][j]; };
+    for (int i = 0; i < H; ++i)
+        for (int j = 0; j < H; ++j) {
+            o.p[i][j] = 0.5 * (a(i, j) + a(i, N - 1 - j));
+            o.m[i][j] = 0.5 * (a(i, j) - a(i, N - 1 - j));
+        }
+    for (int i = 0; i < H; ++i) {
+        o.col[i] = (N & 1) ? a(i, H) : 0.0;
+        o.row[i] = (N & 1) ? a(H, i) : 0.0;
+    }
+}
+
 int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
 {
     constexpr int N = DG_N;
     if (t.n != N) return -1;
-    Tab<N> h;
+    static Tab<N> h;
+    for (int c = 0; c < 10; ++c)
+        for (int i = 0; i < Tab<N>::HC; ++i)
+            for (int j = 0; j < N; ++j) h.Vh[c][i][j] = t.V[i][j];
+    for (int c = 0; c < 6; ++c) {
+        fill_eo<N>(h.Dc[c], t.Dc, false);
+        fill_eo<N>(h.DcT[c], t.Dc, true);
+    }
     for (int i = 0; i < N; ++i) {
-        for (int j = 0; j < N; ++j) {
-            for (int c = 0; c < 8; ++c) h.V[c][i][j] = t.V[i][j];
-            for (int c = 0; c < 6; ++c) h.Dc[c][i][j] = t.Dc[i][j];
-        }
         h.w[i] = t.w[i];
         for (int c = 0; c < 6; ++c) {
             h.L[c][0][i] = t.L0[i];
@@ -40,6 +59,7 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
 {
     constexpr int N = DG_N;
     constexpr int C = Cfg<N>::C;
+    constexpr int THREADS = C * Cfg<N>::TPC;
     if (p.ntasks <= 0) return cudaSuccess;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -50,7 +70,7 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
         g_attr_done[dev] = 1;
     }
     const int64_t grid = (p.ntasks + C - 1) / C;
-    dg_cell_kernel<N><<<(unsigned)grid, C * N * N, Smem<N>::BYTES, s>>>(p);
+    dg_cell_kernel<N><<<(unsigned)grid, THREADS, Smem<N>::BYTES, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -58,7 +78,7 @@ int DG_CAT(cell_info_n, DG_N)(LaunchInfo* info)
 {
     constexpr int N = DG_N;
     info->cells_per_cta = Cfg<N>::C;
-    info->threads = Cfg<N>::C * N * N;
+    info->threads = Cfg<N>::C * Cfg<N>::TPC;
     info->smem = Smem<N>::BYTES;
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, dg_cell_kernel<N>) != cudaSuccess) return -3;
