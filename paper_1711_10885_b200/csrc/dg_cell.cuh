@@ -95,6 +95,15 @@ template <int N> struct FLay {
     static constexpr int SLOT = 12 * ARR;
     __device__ __forceinline__ static int at(int arr, int i1, int i2) { return arr * ARR + i1 + RS * i2; }
 };
+// n = 8: 64 doubles per array, XOR swizzle conflict free for the three access patterns
+// (point (a, b) per lane; lines along i1 and along i2 over 4 consecutive arrays per warp).
+template <> struct FLay<8> {
+    static constexpr int SLOT = 12 * 64;
+    __device__ __forceinline__ static int at(int arr, int i1, int i2)
+    {
+        return 64 * arr + 8 * (i2 ^ (arr & 1)) + (i1 ^ ((i2 >> 1) | ((arr & 1) << 2)));
+    }
+};
 
 template <int N>
 struct Smem {
@@ -288,9 +297,19 @@ dg_cell_kernel(const KParams p)
         lc[1] = (e / p.nloc[0]) % p.nloc[1];
         lc[2] = e / (p.nloc[0] * p.nloc[1]);
     } else {
-        lc[0] = p.task_lo[0] + task % p.task_cnt[0];
-        lc[1] = p.task_lo[1] + (task / p.task_cnt[0]) % p.task_cnt[1];
-        lc[2] = p.task_lo[2] + task / (p.task_cnt[0] * p.task_cnt[1]);
+        // z fastest within a column; columns in tiles of TX x TY (ragged at the box edge)
+        const int64_t nz = p.task_cnt[2], nx = p.task_cnt[0], ny = p.task_cnt[1];
+        const int64_t col = task / nz;
+        const int64_t TX = p.tile[0], TY = p.tile[1];
+        const int64_t ty = col / (TY * nx);
+        const int64_t wy = min(TY, ny - ty * TY);
+        const int64_t cr = col - ty * TY * nx;
+        const int64_t tx = cr / (TX * wy);
+        const int64_t wx = min(TX, nx - tx * TX);
+        const int64_t ci = cr - tx * TX * wy;
+        lc[0] = p.task_lo[0] + tx * TX + ci % wx;
+        lc[1] = p.task_lo[1] + ty * TY + ci / wx;
+        lc[2] = p.task_lo[2] + (task - col * nz);
     }
     const int64_t n3 = (int64_t)NN * N;
     const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * lc[2]);
@@ -323,39 +342,49 @@ dg_cell_kernel(const KParams p)
         if (g >= 0 && g < p.gcells[q]) nbmask |= 1u << f;
     }
     if (do_int) {
+        const int64_t lcx = lc[0], lcy = lc[1], lcz = lc[2];
 #pragma unroll 1
-        for (int f = 0; f < 6; ++f) {
-            if (!((nbmask >> f) & 1u)) continue;
-            const int q = f >> 1, s = f & 1;
-            const int64_t l = lc[q] + (s ? 1 : -1);
-            const double* zn;
-            if (l >= 0 && l < p.nloc[q]) {
-                const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
-                zn = zc + (s ? st : -st) * n3;
-            } else {
-                const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
-                zn = p.ghost[f] + (lc[t1] + p.nloc[t1] * lc[t2]) * n3;
-            }
+        for (int q = 0; q < 3; ++q) {
+            const int64_t lq = (q == 0) ? lcx : (q == 1) ? lcy : lcz;
+            const int64_t nq = (q == 0) ? p.nloc[0] : (q == 1) ? p.nloc[1] : p.nloc[2];
+            const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
+            const int64_t gi = (q == 0) ? (lcy + p.nloc[1] * lcz) : (q == 1) ? (lcx + p.nloc[0] * lcz)
+                                                                              : (lcx + p.nloc[0] * lcy);
             const int se = (q == 0) ? 1 : (q == 1) ? N : NN;
-            const double* thv = s ? T.th0 : T.th1;
-            const double* dthv = s ? T.dth0 : T.dth1;
+            // both neighbours of this direction: loads of the two faces in flight together
+            double rl[P][N], rh[P][N];
+            const bool hl = (nbmask >> (2 * q)) & 1u, hh = (nbmask >> (2 * q + 1)) & 1u;
+            const double* zl = (lq > 0) ? zc - st * n3 : (hl ? p.ghost[2 * q] + gi * n3 : zc);
+            const double* zh = (lq + 1 < nq) ? zc + st * n3 : (hh ? p.ghost[2 * q + 1] + gi * n3 : zc);
 #pragma unroll
             for (int k = 0; k < P; ++k) {
                 const int base = (q == 0) ? N * pa[k] + NN * pb[k] : (q == 1) ? pa[k] + NN * pb[k] : pa[k] + N * pb[k];
 #pragma unroll
-                for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(zn + base + e * se) : 0.0;
+                for (int e = 0; e < N; ++e) {
+                    rl[k][e] = (act[k] && hl) ? __ldg(zl + base + e * se) : 0.0;
+                    rh[k][e] = (act[k] && hh) ? __ldg(zh + base + e * se) : 0.0;
+                }
             }
 #pragma unroll
             for (int k = 0; k < P; ++k) {
-                double su = 0.0, sd = 0.0;
+                // low neighbour (face 2q): its face is x_q = 1; high neighbour (2q+1): x_q = 0
+                double ul = 0.0, dl = 0.0, uh = 0.0, dh = 0.0;
 #pragma unroll
                 for (int e = 0; e < N; ++e) {
-                    su = fma(thv[e], r[k][e], su);
-                    sd = fma(dthv[e], r[k][e], sd);
+                    ul = fma(T.th1[e], rl[k][e], ul);
+                    dl = fma(T.dth1[e], rl[k][e], dl);
+                    uh = fma(T.th0[e], rh[k][e], uh);
+                    dh = fma(T.dth0[e], rh[k][e], dh);
                 }
                 if (act[k]) {
-                    NT[FLay<N>::at(2 * f, pa[k], pb[k])] = su;
-                    NT[FLay<N>::at(2 * f + 1, pa[k], pb[k])] = sd;
+                    if (hl) {
+                        NT[FLay<N>::at(4 * q, pa[k], pb[k])] = ul;
+                        NT[FLay<N>::at(4 * q + 1, pa[k], pb[k])] = dl;
+                    }
+                    if (hh) {
+                        NT[FLay<N>::at(4 * q + 2, pa[k], pb[k])] = uh;
+                        NT[FLay<N>::at(4 * q + 3, pa[k], pb[k])] = dh;
+                    }
                 }
             }
         }
@@ -646,10 +675,10 @@ dg_cell_kernel(const KParams p)
             if (N % 2 == 0) {
 #pragma unroll
                 for (int e = 0; e < N; e += 2)
-                    *reinterpret_cast<double2*>(yc + e) = make_double2(t[k][e], t[k][e + 1]);
+                    __stcs(reinterpret_cast<double2*>(yc + e), make_double2(t[k][e], t[k][e + 1]));
             } else {
 #pragma unroll
-                for (int e = 0; e < N; ++e) yc[e] = t[k][e];
+                for (int e = 0; e < N; ++e) __stcs(yc + e, t[k][e]);
             }
         }
     }
