@@ -41,7 +41,7 @@ struct EO {                        // even-odd form of a centro-antisymmetric ma
 template <int N>
 struct Tab {
     static constexpr int HC = (N + 1) / 2;
-    double Vh[10][HC][N];    // V_ij = theta_j(xi_i), rows i < ceil(n/2); one copy per use site
+    double Vh[12][HC][N];    // V_ij = theta_j(xi_i), rows i < ceil(n/2); one copy per use site
     EO<N> Dc[6];             // collocation derivative Dc_il (row = point, col = value)
     EO<N> DcT[6];            // its transpose
     double w[N];
@@ -107,7 +107,7 @@ template <> struct FLay<8> {
 
 template <int N>
 struct Smem {
-    static constexpr int PER_CELL = 3 * Lay<N>::SLOT + FLay<N>::SLOT;
+    static constexpr int PER_CELL = 2 * Lay<N>::SLOT + FLay<N>::SLOT;
     static constexpr int BYTES = Cfg<N>::C * PER_CELL * 8;
 };
 
@@ -261,6 +261,151 @@ __device__ __forceinline__ FaceOut flux_boundary(const KParams& p, int q, int s,
     return o;
 }
 
+// ---------------------------------------------------------------------------------- kernel pieces
+// Load the lines of the two neighbours across direction q that this thread's pencils need
+// (tangential modal indices (a, bb) fixed, normal index e = 0..n-1).
+template <int N, int P>
+__device__ __forceinline__ void nb_load(const KParams& p, const double* zc, const int64_t n3, int q, const int lc[3],
+                                        unsigned nbmask, const int (&pa)[P], const int (&pb)[P], const bool (&act)[P],
+                                        double (&rl)[P][N], double (&rh)[P][N])
+{
+    constexpr int NN = N * N;
+    const int lq = lc[q];
+    const int nq = (int)p.nloc[q];
+    const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
+    const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
+                                                                        : (lc[0] + p.nloc[0] * lc[1]);
+    const bool hl = (nbmask >> (2 * q)) & 1u, hh = (nbmask >> (2 * q + 1)) & 1u;
+    const double* zl = (lq > 0) ? zc - st * n3 : (hl ? p.ghost[2 * q] + gi * n3 : zc);
+    const double* zh = (lq + 1 < nq) ? zc + st * n3 : (hh ? p.ghost[2 * q + 1] + gi * n3 : zc);
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        if (q == 0 && N % 2 == 0) {
+            const int base = N * pa[k] + NN * pb[k];
+#pragma unroll
+            for (int e = 0; e < N; e += 2) {
+                const double2 vl = (act[k] && hl) ? __ldg(reinterpret_cast<const double2*>(zl + base + e))
+                                                  : make_double2(0.0, 0.0);
+                const double2 vh = (act[k] && hh) ? __ldg(reinterpret_cast<const double2*>(zh + base + e))
+                                                  : make_double2(0.0, 0.0);
+                rl[k][e] = vl.x; rl[k][e + 1] = vl.y;
+                rh[k][e] = vh.x; rh[k][e + 1] = vh.y;
+            }
+        } else {
+            const int se = (q == 0) ? 1 : (q == 1) ? N : NN;
+            const int base = (q == 0) ? N * pa[k] + NN * pb[k] : (q == 1) ? pa[k] + NN * pb[k] : pa[k] + N * pb[k];
+#pragma unroll
+            for (int e = 0; e < N; ++e) {
+                rl[k][e] = (act[k] && hl) ? __ldg(zl + base + e * se) : 0.0;
+                rh[k][e] = (act[k] && hh) ? __ldg(zh + base + e * se) : 0.0;
+            }
+        }
+    }
+}
+
+// Normal-direction-first contraction of the loaded neighbour lines:
+// low neighbour (face 2q) is seen at its x_q = 1, high neighbour (face 2q+1) at x_q = 0.
+template <int N, int P>
+__device__ __forceinline__ void nb_contract(const Tab<N>& T, double* NT, int q, unsigned nbmask, const int (&pa)[P],
+                                           const int (&pb)[P], const bool (&act)[P], const double (&rl)[P][N],
+                                           const double (&rh)[P][N])
+{
+    const bool hl = (nbmask >> (2 * q)) & 1u, hh = (nbmask >> (2 * q + 1)) & 1u;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        double ul = 0.0, dl = 0.0, uh = 0.0, dh = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            ul = fma(T.th1[e], rl[k][e], ul);
+            dl = fma(T.dth1[e], rl[k][e], dl);
+            uh = fma(T.th0[e], rh[k][e], uh);
+            dh = fma(T.dth0[e], rh[k][e], dh);
+        }
+        if (act[k]) {
+            if (hl) {
+                NT[FLay<N>::at(4 * q, pa[k], pb[k])] = ul;
+                NT[FLay<N>::at(4 * q + 1, pa[k], pb[k])] = dl;
+            }
+            if (hh) {
+                NT[FLay<N>::at(4 * q + 2, pa[k], pb[k])] = uh;
+                NT[FLay<N>::at(4 * q + 3, pa[k], pb[k])] = dh;
+            }
+        }
+    }
+}
+
+// Tangential stage of the 4 neighbour-trace arrays of direction q: V along i1 (dim 0) or i2 (dim 1).
+template <int N, int TPC>
+__device__ __forceinline__ void nb_tangential(const double (&Vh)[(N + 1) / 2][N], double* NT, int q, int dim,
+                                             unsigned nbmask, int lane)
+{
+    for (int tk = lane; tk < 4 * N; tk += TPC) {
+        const int arr = 4 * q + tk / N, line = tk % N;
+        if ((nbmask >> (arr >> 1)) & 1u) {
+            double rr[1][N], tt[1][N];
+#pragma unroll
+            for (int e = 0; e < N; ++e) rr[0][e] = NT[dim ? FLay<N>::at(arr, line, e) : FLay<N>::at(arr, e, line)];
+            v_fwd<N, 1>(Vh, rr, tt);
+#pragma unroll
+            for (int e = 0; e < N; ++e) NT[dim ? FLay<N>::at(arr, line, e) : FLay<N>::at(arr, e, line)] = tt[0][e];
+        }
+    }
+}
+
+// Role phase for normal direction q on this thread's q-pencils of u (r[k][e], e along q):
+//   g = Dc u (reference d/dx_hat_q), own traces, face fluxes with the neighbour traces,
+//   x^(q) = W (D_qq/h_q^2 g - b_q/h_q u) [+ x^(0) = W c u for the z role], and
+//   out = Dc^T x^(q) [+ x^(0)] + lifts of the two q-faces (normal direction LAST).
+// W = Delta_T w_a w_b w_e at the pencil's points; Wf = Delta_F,q w_a w_b at its face point.
+template <int N, int P>
+__device__ __forceinline__ void role_q(const KParams& p, const Tab<N>& T, const EO<N>& Dq, const EO<N>& DqT,
+                                      const double (&Ls)[4][N], const double* NT, int q, unsigned nbmask,
+                                      bool do_int, bool do_bnd, bool do_vol, bool with_reaction, const int (&pa)[P],
+                                      const int (&pb)[P], const double (&r)[P][N], double (&out)[P][N])
+{
+    double g[P][N];
+    c_apply<N, P>(Dq, r, g);
+    const double kd = p.Dhat[4 * q], kb = p.kb[q];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const double wab = T.w[pa[k]] * T.w[pb[k]];
+        const double wv = do_vol ? p.dT * wab : 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            const double W = wv * T.w[e];
+            g[k][e] = W * (kd * g[k][e] - kb * r[k][e]);       // x^(q) / h_q   (eq:gauss_points)
+        }
+    }
+    c_apply<N, P>(DqT, g, out);
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const double Wf = p.dF[q] * T.w[pa[k]] * T.w[pb[k]];
+        FaceOut fo[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int f = 2 * q + s;
+            const double uo = dot<N>(Ls[s], r[k]);            // own trace u(x_q = s)
+            const double dref = dot<N>(Ls[2 + s], r[k]);      // own d u / d x_hat_q at x_q = s
+            fo[s].cv = 0.0;
+            fo[s].cg = 0.0;
+            if ((nbmask >> f) & 1u) {
+                if (do_int) {
+                    const double un = NT[FLay<N>::at(2 * f, pa[k], pb[k])];
+                    const double sn = p.Dqq_h[q] * NT[FLay<N>::at(2 * f + 1, pa[k], pb[k])];
+                    fo[s] = flux_interior(p, q, s, Wf, uo, dref, un, sn);
+                }
+            } else if (do_bnd) {
+                fo[s] = flux_boundary(p, q, s, Wf, uo, dref);
+            }
+        }
+        const double wc = (with_reaction && do_vol) ? p.dT * T.w[pa[k]] * T.w[pb[k]] * p.c : 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e)
+            out[k][e] += wc * T.w[e] * r[k][e] + fo[0].cv * Ls[0][e] + fo[0].cg * Ls[2][e] + fo[1].cv * Ls[1][e] +
+                         fo[1].cg * Ls[3][e];
+    }
+}
+
 // ---------------------------------------------------------------------------------- kernel
 template <int N>
 __global__ void __launch_bounds__(Cfg<N>::C * Cfg<N>::TPC, Cfg<N>::MINB)
@@ -280,41 +425,51 @@ dg_cell_kernel(const KParams p)
 
     double* A0 = smem + slot * Smem<N>::PER_CELL;
     double* A1 = A0 + Lay<N>::SLOT;
-    double* A2 = A1 + Lay<N>::SLOT;
-    double* NT = A2 + Lay<N>::SLOT;
+    double* NT = A1 + Lay<N>::SLOT;
 
     auto csync = [&]() {
         if (TPC <= 32) __syncwarp(); else __syncthreads();
     };
 
-    int64_t task = (int64_t)blockIdx.x * C + slot;
-    const bool valid = task < p.ntasks;
-    if (!valid) task = p.ntasks - 1;
-    int64_t lc[3];
+    // ---- cell of this slot (32-bit index math: at most 2^31 cells per rank)
+    unsigned task = blockIdx.x * (unsigned)C + (unsigned)slot;
+    const bool valid = task < (unsigned)p.ntasks;
+    if (!valid) task = (unsigned)p.ntasks - 1u;
+    int lc[3];
     if (p.task_list) {
-        const int64_t e = p.task_list[task];
-        lc[0] = e % p.nloc[0];
-        lc[1] = (e / p.nloc[0]) % p.nloc[1];
-        lc[2] = e / (p.nloc[0] * p.nloc[1]);
+        const unsigned e = (unsigned)p.task_list[task];
+        const unsigned nx = (unsigned)p.nloc[0], ny = (unsigned)p.nloc[1];
+        lc[0] = (int)(e % nx);
+        lc[1] = (int)((e / nx) % ny);
+        lc[2] = (int)(e / (nx * ny));
     } else {
         // z fastest within a column; columns in tiles of TX x TY (ragged at the box edge)
-        const int64_t nz = p.task_cnt[2], nx = p.task_cnt[0], ny = p.task_cnt[1];
-        const int64_t col = task / nz;
-        const int64_t TX = p.tile[0], TY = p.tile[1];
-        const int64_t ty = col / (TY * nx);
-        const int64_t wy = min(TY, ny - ty * TY);
-        const int64_t cr = col - ty * TY * nx;
-        const int64_t tx = cr / (TX * wy);
-        const int64_t wx = min(TX, nx - tx * TX);
-        const int64_t ci = cr - tx * TX * wy;
-        lc[0] = p.task_lo[0] + tx * TX + ci % wx;
-        lc[1] = p.task_lo[1] + ty * TY + ci / wx;
-        lc[2] = p.task_lo[2] + (task - col * nz);
+        const unsigned nz = (unsigned)p.task_cnt[2], nx = (unsigned)p.task_cnt[0], ny = (unsigned)p.task_cnt[1];
+        const unsigned TX = (unsigned)p.tile[0], TY = (unsigned)p.tile[1];
+        const unsigned col = task / nz;
+        const unsigned ty = col / (TY * nx);
+        const unsigned wy = min(TY, ny - ty * TY);
+        const unsigned cr = col - ty * TY * nx;
+        const unsigned tx = cr / (TX * wy);
+        const unsigned wx = min(TX, nx - tx * TX);
+        const unsigned ci = cr - tx * TX * wy;
+        lc[0] = (int)(p.task_lo[0] + tx * TX + ci % wx);
+        lc[1] = (int)(p.task_lo[1] + ty * TY + ci / wx);
+        lc[2] = (int)(p.task_lo[2] + (task - col * nz));
     }
     const int64_t n3 = (int64_t)NN * N;
-    const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * lc[2]);
+    const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * (int64_t)lc[2]);
     const double* zc = p.z + cell * n3;
     const bool do_int = (p.mask & 2u) != 0, do_bnd = (p.mask & 4u) != 0, do_vol = (p.mask & 1u) != 0;
+
+    unsigned nbmask = 0;   // bit f = 2q + s: a neighbour cell (local or on another rank) exists
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+        const int q = f >> 1, s = f & 1;
+        const int64_t g = p.gofs[q] + lc[q] + (s ? 1 : -1);
+        if (g >= 0 && g < p.gcells[q]) nbmask |= 1u << f;
+    }
+    const unsigned nbi = do_int ? nbmask : 0u;   // neighbours whose traces are needed
 
     // this thread's pencils: pencil index pc = lane + k TPC = a + N bb
     int pa[P], pb[P];
@@ -329,338 +484,139 @@ dg_cell_kernel(const KParams p)
     }
 
     double r[P][N], t[P][N];
-
-    // ---------------------------------------------------------------- neighbour traces, step A
-    // Face f = 2q + s: the neighbour lies at lc[q] + (s ? 1 : -1) and its face is x_q = 1 - s.
-    // Normal direction FIRST: contract the neighbour's line through tangential modal indices
-    // (j_t1, j_t2) = (a, bb) with theta(1-s) and theta'(1-s).
-    unsigned nbmask = 0;
+    {
+        double rl[P][N], rh[P][N];
+        // ---- phase 1: x-pencils (y = a, z = bb) from global, V along x -> A0;
+        //      x-neighbour lines loaded alongside and contracted (normal first)
+        nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
-    for (int f = 0; f < 6; ++f) {
-        const int q = f >> 1, s = f & 1;
-        const int64_t g = p.gofs[q] + lc[q] + (s ? 1 : -1);
-        if (g >= 0 && g < p.gcells[q]) nbmask |= 1u << f;
-    }
-    if (do_int) {
-        const int64_t lcx = lc[0], lcy = lc[1], lcz = lc[2];
-#pragma unroll 1
-        for (int q = 0; q < 3; ++q) {
-            const int64_t lq = (q == 0) ? lcx : (q == 1) ? lcy : lcz;
-            const int64_t nq = (q == 0) ? p.nloc[0] : (q == 1) ? p.nloc[1] : p.nloc[2];
-            const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
-            const int64_t gi = (q == 0) ? (lcy + p.nloc[1] * lcz) : (q == 1) ? (lcx + p.nloc[0] * lcz)
-                                                                              : (lcx + p.nloc[0] * lcy);
-            const int se = (q == 0) ? 1 : (q == 1) ? N : NN;
-            // both neighbours of this direction: loads of the two faces in flight together
-            double rl[P][N], rh[P][N];
-            const bool hl = (nbmask >> (2 * q)) & 1u, hh = (nbmask >> (2 * q + 1)) & 1u;
-            const double* zl = (lq > 0) ? zc - st * n3 : (hl ? p.ghost[2 * q] + gi * n3 : zc);
-            const double* zh = (lq + 1 < nq) ? zc + st * n3 : (hh ? p.ghost[2 * q + 1] + gi * n3 : zc);
+        for (int k = 0; k < P; ++k) {
+            const double* src = zc + N * (pa[k] + N * pb[k]);
+            if (N % 2 == 0) {
 #pragma unroll
-            for (int k = 0; k < P; ++k) {
-                const int base = (q == 0) ? N * pa[k] + NN * pb[k] : (q == 1) ? pa[k] + NN * pb[k] : pa[k] + N * pb[k];
-#pragma unroll
-                for (int e = 0; e < N; ++e) {
-                    rl[k][e] = (act[k] && hl) ? __ldg(zl + base + e * se) : 0.0;
-                    rh[k][e] = (act[k] && hh) ? __ldg(zh + base + e * se) : 0.0;
+                for (int e = 0; e < N; e += 2) {
+                    const double2 v = act[k] ? __ldg(reinterpret_cast<const double2*>(src + e)) : make_double2(0.0, 0.0);
+                    r[k][e] = v.x;
+                    r[k][e + 1] = v.y;
                 }
-            }
+            } else {
 #pragma unroll
-            for (int k = 0; k < P; ++k) {
-                // low neighbour (face 2q): its face is x_q = 1; high neighbour (2q+1): x_q = 0
-                double ul = 0.0, dl = 0.0, uh = 0.0, dh = 0.0;
-#pragma unroll
-                for (int e = 0; e < N; ++e) {
-                    ul = fma(T.th1[e], rl[k][e], ul);
-                    dl = fma(T.dth1[e], rl[k][e], dl);
-                    uh = fma(T.th0[e], rh[k][e], uh);
-                    dh = fma(T.dth0[e], rh[k][e], dh);
-                }
-                if (act[k]) {
-                    if (hl) {
-                        NT[FLay<N>::at(4 * q, pa[k], pb[k])] = ul;
-                        NT[FLay<N>::at(4 * q + 1, pa[k], pb[k])] = dl;
-                    }
-                    if (hh) {
-                        NT[FLay<N>::at(4 * q + 2, pa[k], pb[k])] = uh;
-                        NT[FLay<N>::at(4 * q + 3, pa[k], pb[k])] = dh;
-                    }
-                }
+                for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
             }
         }
+        v_fwd<N, P>(T.Vh[0], r, t);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (act[k])
+#pragma unroll
+                for (int e = 0; e < N; ++e) A0[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
+        nb_contract<N, P>(T, NT, 0, nbi, pa, pb, act, rl, rh);
+        csync();
+
+        // ---- phase 2: y-pencils (x = a, z = bb): V along y -> A1; y-neighbours; x-arrays step B
+        nb_load<N, P>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
+        v_fwd<N, P>(T.Vh[1], r, t);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (act[k])
+#pragma unroll
+                for (int e = 0; e < N; ++e) A1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
+        nb_tangential<N, TPC>(T.Vh[2], NT, 0, 0, nbi, lane);
+        nb_contract<N, P>(T, NT, 1, nbi, pa, pb, act, rl, rh);
+        csync();
+
+        // ---- phase 3: z-pencils (x = a, y = bb): u at the Gauss points -> A0; z-neighbours;
+        //      y-arrays step B, x-arrays step C
+        nb_load<N, P>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
+        v_fwd<N, P>(T.Vh[3], r, t);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (act[k])
+#pragma unroll
+                for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
+        nb_tangential<N, TPC>(T.Vh[4], NT, 1, 0, nbi, lane);
+        nb_tangential<N, TPC>(T.Vh[5], NT, 0, 1, nbi, lane);
+        nb_contract<N, P>(T, NT, 2, nbi, pa, pb, act, rl, rh);
+        csync();
     }
 
-    // ---------------------------------------------------------------- (1) evaluate
-    // x-pencils (y = a, z = bb) straight from global memory, V along x
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const double* src = zc + N * (pa[k] + N * pb[k]);
-        if (N % 2 == 0) {
-#pragma unroll
-            for (int e = 0; e < N; e += 2) {
-                const double2 v = act[k] ? __ldg(reinterpret_cast<const double2*>(src + e)) : make_double2(0.0, 0.0);
-                r[k][e] = v.x;
-                r[k][e + 1] = v.y;
-            }
-        } else {
-#pragma unroll
-            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
-        }
-    }
-    v_fwd<N, P>(T.Vh[0], r, t);
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-        if (act[k])
-#pragma unroll
-            for (int e = 0; e < N; ++e) A0[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
-    csync();
-
-    // neighbour traces, step B: V along the first tangential index (12 arrays x N lines)
-    if (do_int) {
-        for (int tk = lane; tk < 12 * N; tk += TPC) {
-            const int arr = tk / N, line = tk - arr * N;
-            if ((nbmask >> (arr >> 1)) & 1u) {
-                double rr[1][N], tt[1][N];
-#pragma unroll
-                for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(arr, e, line)];
-                v_fwd<N, 1>(T.Vh[1], rr, tt);
-#pragma unroll
-                for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, e, line)] = tt[0][e];
-            }
-        }
-    }
-    // y-pencils (x = a, z = bb): V along y
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-#pragma unroll
-        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-    v_fwd<N, P>(T.Vh[2], r, t);
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-        if (act[k])
-#pragma unroll
-            for (int e = 0; e < N; ++e) A1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
-    csync();
-
-    // neighbour traces, step C: V along the second tangential index
-    if (do_int) {
-        for (int tk = lane; tk < 12 * N; tk += TPC) {
-            const int arr = tk / N, line = tk - arr * N;
-            if ((nbmask >> (arr >> 1)) & 1u) {
-                double rr[1][N], tt[1][N];
-#pragma unroll
-                for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(arr, line, e)];
-                v_fwd<N, 1>(T.Vh[3], rr, tt);
-#pragma unroll
-                for (int e = 0; e < N; ++e) NT[FLay<N>::at(arr, line, e)] = tt[0][e];
-            }
-        }
-    }
-    // z-pencils (x = a, y = bb): u at the Gauss points -> A0
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-#pragma unroll
-        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
-    v_fwd<N, P>(T.Vh[4], r, t);
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-        if (act[k])
-#pragma unroll
-            for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
-    csync();   // step C results visible before the z-face fluxes read NT
-
-    // z faces: traces from this z-pencil of u, fluxes -> NT slots (in place, own point)
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const double W = p.dF[2] * T.w[pa[k]] * T.w[pb[k]];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const int f = 4 + s;
-            const double uo = dot<N>(T.L[0][s], t[k]);
-            const double dref = dot<N>(T.L[0][2 + s], t[k]);
-            FaceOut fo = {0.0, 0.0};
-            const int i0 = FLay<N>::at(2 * f, pa[k], pb[k]), i1 = FLay<N>::at(2 * f + 1, pa[k], pb[k]);
-            if ((nbmask >> f) & 1u) {
-                if (do_int) fo = flux_interior(p, 2, s, W, uo, dref, NT[i0], p.Dqq_h[2] * NT[i1]);
-            } else if (do_bnd) {
-                fo = flux_boundary(p, 2, s, W, uo, dref);
-            }
-            if (act[k]) { NT[i0] = fo.cv; NT[i1] = fo.cg; }
-        }
-    }
-
-    // ---------------------------------------------------------------- gradients + x/y faces
-    // x-pencils (y = a, z = bb): d/dx_hat -> A1; x-face traces / fluxes
+    // ---- phase 4: x role -> T1 = Dc^T x^(1) + x-face lifts -> A1; z-arrays step B, y step C
 #pragma unroll
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
-    c_apply<N, P>(T.Dc[0], r, t);
+    role_q<N, P>(p, T, T.Dc[0], T.DcT[0], T.L[0], NT, 0, nbmask, do_int, do_bnd, do_vol, false, pa, pb, r, t);
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
 #pragma unroll
             for (int e = 0; e < N; ++e) A1[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const double W = p.dF[0] * T.w[pa[k]] * T.w[pb[k]];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const int f = s;
-            const double uo = dot<N>(T.L[1][s], r[k]);
-            const double dref = dot<N>(T.L[1][2 + s], r[k]);
-            FaceOut fo = {0.0, 0.0};
-            const int i0 = FLay<N>::at(2 * f, pa[k], pb[k]), i1 = FLay<N>::at(2 * f + 1, pa[k], pb[k]);
-            if ((nbmask >> f) & 1u) {
-                if (do_int) fo = flux_interior(p, 0, s, W, uo, dref, NT[i0], p.Dqq_h[0] * NT[i1]);
-            } else if (do_bnd) {
-                fo = flux_boundary(p, 0, s, W, uo, dref);
-            }
-            if (act[k]) { NT[i0] = fo.cv; NT[i1] = fo.cg; }
-        }
-    }
-    // y-pencils (x = a, z = bb): d/dy_hat -> A2; y-face traces / fluxes
+    nb_tangential<N, TPC>(T.Vh[6], NT, 2, 0, nbi, lane);
+    nb_tangential<N, TPC>(T.Vh[7], NT, 1, 1, nbi, lane);
+    csync();
+
+    // ---- phase 5: y role -> A1 += T2; z-arrays step C
 #pragma unroll
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-    c_apply<N, P>(T.Dc[1], r, t);
+    role_q<N, P>(p, T, T.Dc[1], T.DcT[1], T.L[1], NT, 1, nbmask, do_int, do_bnd, do_vol, false, pa, pb, r, t);
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
 #pragma unroll
-            for (int e = 0; e < N; ++e) A2[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const double W = p.dF[1] * T.w[pa[k]] * T.w[pb[k]];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const int f = 2 + s;
-            const double uo = dot<N>(T.L[2][s], r[k]);
-            const double dref = dot<N>(T.L[2][2 + s], r[k]);
-            FaceOut fo = {0.0, 0.0};
-            const int i0 = FLay<N>::at(2 * f, pa[k], pb[k]), i1 = FLay<N>::at(2 * f + 1, pa[k], pb[k]);
-            if ((nbmask >> f) & 1u) {
-                if (do_int) fo = flux_interior(p, 1, s, W, uo, dref, NT[i0], p.Dqq_h[1] * NT[i1]);
-            } else if (do_bnd) {
-                fo = flux_boundary(p, 1, s, W, uo, dref);
+            for (int e = 0; e < N; ++e) {
+                const int ie = Lay<N>::at(pa[k], e, pb[k]);
+                A1[ie] = A1[ie] + t[k][e];
             }
-            if (act[k]) { NT[i0] = fo.cv; NT[i1] = fo.cg; }
-        }
-    }
+    nb_tangential<N, TPC>(T.Vh[8], NT, 2, 1, nbi, lane);
     csync();
 
-    // ---------------------------------------------------------------- (2) quadrature-point data
-    // z-pencils (x = a, y = bb): u, d/dz_hat; x^(1) -> A1, x^(2) -> A2 (in place);
-    // X = x^(0) + Dc^T x^(3) + z-face lifts -> A0 (in place over u)
+    // ---- phase 6: z role (+ reaction) -> X = T1 + T2 + T3; V^T along z -> A0
 #pragma unroll
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
-    c_apply<N, P>(T.Dc[2], r, t);   // t = d u / dz_hat
-    {
-        double x3[P][N];
+    role_q<N, P>(p, T, T.Dc[2], T.DcT[2], T.L[2], NT, 2, nbmask, do_int, do_bnd, do_vol, true, pa, pb, r, t);
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-            const double wxy = do_vol ? p.dT * T.w[pa[k]] * T.w[pb[k]] : 0.0;
+    for (int k = 0; k < P; ++k)
 #pragma unroll
-            for (int e = 0; e < N; ++e) {
-                const int ie = Lay<N>::at(pa[k], pb[k], e);
-                const double gx = act[k] ? A1[ie] : 0.0;
-                const double gy = act[k] ? A2[ie] : 0.0;
-                const double gz = t[k][e];
-                const double u = r[k][e];
-                const double W = wxy * T.w[e];
-                // x^(r) / h_r = W (sum_s D_rs/(h_r h_s) d_s u_hat - b_r/h_r u)   (eq:gauss_points)
-                const double x1 = W * (p.Dhat[0] * gx + p.Dhat[1] * gy + p.Dhat[2] * gz - p.kb[0] * u);
-                const double x2 = W * (p.Dhat[3] * gx + p.Dhat[4] * gy + p.Dhat[5] * gz - p.kb[1] * u);
-                x3[k][e] = W * (p.Dhat[6] * gx + p.Dhat[7] * gy + p.Dhat[8] * gz - p.kb[2] * u);
-                r[k][e] = W * p.c * u;                               // x^(0)
-                if (act[k]) { A1[ie] = x1; A2[ie] = x2; }
-            }
-        }
-        c_apply<N, P>(T.DcT[0], x3, t);
+        for (int e = 0; e < N; ++e) t[k][e] += act[k] ? A1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
+    v_bwd<N, P>(T.Vh[9], t, r);   // in place: A0 z-positions of this pencil are read only by this thread
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-            const double cv0 = NT[FLay<N>::at(8, pa[k], pb[k])], cg0 = NT[FLay<N>::at(9, pa[k], pb[k])];
-            const double cv1 = NT[FLay<N>::at(10, pa[k], pb[k])], cg1 = NT[FLay<N>::at(11, pa[k], pb[k])];
-            if (act[k])
+    for (int k = 0; k < P; ++k)
+        if (act[k])
 #pragma unroll
-                for (int e = 0; e < N; ++e)
-                    A0[Lay<N>::at(pa[k], pb[k], e)] = r[k][e] + t[k][e] + cv0 * T.L[3][0][e] + cg0 * T.L[3][2][e] +
-                                                      cv1 * T.L[3][1][e] + cg1 * T.L[3][3][e];
-        }
-    }
+            for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = r[k][e];
     csync();
 
-    // x-pencils: Dc^T x^(1) + x-face lifts (in place in A1)
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-#pragma unroll
-        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A1[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
-    c_apply<N, P>(T.DcT[1], r, t);
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const double cv0 = NT[FLay<N>::at(0, pa[k], pb[k])], cg0 = NT[FLay<N>::at(1, pa[k], pb[k])];
-        const double cv1 = NT[FLay<N>::at(2, pa[k], pb[k])], cg1 = NT[FLay<N>::at(3, pa[k], pb[k])];
-        if (act[k])
-#pragma unroll
-            for (int e = 0; e < N; ++e)
-                A1[Lay<N>::at(e, pa[k], pb[k])] = t[k][e] + cv0 * T.L[4][0][e] + cg0 * T.L[4][2][e] +
-                                                  cv1 * T.L[4][1][e] + cg1 * T.L[4][3][e];
-    }
-    // y-pencils: Dc^T x^(2) + y-face lifts (in place in A2)
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-#pragma unroll
-        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A2[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-    c_apply<N, P>(T.DcT[2], r, t);
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const double cv0 = NT[FLay<N>::at(4, pa[k], pb[k])], cg0 = NT[FLay<N>::at(5, pa[k], pb[k])];
-        const double cv1 = NT[FLay<N>::at(6, pa[k], pb[k])], cg1 = NT[FLay<N>::at(7, pa[k], pb[k])];
-        if (act[k])
-#pragma unroll
-            for (int e = 0; e < N; ++e)
-                A2[Lay<N>::at(pa[k], e, pb[k])] = t[k][e] + cv0 * T.L[5][0][e] + cg0 * T.L[5][2][e] +
-                                                  cv1 * T.L[5][1][e] + cg1 * T.L[5][3][e];
-    }
-    csync();
-
-    // ---------------------------------------------------------------- (3) integrate
-    // z-pencils: X = A0 + A1 + A2, V^T along z -> A0
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-            const int ie = Lay<N>::at(pa[k], pb[k], e);
-            r[k][e] = act[k] ? A0[ie] + A1[ie] + A2[ie] : 0.0;
-        }
-    v_bwd<N, P>(T.Vh[5], r, t);
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-        if (act[k])
-#pragma unroll
-            for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
-    csync();
-    // y-pencils: V^T along y (in place)
+    // ---- phase 7: y-pencils: V^T along y (in place)
 #pragma unroll
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-    v_bwd<N, P>(T.Vh[6], r, t);
+    v_bwd<N, P>(T.Vh[10], r, t);
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
 #pragma unroll
             for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
     csync();
-    // x-pencils: V^T along x, then the single store of y (or f - y)
+
+    // ---- phase 8: x-pencils: V^T along x, then the single store of y (or f - y)
 #pragma unroll
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
-    v_bwd<N, P>(T.Vh[7], r, t);
+    v_bwd<N, P>(T.Vh[11], r, t);
     if (valid) {
 #pragma unroll
         for (int k = 0; k < P; ++k) {

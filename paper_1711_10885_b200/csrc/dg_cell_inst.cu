@@ -30,7 +30,7 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
     constexpr int N = DG_N;
     if (t.n != N) return -1;
     static Tab<N> h;
-    for (int c = 0; c < 10; ++c)
+    for (int c = 0; c < 12; ++c)
         for (int i = 0; i < Tab<N>::HC; ++i)
             for (int j = 0; j < N; ++j) h.Vh[c][i][j] = t.V[i][j];
     for (int c = 0; c < 6; ++c) {
