@@ -62,7 +62,7 @@ template <> struct Cfg<4>  { static constexpr int TPC = 8,  P = 2, C = 16, MINB 
 template <> struct Cfg<5>  { static constexpr int TPC = 16, P = 2, C = 8,  MINB = 4; };
 template <> struct Cfg<6>  { static constexpr int TPC = 16, P = 3, C = 4,  MINB = 8; };
 template <> struct Cfg<7>  { static constexpr int TPC = 32, P = 2, C = 1,  MINB = 16; };
-template <> struct Cfg<8>  { static constexpr int TPC = 32, P = 2, C = 1,  MINB = 16; };
+template <> struct Cfg<8>  { static constexpr int TPC = 64, P = 1, C = 1,  MINB = 8; };
 template <> struct Cfg<9>  { static constexpr int TPC = 32, P = 3, C = 1,  MINB = 12; };
 template <> struct Cfg<10> { static constexpr int TPC = 64, P = 2, C = 1,  MINB = 8; };
 template <> struct Cfg<11> { static constexpr int TPC = 64, P = 2, C = 1,  MINB = 8; };

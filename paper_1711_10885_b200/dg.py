@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdg_b200.so")
+LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg_b200.so")
 
 DG_OK, DG_EINVAL, DG_ENOMEM, DG_ECUDA, DG_ENCCL, DG_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 VOLUME, INTERIOR_FACES, BOUNDARY_FACES, ALL, HALO_EXTERNAL = 1, 2, 4, 7, 0x100
