@@ -1,0 +1,93 @@
+"""Single-GPU loopback of the multi-rank path (SURVEY.md 4 "loopback partition test").
+
+P contexts (ranks of a Px x Py x Pz block partition) live on one device; each packs its
+partition layers with the library (dg_halo_pack), the test copies every send buffer into
+the neighbour's receive buffer (standing in for the NCCL exchange; no kernel waits on
+another), and each rank applies with DG_HALO_EXTERNAL. The gathered y must equal the
+single-rank y BIT FOR BIT: every cell runs the same arithmetic whether its neighbour is
+local or a ghost (partition invariance)."""
+import numpy as np
+import pytest
+
+from paper_1711_10885_b200 import configs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+class DevPtr:
+    """A raw device pointer as a torch tensor view (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def as_tensor(ptr, count):
+    return torch.as_tensor(DevPtr(ptr, count), device="cuda")
+
+
+def run_partitioned(cfg, parts, terms):
+    from paper_1711_10885_b200 import dg
+    world = parts[0] * parts[1] * parts[2]
+    ops, zs, ys = [], [], []
+    for r in range(world):
+        op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, rank=r, nranks=world,
+                         parts=parts)
+        z = torch.empty(op.ndofs, dtype=torch.float64, device="cuda")
+        op.fill_uniform_local(z, cfg.seed)
+        op.halo_pack(z)
+        ops.append(op)
+        zs.append(z)
+    torch.cuda.synchronize()
+    for r, op in enumerate(ops):
+        for f in range(6):
+            nb, cnt = op.halo_info(f)
+            if nb < 0:
+                continue
+            src = as_tensor(ops[nb].halo_buffer_ptr(f ^ 1, 0), cnt)
+            dst = as_tensor(op.halo_buffer_ptr(f, 1), cnt)
+            dst.copy_(src)
+    torch.cuda.synchronize()
+    n3 = cfg.n3
+    G = cfg.ncells
+    yg = np.full(cfg.ndofs, np.nan)
+    for r, op in enumerate(ops):
+        y = torch.full_like(zs[r], float("nan"))
+        op.apply(zs[r], y, terms=terms | dg.HALO_EXTERNAL)
+        torch.cuda.synchronize()
+        lo, cnt = op.cell_lo, op.cell_cnt
+        gz, gy, gx = np.meshgrid(np.arange(lo[2], lo[2] + cnt[2]), np.arange(lo[1], lo[1] + cnt[1]),
+                                 np.arange(lo[0], lo[0] + cnt[0]), indexing="ij")
+        own = (gx + G[0] * (gy + G[1] * gz)).reshape(-1)
+        yg.reshape(-1, n3)[own] = y.cpu().numpy().reshape(-1, n3)
+        ys.append(y)
+    for op in ops:
+        op.close()
+    return yg
+
+
+def run_single(cfg, terms):
+    from paper_1711_10885_b200 import dg
+    op = dg.from_config(cfg)
+    z = torch.empty(op.ndofs, dtype=torch.float64, device="cuda")
+    op.fill_uniform_local(z, cfg.seed)
+    y = torch.empty_like(z)
+    op.apply(z, y, terms=terms)
+    torch.cuda.synchronize()
+    op.close()
+    return y.cpu().numpy()
+
+
+@pytest.mark.parametrize("k,ncells,parts", [
+    (2, (6, 4, 4), (2, 1, 1)), (2, (6, 4, 4), (2, 2, 1)), (3, (4, 4, 4), (2, 2, 2)),
+    (7, (4, 4, 4), (2, 2, 2)), (7, (8, 4, 2), (2, 2, 1)), (1, (4, 6, 8), (1, 2, 4)), (10, (2, 2, 4), (1, 1, 2)),
+])
+def test_partitioned_equals_single_bitwise(k, ncells, parts):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = configs.small(k, ncells=ncells, hi=(1.5, 1.0, 0.75), b=(1.0, -0.5, 0.25), c=0.3)
+    for terms in (7, 2):
+        ys = run_single(cfg, terms)
+        yp = run_partitioned(cfg, parts, terms)
+        assert np.array_equal(yp, ys)
