@@ -151,18 +151,18 @@ def cpu_oracle_rate(cfg, z_host, budget_s, seed=0):
     return rate, cores, text, dt
 
 
-def load_traffic(cfg):
-    """dram bytes per launch of the cell kernel from the committed ncu --set full summary (or None)."""
+def load_ncu(cfg):
+    """The committed ncu --set full summary of the cell kernel for this workload (or {})."""
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
         ent = d.get(cfg.name)
         if ent and ent.get("ndofs") == cfg.ndofs // max(1, cfg.parts[0] * cfg.parts[1] * cfg.parts[2]):
-            return ent.get("dram_bytes_per_launch")
+            return ent
     except Exception:
         pass
-    return None
+    return {}
 
 
 def measured_peaks():
@@ -291,9 +291,16 @@ def run_ours(args, rank, world, local_rank):
     kern_t = tk / args.steps   # one cell-kernel pass over all local cells per apply (2 launches at N > 1)
     achieved = flops_launch_rank / kern_t / 1e12
     peak = perfmodel.fp64_peak_tflops(clk["sm_max_mhz"] or 1965.0)
-    traffic = load_traffic(cfg)
+    ncu = load_ncu(cfg)
+    traffic = ncu.get("dram_bytes_per_launch")
+    exec_per_dof = ncu.get("executed_flops_per_dof")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic,
+            "traffic_algorithmic_bytes": 16.0 * op.ndofs,
+            "executed_flops_per_dof": exec_per_dof,
+            "executed_achieved": (exec_per_dof * op.ndofs / kern_t / 1e12) if exec_per_dof else None,
+            "executed_frac": (exec_per_dof * op.ndofs / kern_t / 1e12 / peak) if exec_per_dof else None,
+            "ncu_source": "profiles/ncu_full_summary.json (ncu --set full, --clock-control none)" if ncu else None,
             "kernel": "dg_cell_kernel<%d> (FP64 DFMA pipe)" % (cfg.k + 1),
             "flops_basis": "paper model FLOPDOF_vol+FLOPDOF_face(3,%d) = %.1f flop/DOF x %d DOFs per launch "
                            "(PAPER.md:675-676); the kernel executes fewer (collocation variant, DESIGN.md)"
