@@ -525,7 +525,7 @@ dg_cell_kernel(const KParams p)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) A1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
-        nb_tangential<N, TPC>(T.Vh[2], NT, 0, 0, nbi, lane);
+        nb_tangential<N, TPC>(T.Vh[2], NT, 0, 0, nbi, (lane + TPC / 2) % TPC);
         nb_contract<N, P>(T, NT, 1, nbi, pa, pb, act, rl, rh);
         csync();
 
@@ -543,7 +543,7 @@ dg_cell_kernel(const KParams p)
 #pragma unroll
                 for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
         nb_tangential<N, TPC>(T.Vh[4], NT, 1, 0, nbi, lane);
-        nb_tangential<N, TPC>(T.Vh[5], NT, 0, 1, nbi, lane);
+        nb_tangential<N, TPC>(T.Vh[5], NT, 0, 1, nbi, (lane + TPC / 2) % TPC);
         nb_contract<N, P>(T, NT, 2, nbi, pa, pb, act, rl, rh);
         csync();
     }
@@ -560,7 +560,7 @@ dg_cell_kernel(const KParams p)
 #pragma unroll
             for (int e = 0; e < N; ++e) A1[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
     nb_tangential<N, TPC>(T.Vh[6], NT, 2, 0, nbi, lane);
-    nb_tangential<N, TPC>(T.Vh[7], NT, 1, 1, nbi, lane);
+    nb_tangential<N, TPC>(T.Vh[7], NT, 1, 1, nbi, (lane + TPC / 2) % TPC);
     csync();
 
     // ---- phase 5: y role -> A1 += T2; z-arrays step C
