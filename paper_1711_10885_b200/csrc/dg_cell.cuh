@@ -56,16 +56,22 @@ __constant__ Tab<DG_N> g_tab;
 
 // TPC threads per cell, P pencils per thread (TPC * P >= n^2), C cells per CTA.
 template <int N> struct Cfg;
-template <> struct Cfg<2>  { static constexpr int TPC = 4,  P = 1, C = 32, MINB = 8; };
-template <> struct Cfg<3>  { static constexpr int TPC = 8,  P = 2, C = 16, MINB = 8; };
-template <> struct Cfg<4>  { static constexpr int TPC = 8,  P = 2, C = 16, MINB = 6; };
-template <> struct Cfg<5>  { static constexpr int TPC = 16, P = 2, C = 8,  MINB = 4; };
-template <> struct Cfg<6>  { static constexpr int TPC = 16, P = 3, C = 4,  MINB = 8; };
-template <> struct Cfg<7>  { static constexpr int TPC = 32, P = 2, C = 1,  MINB = 16; };
-template <> struct Cfg<8>  { static constexpr int TPC = 64, P = 1, C = 1,  MINB = 8; };
-template <> struct Cfg<9>  { static constexpr int TPC = 32, P = 3, C = 1,  MINB = 12; };
-template <> struct Cfg<10> { static constexpr int TPC = 64, P = 2, C = 1,  MINB = 8; };
-template <> struct Cfg<11> { static constexpr int TPC = 64, P = 2, C = 1,  MINB = 8; };
+// Build-time override of this TU's configuration (variant sweeps: tools/tune_cfg.py).
+#ifdef DG_TPC
+#define DG_OVR(n, ov, d) ((DG_N) == (n) ? (ov) : (d))
+#else
+#define DG_OVR(n, ov, d) (d)
+#endif
+template <> struct Cfg<2> { static constexpr int TPC = DG_OVR(2, DG_TPC, 8), P = DG_OVR(2, DG_P, 1), C = DG_OVR(2, DG_C, 16), MINB = DG_OVR(2, DG_MINB, 8); };
+template <> struct Cfg<3> { static constexpr int TPC = DG_OVR(3, DG_TPC, 16), P = DG_OVR(3, DG_P, 1), C = DG_OVR(3, DG_C, 8), MINB = DG_OVR(3, DG_MINB, 8); };
+template <> struct Cfg<4> { static constexpr int TPC = DG_OVR(4, DG_TPC, 16), P = DG_OVR(4, DG_P, 1), C = DG_OVR(4, DG_C, 4), MINB = DG_OVR(4, DG_MINB, 8); };
+template <> struct Cfg<5> { static constexpr int TPC = DG_OVR(5, DG_TPC, 32), P = DG_OVR(5, DG_P, 1), C = DG_OVR(5, DG_C, 1), MINB = DG_OVR(5, DG_MINB, 16); };
+template <> struct Cfg<6> { static constexpr int TPC = DG_OVR(6, DG_TPC, 32), P = DG_OVR(6, DG_P, 2), C = DG_OVR(6, DG_C, 1), MINB = DG_OVR(6, DG_MINB, 16); };
+template <> struct Cfg<7> { static constexpr int TPC = DG_OVR(7, DG_TPC, 64), P = DG_OVR(7, DG_P, 1), C = DG_OVR(7, DG_C, 1), MINB = DG_OVR(7, DG_MINB, 10); };
+template <> struct Cfg<8> { static constexpr int TPC = DG_OVR(8, DG_TPC, 64), P = DG_OVR(8, DG_P, 1), C = DG_OVR(8, DG_C, 1), MINB = DG_OVR(8, DG_MINB, 8); };
+template <> struct Cfg<9> { static constexpr int TPC = DG_OVR(9, DG_TPC, 96), P = DG_OVR(9, DG_P, 1), C = DG_OVR(9, DG_C, 1), MINB = DG_OVR(9, DG_MINB, 5); };
+template <> struct Cfg<10> { static constexpr int TPC = DG_OVR(10, DG_TPC, 64), P = DG_OVR(10, DG_P, 2), C = DG_OVR(10, DG_C, 1), MINB = DG_OVR(10, DG_MINB, 6); };
+template <> struct Cfg<11> { static constexpr int TPC = DG_OVR(11, DG_TPC, 128), P = DG_OVR(11, DG_P, 1), C = DG_OVR(11, DG_C, 1), MINB = DG_OVR(11, DG_MINB, 4); };
 
 // Shared-memory layout of one n^3 cell array: x-, y- and z-pencil accesses of a warp are
 // (nearly) bank-conflict free (searched offline; n = 8 uses an XOR swizzle that is conflict
