@@ -1,7 +1,11 @@
 // One translation unit per basis size n = k+1 (compiled with -DDG_N=n): the
 // fused cell kernel instantiation, its __constant__ table upload and launcher.
 #include "dg_cell.cuh"
+#if DG_N == 8
+#include "dg_mma8.cuh"
+#endif
 
+#include <cstdlib>
 #include <cstring>
 
 #define DG_CAT2(a, b) a##b
@@ -50,7 +54,43 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
         h.dth0[i] = t.dth0[i];
         h.dth1[i] = t.dth1[i];
     }
-    return cudaMemcpyToSymbol(g_tab, &h, sizeof(h)) == cudaSuccess ? 0 : -3;
+    if (cudaMemcpyToSymbol(g_tab, &h, sizeof(h)) != cudaSuccess) return -3;
+#if DG_N == 8
+    // per-lane DMMA fragments (dg_mma8.cuh): lane l -> g = l >> 2, t = l & 3
+    static double fr[32][16];
+    auto Lm = [&](int i, int r) { return r == 0 ? t.L0[i] : r == 1 ? t.L1[i] : r == 2 ? t.LD0[i] : r == 3 ? t.LD1[i] : 0.0; };
+    for (int l = 0; l < 32; ++l) {
+        const int g = l >> 2, tt = l & 3;
+        for (int c = 0; c < 2; ++c) {
+            fr[l][m8::F_VF0 + c] = t.V[g][2 * tt + c];
+            fr[l][m8::F_VB0 + c] = t.V[2 * tt + c][g];
+            fr[l][m8::F_DC0 + c] = t.Dc[g][2 * tt + c];
+            fr[l][m8::F_DT0 + c] = t.Dc[2 * tt + c][g];
+            fr[l][m8::F_LT0 + c] = Lm(2 * tt + c, g);
+            fr[l][m8::F_WT0 + c] = t.w[2 * tt + c];
+        }
+        fr[l][m8::F_LL] = Lm(g, tt);
+        fr[l][m8::F_WG] = t.w[g];
+        for (int k = m8::F_COUNT; k < 16; ++k) fr[l][k] = 0.0;
+    }
+    if (cudaMemcpyToSymbol(m8::g_frag, fr, sizeof(fr)) != cudaSuccess) return -3;
+#endif
+    return 0;
+}
+
+// n = 8: the DMMA kernel with DG_CELL_KERNEL=mma (default: the SIMT kernel while it is faster)
+static bool use_mma()
+{
+#if DG_N == 8
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("DG_CELL_KERNEL");
+        v = (e && std::strcmp(e, "mma") == 0) ? 1 : 0;
+    }
+    return v == 1;
+#else
+    return false;
+#endif
 }
 
 static int g_attr_done[64];
@@ -63,6 +103,20 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
     if (p.ntasks <= 0) return cudaSuccess;
     int dev = 0;
     cudaGetDevice(&dev);
+#if DG_N == 8
+    if (use_mma()) {
+        static int done[64];
+        constexpr int BYTES = m8::C * m8::PER_CELL * 8;
+        if (dev >= 0 && dev < 64 && !done[dev]) {
+            cudaError_t e = cudaFuncSetAttribute(m8::dg_cell_mma8, cudaFuncAttributeMaxDynamicSharedMemorySize, BYTES);
+            if (e != cudaSuccess) return e;
+            done[dev] = 1;
+        }
+        const int64_t grid = (p.ntasks + m8::C - 1) / m8::C;
+        m8::dg_cell_mma8<<<(unsigned)grid, 32 * m8::C, BYTES, s>>>(p);
+        return cudaGetLastError();
+    }
+#endif
     if (dev >= 0 && dev < 64 && !g_attr_done[dev]) {
         cudaError_t e = cudaFuncSetAttribute(dg_cell_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Smem<N>::BYTES);
@@ -77,6 +131,24 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
 int DG_CAT(cell_info_n, DG_N)(LaunchInfo* info)
 {
     constexpr int N = DG_N;
+#if DG_N == 8
+    if (use_mma()) {
+        constexpr int BYTES = m8::C * m8::PER_CELL * 8;
+        info->cells_per_cta = m8::C;
+        info->threads = 32 * m8::C;
+        info->smem = BYTES;
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, m8::dg_cell_mma8) != cudaSuccess) return -3;
+        info->regs = fa.numRegs;
+        if (cudaFuncSetAttribute(m8::dg_cell_mma8, cudaFuncAttributeMaxDynamicSharedMemorySize, BYTES) != cudaSuccess)
+            return -3;
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, m8::dg_cell_mma8, info->threads, BYTES) != cudaSuccess)
+            return -3;
+        info->ctas_per_sm = blocks;
+        return 0;
+    }
+#endif
     info->cells_per_cta = Cfg<N>::C;
     info->threads = Cfg<N>::C * Cfg<N>::TPC;
     info->smem = Smem<N>::BYTES;
