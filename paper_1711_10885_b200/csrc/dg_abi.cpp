@@ -2,6 +2,7 @@
 #include "../../include/dg.h"
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -189,6 +190,10 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
     // grouped in 4 x 16 tiles, so a cell's neighbours are touched within ~4096 tasks.
     p.tile[0] = 4;
     p.tile[1] = 16;
+    if (const char* e = std::getenv("DG_TILE")) {   // experiments: "TX,TY"
+        long tx = 0, ty = 0;
+        if (std::sscanf(e, "%ld,%ld", &tx, &ty) == 2 && tx > 0 && ty > 0) { p.tile[0] = tx; p.tile[1] = ty; }
+    }
 
     if (ctx->partitioned) {
         for (int f = 0; f < 6; ++f) {
