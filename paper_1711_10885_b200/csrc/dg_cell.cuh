@@ -47,6 +47,10 @@ struct Tab {
     double w[N];
     double L[6][4][N];       // per use site: L_l(0), L_l(1), L'_l(0), L'_l(1)
     double th0[N], th1[N], dth0[N], dth1[N];
+    // even-odd forms used by the roles (one copy per direction):
+    EO<N> DcTw[3];                         // Dc^T diag(w): Gauss weights folded into the transposed stage
+    double Le[3][4][(N / 2) > 0 ? N / 2 : 1];  // (L0_i +- L0_{n-1-i})/2, (L'0_i +- L'0_{n-1-i})/2, i < n/2
+    double Lmid[3][2];                     // L0_H, L'0_H (odd n)
 };
 
 #ifndef DG_N
@@ -412,6 +416,174 @@ __device__ __forceinline__ void role_q(const KParams& p, const Tab<N>& T, const 
     }
 }
 
+// c_apply that also returns the even/odd sums s_j = r_j + r_{n-1-j}, d_j = r_j - r_{n-1-j}
+template <int N, int P>
+__device__ __forceinline__ void c_apply_sd(const EO<N>& A, const double (&r)[P][N], double (&t)[P][N],
+                                           double (&s)[P][(N / 2) > 0 ? N / 2 : 1],
+                                           double (&d)[P][(N / 2) > 0 ? N / 2 : 1])
+{
+    constexpr int H = N / 2;
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            s[k][j] = r[k][j] + r[k][N - 1 - j];
+            d[k][j] = r[k][j] - r[k][N - 1 - j];
+        }
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        double Pp[P], Q[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            Pp[k] = (N & 1) ? A.col[i] * r[k][H] : 0.0;
+            Q[k] = 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < H; ++j)
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                Pp[k] = fma(A.p[i][j], s[k][j], Pp[k]);
+                Q[k] = fma(A.m[i][j], d[k][j], Q[k]);
+            }
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            t[k][i] = Pp[k] + Q[k];
+            t[k][N - 1 - i] = Q[k] - Pp[k];
+        }
+    }
+    if (N & 1) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < H; ++j) acc = fma(A.row[j], d[k][j], acc);
+            t[k][H] = acc;
+        }
+    }
+}
+
+// c_apply with an even/odd-paired addend merged into the accumulators:
+// t_i += qa_i + pb_i, t_{n-1-i} += qa_i - pb_i (i < n/2), t_H += mid (odd n)
+template <int N, int P>
+__device__ __forceinline__ void c_apply_add(const EO<N>& A, const double (&r)[P][N], double (&t)[P][N],
+                                            const double (&qa)[P][(N / 2) > 0 ? N / 2 : 1],
+                                            const double (&pb)[P][(N / 2) > 0 ? N / 2 : 1], const double (&mid)[P])
+{
+    constexpr int H = N / 2;
+    double s[P][H > 0 ? H : 1], d[P][H > 0 ? H : 1];
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            s[k][j] = r[k][j] + r[k][N - 1 - j];
+            d[k][j] = r[k][j] - r[k][N - 1 - j];
+        }
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        double Pp[P], Q[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            Pp[k] = (N & 1) ? fma(A.col[i], r[k][H], pb[k][i]) : pb[k][i];
+            Q[k] = qa[k][i];
+        }
+#pragma unroll
+        for (int j = 0; j < H; ++j)
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                Pp[k] = fma(A.p[i][j], s[k][j], Pp[k]);
+                Q[k] = fma(A.m[i][j], d[k][j], Q[k]);
+            }
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            t[k][i] = Pp[k] + Q[k];
+            t[k][N - 1 - i] = Q[k] - Pp[k];
+        }
+    }
+    if (N & 1) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            double acc = mid[k];
+#pragma unroll
+            for (int j = 0; j < H; ++j) acc = fma(A.row[j], d[k][j], acc);
+            t[k][H] = acc;
+        }
+    }
+}
+
+// Role of direction q (even-odd form): traces from the even/odd sums of the Dc stage,
+// Gauss weights folded into Dc^T diag(w), face lifts merged into the Dc^T accumulators.
+template <int N, int P>
+__device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const double* NT, int q, unsigned nbmask,
+                                        bool do_int, bool do_bnd, bool do_vol, bool with_reaction,
+                                        const int (&pa)[P], const int (&pb)[P], const double (&r)[P][N],
+                                        double (&out)[P][N])
+{
+    constexpr int H = N / 2;
+    constexpr int HH = H > 0 ? H : 1;
+    double g[P][N], s[P][HH], d[P][HH];
+    c_apply_sd<N, P>(T.Dc[q], r, g, s, d);
+    const double* Lp = T.Le[q][0];
+    const double* Lm = T.Le[q][1];
+    const double* LDp = T.Le[q][2];
+    const double* LDm = T.Le[q][3];
+    double qa[P][HH], pbv[P][HH], mid[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const double wab = T.w[pa[k]] * T.w[pb[k]];
+        // own traces u(0), u(1), u'(0), u'(1) from the even/odd sums
+        double A = (N & 1) ? T.Lmid[q][0] * r[k][H] : 0.0, B = 0.0;
+        double Ad = (N & 1) ? T.Lmid[q][1] * r[k][H] : 0.0, Bd = 0.0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            A = fma(Lp[i], s[k][i], A);
+            B = fma(Lm[i], d[k][i], B);
+            Ad = fma(LDp[i], s[k][i], Ad);
+            Bd = fma(LDm[i], d[k][i], Bd);
+        }
+        const double tr_u[2] = {A + B, A - B}, tr_d[2] = {Ad + Bd, Bd - Ad};
+        const double Wf = p.dF[q] * wab;
+        FaceOut fo[2];
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd) {
+            const int f = 2 * q + sd;
+            fo[sd].cv = 0.0;
+            fo[sd].cg = 0.0;
+            if ((nbmask >> f) & 1u) {
+                if (do_int) {
+                    const double un = NT[FLay<N>::at(2 * f, pa[k], pb[k])];
+                    const double sn = p.Dqq_h[q] * NT[FLay<N>::at(2 * f + 1, pa[k], pb[k])];
+                    fo[sd] = flux_interior(p, q, sd, Wf, tr_u[sd], tr_d[sd], un, sn);
+                }
+            } else if (do_bnd) {
+                fo[sd] = flux_boundary(p, q, sd, Wf, tr_u[sd], tr_d[sd]);
+            }
+        }
+        // lift (normal direction LAST) as even/odd addends of the Dc^T stage
+        const double Pc = fo[0].cv + fo[1].cv, Mc = fo[0].cv - fo[1].cv;
+        const double Qc = fo[0].cg - fo[1].cg, Rc = fo[0].cg + fo[1].cg;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            qa[k][i] = fma(Pc, Lp[i], Qc * LDp[i]);
+            pbv[k][i] = fma(Mc, Lm[i], Rc * LDm[i]);
+        }
+        mid[k] = (N & 1) ? fma(Pc, T.Lmid[q][0], Qc * T.Lmid[q][1]) : 0.0;
+        // quadrature-point data with the weights folded into Dc^T diag(w) (eq:gauss_points)
+        const double sw = do_vol ? p.dT * wab : 0.0;
+        const double kd = sw * p.Dhat[4 * q], kb = sw * p.kb[q];
+#pragma unroll
+        for (int e = 0; e < N; ++e) g[k][e] = fma(kd, g[k][e], -kb * r[k][e]);
+    }
+    c_apply_add<N, P>(T.DcTw[q], g, out, qa, pbv, mid);
+    if (with_reaction && do_vol) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const double wc = p.dT * T.w[pa[k]] * T.w[pb[k]] * p.c;
+#pragma unroll
+            for (int e = 0; e < N; ++e) out[k][e] = fma(wc * T.w[e], r[k][e], out[k][e]);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------------- kernel
 template <int N>
 __global__ void __launch_bounds__(Cfg<N>::C * Cfg<N>::TPC, Cfg<N>::MINB)
@@ -559,7 +731,7 @@ dg_cell_kernel(const KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
-    role_q<N, P>(p, T, T.Dc[0], T.DcT[0], T.L[0], NT, 0, nbmask, do_int, do_bnd, do_vol, false, pa, pb, r, t);
+    role_eo<N, P>(p, T, NT, 0, nbmask, do_int, do_bnd, do_vol, false, pa, pb, r, t);
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
@@ -574,7 +746,7 @@ dg_cell_kernel(const KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-    role_q<N, P>(p, T, T.Dc[1], T.DcT[1], T.L[1], NT, 1, nbmask, do_int, do_bnd, do_vol, false, pa, pb, r, t);
+    role_eo<N, P>(p, T, NT, 1, nbmask, do_int, do_bnd, do_vol, false, pa, pb, r, t);
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
@@ -591,7 +763,7 @@ dg_cell_kernel(const KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
-    role_q<N, P>(p, T, T.Dc[2], T.DcT[2], T.L[2], NT, 2, nbmask, do_int, do_bnd, do_vol, true, pa, pb, r, t);
+    role_eo<N, P>(p, T, NT, 2, nbmask, do_int, do_bnd, do_vol, true, pa, pb, r, t);
 #pragma unroll
     for (int k = 0; k < P; ++k)
 #pragma unroll

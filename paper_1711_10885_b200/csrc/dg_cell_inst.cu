@@ -41,6 +41,23 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
         fill_eo<N>(h.Dc[c], t.Dc, false);
         fill_eo<N>(h.DcT[c], t.Dc, true);
     }
+    {
+        static double Aw[NMAX][NMAX];   // Dc^T diag(w)
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) Aw[i][j] = t.Dc[j][i] * t.w[j];
+        constexpr int H = N / 2;
+        for (int c = 0; c < 3; ++c) {
+            fill_eo<N>(h.DcTw[c], Aw, false);
+            for (int i = 0; i < H; ++i) {
+                h.Le[c][0][i] = 0.5 * (t.L0[i] + t.L0[N - 1 - i]);
+                h.Le[c][1][i] = 0.5 * (t.L0[i] - t.L0[N - 1 - i]);
+                h.Le[c][2][i] = 0.5 * (t.LD0[i] + t.LD0[N - 1 - i]);
+                h.Le[c][3][i] = 0.5 * (t.LD0[i] - t.LD0[N - 1 - i]);
+            }
+            h.Lmid[c][0] = (N & 1) ? t.L0[H] : 0.0;
+            h.Lmid[c][1] = (N & 1) ? t.LD0[H] : 0.0;
+        }
+    }
     for (int i = 0; i < N; ++i) {
         h.w[i] = t.w[i];
         for (int c = 0; c < 6; ++c) {
