@@ -20,7 +20,8 @@ VOLUME, INTERIOR, BOUNDARY, ALL = 1, 2, 4, 7
 class _Problem(ctypes.Structure):
     _fields_ = [("nc", ctypes.c_int64 * 3), ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
                 ("k", ctypes.c_int), ("D", ctypes.c_double * 9), ("b", ctypes.c_double * 3),
-                ("c", ctypes.c_double), ("sigma", ctypes.c_double)]
+                ("c", ctypes.c_double), ("sigma", ctypes.c_double), ("periodic", ctypes.c_int * 3),
+                ("Dcell", ctypes.c_void_p)]
 
 
 def build(force=False):
@@ -48,8 +49,11 @@ def lib():
     return _lib
 
 
-def _problem(ncells, lo, hi, k, D, b, c, sigma):
+def _problem(ncells, lo, hi, k, D, b, c, sigma, periodic=(0, 0, 0), Dcell=None):
     P = _Problem()
+    for q in range(3):
+        P.periodic[q] = 1 if periodic[q] else 0
+    P.Dcell = None if Dcell is None else Dcell.ctypes.data
     for q in range(3):
         P.nc[q] = int(ncells[q])
         P.lo[q] = float(lo[q])
@@ -74,17 +78,23 @@ def tables(k):
     return arrs
 
 
-def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL, cells=None, nthreads=0):
+def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL, cells=None, nthreads=0, periodic=(0, 0, 0), Dcell=None):
     """y = A z (mask selects volume / interior-face / boundary-face terms).
 
     cells=None: full vector. cells=int64 array: returns the compact blocks of
-    those cells only, shape (len(cells), n^3) (sampled mode). Returns (y, threads)."""
+    those cells only, shape (len(cells), n^3) (sampled mode). Returns (y, threads).
+    periodic[q]: glue the two sides normal to q (NEXT-1). Dcell: per-cell diffusion
+    tensors, array [ncells_total, 3, 3] in global cell order (NEXT-1; D is then ignored)."""
     n3 = (k + 1) ** 3
     ncell_total = int(ncells[0]) * int(ncells[1]) * int(ncells[2])
     z = np.ascontiguousarray(z, dtype=np.float64)
     if z.size != ncell_total * n3:
         raise ValueError("z has %d entries, expected %d" % (z.size, ncell_total * n3))
-    P = _problem(ncells, lo, hi, k, D, b, c, sigma)
+    if Dcell is not None:
+        Dcell = np.ascontiguousarray(Dcell, dtype=np.float64).reshape(-1, 9)
+        if Dcell.shape[0] != ncell_total:
+            raise ValueError("Dcell has %d tensors, expected %d" % (Dcell.shape[0], ncell_total))
+    P = _problem(ncells, lo, hi, k, D, b, c, sigma, periodic, Dcell)
     if cells is None:
         y = np.zeros(ncell_total * n3)
         used = lib().o1_apply(ctypes.byref(P), z.ctypes.data, y.ctypes.data, mask, None, 0, 0, nthreads)

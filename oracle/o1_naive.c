@@ -22,6 +22,15 @@
  *   boundary: [[v]] = {v}_w = v-, gamma = delta*sigma             (C-6)
  *   upwind flux Phi(u-,u+,b_nu) = b_nu u- if b_nu >= 0 else b_nu u+ 
  *   Dirichlet data g = 0 inside A (enters only the RHS)           (C-9)
+ *
+ * NEXT-1 (the paper's Problem A):
+ *   periodic[q] != 0: the two box sides normal to q are glued; the wrap face between
+ *     cell N_q-1 (T-) and cell 0 (T+) is an ordinary interior face with nu = +e_q
+ *     ("periodic boundaries in the same way as regular processor boundaries", :940-942)
+ *   Dcell != NULL: a diffusion tensor per cell (9 doubles row-major, global cell order),
+ *     constant inside each cell (Problem A, :945-946); D- and D+ of a face are the
+ *     tensors of T- and T+, delta+- = nu^T D+- nu, weights w- = d+/(d-+d+),
+ *     w+ = d-/(d-+d+) (:274-281) and gamma = <d-,d+> sigma (:293, :328-333) become live.
  */
 #include <math.h>
 #include <stdint.h>
@@ -39,6 +48,8 @@ typedef struct {
     double b[3];       /* velocity */
     double c;          /* reaction */
     double sigma;      /* D-independent penalty factor (C-4) */
+    int periodic[3];   /* per direction: 0 = both sides weak Dirichlet, 1 = periodic (NEXT-1) */
+    const double* Dcell; /* NULL: D above everywhere; else per-cell tensors [cell][9] (NEXT-1) */
 } o1_problem;
 
 enum { O1_VOLUME = 1, O1_INTERIOR = 2, O1_BOUNDARY = 4 };
@@ -184,7 +195,7 @@ static void o1_cell(const o1_problem* P, const o1_tab* T, const double* z, int64
     ic[2] = e / (P->nc[0] * P->nc[1]);
     int64_t stride[3] = {1, P->nc[0], P->nc[0] * P->nc[1]};
     const double* zc = z + e * n3;
-    const double* D = P->D;
+    const double* D = P->Dcell ? P->Dcell + 9 * e : P->D;   /* this cell's tensor */
     double dT = T->h[0] * T->h[1] * T->h[2];
     memset(yc, 0, sizeof(double) * n3);
 
@@ -212,9 +223,17 @@ static void o1_cell(const o1_problem* P, const o1_tab* T, const double* z, int64
         for (int s = 0; s < 2; ++s) {
             int64_t nb_i = ic[q] + (s ? 1 : -1);
             int interior = (nb_i >= 0 && nb_i < P->nc[q]);
+            if (!interior && P->periodic[q]) {                  /* wrap: glued box sides */
+                nb_i = (nb_i < 0) ? P->nc[q] - 1 : 0;
+                interior = 1;
+            }
             if (interior && !(mask & O1_INTERIOR)) continue;
             if (!interior && !(mask & O1_BOUNDARY)) continue;
-            const double* zn = interior ? z + (e + (s ? stride[q] : -stride[q])) * n3 : NULL;
+            int64_t enb = e + (nb_i - ic[q]) * stride[q];       /* neighbour cell id */
+            const double* zn = interior ? z + enb * n3 : NULL;
+            const double* Dn = (interior && P->Dcell) ? P->Dcell + 9 * enb : D;
+            const double* Dm_ = s ? D : Dn;                     /* tensor of T- */
+            const double* Dp_ = s ? Dn : D;                     /* tensor of T+ */
             for (int b2 = 0; b2 < m; ++b2)
                 for (int b1 = 0; b1 < m; ++b1) {
                     int pown[3], pnb[3];
@@ -230,9 +249,9 @@ static void o1_cell(const o1_problem* P, const o1_tab* T, const double* z, int64
                         double um = s ? u : un, up = s ? un : u;
                         const double* gm = s ? g : gn;
                         const double* gp = s ? gn : g;
-                        double sm = D[3 * q + 0] * gm[0] + D[3 * q + 1] * gm[1] + D[3 * q + 2] * gm[2];
-                        double sp = D[3 * q + 0] * gp[0] + D[3 * q + 1] * gp[1] + D[3 * q + 2] * gp[2];
-                        double dm = Dqq, dp = Dqq;                 /* delta = nu^T D nu */
+                        double sm = Dm_[3 * q + 0] * gm[0] + Dm_[3 * q + 1] * gm[1] + Dm_[3 * q + 2] * gm[2];
+                        double sp = Dp_[3 * q + 0] * gp[0] + Dp_[3 * q + 1] * gp[1] + Dp_[3 * q + 2] * gp[2];
+                        double dm = Dm_[3 * q + q], dp = Dp_[3 * q + q];  /* delta = nu^T D nu */
                         double wm, wp;
                         if (dm + dp == 0.0) { wm = 0.5; wp = 0.5; }  /* C-5 */
                         else { wm = dp / (dm + dp); wp = dm / (dm + dp); }

@@ -19,6 +19,11 @@ Every face integral is written as a bilinear form over the COMBINED trial and
 test spaces of the two adjacent cells, evaluated at the tensor Gauss points of
 the face, and scattered into the global matrix. No sum factorization, no
 splitting into the per-cell formulas used by O-1.
+
+NEXT-1 (the paper's Problem A): `periodic[q]` glues the two box
+sides normal to q (the wrap face is an interior face, T- = the last cell, nu = +e_q);
+`Dcell[e]` gives cell e its own tensor, so D-, D+, the weights w+- and the harmonic
+penalty <d-, d+> differ per face.
 """
 import numpy as np
 
@@ -56,31 +61,35 @@ def _basis_on(n, pts_per_dir, h):
     return phi, grad
 
 
-def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0):
+def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic=(0, 0, 0), Dcell=None):
     """Dense A (N x N), N = prod(ncells) * (k+1)^3, cell-major global order (C-3).
 
     avg_sign = -1 selects the weighted average exactly as PAPER.md:271 prints it
     ({v}_w = w- v- - w+ v+); used only by the test that shows this reading is
-    inconsistent (reading C-1). The oracle's operator is avg_sign = +1."""
+    inconsistent (reading C-1). The oracle's operator is avg_sign = +1.
+    periodic / Dcell ([ncell, 3, 3]): NEXT-1, see the module docstring."""
     nc = [int(v) for v in ncells]
     n = k + 1
     n3 = n ** 3
-    D = np.asarray(D, dtype=np.float64).reshape(3, 3)
     b = np.asarray(b, dtype=np.float64)
+    ncell0 = nc[0] * nc[1] * nc[2]
+    if Dcell is None:
+        Dcell = np.tile(np.asarray(D, dtype=np.float64).reshape(1, 3, 3), (ncell0, 1, 1))
+    Dcell = np.asarray(Dcell, dtype=np.float64).reshape(ncell0, 3, 3)
     h = [(hi[q] - lo[q]) / nc[q] for q in range(3)]
     dT = h[0] * h[1] * h[2]
     ncell = nc[0] * nc[1] * nc[2]
     A = np.zeros((ncell * n3, ncell * n3))
     xi, w = gauss01(n)
 
-    # ---- volume block (identical for every cell: constant coefficients, uniform cells)
+    # ---- volume blocks (coefficients constant per cell, uniform cells)
     if mask & VOLUME:
         phi, grad = _basis_on(n, [xi, xi, xi], h)
         W = dT * np.einsum("a,b,c->cba", w, w, w).reshape(-1)
-        # integrand (D grad u - b u) . grad v + c u v, u = phi_j (columns), v = phi_i (rows)
-        flux = np.einsum("rs,spj->rpj", D, grad) - b[:, None, None] * phi[None, :, :]
-        Avol = np.einsum("p,rpi,rpj->ij", W, grad, flux) + c * np.einsum("p,pi,pj->ij", W, phi, phi)
         for e in range(ncell):
+            # integrand (D grad u - b u) . grad v + c u v, u = phi_j (columns), v = phi_i (rows)
+            flux = np.einsum("rs,spj->rpj", Dcell[e], grad) - b[:, None, None] * phi[None, :, :]
+            Avol = np.einsum("p,rpi,rpj->ij", W, grad, flux) + c * np.einsum("p,pi,pj->ij", W, phi, phi)
             A[e * n3:(e + 1) * n3, e * n3:(e + 1) * n3] += Avol
 
     # ---- faces
@@ -90,7 +99,6 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0):
         Wf = dF * np.einsum("a,b->ba", w, w).reshape(-1)   # tangential point p = pt1 + m*pt2
         nu = np.zeros(3)
         nu[q] = 1.0
-        delta = nu @ D @ nu
 
         def face_basis(s):
             pts = [None, None, None]
@@ -109,17 +117,18 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0):
                     ic = [ix, iy, iz]
                     e = _cell_index(ix, iy, iz, nc)
                     # interior face with this cell as T- (low side) and its +q neighbour as T+
-                    if ic[q] + 1 < nc[q] and (mask & INTERIOR):
+                    if (ic[q] + 1 < nc[q] or periodic[q]) and (mask & INTERIOR):
                         jc = list(ic)
-                        jc[q] += 1
+                        jc[q] = (jc[q] + 1) % nc[q]
                         f = _cell_index(jc[0], jc[1], jc[2], nc)
+                        Dm, Dp = Dcell[e], Dcell[f]
                         npts = phi1.shape[0]
                         Z = np.zeros((npts, n3))
                         um = np.hstack([phi1, Z])              # u- of combined trial [T- dofs, T+ dofs]
                         up = np.hstack([Z, phi0])              # u+
                         gm = np.concatenate([grad1, np.zeros_like(grad1)], axis=2)
                         gp = np.concatenate([np.zeros_like(grad0), grad0], axis=2)
-                        dm = dp = delta
+                        dm, dp = nu @ Dm @ nu, nu @ Dp @ nu
                         if dm + dp == 0.0:
                             wm = wp = 0.5
                         else:
@@ -127,19 +136,24 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0):
                         gam = (0.0 if dm + dp == 0.0 else 2 * dm * dp / (dm + dp)) * sigma
                         bnu = b @ nu
                         Phi = bnu * um if bnu >= 0 else bnu * up          # linear in the trial function
-                        nDg = np.einsum("r,rs,spj->pj", nu, D, wm * gm + avg_sign * wp * gp)   # nu.{D grad .}_w
+                        nDg = (wm * np.einsum("r,rs,spj->pj", nu, Dm, gm)
+                               + avg_sign * wp * np.einsum("r,rs,spj->pj", nu, Dp, gp))   # nu.{D grad .}_w
                         jump = um - up
                         # rows: test functions (same combined space), columns: trial functions
                         B = (np.einsum("p,pi,pj->ij", Wf, jump, Phi)
                              - np.einsum("p,pi,pj->ij", Wf, jump, nDg)
                              - np.einsum("p,pi,pj->ij", Wf, nDg, jump)
                              + gam * np.einsum("p,pi,pj->ij", Wf, jump, jump))
-                        idx = np.r_[e * n3:(e + 1) * n3, f * n3:(f + 1) * n3]
-                        A[np.ix_(idx, idx)] += B
+                        # scatter the 2x2 blocks (e == f when a periodic direction has one cell)
+                        for bi, ci in ((0, e), (1, f)):
+                            for bj, cj in ((0, e), (1, f)):
+                                A[ci * n3:(ci + 1) * n3, cj * n3:(cj + 1) * n3] += \
+                                    B[bi * n3:(bi + 1) * n3, bj * n3:(bj + 1) * n3]
                     # boundary faces of this cell in direction q
                     if mask & BOUNDARY:
                         for s in (0, 1):
-                            if (s == 0 and ic[q] == 0) or (s == 1 and ic[q] == nc[q] - 1):
+                            if not periodic[q] and ((s == 0 and ic[q] == 0) or (s == 1 and ic[q] == nc[q] - 1)):
+                                D = Dcell[e]
                                 phs, grs = (phi1, grad1) if s == 1 else (phi0, grad0)
                                 nuo = nu * (1.0 if s == 1 else -1.0)
                                 bnu = b @ nuo

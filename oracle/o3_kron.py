@@ -49,8 +49,9 @@ def ref_1d(n):
     return K, C, t0, t1, d0, d1
 
 
-def line_operator(N, n, h, Dqq, bq, sigma, mask=ALL):
-    """Sparse (N n) x (N n) 1D operator L_q."""
+def line_operator(N, n, h, Dqq, bq, sigma, mask=ALL, periodic=False):
+    """Sparse (N n) x (N n) 1D operator L_q. periodic: the face between cell N-1 (T-) and
+    cell 0 (T+) is an interior face with the same blocks (NEXT-1)."""
     K, C, t0, t1, d0, d1 = ref_1d(n)
     f1, f0 = Dqq * d1 / h, Dqq * d0 / h
     gam = Dqq * sigma
@@ -63,14 +64,15 @@ def line_operator(N, n, h, Dqq, bq, sigma, mask=ALL):
     for e in range(N):
         if mask & VOLUME:
             add(e, e, (Dqq / h) * K - bq * C)
-        if (mask & INTERIOR) and e + 1 < N:
+        if (mask & INTERIOR) and (e + 1 < N or periodic):
             up = 1.0 if bq >= 0 else 0.0
             dn = 1.0 - up
+            e1 = (e + 1) % N
             add(e, e, up * bq * o(t1, t1) - 0.5 * o(t1, f1) - 0.5 * o(f1, t1) + gam * o(t1, t1))
-            add(e, e + 1, dn * bq * o(t1, t0) - 0.5 * o(t1, f0) + 0.5 * o(f1, t0) - gam * o(t1, t0))
-            add(e + 1, e, -up * bq * o(t0, t1) + 0.5 * o(t0, f1) - 0.5 * o(f0, t1) - gam * o(t0, t1))
-            add(e + 1, e + 1, -dn * bq * o(t0, t0) + 0.5 * o(t0, f0) + 0.5 * o(f0, t0) + gam * o(t0, t0))
-    if mask & BOUNDARY:
+            add(e, e1, dn * bq * o(t1, t0) - 0.5 * o(t1, f0) + 0.5 * o(f1, t0) - gam * o(t1, t0))
+            add(e1, e, -up * bq * o(t0, t1) + 0.5 * o(t0, f1) - 0.5 * o(f0, t1) - gam * o(t0, t1))
+            add(e1, e1, -dn * bq * o(t0, t0) + 0.5 * o(t0, f0) + 0.5 * o(f0, t0) + gam * o(t0, t0))
+    if (mask & BOUNDARY) and not periodic:
         fn = -f0
         bl = -bq
         add(0, 0, (bl if bl >= 0 else 0.0) * o(t0, t0) - o(t0, fn) - o(fn, t0) + gam * o(t0, t0))
@@ -88,8 +90,9 @@ def line_operator(N, n, h, Dqq, bq, sigma, mask=ALL):
                          shape=(N * n, N * n))
 
 
-def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL):
-    """y = A z for diagonal D (raises for off-diagonal D). z, y cell-major (C-3)."""
+def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL, periodic=(0, 0, 0)):
+    """y = A z for diagonal D (raises for off-diagonal D). z, y cell-major (C-3).
+    periodic[q]: glue the sides normal to q (NEXT-1)."""
     D = np.asarray(D, dtype=np.float64).reshape(3, 3)
     if np.any(D - np.diag(np.diag(D))):
         raise ValueError("O-3 covers diagonal D only")
@@ -105,7 +108,7 @@ def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL):
     # the other directions give the factor dT / h_q
     lmask = mask & (INTERIOR | BOUNDARY | VOLUME)
     for q, (N, axis) in enumerate(((nx, 2), (ny, 1), (nz, 0))):
-        L = line_operator(N, n, h[q], D[q, q], b[q], sigma, lmask)
+        L = line_operator(N, n, h[q], D[q, q], b[q], sigma, lmask, bool(periodic[q]))
         fac = dT / h[q]
         Zm = np.moveaxis(Z, axis, -1)
         shp = Zm.shape

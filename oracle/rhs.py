@@ -53,11 +53,37 @@ def _cell_points(lo, h, ic, xi):
     return [lo[q] + (ic[q] + xi) * h[q] for q in range(3)]
 
 
-def consistency_data(ncells, lo, hi, k, D, b, c, sigma, seed=0):
-    """Return (z_star, F) for a seeded random u* in Q_k (all boundary faces Dirichlet)."""
+class KinkedField:
+    """u*(x) continuous and piecewise linear in x with a kink at every cell interface
+    x = lo + i h_x; on layer i the slope is F / d_i, so the normal flux d_i du/dx = F is
+    continuous across every face although D jumps (NEXT-1: discontinuous per-cell D).
+    u* lies in Q_1 on each cell, so it is reproduced exactly for every k >= 1."""
+
+    def __init__(self, lo, hx, d_layers, flux, u0):
+        self.lo, self.hx = float(lo), float(hx)
+        self.slope = flux / np.asarray(d_layers, float)
+        self.u_at = u0 + np.concatenate([[0.0], np.cumsum(self.slope * hx)])   # u at the layer starts
+
+    def eval(self, x, y, z, d=(0, 0, 0)):
+        x = np.asarray(x, float)
+        i = np.clip(np.floor((x - self.lo) / self.hx + 1e-12).astype(int), 0, len(self.slope) - 1)
+        if d[1] or d[2] or d[0] > 1:
+            vx = np.zeros_like(x)
+        elif d[0] == 1:
+            vx = self.slope[i]
+        else:
+            vx = self.u_at[i] + self.slope[i] * (x - (self.lo + i * self.hx))
+        return np.broadcast_to(vx[None, None, :], (np.size(z), np.size(y), np.size(x))).copy()
+
+
+def consistency_data(ncells, lo, hi, k, D, b, c, sigma, seed=0, Dcell=None, field=None):
+    """Return (z_star, F) for a seeded random u* in Q_k (all boundary faces Dirichlet).
+
+    Dcell ([ncell, 3, 3], NEXT-1): per-cell tensors for f and the Dirichlet terms of l_h.
+    field: any object with eval(x, y, z, d) (default: PolyField of degree k with `seed`)."""
     nc = [int(v) for v in ncells]
     n = k + 1
-    D = np.asarray(D, float).reshape(3, 3)
+    D0 = np.asarray(D, float).reshape(3, 3)
     b = np.asarray(b, float)
     h = [(hi[q] - lo[q]) / nc[q] for q in range(3)]
     dT = h[0] * h[1] * h[2]
@@ -65,7 +91,7 @@ def consistency_data(ncells, lo, hi, k, D, b, c, sigma, seed=0):
     th, dth = theta(n, xi)          # [point, basis]
     t0, d0 = theta(n, [0.0])
     t1, d1 = theta(n, [1.0])
-    u = PolyField(k, lo, hi, seed)
+    u = PolyField(k, lo, hi, seed) if field is None else field
     ncell = nc[0] * nc[1] * nc[2]
     z = np.zeros((ncell, n, n, n))   # [e][jz][jy][jx]
     F = np.zeros((ncell, n, n, n))
@@ -75,6 +101,7 @@ def consistency_data(ncells, lo, hi, k, D, b, c, sigma, seed=0):
             for ix in range(nc[0]):
                 ic = (ix, iy, iz)
                 e = ix + nc[0] * (iy + nc[1] * iz)
+                D = D0 if Dcell is None else np.asarray(Dcell[e], float).reshape(3, 3)
                 X, Y, Zc = _cell_points(lo, h, ic, xi)
                 us = u.eval(X, Y, Zc)
                 # L2 projection (orthonormal basis, mass = Delta_T I): z_j = (1/Delta_T) int u* phi_j
