@@ -46,7 +46,8 @@ typedef struct dg_ctx dg_ctx;  /* opaque: tables, halo buffers, NCCL communicato
 typedef struct {
     int64_t ncells[3];   /* GLOBAL structured box mesh: cells per direction (>= 1) */
     double  lo[3], hi[3];/* box corners, hi > lo; uniform cuboid cells h_q = (hi-lo)/ncells */
-    int     bc[6];       /* per side (x-,x+,y-,y+,z-,z+): DG_BC_DIRICHLET only (periodic: later) */
+    int     bc[6];       /* per side (x-,x+,y-,y+,z-,z+): DG_BC_DIRICHLET or DG_BC_PERIODIC
+                            (periodic must be set on both sides of a direction) */
     int     parts[3];    /* rank grid Px,Py,Pz; product == nranks; each must divide ncells */
 } dg_mesh_desc;
 
@@ -58,18 +59,28 @@ enum { DG_VOLUME = 1, DG_INTERIOR_FACES = 2, DG_BOUNDARY_FACES = 4, DG_ALL = 7,
           skip the pack + NCCL exchange. Used by single-process loopback tests. */
        DG_HALO_EXTERNAL = 0x100 };
 
-enum { DG_BC_DIRICHLET = 0 };
+/* Boundary conditions per box side.
+ *   DG_BC_DIRICHLET: weak Dirichlet with g = 0 inside A (reading C-9; g enters only f).
+ *   DG_BC_PERIODIC : the two sides of a direction are glued; the wrap face between the last
+ *                    and the first cell layer is an interior face with nu = +e_q, treated like
+ *                    a processor boundary (the paper's benchmark setting;
+ *                    DESIGN.md reading N-1). Split over ranks, the wrap neighbour is the rank
+ *                    at the other end of the rank grid. */
+enum { DG_BC_DIRICHLET = 0, DG_BC_PERIODIC = 1 };
 
 /*
  * Create a context on CUDA device `device` for rank `rank` of `nranks`.
  *   k      polynomial degree, 1 <= k <= 10 (n = k+1 basis functions and Gauss points per direction)
  *   D      3x3 row-major diffusion tensor, symmetric positive semi-definite
- *          (D = 0 is accepted: the mass-matrix invariant); off-diagonal D -> DG_EUNSUPPORTED (v1)
+ *          (D = 0 is accepted: the mass-matrix invariant). A diagonal D runs on the fused
+ *          constant-coefficient kernel; a full D (off-diagonal entries, PAPER.md:202-205, :436;
+ *          reading C-16) on the general-coefficient kernel (dg_set_diffusion)
  *   b      constant velocity (div b = 0), c reaction coefficient, sigma >= 0 penalty factor
  *   nccl_unique_id  128-byte ncclUniqueId broadcast by the caller; NULL iff nranks == 1
  *                   or iff the caller drives the halo itself (DG_HALO_EXTERNAL)
- * Errors: DG_EINVAL (k, mesh, D not symmetric / negative diagonal, sigma < 0, parts),
- *         DG_EUNSUPPORTED (bc != Dirichlet, off-diagonal D), DG_ECUDA, DG_ENCCL, DG_ENOMEM.
+ * Errors: DG_EINVAL (k, mesh, D not symmetric / negative diagonal, sigma < 0, parts, periodic
+ *         on one side of a direction only), DG_EUNSUPPORTED (unknown bc),
+ *         DG_ECUDA, DG_ENCCL, DG_ENOMEM.
  * Not timed; uploads tables and allocates the halo buffers.
  */
 int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const double D[9], const double b[3],
@@ -103,13 +114,30 @@ int dg_sync(dg_ctx* ctx);
 int dg_destroy(dg_ctx* ctx);
 const char* dg_strerror(int code);
 
+/* Per-cell diffusion tensors (NEXT-1: the paper's Problem A, "tensor-valued diffusion
+ * coefficients ... constant per cell ... weighted averaging across cell boundaries for
+ * discontinuous coefficients"). Dcell: caller-owned DEVICE array of this
+ * rank's local cells x 9 doubles (row-major 3x3, symmetric PSD), local cell order (C-3);
+ * the library copies it (6 unique entries per cell) and, with nranks > 1, exchanges the
+ * partition-layer tensors with the neighbour ranks (collective; skipped with
+ * flags = DG_HALO_EXTERNAL: the caller then fills the receive layers, dg_halo_buffer
+ * which = 3). On a face the tensors D-, D+ of its two cells give delta = nu^T D nu per side,
+ * the weights w- = d+/(d- + d+), w+ = d-/(d- + d+) and the penalty
+ * gamma = <d-, d+> sigma. Subsequent applies use the
+ * general-coefficient kernel. Dcell = NULL reverts to the constant D of dg_setup.
+ * Synchronous on `stream`. Errors: DG_EINVAL (non-symmetric / non-finite / negative diagonal
+ * entry, bad flags), DG_ENOMEM, DG_ECUDA, DG_ENCCL. Not timed. */
+int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags, void* stream);
+
 /* ---- halo plumbing (multi-rank; also used by the single-process loopback test) ----
  * face f = 2q + s (q = direction, s = 0 low / 1 high side of this rank's box).
  * neighbor_rank = -1 when the face lies on the domain boundary. count = doubles in the
  * layer (cells of the face layer x n^3). */
 int dg_halo_info(const dg_ctx* ctx, int face, int* neighbor_rank, int64_t* count);
 /* which = 0: send buffer (this rank's own boundary layer, filled by dg_halo_pack),
-   which = 1: receive buffer (the neighbour's layer adjacent to this face, read by the kernel). */
+   which = 1: receive buffer (the neighbour's layer adjacent to this face, read by the kernel),
+   which = 2 / 3: the same for the per-cell diffusion field (6 doubles per layer cell;
+   count / n^3 * 6 doubles; allocated by dg_set_diffusion, NULL before). */
 int dg_halo_buffer(dg_ctx* ctx, int face, int which, double** ptr);
 int dg_halo_pack(dg_ctx* ctx, const double* z, void* stream);
 

@@ -21,6 +21,7 @@ class Config:
     sigma: float
     seed: int
     parts: Tuple[int, int, int] = (1, 1, 1)
+    periodic: Tuple[int, int, int] = (0, 0, 0)
 
     @property
     def n3(self):

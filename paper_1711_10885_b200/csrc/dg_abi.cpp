@@ -17,6 +17,7 @@ using namespace dg;
 struct dg_ctx {
     int device = 0, rank = 0, nranks = 1, k = 1, n = 2, n3 = 8;
     int parts[3] = {1, 1, 1}, pc[3] = {0, 0, 0};
+    int per[3] = {0, 0, 0};
     int64_t nloc[3] = {0, 0, 0}, gofs[3] = {0, 0, 0}, gcells[3] = {0, 0, 0};
     int64_t ndofs = 0;
     int nbr[6] = {-1, -1, -1, -1, -1, -1};
@@ -32,6 +33,13 @@ struct dg_ctx {
     ncclComm_t comm = nullptr;
     double* hz = nullptr;            // device staging for dg_apply_host
     double* hy = nullptr;
+    // general-coefficient path (full / per-cell D, dg_gen.cuh)
+    bool general = false;            // launch dg_gen_kernel instead of dg_cell_kernel
+    double Dconst[9] = {0};          // the tensor given to dg_setup
+    double* dfield = nullptr;        // [local cell][6]
+    double* dsend[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    double* drecv[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int* dbad = nullptr;             // validation flag of dg_set_diffusion
     KParams base;
 };
 
@@ -68,6 +76,12 @@ static void free_ctx(dg_ctx* c)
         if (c->recvbuf[f]) cudaFree(c->recvbuf[f]);
     }
     if (c->shell) cudaFree(c->shell);
+    if (c->dfield) cudaFree(c->dfield);
+    if (c->dbad) cudaFree(c->dbad);
+    for (int f = 0; f < 6; ++f) {
+        if (c->dsend[f]) cudaFree(c->dsend[f]);
+        if (c->drecv[f]) cudaFree(c->drecv[f]);
+    }
     if (c->hz) cudaFree(c->hz);
     if (c->hy) cudaFree(c->hy);
     if (c->comm) {
@@ -115,10 +129,9 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
     }
     if (!std::isfinite(c) || !std::isfinite(sigma) || sigma < 0.0) return DG_EINVAL;
     for (int f = 0; f < 6; ++f)
-        if (mesh->bc[f] != DG_BC_DIRICHLET) return DG_EUNSUPPORTED;
-    for (int r = 0; r < 3; ++r)
-        for (int s = 0; s < 3; ++s)
-            if (r != s && D[3 * r + s] != 0.0) return DG_EUNSUPPORTED;   // full D: not in v1
+        if (mesh->bc[f] != DG_BC_DIRICHLET && mesh->bc[f] != DG_BC_PERIODIC) return DG_EUNSUPPORTED;
+    for (int q = 0; q < 3; ++q)   // periodic glues the two sides of a direction: both or neither
+        if ((mesh->bc[2 * q] == DG_BC_PERIODIC) != (mesh->bc[2 * q + 1] == DG_BC_PERIODIC)) return DG_EINVAL;
 
     dg_ctx* ctx = new (std::nothrow) dg_ctx();
     if (!ctx) return DG_ENOMEM;
@@ -153,12 +166,16 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
         ctx->gofs[q] = ctx->nloc[q] * ctx->pc[q];
     }
     ctx->ndofs = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2] * (int64_t)ctx->n3;
+    for (int q = 0; q < 3; ++q) ctx->per[q] = mesh->bc[2 * q] == DG_BC_PERIODIC;
     for (int q = 0; q < 3; ++q)
         for (int s = 0; s < 2; ++s) {
             int pcn[3] = {ctx->pc[0], ctx->pc[1], ctx->pc[2]};
             pcn[q] += s ? 1 : -1;
             const int f = 2 * q + s;
-            if (pcn[q] >= 0 && pcn[q] < ctx->parts[q]) {
+            // periodic and split along q: the wrap neighbour is the rank at the other end;
+            // periodic and not split: the wrap is local to this rank (KParams::wrap)
+            if (ctx->per[q] && ctx->parts[q] > 1) pcn[q] = (pcn[q] + ctx->parts[q]) % ctx->parts[q];
+            if (pcn[q] >= 0 && pcn[q] < ctx->parts[q] && !(ctx->per[q] && ctx->parts[q] == 1)) {
                 ctx->nbr[f] = pcn[0] + ctx->parts[0] * (pcn[1] + ctx->parts[1] * pcn[2]);
                 ctx->partitioned = true;
             }
@@ -180,7 +197,11 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
         p.bq[q] = b[q];
         p.Dqq_h[q] = D[4 * q] / h[q];
         p.gam[q] = D[4 * q] * sigma;     // <delta, delta> = delta for constant D
+        p.per[q] = ctx->per[q];
+        p.wrap[q] = ctx->per[q] && ctx->parts[q] == 1;
+        p.h[q] = h[q];
     }
+    p.sigma = sigma;
     for (int r = 0; r < 3; ++r)
         for (int s = 0; s < 3; ++s) p.Dhat[3 * r + s] = D[3 * r + s] / (h[r] * h[s]);
     p.c = c;
@@ -245,7 +266,97 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
         for (int q = 0; q < 3; ++q) { ctx->inner_lo[q] = 0; ctx->inner_cnt[q] = ctx->nloc[q]; }
     }
     for (int f = 0; f < 6; ++f) p.ghost[f] = ctx->recvbuf[f];
+    for (int i = 0; i < 9; ++i) ctx->Dconst[i] = D[i];
+    // a full (off-diagonal) constant tensor runs on the general-coefficient kernel with a
+    // constant per-cell field; a diagonal one on the fast kernel
+    bool offdiag = false;
+    for (int r = 0; r < 3; ++r)
+        for (int s = 0; s < 3; ++s)
+            if (r != s && D[3 * r + s] != 0.0) offdiag = true;
+    if (offdiag) {
+        int rc = dg_set_diffusion(ctx, nullptr, 0, nullptr);
+        if (rc == DG_OK) rc = cuda_rc(cudaStreamSynchronize(nullptr));
+        if (rc != DG_OK) { free_ctx(ctx); return rc; }
+    }
     *out = ctx;
+    return DG_OK;
+}
+
+static int alloc_dfield(dg_ctx* ctx)
+{
+    const int64_t ncell = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2];
+    if (!ctx->dfield && cudaMalloc(&ctx->dfield, (size_t)ncell * 6 * sizeof(double)) != cudaSuccess) return DG_ENOMEM;
+    if (!ctx->dbad && cudaMalloc(&ctx->dbad, sizeof(int)) != cudaSuccess) return DG_ENOMEM;
+    for (int f = 0; f < 6; ++f) {
+        if (ctx->nbr[f] < 0 || ctx->dsend[f]) continue;
+        const size_t bytes = (size_t)(ctx->halo_count[f] / ctx->n3) * 6 * sizeof(double);
+        if (cudaMalloc(&ctx->dsend[f], bytes) != cudaSuccess || cudaMalloc(&ctx->drecv[f], bytes) != cudaSuccess)
+            return DG_ENOMEM;
+    }
+    KParams& p = ctx->base;
+    p.Dfield = ctx->dfield;
+    for (int f = 0; f < 6; ++f) p.Dghost[f] = ctx->drecv[f];
+    return DG_OK;
+}
+
+extern "C" int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags, void* stream)
+{
+    if (!ctx || (flags & ~(unsigned)DG_HALO_EXTERNAL)) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t ncell = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2];
+    bool offdiag = false;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+            if (r != c && ctx->Dconst[3 * r + c] != 0.0) offdiag = true;
+    if (!Dcell && !offdiag) {          // back to the constant diagonal tensor of dg_setup
+        ctx->general = false;
+        return DG_OK;
+    }
+    int rc = alloc_dfield(ctx);
+    if (rc != DG_OK) return rc;
+    if (!Dcell) {
+        // constant tensor: field and neighbour layers are the same constant (no exchange)
+        DG_CUDA(launch_dfield_const(ctx->dfield, ctx->Dconst, ncell, s));
+        for (int f = 0; f < 6; ++f)
+            if (ctx->drecv[f])
+                DG_CUDA(launch_dfield_const(ctx->drecv[f], ctx->Dconst, ctx->halo_count[f] / ctx->n3, s));
+        ctx->general = true;
+        return DG_OK;
+    }
+    DG_CUDA(cudaMemsetAsync(ctx->dbad, 0, sizeof(int), s));
+    DG_CUDA(launch_dfield_pack(Dcell, ctx->dfield, ctx->dbad, ncell, s));
+    int bad = 0;
+    DG_CUDA(cudaMemcpyAsync(&bad, ctx->dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DG_CUDA(cudaStreamSynchronize(s));
+    if (bad) return DG_EINVAL;
+    if (ctx->partitioned) {
+        // the neighbour ranks' boundary layers of the field (setup-time, synchronous)
+        for (int f = 0; f < 6; ++f)
+            if (ctx->nbr[f] >= 0) DG_CUDA(launch_pack(ctx->dfield, ctx->dsend[f], 6, ctx->nloc, f, s));
+        if (!(flags & DG_HALO_EXTERNAL)) {
+            if (!ctx->comm) return DG_ENCCL;
+            const NcclApi* api = nccl_api();
+            if (!api) return DG_ENCCL;
+            if (api->ncclGroupStart() != 0) return DG_ENCCL;
+            for (int f = 0; f < 6; ++f) {   // same pairing rule as the z halo (send f, receive f^1)
+                const int fr = f ^ 1;
+                if (ctx->nbr[f] >= 0 && api->ncclSend(ctx->dsend[f], (size_t)(ctx->halo_count[f] / ctx->n3) * 6,
+                                                      dgNcclFloat64, ctx->nbr[f], ctx->comm, s) != 0) {
+                    api->ncclGroupEnd();
+                    return DG_ENCCL;
+                }
+                if (ctx->nbr[fr] >= 0 && api->ncclRecv(ctx->drecv[fr], (size_t)(ctx->halo_count[fr] / ctx->n3) * 6,
+                                                       dgNcclFloat64, ctx->nbr[fr], ctx->comm, s) != 0) {
+                    api->ncclGroupEnd();
+                    return DG_ENCCL;
+                }
+            }
+            if (api->ncclGroupEnd() != 0) return DG_ENCCL;
+        }
+        DG_CUDA(cudaStreamSynchronize(s));
+    }
+    ctx->general = true;
     return DG_OK;
 }
 
@@ -264,10 +375,12 @@ extern "C" int dg_partition(const dg_mesh_desc* mesh, int rank, int nranks, int6
         const int64_t nl = mesh->ncells[q] / mesh->parts[q];
         if (cell_lo) cell_lo[q] = nl * pc[q];
         if (cell_cnt) cell_cnt[q] = nl;
+        const bool per = mesh->bc[2 * q] == DG_BC_PERIODIC;
         for (int s = 0; s < 2; ++s) {
             int pn[3] = {pc[0], pc[1], pc[2]};
             pn[q] += s ? 1 : -1;
-            if (nbr) nbr[2 * q + s] = (pn[q] >= 0 && pn[q] < mesh->parts[q])
+            if (per && mesh->parts[q] > 1) pn[q] = (pn[q] + mesh->parts[q]) % mesh->parts[q];
+            if (nbr) nbr[2 * q + s] = (pn[q] >= 0 && pn[q] < mesh->parts[q] && !(per && mesh->parts[q] == 1))
                                           ? pn[0] + mesh->parts[0] * (pn[1] + mesh->parts[1] * pn[2]) : -1;
         }
     }
@@ -301,7 +414,7 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         p.task_list = nullptr;
         for (int q = 0; q < 3; ++q) { p.task_lo[q] = 0; p.task_cnt[q] = ctx->nloc[q]; }
         p.ntasks = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2];
-        return cuda_rc(launch_cell(ctx->k, p, s));
+        return cuda_rc(ctx->general ? launch_gen(ctx->k, p, s) : launch_cell(ctx->k, p, s));
     }
     // (iv) of SURVEY.md 3: pack partition layers, exchange on the comm stream, overlap with inner cells
     const bool need_comm = !external && (p.mask & DG_INTERIOR_FACES);
@@ -314,11 +427,19 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         DG_CUDA(cudaEventRecord(ctx->ev_packed, s));
         DG_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
         if (api->ncclGroupStart() != 0) return DG_ENCCL;
+        // Per peer, NCCL matches sends and receives in issue order. My layer of face fc lands in the
+        // peer's receive buffer of face fc^1, so receives are issued in the order fc^1: with two ranks
+        // along a periodic direction both faces talk to the same peer and this keeps them paired.
         for (int fc = 0; fc < 6; ++fc) {
-            if (ctx->nbr[fc] < 0) continue;
-            if (api->ncclSend(ctx->sendbuf[fc], (size_t)ctx->halo_count[fc], dgNcclFloat64, ctx->nbr[fc], ctx->comm,
-                              ctx->comm_stream) != 0 ||
-                api->ncclRecv(ctx->recvbuf[fc], (size_t)ctx->halo_count[fc], dgNcclFloat64, ctx->nbr[fc], ctx->comm,
+            const int fr = fc ^ 1;
+            if (ctx->nbr[fc] >= 0 &&
+                api->ncclSend(ctx->sendbuf[fc], (size_t)ctx->halo_count[fc], dgNcclFloat64, ctx->nbr[fc], ctx->comm,
+                              ctx->comm_stream) != 0) {
+                api->ncclGroupEnd();
+                return DG_ENCCL;
+            }
+            if (ctx->nbr[fr] >= 0 &&
+                api->ncclRecv(ctx->recvbuf[fr], (size_t)ctx->halo_count[fr], dgNcclFloat64, ctx->nbr[fr], ctx->comm,
                               ctx->comm_stream) != 0) {
                 api->ncclGroupEnd();
                 return DG_ENCCL;
@@ -331,11 +452,14 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
     p.task_list = nullptr;
     for (int q = 0; q < 3; ++q) { p.task_lo[q] = ctx->inner_lo[q]; p.task_cnt[q] = ctx->inner_cnt[q]; }
     p.ntasks = ctx->inner_cnt[0] * ctx->inner_cnt[1] * ctx->inner_cnt[2];
-    DG_CUDA(launch_cell(ctx->k, p, s));
+    auto launch = [&](const KParams& kp) {
+        return ctx->general ? launch_gen(ctx->k, kp, s) : launch_cell(ctx->k, kp, s);
+    };
+    DG_CUDA(launch(p));
     if (need_comm) DG_CUDA(cudaStreamWaitEvent(s, ctx->ev_recv, 0));
     p.task_list = ctx->shell;
     p.ntasks = ctx->nshell;
-    return cuda_rc(launch_cell(ctx->k, p, s));
+    return cuda_rc(launch(p));
 }
 
 extern "C" int dg_apply(dg_ctx* ctx, const double* z, double* y, void* stream)
@@ -407,8 +531,9 @@ extern "C" int dg_halo_info(const dg_ctx* ctx, int face, int* neighbor_rank, int
 
 extern "C" int dg_halo_buffer(dg_ctx* ctx, int face, int which, double** ptr)
 {
-    if (!ctx || face < 0 || face > 5 || (which != 0 && which != 1) || !ptr) return DG_EINVAL;
-    *ptr = which ? ctx->recvbuf[face] : ctx->sendbuf[face];
+    if (!ctx || face < 0 || face > 5 || which < 0 || which > 3 || !ptr) return DG_EINVAL;
+    *ptr = which == 0 ? ctx->sendbuf[face] : which == 1 ? ctx->recvbuf[face]
+         : which == 2 ? ctx->dsend[face] : ctx->drecv[face];
     return DG_OK;
 }
 

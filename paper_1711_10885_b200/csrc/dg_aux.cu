@@ -78,3 +78,53 @@ cudaError_t launch_fill_uniform_local(double* dst, int n3, const int64_t nloc[3]
 }
 
 }  // namespace dg
+
+namespace dg {
+
+// Per-cell tensors [cell][9] (row-major) -> [cell][6] = D00 D11 D22 D01 D02 D12 with
+// validation: symmetric, finite, nonnegative diagonal (PSD necessary conditions); *bad != 0
+// on violation (dg_set_diffusion returns DG_EINVAL).
+__global__ void dfield_pack_kernel(const double* __restrict__ D9, double* __restrict__ D6, int* bad, int64_t ncell)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncell; e += (int64_t)gridDim.x * blockDim.x) {
+        const double* d = D9 + 9 * e;
+        bool ok = true;
+        for (int i = 0; i < 9; ++i) ok = ok && isfinite(d[i]);
+        ok = ok && d[1] == d[3] && d[2] == d[6] && d[5] == d[7] && d[0] >= 0.0 && d[4] >= 0.0 && d[8] >= 0.0;
+        if (!ok) atomicOr(bad, 1);
+        double* o = D6 + 6 * e;
+        o[0] = d[0]; o[1] = d[4]; o[2] = d[8]; o[3] = d[1]; o[4] = d[2]; o[5] = d[5];
+    }
+}
+
+__global__ void dfield_const_kernel(double* __restrict__ D6, double d0, double d1, double d2, double d3, double d4,
+                                    double d5, int64_t ncell)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncell; e += (int64_t)gridDim.x * blockDim.x) {
+        double* o = D6 + 6 * e;
+        o[0] = d0; o[1] = d1; o[2] = d2; o[3] = d3; o[4] = d4; o[5] = d5;
+    }
+}
+
+static unsigned blocks_for(int64_t n)
+{
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    return (unsigned)(b > 0 ? b : 1);
+}
+
+cudaError_t launch_dfield_pack(const double* D9, double* D6, int* bad, int64_t ncell, cudaStream_t s)
+{
+    if (ncell == 0) return cudaSuccess;
+    dfield_pack_kernel<<<blocks_for(ncell), 256, 0, s>>>(D9, D6, bad, ncell);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dfield_const(double* D6, const double D[9], int64_t ncell, cudaStream_t s)
+{
+    if (ncell == 0) return cudaSuccess;
+    dfield_const_kernel<<<blocks_for(ncell), 256, 0, s>>>(D6, D[0], D[4], D[8], D[1], D[2], D[5], ncell);
+    return cudaGetLastError();
+}
+
+}  // namespace dg

@@ -47,6 +47,7 @@ struct Tab {
     double w[N];
     double L[6][4][N];       // per use site: L_l(0), L_l(1), L'_l(0), L'_l(1)
     double th0[N], th1[N], dth0[N], dth1[N];
+    double Gh[HC][N];        // G_ij = theta'_j(xi_i), rows i < ceil(n/2) (general kernel, even-odd)
     // even-odd forms used by the roles (one copy per direction):
     EO<N> DcTw[3];                         // Dc^T diag(w): Gauss weights folded into the transposed stage
     double Le[3][4][(N / 2) > 0 ? N / 2 : 1];  // (L0_i +- L0_{n-1-i})/2, (L'0_i +- L'0_{n-1-i})/2, i < n/2
@@ -286,8 +287,9 @@ __device__ __forceinline__ void nb_load(const KParams& p, const double* zc, cons
     const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
                                                                         : (lc[0] + p.nloc[0] * lc[1]);
     const bool hl = (nbmask >> (2 * q)) & 1u, hh = (nbmask >> (2 * q + 1)) & 1u;
-    const double* zl = (lq > 0) ? zc - st * n3 : (hl ? p.ghost[2 * q] + gi * n3 : zc);
-    const double* zh = (lq + 1 < nq) ? zc + st * n3 : (hh ? p.ghost[2 * q + 1] + gi * n3 : zc);
+    const int64_t wst = (int64_t)(nq - 1) * st * n3;   // periodic wrap inside this rank's box
+    const double* zl = (lq > 0) ? zc - st * n3 : (p.wrap[q] ? zc + wst : (hl ? p.ghost[2 * q] + gi * n3 : zc));
+    const double* zh = (lq + 1 < nq) ? zc + st * n3 : (p.wrap[q] ? zc - wst : (hh ? p.ghost[2 * q + 1] + gi * n3 : zc));
 #pragma unroll
     for (int k = 0; k < P; ++k) {
         if (q == 0 && N % 2 == 0) {
@@ -645,7 +647,7 @@ dg_cell_kernel(const KParams p)
     for (int f = 0; f < 6; ++f) {
         const int q = f >> 1, s = f & 1;
         const int64_t g = p.gofs[q] + lc[q] + (s ? 1 : -1);
-        if (g >= 0 && g < p.gcells[q]) nbmask |= 1u << f;
+        if (p.per[q] || (g >= 0 && g < p.gcells[q])) nbmask |= 1u << f;
     }
     const unsigned nbi = do_int ? nbmask : 0u;   // neighbours whose traces are needed
 

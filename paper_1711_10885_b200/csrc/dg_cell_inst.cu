@@ -1,6 +1,7 @@
 // One translation unit per basis size n = k+1 (compiled with -DDG_N=n): the
 // fused cell kernel instantiation, its __constant__ table upload and launcher.
 #include "dg_cell.cuh"
+#include "dg_gen.cuh"
 #if DG_N == 8
 #include "dg_mma8.cuh"
 #endif
@@ -37,6 +38,8 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
     for (int c = 0; c < 12; ++c)
         for (int i = 0; i < Tab<N>::HC; ++i)
             for (int j = 0; j < N; ++j) h.Vh[c][i][j] = t.V[i][j];
+    for (int i = 0; i < Tab<N>::HC; ++i)
+        for (int j = 0; j < N; ++j) h.Gh[i][j] = t.G[i][j];
     for (int c = 0; c < 6; ++c) {
         fill_eo<N>(h.Dc[c], t.Dc, false);
         fill_eo<N>(h.DcT[c], t.Dc, true);
@@ -121,7 +124,7 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
     int dev = 0;
     cudaGetDevice(&dev);
 #if DG_N == 8
-    if (use_mma()) {
+    if (use_mma() && !(p.per[0] | p.per[1] | p.per[2])) {   // the DMMA variant has no periodic wrap
         static int done[64];
         constexpr int BYTES = m8::C * m8::PER_CELL * 8;
         if (dev >= 0 && dev < 64 && !done[dev]) {
@@ -142,6 +145,27 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
     }
     const int64_t grid = (p.ntasks + C - 1) / C;
     dg_cell_kernel<N><<<(unsigned)grid, THREADS, Smem<N>::BYTES, s>>>(p);
+    return cudaGetLastError();
+}
+
+static int g_gen_attr_done[64];
+
+// general-coefficient kernel (full / per-cell D; dg_gen.cuh)
+cudaError_t DG_CAT(launch_gen_n, DG_N)(const KParams& p, cudaStream_t s)
+{
+    constexpr int N = DG_N;
+    constexpr int C = Cfg<N>::C;
+    if (p.ntasks <= 0) return cudaSuccess;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !g_gen_attr_done[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(dg_gen_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             GSmem<N>::BYTES);
+        if (e != cudaSuccess) return e;
+        g_gen_attr_done[dev] = 1;
+    }
+    const int64_t grid = (p.ntasks + C - 1) / C;
+    dg_gen_kernel<N><<<(unsigned)grid, C * Cfg<N>::TPC, GSmem<N>::BYTES, s>>>(p);
     return cudaGetLastError();
 }
 

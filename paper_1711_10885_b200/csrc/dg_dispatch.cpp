@@ -6,6 +6,7 @@ namespace dg {
 #define DG_DECL(n)                                            \
     int upload_tables_n##n(const HostTables&);                \
     cudaError_t launch_cell_n##n(const KParams&, cudaStream_t); \
+    cudaError_t launch_gen_n##n(const KParams&, cudaStream_t);  \
     int cell_info_n##n(LaunchInfo*);
 DG_DECL(2) DG_DECL(3) DG_DECL(4) DG_DECL(5) DG_DECL(6) DG_DECL(7) DG_DECL(8) DG_DECL(9) DG_DECL(10) DG_DECL(11)
 
@@ -28,6 +29,13 @@ cudaError_t launch_cell(int k, const KParams& p, cudaStream_t s)
 {
 #define DG_LA(n) launch_cell_n##n(p, s)
     DG_CASES(DG_LA)
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gen(int k, const KParams& p, cudaStream_t s)
+{
+#define DG_LG(n) launch_gen_n##n(p, s)
+    DG_CASES(DG_LG)
     return cudaErrorInvalidValue;
 }
 

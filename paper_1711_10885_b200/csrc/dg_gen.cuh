@@ -1,0 +1,506 @@
+// General-coefficient cell kernel: y = A z for the WSIPG operator of arXiv 1711.10885 with
+// a FULL symmetric diffusion tensor per cell (the paper's Problem A: "tensor-valued
+// diffusion coefficients", "constant per cell", "weighted averaging across cell boundaries
+// for discontinuous coefficients"), FP64, sm_100a.
+//
+// What changes against dg_cell_kernel (constant diagonal D):
+//   * volume: the flux x^(r) = W (sum_s D_rs/(h_r h_s) d_s u - b_r/h_r u) couples the three
+//     reference derivatives at every Gauss point (eq:gauss_points), so the
+//     gradient is formed first (collocation derivatives Dc along x, y, z into three arrays),
+//     the pointwise flux second and the transposed stages Dc_r^T last (eq:evalblf :425-444);
+//   * faces: nu.D grad u = D_qq d_q u + D_qt1 d_t1 u + D_qt2 d_t2 u needs tangential
+//     derivatives of both traces: on the neighbour side the face sum
+//     factorization (normal first, :623-627) runs its tangential stages with V and G
+//     (G_ij = theta'_j(xi_i)); on the own side Dc is applied along the face lines to the
+//     extrapolated trace;
+//   * weights w-+ = d+-/(d- + d+), penalty gamma = <d-, d+> sigma with d = nu^T D nu of each
+//     side (reading C-5 for d- + d+ = 0);
+//   * the test-gradient term -w J nu.D grad(phi) (eq:blf :312) lifts its normal part with
+//     L'(s) along the normal and its tangential parts with Dc^T along the face lines, into
+//     the quadrature-space accumulator before the V^T stages (normal direction LAST).
+// Each cell still writes only its own y block once (owner computes, no atomics).
+#pragma once
+#include "dg_cell.cuh"
+
+namespace dg {
+
+// index of D_rs in the 6-vector D00 D11 D22 D01 D02 D12
+__host__ __device__ __forceinline__ constexpr int dsym(int r, int s)
+{
+    return r == s ? r : (r + s == 1 ? 3 : (r + s == 2 ? 4 : 5));
+}
+
+// t[i] = sum_j G_ij r[j] (G_{n-1-i,j} = (-1)^(j+1) G_ij: even-odd form)
+template <int N>
+__device__ __forceinline__ void g_fwd(const double (&Gh)[(N + 1) / 2][N], const double (&r)[N], double (&t)[N])
+{
+    constexpr int H = N / 2;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        double E = 0.0, O = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (j & 1) O = fma(Gh[i][j], r[j], O);
+            else E = fma(Gh[i][j], r[j], E);
+        }
+        t[i] = E + O;
+        t[N - 1 - i] = O - E;
+    }
+    if (N & 1) {
+        double O = 0.0;
+#pragma unroll
+        for (int j = 1; j < N; j += 2) O = fma(Gh[H][j], r[j], O);
+        t[H] = O;
+    }
+}
+
+// pointer to the 6-vector D of the neighbour across face f (nullptr: no neighbour)
+__device__ __forceinline__ const double* nb_dfield(const KParams& p, const int lc[3], int f, unsigned nbmask)
+{
+    if (!((nbmask >> f) & 1u)) return nullptr;
+    const int q = f >> 1, s = f & 1;
+    const int nq = (int)p.nloc[q];
+    int l[3] = {lc[0], lc[1], lc[2]};
+    const int lq = lc[q] + (s ? 1 : -1);
+    if (lq >= 0 && lq < nq) {
+        l[q] = lq;
+    } else if (p.wrap[q]) {
+        l[q] = (lq < 0) ? nq - 1 : 0;
+    } else {
+        const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
+                                                                            : (lc[0] + p.nloc[0] * lc[1]);
+        return p.Dghost[f] + 6 * gi;
+    }
+    return p.Dfield + 6 * (l[0] + p.nloc[0] * (l[1] + p.nloc[1] * (int64_t)l[2]));
+}
+
+template <int N>
+struct GSmem {
+    static constexpr int PER_CELL = 4 * Lay<N>::SLOT + 2 * FLay<N>::SLOT;
+    static constexpr int BYTES = Cfg<N>::C * PER_CELL * 8;
+};
+
+template <int N>
+__global__ void __launch_bounds__(Cfg<N>::C * Cfg<N>::TPC)
+dg_gen_kernel(const KParams p)
+{
+    constexpr int TPC = Cfg<N>::TPC, P = Cfg<N>::P, C = Cfg<N>::C;
+    constexpr int NN = N * N;
+    static_assert(TPC * P >= NN, "pencil slots");
+    static_assert(TPC <= 32 || C == 1, "multi-warp cells use CTA barriers: one cell per CTA");
+    extern __shared__ double smem[];
+    const Tab<N>& T = g_tab;
+
+    const int tid = threadIdx.x;
+    const int slot = tid / TPC;
+    const int lane = tid - slot * TPC;
+    double* A0 = smem + slot * GSmem<N>::PER_CELL;   // u, then the quadrature-space accumulator
+    double* X0 = A0 + Lay<N>::SLOT;                  // d_x u -> x^(1)   (also a stage temporary)
+    double* X1 = X0 + Lay<N>::SLOT;                  // d_y u -> x^(2)
+    double* X2 = X1 + Lay<N>::SLOT;                  // d_z u -> x^(3)
+    double* NT = X2 + Lay<N>::SLOT;                  // neighbour face arrays (2 per face)
+    double* OT = NT + FLay<N>::SLOT;                 // own face arrays (2 per face)
+    auto csync = [&]() {
+        if (TPC <= 32) __syncwarp(); else __syncthreads();
+    };
+
+    unsigned task = blockIdx.x * (unsigned)C + (unsigned)slot;
+    const bool valid = task < (unsigned)p.ntasks;
+    if (!valid) task = (unsigned)p.ntasks - 1u;
+    int lc[3];
+    {
+        const unsigned e = p.task_list ? (unsigned)p.task_list[task] : 0u;
+        if (p.task_list) {
+            const unsigned nx = (unsigned)p.nloc[0], ny = (unsigned)p.nloc[1];
+            lc[0] = (int)(e % nx);
+            lc[1] = (int)((e / nx) % ny);
+            lc[2] = (int)(e / (nx * ny));
+        } else {
+            const unsigned nz = (unsigned)p.task_cnt[2], nx = (unsigned)p.task_cnt[0], ny = (unsigned)p.task_cnt[1];
+            const unsigned TX = (unsigned)p.tile[0], TY = (unsigned)p.tile[1];
+            const unsigned col = task / nz;
+            const unsigned ty = col / (TY * nx);
+            const unsigned wy = min(TY, ny - ty * TY);
+            const unsigned cr = col - ty * TY * nx;
+            const unsigned tx = cr / (TX * wy);
+            const unsigned wx = min(TX, nx - tx * TX);
+            const unsigned ci = cr - tx * TX * wy;
+            lc[0] = (int)(p.task_lo[0] + tx * TX + ci % wx);
+            lc[1] = (int)(p.task_lo[1] + ty * TY + ci / wx);
+            lc[2] = (int)(p.task_lo[2] + (task - col * nz));
+        }
+    }
+    const int64_t n3 = (int64_t)NN * N;
+    const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * (int64_t)lc[2]);
+    const double* zc = p.z + cell * n3;
+    const bool do_int = (p.mask & 2u) != 0, do_bnd = (p.mask & 4u) != 0, do_vol = (p.mask & 1u) != 0;
+
+    unsigned nbmask = 0;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+        const int q = f >> 1, s = f & 1;
+        const int64_t g = p.gofs[q] + lc[q] + (s ? 1 : -1);
+        if (p.per[q] || (g >= 0 && g < p.gcells[q])) nbmask |= 1u << f;
+    }
+    const unsigned nbi = do_int ? nbmask : 0u;                   // neighbour traces needed
+    const unsigned fact = (do_int ? nbmask : 0u) | (do_bnd ? (~nbmask & 63u) : 0u);   // faces with a term
+    double Dw[6];                                                // this cell's tensor
+#pragma unroll
+    for (int i = 0; i < 6; ++i) Dw[i] = __ldg(p.Dfield + 6 * cell + i);
+
+    int pa[P], pb[P];
+    bool act[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const int pc = lane + k * TPC;
+        act[k] = pc < NN;
+        const int pcc = act[k] ? pc : 0;
+        pa[k] = pcc % N;
+        pb[k] = pcc / N;
+    }
+
+    double r[P][N], t[P][N];
+    // ---------------------------------------------------------------- P1-P3: u at the Gauss points
+    {
+        double rl[P][N], rh[P][N];
+        nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const double* src = zc + N * (pa[k] + N * pb[k]);
+#pragma unroll
+            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
+        }
+        v_fwd<N, P>(T.Vh[0], r, t);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (act[k])
+#pragma unroll
+                for (int e = 0; e < N; ++e) X0[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
+        nb_contract<N, P>(T, NT, 0, nbi, pa, pb, act, rl, rh);
+        csync();
+
+        nb_load<N, P>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
+        v_fwd<N, P>(T.Vh[1], r, t);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (act[k])
+#pragma unroll
+                for (int e = 0; e < N; ++e) X1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
+        nb_contract<N, P>(T, NT, 1, nbi, pa, pb, act, rl, rh);
+        csync();
+
+        nb_load<N, P>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
+        nb_contract<N, P>(T, NT, 2, nbi, pa, pb, act, rl, rh);
+    }
+    v_fwd<N, P>(T.Vh[2], r, t);                                  // t = u on this thread's z-pencils
+    {
+        double g[P][N];
+        c_apply<N, P>(T.Dc[0], t, g);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (act[k]) {
+#pragma unroll
+                for (int e = 0; e < N; ++e) {
+                    A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
+                    X2[Lay<N>::at(pa[k], pb[k], e)] = g[k][e];
+                }
+                // own z-face traces: u and the reference normal derivative at z = 0, 1
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    OT[FLay<N>::at(2 * (4 + s), pa[k], pb[k])] = dot<N>(T.L[0][s], t[k]);
+                    OT[FLay<N>::at(2 * (4 + s) + 1, pa[k], pb[k])] = dot<N>(T.L[0][2 + s], t[k]);
+                }
+            }
+    }
+    csync();
+
+    // ---------------------------------------------------------------- P4: d_x u, d_y u, own x/y traces;
+    //                                                                  neighbour tangential stage 1
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int e = 0; e < N; ++e)
+                r[k][e] = act[k] ? A0[q == 0 ? Lay<N>::at(e, pa[k], pb[k]) : Lay<N>::at(pa[k], e, pb[k])] : 0.0;
+        c_apply<N, P>(T.Dc[1 + q], r, t);
+        double* X = q == 0 ? X0 : X1;
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (act[k]) {
+#pragma unroll
+                for (int e = 0; e < N; ++e)
+                    X[q == 0 ? Lay<N>::at(e, pa[k], pb[k]) : Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    OT[FLay<N>::at(2 * (2 * q + s), pa[k], pb[k])] = dot<N>(T.L[1][s], r[k]);
+                    OT[FLay<N>::at(2 * (2 * q + s) + 1, pa[k], pb[k])] = dot<N>(T.L[1][2 + s], r[k]);
+                }
+            }
+    }
+    // neighbour stage 1 (lines along i1): Va = V a, E = D+_qq/h_q V d + D+_qt1/h_t1 G a
+    for (int tk = lane; tk < 6 * N; tk += TPC) {
+        const int f = tk / N, line = tk - f * N, q = f >> 1;
+        if (!((nbi >> f) & 1u)) continue;
+        const int t1 = (q == 0) ? 1 : 0;
+        const double* Dn = nb_dfield(p, lc, f, nbmask);
+        const double cqq = __ldg(Dn + q) / p.h[q], cq1 = __ldg(Dn + dsym(q, t1)) / p.h[t1];
+        double a[N], d[N], va[N], ga[N], vd[N];
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            a[e] = NT[FLay<N>::at(2 * f, e, line)];
+            d[e] = NT[FLay<N>::at(2 * f + 1, e, line)];
+        }
+        {
+            double rr[1][N], tt[1][N];
+#pragma unroll
+            for (int e = 0; e < N; ++e) rr[0][e] = a[e];
+            v_fwd<N, 1>(T.Vh[3], rr, tt);
+#pragma unroll
+            for (int e = 0; e < N; ++e) { va[e] = tt[0][e]; rr[0][e] = d[e]; }
+            v_fwd<N, 1>(T.Vh[4], rr, tt);
+#pragma unroll
+            for (int e = 0; e < N; ++e) vd[e] = tt[0][e];
+        }
+        g_fwd<N>(T.Gh, a, ga);
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            NT[FLay<N>::at(2 * f, e, line)] = va[e];
+            NT[FLay<N>::at(2 * f + 1, e, line)] = fma(cqq, vd[e], cq1 * ga[e]);
+        }
+    }
+    csync();
+
+    // ---------------------------------------------------------------- P5: neighbour stage 2, own pass A,
+    //                                                                  pointwise volume data
+    for (int tk = lane; tk < 12 * N; tk += TPC) {
+        const int f = (tk >= 6 * N) ? (tk - 6 * N) / N : tk / N;
+        const int line = tk % N, q = f >> 1;
+        const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+        if (tk < 6 * N) {
+            // neighbour stage 2 (lines along i2): u+ = V Va, s+ = V E + D+_qt2/h_t2 G Va
+            if (!((nbi >> f) & 1u)) continue;
+            const double* Dn = nb_dfield(p, lc, f, nbmask);
+            const double cq2 = __ldg(Dn + dsym(q, t2)) / p.h[t2];
+            double rr[1][N], tt[1][N], va[N], gv[N];
+#pragma unroll
+            for (int e = 0; e < N; ++e) va[e] = NT[FLay<N>::at(2 * f, line, e)];
+#pragma unroll
+            for (int e = 0; e < N; ++e) rr[0][e] = va[e];
+            v_fwd<N, 1>(T.Vh[5], rr, tt);
+#pragma unroll
+            for (int e = 0; e < N; ++e) {
+                NT[FLay<N>::at(2 * f, line, e)] = tt[0][e];
+                rr[0][e] = NT[FLay<N>::at(2 * f + 1, line, e)];
+            }
+            v_fwd<N, 1>(T.Vh[6], rr, tt);
+            g_fwd<N>(T.Gh, va, gv);
+#pragma unroll
+            for (int e = 0; e < N; ++e) NT[FLay<N>::at(2 * f + 1, line, e)] = fma(cq2, gv[e], tt[0][e]);
+        } else {
+            // own pass A (lines along i1): s_part = D_qq/h_q d_n u + D_qt1/h_t1 Dc u-
+            if (!((fact >> f) & 1u)) continue;
+            const double cqq = Dw[q] / p.h[q], cq1 = Dw[dsym(q, t1)] / p.h[t1];
+            double rr[1][N], tt[1][N];
+#pragma unroll
+            for (int e = 0; e < N; ++e) rr[0][e] = OT[FLay<N>::at(2 * f, e, line)];
+            c_apply<N, 1>(T.Dc[3], rr, tt);
+#pragma unroll
+            for (int e = 0; e < N; ++e) {
+                const int ix = FLay<N>::at(2 * f + 1, e, line);
+                OT[ix] = fma(cqq, OT[ix], cq1 * tt[0][e]);
+            }
+        }
+    }
+    {
+        // x^(r) = W (sum_s D_rs/(h_r h_s) d_s u - b_r/h_r u), accumulator A0 = W c u   (eq:gauss_points)
+        double Dh[3][3];
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+            for (int ss = 0; ss < 3; ++ss) Dh[rr][ss] = Dw[dsym(rr, ss)] / (p.h[rr] * p.h[ss]);
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            if (!act[k]) continue;
+            const double wab = do_vol ? p.dT * T.w[pa[k]] * T.w[pb[k]] : 0.0;
+#pragma unroll
+            for (int e = 0; e < N; ++e) {
+                const int ix = Lay<N>::at(pa[k], pb[k], e);
+                const double W = wab * T.w[e];
+                const double u = A0[ix], g0 = X0[ix], g1 = X1[ix], g2 = X2[ix];
+                X0[ix] = W * (Dh[0][0] * g0 + Dh[0][1] * g1 + Dh[0][2] * g2 - p.kb[0] * u);
+                X1[ix] = W * (Dh[1][0] * g0 + Dh[1][1] * g1 + Dh[1][2] * g2 - p.kb[1] * u);
+                X2[ix] = W * (Dh[2][0] * g0 + Dh[2][1] * g1 + Dh[2][2] * g2 - p.kb[2] * u);
+                A0[ix] = W * p.c * u;
+            }
+        }
+    }
+    csync();
+
+    // ---------------------------------------------------------------- P6: own pass B, fluxes, Dc^T along i2
+    for (int tk = lane; tk < 6 * N; tk += TPC) {
+        const int f = tk / N, line = tk - f * N, q = f >> 1, sd = f & 1;
+        if (!((fact >> f) & 1u)) continue;
+        const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+        const bool interior = (nbmask >> f) & 1u;
+        const double dme = Dw[q];
+        const double cq2 = Dw[dsym(q, t2)] / p.h[t2];
+        const double cn = dme / p.h[q], c1 = Dw[dsym(q, t1)] / p.h[t1];
+        double uo[N], so[N], cv[N], ct1[N], cgn[N];
+        {
+            double rr[1][N], tt[1][N];
+#pragma unroll
+            for (int e = 0; e < N; ++e) uo[e] = rr[0][e] = OT[FLay<N>::at(2 * f, line, e)];
+            c_apply<N, 1>(T.Dc[4], rr, tt);
+#pragma unroll
+            for (int e = 0; e < N; ++e) so[e] = fma(cq2, tt[0][e], OT[FLay<N>::at(2 * f + 1, line, e)]);
+        }
+        double dnb = 0.0;
+        if (interior) dnb = __ldg(nb_dfield(p, lc, f, nbmask) + q);
+        const double dm = sd ? dme : dnb, dp = sd ? dnb : dme;     // delta of T-, T+
+        const double dsum = dm + dp;
+        const double wm = dsum == 0.0 ? 0.5 : dp / dsum, wp = dsum == 0.0 ? 0.5 : dm / dsum;   // C-5
+        const double gam = interior ? (dsum == 0.0 ? 0.0 : 2.0 * dm * dp / dsum) * p.sigma : dme * p.sigma;
+        const double wself = sd ? wm : wp;
+        const double bq = p.bq[q];
+        double c2[N];
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            const double Wf = p.dF[q] * T.w[line] * T.w[e];        // face point (i1 = line, i2 = e)
+            double coef;
+            if (interior) {
+                const double un = NT[FLay<N>::at(2 * f, line, e)], sn = NT[FLay<N>::at(2 * f + 1, line, e)];
+                const double um = sd ? uo[e] : un, up = sd ? un : uo[e];
+                const double sm = sd ? so[e] : sn, sp = sd ? sn : so[e];
+                const double Phi = (bq >= 0.0) ? bq * um : bq * up;   // upwind flux
+                const double J = um - up;
+                const double com = Phi - (wm * sm + wp * sp) + gam * J;
+                cv[e] = sd ? Wf * com : -Wf * com;
+                coef = -Wf * wself * J;                                // coefficient of e_q.D grad(phi)
+            } else {
+                const double nu = sd ? 1.0 : -1.0;                     // outward normal
+                const double bn = nu * bq;
+                const double Phi = (bn >= 0.0) ? bn * uo[e] : 0.0;
+                cv[e] = Wf * (Phi - nu * so[e] + gam * uo[e]);
+                coef = -Wf * uo[e] * nu;
+            }
+            cgn[e] = coef * cn;
+            ct1[e] = coef * c1;
+            c2[e] = coef * cq2;
+        }
+        {
+            double rr[1][N], tt[1][N];
+#pragma unroll
+            for (int e = 0; e < N; ++e) rr[0][e] = c2[e];
+            c_apply<N, 1>(T.DcT[0], rr, tt);                          // tangential test derivative along i2
+#pragma unroll
+            for (int e = 0; e < N; ++e) {
+                OT[FLay<N>::at(2 * f, line, e)] = cv[e] + tt[0][e];
+                OT[FLay<N>::at(2 * f + 1, line, e)] = cgn[e];
+                NT[FLay<N>::at(2 * f, line, e)] = ct1[e];
+            }
+        }
+    }
+    csync();
+
+    // ---------------------------------------------------------------- P7: Dc^T along i1 of the t1 parts
+    for (int tk = lane; tk < 6 * N; tk += TPC) {
+        const int f = tk / N, line = tk - f * N;
+        if (!((fact >> f) & 1u)) continue;
+        double rr[1][N], tt[1][N];
+#pragma unroll
+        for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(2 * f, e, line)];
+        c_apply<N, 1>(T.DcT[1], rr, tt);
+#pragma unroll
+        for (int e = 0; e < N; ++e) OT[FLay<N>::at(2 * f, e, line)] += tt[0][e];
+    }
+    csync();
+
+    // ---------------------------------------------------------------- P8-P10: roles, A0 += Dc_q^T x^(q) + lifts
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        double* X = q == 0 ? X0 : (q == 1 ? X1 : X2);
+        auto at = [&](int k, int e) {
+            return q == 0 ? Lay<N>::at(e, pa[k], pb[k]) : (q == 1 ? Lay<N>::at(pa[k], e, pb[k]) : Lay<N>::at(pa[k], pb[k], e));
+        };
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X[at(k, e)] : 0.0;
+        c_apply<N, P>(T.DcT[2 + q], r, t);
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            if (!act[k]) continue;
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const int f = 2 * q + s;
+                if (!((fact >> f) & 1u)) continue;
+                const double cv = OT[FLay<N>::at(2 * f, pa[k], pb[k])];
+                const double cg = OT[FLay<N>::at(2 * f + 1, pa[k], pb[k])];
+#pragma unroll
+                for (int e = 0; e < N; ++e) t[k][e] = fma(cv, T.L[2][s][e], fma(cg, T.L[2][2 + s][e], t[k][e]));
+            }
+        }
+        if (q < 2) {
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+                if (act[k])
+#pragma unroll
+                    for (int e = 0; e < N; ++e) A0[at(k, e)] += t[k][e];
+            csync();
+        } else {
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+#pragma unroll
+                for (int e = 0; e < N; ++e) t[k][e] += act[k] ? A0[at(k, e)] : 0.0;
+        }
+    }
+    // ---------------------------------------------------------------- P10-P12: V^T along z, y, x; store
+    v_bwd<N, P>(T.Vh[9], t, r);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = r[k][e];
+    csync();
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
+    v_bwd<N, P>(T.Vh[10], r, t);
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (act[k])
+#pragma unroll
+            for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
+    csync();
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
+    v_bwd<N, P>(T.Vh[11], r, t);
+    if (valid) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            if (!act[k]) continue;
+            const int64_t off = cell * n3 + N * (pa[k] + N * pb[k]);
+            double* yc = p.y + off;
+            if (p.f) {
+#pragma unroll
+                for (int e = 0; e < N; ++e) t[k][e] = __ldg(p.f + off + e) - t[k][e];
+            }
+#pragma unroll
+            for (int e = 0; e < N; ++e) __stcs(yc + e, t[k][e]);
+        }
+    }
+}
+
+}  // namespace dg

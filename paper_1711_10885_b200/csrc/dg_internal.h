@@ -19,6 +19,7 @@ struct HostTables {
     double LD0[NMAX], LD1[NMAX];  // L'_l(0), L'_l(1)
     double th0[NMAX], th1[NMAX];  // theta_j(0), theta_j(1)       (B^(d) of PAPER.md:528-545)
     double dth0[NMAX], dth1[NMAX];// theta'_j(0), theta'_j(1)
+    double G[NMAX][NMAX];    // G[i][j]  = theta'_j(xi_i)   (reference derivative, modal -> Gauss points)
 };
 int build_tables(int k, HostTables* t);
 
@@ -45,6 +46,13 @@ struct KParams {
     double gam[3];            // gamma = <D_qq, D_qq> sigma = D_qq sigma
     double bq[3];             // b_q
     unsigned mask;
+    int per[3];               // direction q periodic (every cell has both q-neighbours; NEXT-1)
+    int wrap[3];              // periodic AND unpartitioned along q: the wrap neighbour is local
+    // general-coefficient kernel (full / per-cell D; NEXT-1):
+    const double* Dfield;     // [local cell][6] = D00 D11 D22 D01 D02 D12
+    const double* Dghost[6];  // neighbour-rank layers of Dfield per face (nullptr: none)
+    double sigma;
+    double h[3];
 };
 
 struct LaunchInfo {
@@ -54,10 +62,13 @@ struct LaunchInfo {
 // Per-degree launchers (one translation unit per n, dg_cell_n<N>.cu).
 int upload_tables(int k, const HostTables& t);          // to this device's __constant__ bank
 cudaError_t launch_cell(int k, const KParams& p, cudaStream_t s);
+cudaError_t launch_gen(int k, const KParams& p, cudaStream_t s);      // general-coefficient kernel
 int cell_launch_info(int k, LaunchInfo* info);
 
 // Halo / inputs kernels (dg_aux.cu).
 cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc[3], int face, cudaStream_t s);
+cudaError_t launch_dfield_pack(const double* D9, double* D6, int* bad, int64_t ncell, cudaStream_t s);
+cudaError_t launch_dfield_const(double* D6, const double D9[9], int64_t ncell, cudaStream_t s);
 cudaError_t launch_fill_uniform(double* dst, int64_t count, uint64_t seed, int64_t offset, cudaStream_t s);
 cudaError_t launch_fill_uniform_local(double* dst, int n3, const int64_t nloc[3], const int64_t gofs[3],
                                       const int64_t gcells[3], uint64_t seed, cudaStream_t s);

@@ -74,7 +74,10 @@ int build_tables(int k, HostTables* t)
     for (int i = 0; i < m; ++i) {
         t->xi[i] = (double)xi[i];
         t->w[i] = (double)w[i];
-        for (int j = 0; j < n; ++j) t->V[i][j] = (double)th[i][j];
+        for (int j = 0; j < n; ++j) {
+            t->V[i][j] = (double)th[i][j];
+            t->G[i][j] = (double)dth[i][j];
+        }
         for (int l = 0; l < m; ++l) {
             ld s = 0;
             for (int j = 0; j < n; ++j) s += dth[i][j] * th[l][j];

@@ -17,11 +17,12 @@ LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg_b200.so")
 
 DG_OK, DG_EINVAL, DG_ENOMEM, DG_ECUDA, DG_ENCCL, DG_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 VOLUME, INTERIOR_FACES, BOUNDARY_FACES, ALL, HALO_EXTERNAL = 1, 2, 4, 7, 0x100
-BC_DIRICHLET = 0
+BC_DIRICHLET, BC_PERIODIC = 0, 1
 
 EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residual", "dg_apply_host",
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
-            "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition"]
+            "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
+            "dg_set_diffusion"]
 
 
 class DGError(RuntimeError):
@@ -73,6 +74,7 @@ def lib():
         L.dg_nccl_unique_id.argtypes = [vp]
         L.dg_get_kernel_info.argtypes = [vp, ctypes.POINTER(KernelInfo)]
         L.dg_partition.argtypes = [ctypes.POINTER(MeshDesc), ctypes.c_int, ctypes.c_int, vp, vp, vp]
+        L.dg_set_diffusion.argtypes = [vp, vp, ctypes.c_uint, vp]
         for name in EXPORTED:
             if name != "dg_strerror":
                 getattr(L, name).restype = ctypes.c_int
@@ -124,9 +126,14 @@ def mesh_desc(ncells, lo, hi, parts=(1, 1, 1), bc=(BC_DIRICHLET,) * 6):
     return m
 
 
-def partition(ncells, parts, rank):
+def bc_from_periodic(periodic):
+    """bc[6] with both sides of every periodic direction glued, the others Dirichlet."""
+    return tuple(BC_PERIODIC if periodic[f >> 1] else BC_DIRICHLET for f in range(6))
+
+
+def partition(ncells, parts, rank, periodic=(0, 0, 0)):
     """Host-only block partition (dg_partition): (cell_lo, cell_cnt, neighbour rank per face)."""
-    m = mesh_desc(ncells, (0, 0, 0), (1, 1, 1), parts)
+    m = mesh_desc(ncells, (0, 0, 0), (1, 1, 1), parts, bc_from_periodic(periodic))
     lo = (ctypes.c_int64 * 3)()
     cnt = (ctypes.c_int64 * 3)()
     nb = (ctypes.c_int * 6)()
@@ -189,6 +196,14 @@ class Operator:
         _check(lib().dg_apply_host(self._h, a_ptr(z_host), a_ptr(y_host)), "dg_apply_host")
         return y_host
 
+    def set_diffusion(self, Dcell, flags=0, stream=None):
+        """Per-cell tensors: CUDA float64 tensor of local cells x 9 (row-major), or None to
+        revert to the constant D of the constructor (dg_set_diffusion)."""
+        if Dcell is not None:
+            ncell = self.ndofs // self.n3
+            _dev_vec(Dcell, ncell * 9, "Dcell")
+        _check(lib().dg_set_diffusion(self._h, _ptr(Dcell), flags, _stream(stream)), "dg_set_diffusion")
+
     def fill_uniform_local(self, t, seed, stream=None):
         _dev_vec(t, self.ndofs, "t")
         _check(lib().dg_fill_uniform_local(self._h, _ptr(t), seed, _stream(stream)), "dg_fill_uniform_local")
@@ -241,4 +256,6 @@ def a_ptr(a):
 
 
 def from_config(cfg, **kw):
+    if getattr(cfg, "periodic", (0, 0, 0)) != (0, 0, 0) and "bc" not in kw:
+        kw["bc"] = bc_from_periodic(cfg.periodic)
     return Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, **kw)

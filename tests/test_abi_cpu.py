@@ -56,8 +56,8 @@ def setup_rc(k=2, ncells=(2, 2, 2), lo=(0, 0, 0), hi=(1, 1, 1), D=(1, 0, 0, 0, 1
     (dict(parts=(2, 1, 1)), dg.DG_EINVAL),                          # product != nranks
     (dict(parts=(3, 1, 1), nranks=3), dg.DG_EINVAL),                # does not divide ncells
     (dict(nranks=1, rank=1), dg.DG_EINVAL),
-    (dict(bc=(1, 0, 0, 0, 0, 0)), dg.DG_EUNSUPPORTED),              # periodic: later
-    (dict(D=(1, 0.5, 0, 0.5, 1, 0, 0, 0, 1)), dg.DG_EUNSUPPORTED),  # full D: later
+    (dict(bc=(1, 0, 0, 0, 0, 0)), dg.DG_EINVAL),                    # periodic on one side only
+    (dict(bc=(7, 7, 0, 0, 0, 0)), dg.DG_EUNSUPPORTED),              # unknown boundary condition
 ])
 def test_setup_validation(kw, code):
     assert setup_rc(**kw) == code
