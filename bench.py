@@ -55,6 +55,8 @@ def workload(name, world):
     if name == "c5strong":
         grid = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}[world]
         return configs.c5_strong(grid)
+    if name.startswith("a-k"):
+        return configs.problem_a(int(name[3:]), world)
     cfg = configs.by_name(name)
     if world != 1:
         raise SystemExit("workload %s is single-GPU" % name)
@@ -62,9 +64,12 @@ def workload(name, world):
 
 
 def workload_desc(cfg, world):
-    return {"workload": "%s: %dx%dx%d cells, k=%d, %d DOFs, box %s-%s, D=%s, b=%s, c=%g, sigma=%g, Dirichlet, seed %d"
+    dtxt = ("per-cell SPD tensor field (inputs.tensor_field_*, seed %d)" % cfg.dfield_seed
+            if cfg.dfield_seed >= 0 else str(list(cfg.D)))
+    bc = "periodic" if all(cfg.periodic) else ("Dirichlet" if not any(cfg.periodic) else "periodic %s" % (cfg.periodic,))
+    return {"workload": "%s: %dx%dx%d cells, k=%d, %d DOFs, box %s-%s, D=%s, b=%s, c=%g, sigma=%g, %s, seed %d"
                         % (cfg.name, cfg.ncells[0], cfg.ncells[1], cfg.ncells[2], cfg.k, cfg.ndofs,
-                           list(cfg.lo), list(cfg.hi), list(cfg.D), list(cfg.b), cfg.c, cfg.sigma, cfg.seed),
+                           list(cfg.lo), list(cfg.hi), dtxt, list(cfg.b), cfg.c, cfg.sigma, bc, cfg.seed),
             "k": cfg.k, "ncells": list(cfg.ncells), "ndofs": cfg.ndofs, "parts": list(cfg.parts),
             "parallelism": "block %dx%dx%d" % tuple(cfg.parts) if world > 1 else "1 GPU",
             "l2": "no flush: z and y are %.2f GB each per GPU (> 126 MB L2)" % (cfg.ndofs / world * 8 / 1e9)}
@@ -132,18 +137,27 @@ def sample_cells(cfg, count, seed=0):
     return np.unique(np.r_[special, extra]).astype(np.int64)[:max(count, 1)]
 
 
+def oracle_kw(cfg):
+    """periodic / per-cell tensor keywords of the oracle for this workload (host field, global order)."""
+    kw = {"periodic": cfg.periodic}
+    if cfg.dfield_seed >= 0:
+        kw["Dcell"] = inputs.tensor_field_cells(np.arange(cfg.ncell), cfg.dfield_seed)
+    return kw
+
+
 def cpu_oracle_rate(cfg, z_host, budget_s, seed=0):
     """O-1 (oracle, as it stands) on a bounded sample of cells; returns (DOF/s, cores, sample text, seconds)."""
     from oracle import o1   # only bench.py's cpu_baseline / reference legs may touch oracle/
+    kw = oracle_kw(cfg)
     probe = sample_cells(cfg, 16, seed)
     t0 = time.perf_counter()
-    _, cores = o1.apply(*cfg.args(), z_host, cells=probe)
+    _, cores = o1.apply(*cfg.args(), z_host, cells=probe, **kw)
     dt = max(time.perf_counter() - t0, 1e-6)
     per_cell = dt / probe.size
     count = int(min(max(budget_s / per_cell, 16), cfg.ncell))
     cells = sample_cells(cfg, count, seed + 1)
     t0 = time.perf_counter()
-    _, cores = o1.apply(*cfg.args(), z_host, cells=cells)
+    _, cores = o1.apply(*cfg.args(), z_host, cells=cells, **kw)
     dt = time.perf_counter() - t0
     rate = cells.size * cfg.n3 / dt
     text = ("O-1 naive quadrature (C/OpenMP, -O3) on %d of %d cells of %s (seeded random + all boundary types); "
@@ -173,6 +187,13 @@ def measured_peaks():
         return {}
 
 
+def vs_baseline(cfg, value):
+    """value / the paper's number for the SAME workload: only Problem A has one (Table 1)."""
+    if cfg.dfield_seed >= 0 and all(cfg.periodic) and cfg.k in perfmodel.PAPER_TABLE1_A_MDOFS:
+        return value / (perfmodel.PAPER_TABLE1_A_MDOFS[cfg.k] * 1e6)
+    return None
+
+
 # ------------------------------------------------------------------------------------------ reference
 def run_reference(args, rank, world):
     if rank != 0:
@@ -184,19 +205,20 @@ def run_reference(args, rank, world):
         pass
     o1.build()
     z = inputs.uniform(cfg.ndofs, cfg.seed)
+    kw = oracle_kw(cfg)
     budget = args.ref_seconds / max(1, args.steps + args.warmup)
     probe = sample_cells(cfg, 8, 0)
     t0 = time.perf_counter()
-    o1.apply(*cfg.args(), z, cells=probe)
+    o1.apply(*cfg.args(), z, cells=probe, **kw)
     per_cell = max(time.perf_counter() - t0, 1e-6) / probe.size
     count = int(min(max(budget / per_cell, 8), cfg.ncell))
     cells = sample_cells(cfg, count, 1)
     cores = 0
     for _ in range(args.warmup):
-        _, cores = o1.apply(*cfg.args(), z, cells=cells)
+        _, cores = o1.apply(*cfg.args(), z, cells=cells, **kw)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        _, cores = o1.apply(*cfg.args(), z, cells=cells)
+        _, cores = o1.apply(*cfg.args(), z, cells=cells, **kw)
     dt = time.perf_counter() - t0
     rate = args.steps * cells.size * cfg.n3 / dt
     sample = ("each step: O-1 naive quadrature (C/OpenMP) on %d of %d cells of %s (seeded random + all boundary "
@@ -231,7 +253,10 @@ def run_ours(args, rank, world, local_rank):
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().tolist())
     op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, device=local_rank, rank=rank,
-                     nranks=world, parts=cfg.parts, nccl_id=nccl_id)
+                     nranks=world, parts=cfg.parts, nccl_id=nccl_id, bc=dg.bc_from_periodic(cfg.periodic))
+    if cfg.dfield_seed >= 0:
+        op.set_tensor_field(cfg.dfield_seed)
+    general = cfg.dfield_seed >= 0 or any(cfg.D[i] != 0 for i in (1, 2, 3, 5, 6, 7))
     info = op.kernel_info()
     z = torch.empty(op.ndofs, dtype=torch.float64, device=dev)
     y = torch.empty_like(z)
@@ -301,7 +326,7 @@ def run_ours(args, rank, world, local_rank):
             "executed_achieved": (exec_per_dof * op.ndofs / kern_t / 1e12) if exec_per_dof else None,
             "executed_frac": (exec_per_dof * op.ndofs / kern_t / 1e12 / peak) if exec_per_dof else None,
             "ncu_source": "profiles/ncu_full_summary.json (ncu --set full, --clock-control none)" if ncu else None,
-            "kernel": "dg_cell_kernel<%d> (FP64 DFMA pipe)" % (cfg.k + 1),
+            "kernel": "%s<%d> (FP64 DFMA pipe)" % ("dg_gen_kernel" if general else "dg_cell_kernel", cfg.k + 1),
             "flops_basis": "paper model FLOPDOF_vol+FLOPDOF_face(3,%d) = %.1f flop/DOF x %d DOFs per launch "
                            "(PAPER.md:675-676); the kernel executes fewer (collocation variant, DESIGN.md)"
                            % (cfg.k, per_dof, op.ndofs),
@@ -339,7 +364,8 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-               "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based uniform[-1,1] z, C-13)",
+               "vs_baseline": vs_baseline(cfg, value), "dtype": "f64",
+               "data": "synthetic (seeded counter-based uniform[-1,1] z, C-13)",
                "config": workload_desc(cfg, world),
                "gflops_model": per_dof * value / 1e9,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
@@ -360,7 +386,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default=None,
-                    help="default: C3 (N=1) / C3-per-GPU weak (N>1); also c1, c2, c4-kK, c5weak, c5strong")
+                    help="default: C3 (N=1) / C3-per-GPU weak (N>1); also c1, c2, c4-kK, c5weak, c5strong, "
+                         "a-kK (the paper's Problem A: periodic, per-cell tensor D, ~4e8 DOFs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

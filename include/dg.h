@@ -147,6 +147,11 @@ int dg_fill_uniform(double* dst, int64_t count, uint64_t seed, int64_t offset, v
 /* Fill this rank's local vector with the values of the GLOBAL DOF indices it owns. */
 int dg_fill_uniform_local(dg_ctx* ctx, double* dst, uint64_t seed, void* stream);
 
+/* Per-cell inputs of this rank's cells: dst[per_cell * l + i] = U(seed, per_cell * e + i) for
+   local cell l with GLOBAL cell index e (e.g. per_cell = 6 for the Problem A tensor field,
+   paper_1711_10885_b200/inputs.py). */
+int dg_fill_uniform_cells(dg_ctx* ctx, double* dst, int per_cell, uint64_t seed, void* stream);
+
 /* Create a 128-byte ncclUniqueId (rank 0 calls this and broadcasts it). */
 int dg_nccl_unique_id(void* out128);
 

@@ -22,6 +22,7 @@ class Config:
     seed: int
     parts: Tuple[int, int, int] = (1, 1, 1)
     periodic: Tuple[int, int, int] = (0, 0, 0)
+    dfield_seed: int = -1          # >= 0: per-cell tensor field inputs.tensor_field_* (Problem A)
 
     @property
     def n3(self):
@@ -96,11 +97,26 @@ def c3_weak(P=1):
                   sigma_for(7, 1.0 / 64), 2, (px, py, pz))
 
 
+def problem_a(k, P=1):
+    """The paper's Problem A (Table 1 protocol :933-936) as a synthetic stand-in:
+    periodic in every direction, axis-parallel unit-box mesh of N^3 cubes with N = round(736.8/(k+1))
+    so the DOF count is ~4e8 (3.2 GB vectors), q = 2p (n = m = k+1), a per-cell SPD tensor field
+    (inputs.tensor_field_*, seed 6), b = (1, 1/2, 1/4), c = 1, sigma = 3k(k+2)N (as C-20).
+    P > 1: the same block per GPU on a Px x Py x Pz grid (weak scaling)."""
+    N = int(round(736.8 / (k + 1)))
+    px, py, pz = _WEAK_GRID[P]
+    nc = (N * px, N * py, N * pz)
+    return Config("A-k%d" % k if P == 1 else "A-k%d-P%d" % (k, P), nc, (0, 0, 0), (float(px), float(py), float(pz)),
+                  k, I3, B_A, 1.0, sigma_for(k, 1.0 / N), 5, (px, py, pz), (1, 1, 1), 6)
+
+
 def by_name(name):
     name = name.lower()
     table = {"c1": c1, "c2": c2, "c3": c3, "c5strong": c5_strong, "c5weak": c5_weak}
     if name.startswith("c4-k"):
         return c4(int(name[4:]))
+    if name.startswith("a-k"):
+        return problem_a(int(name[3:]))
     return table[name]()
 
 

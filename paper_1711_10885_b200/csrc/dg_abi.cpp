@@ -559,6 +559,13 @@ extern "C" int dg_fill_uniform_local(dg_ctx* ctx, double* dst, uint64_t seed, vo
     return cuda_rc(launch_fill_uniform_local(dst, ctx->n3, ctx->nloc, ctx->gofs, ctx->gcells, seed, (cudaStream_t)stream));
 }
 
+extern "C" int dg_fill_uniform_cells(dg_ctx* ctx, double* dst, int per_cell, uint64_t seed, void* stream)
+{
+    if (!ctx || !dst || per_cell < 1) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    return cuda_rc(launch_fill_uniform_local(dst, per_cell, ctx->nloc, ctx->gofs, ctx->gcells, seed, (cudaStream_t)stream));
+}
+
 extern "C" int dg_get_kernel_info(const dg_ctx* ctx, dg_kernel_info* info)
 {
     if (!ctx || !info) return DG_EINVAL;

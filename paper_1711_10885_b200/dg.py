@@ -22,7 +22,7 @@ BC_DIRICHLET, BC_PERIODIC = 0, 1
 EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residual", "dg_apply_host",
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
-            "dg_set_diffusion"]
+            "dg_set_diffusion", "dg_fill_uniform_cells"]
 
 
 class DGError(RuntimeError):
@@ -75,6 +75,7 @@ def lib():
         L.dg_get_kernel_info.argtypes = [vp, ctypes.POINTER(KernelInfo)]
         L.dg_partition.argtypes = [ctypes.POINTER(MeshDesc), ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.dg_set_diffusion.argtypes = [vp, vp, ctypes.c_uint, vp]
+        L.dg_fill_uniform_cells.argtypes = [vp, vp, ctypes.c_int, u64, vp]
         for name in EXPORTED:
             if name != "dg_strerror":
                 getattr(L, name).restype = ctypes.c_int
@@ -203,6 +204,23 @@ class Operator:
             ncell = self.ndofs // self.n3
             _dev_vec(Dcell, ncell * 9, "Dcell")
         _check(lib().dg_set_diffusion(self._h, _ptr(Dcell), flags, _stream(stream)), "dg_set_diffusion")
+
+    def fill_uniform_cells(self, t, per_cell, seed, stream=None):
+        """t[per_cell * l + i] = U(seed, per_cell * e_global(l) + i) (dg_fill_uniform_cells)."""
+        _dev_vec(t, self.ndofs // self.n3 * per_cell, "t")
+        _check(lib().dg_fill_uniform_cells(self._h, _ptr(t), per_cell, seed, _stream(stream)),
+               "dg_fill_uniform_cells")
+
+    def set_tensor_field(self, seed, stream=None):
+        """The seeded Problem A tensor field (inputs.tensor_field_from_uniforms) of this rank's cells."""
+        import torch
+        from . import inputs
+        ncell = self.ndofs // self.n3
+        u6 = torch.empty(ncell * 6, dtype=torch.float64, device="cuda:%d" % self.device)
+        self.fill_uniform_cells(u6, 6, seed, stream)
+        D9 = inputs.tensor_field_from_uniforms(u6.view(ncell, 6))
+        self.set_diffusion(D9.view(-1), stream=stream)
+        del u6, D9
 
     def fill_uniform_local(self, t, seed, stream=None):
         _dev_vec(t, self.ndofs, "t")

@@ -47,3 +47,25 @@ def uniform_cells(cells, n3, seed, ncells_global=None):
     cells = np.asarray(cells, dtype=np.uint64)
     g = cells[:, None] * np.uint64(n3) + np.arange(n3, dtype=np.uint64)[None, :]
     return uniform_from_index(g, seed)
+
+
+# ---- Problem A coefficient field (NEXT-1; PAPER.md:944-946: tensor-valued, constant per cell)
+# Per cell e (GLOBAL cell index), six uniforms u_i = U(seed, 6 e + i) give a symmetric,
+# strictly diagonally dominant (hence SPD) tensor
+#     D00, D11, D22 = 1.5 + 0.5 u_0..2  in [1, 2],   D01, D02, D12 = 0.25 u_3..5  in [-1/4, 1/4].
+# Scales are powers of two, so every entry is the same double on the host (numpy) and on
+# the device (torch ops on dg_fill_uniform_cells output): partition- and device-independent.
+def tensor_field_from_uniforms(u6):
+    """[ncell, 6] uniforms -> [ncell, 9] row-major tensors (numpy or torch arrays)."""
+    d = 1.5 + 0.5 * u6[:, 0:3]
+    o = 0.25 * u6[:, 3:6]
+    cols = [d[:, 0], o[:, 0], o[:, 1], o[:, 0], d[:, 1], o[:, 2], o[:, 1], o[:, 2], d[:, 2]]
+    if isinstance(u6, np.ndarray):
+        return np.stack(cols, axis=1)
+    import torch
+    return torch.stack(cols, dim=1).contiguous()
+
+
+def tensor_field_cells(cells, seed):
+    """Host tensors [len(cells), 9] of the Problem A field for explicit global cell indices."""
+    return tensor_field_from_uniforms(uniform_cells(cells, 6, seed))

@@ -48,3 +48,11 @@ FP64_FMA_PER_CLK_PER_SM = 64
 
 def fp64_peak_tflops(sm_mhz=1965.0):
     return B200_SMS * FP64_FMA_PER_CLK_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+
+
+# The paper's only throughput numbers for this operator: Table 1, Problem A (periodic,
+# axis-parallel, per-cell tensor D, q = 2p, ~4e8 DOFs; 2x16-core Haswell node), full operator
+# application in MDOF/s. Context for the Problem A
+# bench workload (configs.problem_a), not the target.
+PAPER_TABLE1_A_MDOFS = {1: 170.2, 2: 393.0, 3: 537.8, 4: 595.0, 5: 617.2, 6: 599.0, 7: 570.1, 8: 540.6,
+                        9: 504.8, 10: 471.3}

@@ -27,13 +27,24 @@ def as_tensor(ptr, count):
     return torch.as_tensor(DevPtr(ptr, count), device="cuda")
 
 
-def run_partitioned(cfg, parts, terms):
+def local_cells(cfg, lo, cnt):
+    G = cfg.ncells
+    gz, gy, gx = np.meshgrid(np.arange(lo[2], lo[2] + cnt[2]), np.arange(lo[1], lo[1] + cnt[1]),
+                             np.arange(lo[0], lo[0] + cnt[0]), indexing="ij")
+    return (gx + G[0] * (gy + G[1] * gz)).reshape(-1)
+
+
+def run_partitioned(cfg, parts, terms, periodic=(0, 0, 0), Dcell=None):
     from paper_1711_10885_b200 import dg
     world = parts[0] * parts[1] * parts[2]
     ops, zs, ys = [], [], []
     for r in range(world):
         op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, rank=r, nranks=world,
-                         parts=parts)
+                         parts=parts, bc=dg.bc_from_periodic(periodic))
+        if Dcell is not None:
+            own = local_cells(cfg, op.cell_lo, op.cell_cnt)
+            op.set_diffusion(torch.from_numpy(np.ascontiguousarray(Dcell[own]).reshape(-1)).cuda(),
+                             flags=dg.HALO_EXTERNAL)
         z = torch.empty(op.ndofs, dtype=torch.float64, device="cuda")
         op.fill_uniform_local(z, cfg.seed)
         op.halo_pack(z)
@@ -48,6 +59,9 @@ def run_partitioned(cfg, parts, terms):
             src = as_tensor(ops[nb].halo_buffer_ptr(f ^ 1, 0), cnt)
             dst = as_tensor(op.halo_buffer_ptr(f, 1), cnt)
             dst.copy_(src)
+            if Dcell is not None:    # the diffusion-field layers (which = 2 / 3)
+                dc = cnt // cfg.n3 * 6
+                as_tensor(op.halo_buffer_ptr(f, 3), dc).copy_(as_tensor(ops[nb].halo_buffer_ptr(f ^ 1, 2), dc))
     torch.cuda.synchronize()
     n3 = cfg.n3
     G = cfg.ncells
@@ -67,9 +81,11 @@ def run_partitioned(cfg, parts, terms):
     return yg
 
 
-def run_single(cfg, terms):
+def run_single(cfg, terms, periodic=(0, 0, 0), Dcell=None):
     from paper_1711_10885_b200 import dg
-    op = dg.from_config(cfg)
+    op = dg.from_config(cfg, bc=dg.bc_from_periodic(periodic))
+    if Dcell is not None:
+        op.set_diffusion(torch.from_numpy(np.ascontiguousarray(Dcell).reshape(-1)).cuda())
     z = torch.empty(op.ndofs, dtype=torch.float64, device="cuda")
     op.fill_uniform_local(z, cfg.seed)
     y = torch.empty_like(z)
@@ -90,4 +106,26 @@ def test_partitioned_equals_single_bitwise(k, ncells, parts):
     for terms in (7, 2):
         ys = run_single(cfg, terms)
         yp = run_partitioned(cfg, parts, terms)
+        assert np.array_equal(yp, ys)
+
+
+@pytest.mark.parametrize("k,ncells,parts,periodic", [
+    (2, (6, 4, 4), (2, 1, 1), (1, 0, 0)), (3, (4, 4, 4), (2, 2, 2), (1, 1, 1)), (7, (4, 4, 2), (2, 2, 1), (1, 1, 1)),
+    (7, (4, 4, 2), (2, 2, 1), (0, 0, 1)), (1, (4, 6, 8), (1, 2, 4), (0, 1, 1)),
+])
+@pytest.mark.parametrize("percell", [False, True])
+def test_partitioned_periodic_percell_equals_single_bitwise(k, ncells, parts, periodic, percell):
+    """Periodic wrap across ranks (two ranks along a direction: both faces talk to the same
+    peer) and per-cell tensors whose partition layers travel with the halo (NEXT-1)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = configs.small(k, ncells=ncells, hi=(1.5, 1.0, 0.75), b=(1.0, -0.5, 0.25), c=0.3)
+    Dc = None
+    if percell:
+        rng = np.random.default_rng(k)
+        M = rng.normal(size=(cfg.ncell, 3, 3))
+        Dc = (np.einsum("eij,ekj->eik", M, M) + 0.5 * np.eye(3)).reshape(cfg.ncell, 9)
+    for terms in (7, 2):
+        ys = run_single(cfg, terms, periodic, Dc)
+        yp = run_partitioned(cfg, parts, terms, periodic, Dc)
         assert np.array_equal(yp, ys)

@@ -226,3 +226,20 @@ def test_problem_a_k7_sampled_vs_o1():
     cells = np.unique(np.r_[[0, nx - 1, nx * ny - 1, cfg.ncell - 1], rng.integers(0, cfg.ncell, 200)]).astype(np.int64)
     ys, _ = o1.apply(*cfg.args(), zn, cells=cells, periodic=(1, 1, 1), Dcell=Dc)
     assert np.abs(yn.reshape(-1, cfg.n3)[cells] - ys).max() <= TOL * np.abs(yn).max()
+
+
+def test_device_tensor_field_matches_host_recipe():
+    from paper_1711_10885_b200 import dg
+    cfg = configs.small(2, ncells=(5, 4, 3))
+    # rank 1 of a 1x2x1 split (halo driven by the caller: no NCCL): global != local cell index
+    op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, rank=1, nranks=2,
+                     parts=(1, 2, 1))
+    u6 = torch.empty(op.ndofs // op.n3 * 6, dtype=torch.float64, device="cuda")
+    op.fill_uniform_cells(u6, 6, 6)
+    D_dev = inputs.tensor_field_from_uniforms(u6.view(-1, 6)).cpu().numpy()
+    lo, cnt = op.cell_lo, op.cell_cnt
+    gz, gy, gx = np.meshgrid(np.arange(lo[2], lo[2] + cnt[2]), np.arange(lo[1], lo[1] + cnt[1]),
+                             np.arange(lo[0], lo[0] + cnt[0]), indexing="ij")
+    own = (gx + cfg.ncells[0] * (gy + cfg.ncells[1] * gz)).reshape(-1)
+    assert np.array_equal(D_dev, inputs.tensor_field_cells(own, 6))
+    op.close()

@@ -10,6 +10,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 cfg = configs.by_name(name)
 op = dg.from_config(cfg)
+if cfg.dfield_seed >= 0:
+    op.set_tensor_field(cfg.dfield_seed)
 print(cfg.name, "ndofs", cfg.ndofs, op.kernel_info(), flush=True)
 z = torch.empty(cfg.ndofs, dtype=torch.float64, device="cuda")
 y = torch.empty_like(z)
