@@ -352,7 +352,7 @@ def run_ours(args, rank, world, local_rank):
             te = float(tt[0])
         e2e = {"value": total_dofs * ke / te, "unit": UNIT, "h2d_bytes_per_step": op.ndofs * 8 * world,
                "d2h_bytes_per_step": op.ndofs * 8 * world, "steps": ke,
-               "path": "dg_apply_host (pinned host z -> H2D -> fused kernel -> D2H y), wall clock, max over ranks"}
+               "path": "dg_apply_host (pinned host z; z-slab pipeline: H2D / fused kernel / D2H overlapped on 3 streams), wall clock, max over ranks"}
 
     # ---- CPU baseline: the oracle on the host cores (rank 0, N = 1 only)
     cpu = None

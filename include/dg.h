@@ -106,7 +106,9 @@ int dg_apply_ex(dg_ctx* ctx, const double* z, double* y, unsigned terms, void* s
 int dg_residual(dg_ctx* ctx, const double* z, const double* f, double* r, void* stream);
 
 /* End-to-end variant with HOST buffers: z_host, y_host are host pointers (pinned for speed)
-   of ndofs doubles; copies in, applies, copies out on an internal stream; synchronous. */
+   of ndofs doubles; synchronous. Single-rank contexts without z-periodicity run a slab
+   pipeline: z-slabs are copied in, applied and copied out on three internal streams, so
+   both transfer directions and the kernel overlap; otherwise copy in, apply, copy out. */
 int dg_apply_host(dg_ctx* ctx, const double* z_host, double* y_host);
 
 /* Wait for all work of the context; surfaces asynchronous CUDA / NCCL errors. */

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <new>
 #include <vector>
@@ -28,7 +29,8 @@ struct dg_ctx {
     int64_t inner_lo[3] = {0, 0, 0}, inner_cnt[3] = {0, 0, 0};   // cells needing no remote data
     int64_t* shell = nullptr;        // device list of the partition-layer cells
     int64_t nshell = 0;
-    cudaStream_t comm_stream = nullptr, host_stream = nullptr;
+    cudaStream_t comm_stream = nullptr, host_stream = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
+    cudaEvent_t ev_slab[2] = {nullptr, nullptr}, ev_done = nullptr;   // dg_apply_host pipeline
     cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
     ncclComm_t comm = nullptr;
     double* hz = nullptr;            // device staging for dg_apply_host
@@ -90,6 +92,11 @@ static void free_ctx(dg_ctx* c)
     }
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->host_stream) cudaStreamDestroy(c->host_stream);
+    if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+    if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
+    for (int i = 0; i < 2; ++i)
+        if (c->ev_slab[i]) cudaEventDestroy(c->ev_slab[i]);
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
     if (c->ev_packed) cudaEventDestroy(c->ev_packed);
     if (c->ev_recv) cudaEventDestroy(c->ev_recv);
     delete c;
@@ -478,17 +485,71 @@ extern "C" int dg_residual(dg_ctx* ctx, const double* z, const double* f, double
     return apply_impl(ctx, z, f, r, DG_ALL, (cudaStream_t)stream);
 }
 
+// Slab pipeline of dg_apply_host (single-rank contexts): the cell box is cut into z-slabs
+// (z is the slowest index, so a slab is one contiguous chunk of every vector). Slab i's
+// H2D copy (stream h2d), the kernel over slab i-1 (stream host_stream; its upper z-neighbours
+// live in slab i) and the D2H copy of slab i-2's y (stream d2h) overlap, so the host <-> device
+// transfers in both directions (separate copy engines) hide each other and the kernel.
+static int apply_host_pipelined(dg_ctx* ctx, const double* z_host, double* y_host)
+{
+    const int64_t nz = ctx->nloc[2];
+    const int64_t layer = ctx->nloc[0] * ctx->nloc[1] * (int64_t)ctx->n3;   // doubles per z-layer
+    int64_t S = (nz + 15) / 16;                                              // <= 16 slabs
+    if (S < 1) S = 1;
+    const int64_t nslab = (nz + S - 1) / S;
+    cudaStream_t sc = ctx->host_stream, sh = ctx->h2d_stream, sd = ctx->d2h_stream;
+    for (int64_t i = 0; i <= nslab; ++i) {
+        if (i < nslab) {   // H2D of slab i
+            const int64_t z0 = i * S, cnt = std::min(S, nz - z0);
+            DG_CUDA(cudaMemcpyAsync(ctx->hz + z0 * layer, z_host + z0 * layer, (size_t)(cnt * layer) * sizeof(double),
+                                    cudaMemcpyHostToDevice, sh));
+            DG_CUDA(cudaEventRecord(ctx->ev_slab[i & 1], sh));
+            DG_CUDA(cudaStreamWaitEvent(sc, ctx->ev_slab[i & 1], 0));
+        }
+        if (i >= 1) {      // kernel over slab i-1 (all of its neighbours are resident now)
+            const int64_t z0 = (i - 1) * S, cnt = std::min(S, nz - z0);
+            KParams p = ctx->base;
+            p.z = ctx->hz;
+            p.y = ctx->hy;
+            p.f = nullptr;
+            p.mask = DG_ALL;
+            p.task_list = nullptr;
+            p.task_lo[0] = 0; p.task_lo[1] = 0; p.task_lo[2] = z0;
+            p.task_cnt[0] = ctx->nloc[0]; p.task_cnt[1] = ctx->nloc[1]; p.task_cnt[2] = cnt;
+            p.ntasks = ctx->nloc[0] * ctx->nloc[1] * cnt;
+            DG_CUDA(ctx->general ? launch_gen(ctx->k, p, sc) : launch_cell(ctx->k, p, sc));
+            DG_CUDA(cudaEventRecord(ctx->ev_done, sc));
+            DG_CUDA(cudaStreamWaitEvent(sd, ctx->ev_done, 0));
+            DG_CUDA(cudaMemcpyAsync(y_host + z0 * layer, ctx->hy + z0 * layer, (size_t)(cnt * layer) * sizeof(double),
+                                    cudaMemcpyDeviceToHost, sd));
+        }
+    }
+    DG_CUDA(cudaStreamSynchronize(sd));
+    DG_CUDA(cudaStreamSynchronize(sc));
+    return DG_OK;
+}
+
 extern "C" int dg_apply_host(dg_ctx* ctx, const double* z_host, double* y_host)
 {
     if (!ctx || !z_host || !y_host) return DG_EINVAL;
     DG_CUDA(cudaSetDevice(ctx->device));
     const size_t bytes = (size_t)ctx->ndofs * sizeof(double);
-    if (!ctx->host_stream && cudaStreamCreateWithFlags(&ctx->host_stream, cudaStreamNonBlocking) != cudaSuccess)
-        return DG_ECUDA;
+    if (!ctx->host_stream) {
+        if (cudaStreamCreateWithFlags(&ctx->host_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_slab[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_slab[1], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming) != cudaSuccess)
+            return DG_ECUDA;
+    }
     if (!ctx->hz) {
         if (cudaMalloc(&ctx->hz, bytes) != cudaSuccess) return DG_ENOMEM;
         if (cudaMalloc(&ctx->hy, bytes) != cudaSuccess) { cudaFree(ctx->hz); ctx->hz = nullptr; return DG_ENOMEM; }
     }
+    if (!ctx->partitioned && !ctx->per[2]) return apply_host_pipelined(ctx, z_host, y_host);
+    // partitioned (halo exchange needs the whole local z) or z-periodic (slab 0 needs the last
+    // slab): copy in, apply, copy out
     DG_CUDA(cudaMemcpyAsync(ctx->hz, z_host, bytes, cudaMemcpyHostToDevice, ctx->host_stream));
     int rc = apply_impl(ctx, ctx->hz, nullptr, ctx->hy, DG_ALL, ctx->host_stream);
     if (rc != DG_OK) return rc;
