@@ -253,29 +253,19 @@ dg_gen_kernel(const KParams p)
         const int t1 = (q == 0) ? 1 : 0;
         const double* Dn = nb_dfield(p, lc, f, nbmask);
         const double cqq = __ldg(Dn + q) / p.h[q], cq1 = __ldg(Dn + dsym(q, t1)) / p.h[t1];
-        double a[N], d[N], va[N], ga[N], vd[N];
+        double rr[1][N], tt[1][N], ga[N];
+#pragma unroll
+        for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(2 * f, e, line)];
+        g_fwd<N>(T.Gh, rr[0], ga);
+        v_fwd<N, 1>(T.Vh[3], rr, tt);
 #pragma unroll
         for (int e = 0; e < N; ++e) {
-            a[e] = NT[FLay<N>::at(2 * f, e, line)];
-            d[e] = NT[FLay<N>::at(2 * f + 1, e, line)];
+            NT[FLay<N>::at(2 * f, e, line)] = tt[0][e];
+            rr[0][e] = NT[FLay<N>::at(2 * f + 1, e, line)];
         }
-        {
-            double rr[1][N], tt[1][N];
+        v_fwd<N, 1>(T.Vh[4], rr, tt);
 #pragma unroll
-            for (int e = 0; e < N; ++e) rr[0][e] = a[e];
-            v_fwd<N, 1>(T.Vh[3], rr, tt);
-#pragma unroll
-            for (int e = 0; e < N; ++e) { va[e] = tt[0][e]; rr[0][e] = d[e]; }
-            v_fwd<N, 1>(T.Vh[4], rr, tt);
-#pragma unroll
-            for (int e = 0; e < N; ++e) vd[e] = tt[0][e];
-        }
-        g_fwd<N>(T.Gh, a, ga);
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-            NT[FLay<N>::at(2 * f, e, line)] = va[e];
-            NT[FLay<N>::at(2 * f + 1, e, line)] = fma(cqq, vd[e], cq1 * ga[e]);
-        }
+        for (int e = 0; e < N; ++e) NT[FLay<N>::at(2 * f + 1, e, line)] = fma(cqq, tt[0][e], cq1 * ga[e]);
     }
     csync();
 
@@ -354,7 +344,7 @@ dg_gen_kernel(const KParams p)
         const double dme = Dw[q];
         const double cq2 = Dw[dsym(q, t2)] / p.h[t2];
         const double cn = dme / p.h[q], c1 = Dw[dsym(q, t1)] / p.h[t1];
-        double uo[N], so[N], cv[N], ct1[N], cgn[N];
+        double uo[N], so[N], cv[N];
         {
             double rr[1][N], tt[1][N];
 #pragma unroll
@@ -392,9 +382,9 @@ dg_gen_kernel(const KParams p)
                 cv[e] = Wf * (Phi - nu * so[e] + gam * uo[e]);
                 coef = -Wf * uo[e] * nu;
             }
-            cgn[e] = coef * cn;
-            ct1[e] = coef * c1;
-            c2[e] = coef * cq2;
+            OT[FLay<N>::at(2 * f + 1, line, e)] = coef * cn;         // normal part (lifted with L')
+            NT[FLay<N>::at(2 * f, line, e)] = coef * c1;             // t1 part (Dc^T along i1 in P7)
+            c2[e] = coef * cq2;                                      // t2 part (Dc^T along i2 below)
         }
         {
             double rr[1][N], tt[1][N];
@@ -402,11 +392,7 @@ dg_gen_kernel(const KParams p)
             for (int e = 0; e < N; ++e) rr[0][e] = c2[e];
             c_apply<N, 1>(T.DcT[0], rr, tt);                          // tangential test derivative along i2
 #pragma unroll
-            for (int e = 0; e < N; ++e) {
-                OT[FLay<N>::at(2 * f, line, e)] = cv[e] + tt[0][e];
-                OT[FLay<N>::at(2 * f + 1, line, e)] = cgn[e];
-                NT[FLay<N>::at(2 * f, line, e)] = ct1[e];
-            }
+            for (int e = 0; e < N; ++e) OT[FLay<N>::at(2 * f, line, e)] = cv[e] + tt[0][e];
         }
     }
     csync();
