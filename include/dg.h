@@ -158,7 +158,8 @@ int dg_fill_uniform_cells(dg_ctx* ctx, double* dst, int per_cell, uint64_t seed,
 int dg_nccl_unique_id(void* out128);
 
 /* Library / kernel facts for the harness: kernel launches per dg_apply, threads and
-   cells per CTA, dynamic shared memory per CTA, registers per thread. */
+   cells per CTA, dynamic shared memory per CTA, registers per thread, of the kernel the
+   next apply launches (the general-coefficient kernel after dg_set_diffusion / full D). */
 typedef struct {
     int launches_per_apply;
     int cells_per_cta;

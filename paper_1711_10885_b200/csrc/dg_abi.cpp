@@ -632,7 +632,7 @@ extern "C" int dg_get_kernel_info(const dg_ctx* ctx, dg_kernel_info* info)
     if (!ctx || !info) return DG_EINVAL;
     DG_CUDA(cudaSetDevice(ctx->device));
     LaunchInfo li;
-    if (cell_launch_info(ctx->k, &li) != 0) return DG_ECUDA;
+    if ((ctx->general ? gen_launch_info(ctx->k, &li) : cell_launch_info(ctx->k, &li)) != 0) return DG_ECUDA;
     info->launches_per_apply = ctx->partitioned ? 2 : 1;
     info->cells_per_cta = li.cells_per_cta;
     info->threads_per_cta = li.threads;

@@ -169,6 +169,26 @@ cudaError_t DG_CAT(launch_gen_n, DG_N)(const KParams& p, cudaStream_t s)
     return cudaGetLastError();
 }
 
+int DG_CAT(gen_info_n, DG_N)(LaunchInfo* info)
+{
+    constexpr int N = DG_N;
+    info->cells_per_cta = Cfg<N>::C;
+    info->threads = Cfg<N>::C * Cfg<N>::TPC;
+    info->smem = GSmem<N>::BYTES;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, dg_gen_kernel<N>) != cudaSuccess) return -3;
+    info->regs = fa.numRegs;
+    if (cudaFuncSetAttribute(dg_gen_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, GSmem<N>::BYTES) !=
+        cudaSuccess)
+        return -3;
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_gen_kernel<N>, info->threads, GSmem<N>::BYTES) !=
+        cudaSuccess)
+        return -3;
+    info->ctas_per_sm = blocks;
+    return 0;
+}
+
 int DG_CAT(cell_info_n, DG_N)(LaunchInfo* info)
 {
     constexpr int N = DG_N;

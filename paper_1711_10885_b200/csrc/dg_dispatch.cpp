@@ -7,7 +7,8 @@ namespace dg {
     int upload_tables_n##n(const HostTables&);                \
     cudaError_t launch_cell_n##n(const KParams&, cudaStream_t); \
     cudaError_t launch_gen_n##n(const KParams&, cudaStream_t);  \
-    int cell_info_n##n(LaunchInfo*);
+    int cell_info_n##n(LaunchInfo*);                          \
+    int gen_info_n##n(LaunchInfo*);
 DG_DECL(2) DG_DECL(3) DG_DECL(4) DG_DECL(5) DG_DECL(6) DG_DECL(7) DG_DECL(8) DG_DECL(9) DG_DECL(10) DG_DECL(11)
 
 #define DG_CASES(call)                                                                                  \
@@ -37,6 +38,13 @@ cudaError_t launch_gen(int k, const KParams& p, cudaStream_t s)
 #define DG_LG(n) launch_gen_n##n(p, s)
     DG_CASES(DG_LG)
     return cudaErrorInvalidValue;
+}
+
+int gen_launch_info(int k, LaunchInfo* info)
+{
+#define DG_GI(n) gen_info_n##n(info)
+    DG_CASES(DG_GI)
+    return -1;
 }
 
 int cell_launch_info(int k, LaunchInfo* info)

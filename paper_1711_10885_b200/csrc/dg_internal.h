@@ -64,6 +64,7 @@ int upload_tables(int k, const HostTables& t);          // to this device's __co
 cudaError_t launch_cell(int k, const KParams& p, cudaStream_t s);
 cudaError_t launch_gen(int k, const KParams& p, cudaStream_t s);      // general-coefficient kernel
 int cell_launch_info(int k, LaunchInfo* info);
+int gen_launch_info(int k, LaunchInfo* info);
 
 // Halo / inputs kernels (dg_aux.cu).
 cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc[3], int face, cudaStream_t s);
