@@ -149,7 +149,8 @@ def cpu_oracle_rate(cfg, z_host, budget_s, seed=0):
     """O-1 (oracle, as it stands) on a bounded sample of cells; returns (DOF/s, cores, sample text, seconds)."""
     from oracle import o1   # only bench.py's cpu_baseline / reference legs may touch oracle/
     kw = oracle_kw(cfg)
-    probe = sample_cells(cfg, 16, seed)
+    probe = sample_cells(cfg, 512, seed)    # large enough to amortise the thread start-up
+    o1.apply(*cfg.args(), z_host, cells=probe[:32], **kw)
     t0 = time.perf_counter()
     _, cores = o1.apply(*cfg.args(), z_host, cells=probe, **kw)
     dt = max(time.perf_counter() - t0, 1e-6)
@@ -157,12 +158,23 @@ def cpu_oracle_rate(cfg, z_host, budget_s, seed=0):
     count = int(min(max(budget_s / per_cell, 16), cfg.ncell))
     cells = sample_cells(cfg, count, seed + 1)
     t0 = time.perf_counter()
-    _, cores = o1.apply(*cfg.args(), z_host, cells=cells, **kw)
+    yo, cores = o1.apply(*cfg.args(), z_host, cells=cells, **kw)
     dt = time.perf_counter() - t0
     rate = cells.size * cfg.n3 / dt
     text = ("O-1 naive quadrature (C/OpenMP, -O3) on %d of %d cells of %s (seeded random + all boundary types); "
-            "%.1f s on %d threads" % (cells.size, cfg.ncell, cfg.name, dt, cores))
-    return rate, cores, text, dt
+            "%.1f s on %d threads of %s" % (cells.size, cfg.ncell, cfg.name, dt, cores, cpu_model()))
+    return rate, cores, text, dt, cells, yo
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown CPU"
 
 
 def load_ncu(cfg):
@@ -300,6 +312,17 @@ def run_ours(args, rank, world, local_rank):
     else:
         tk_local = t_local
     clk = clocks.stop()
+    # per-step distribution (separate, after the timed region): median / min of single applies
+    step_ms = []
+    if world == 1:
+        for _ in range(min(args.steps, 20)):
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            op.apply(z, y)
+            s1.record(stream)
+            s1.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
     t = t_local
     tk = tk_local
     if world > 1:
@@ -317,11 +340,21 @@ def run_ours(args, rank, world, local_rank):
     achieved = flops_launch_rank / kern_t / 1e12
     peak = perfmodel.fp64_peak_tflops(clk["sm_max_mhz"] or 1965.0)
     ncu = load_ncu(cfg)
+    hbm_peak = None
+    try:
+        mp = measured_peaks()
+        hbm_peak = float(mp.get("hbm_copy_gbs") or mp.get("hbm_gbs") or mp.get("hbm", {}).get("copy_gbs"))
+    except Exception:
+        hbm_peak = None
     traffic = ncu.get("dram_bytes_per_launch")
     exec_per_dof = ncu.get("executed_flops_per_dof")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic,
             "traffic_algorithmic_bytes": 16.0 * op.ndofs,
+            "hbm_gbs_at_traffic": (traffic / kern_t / 1e9) if traffic else None,
+            "hbm_frac_of_measured_copy": ((traffic / kern_t / 1e9) / hbm_peak) if (traffic and hbm_peak) else None,
+            "ncu_fp64_pipe_pct": ncu.get("fp64_pipe_pct"), "ncu_smem_wavefront_pct": ncu.get("smem_wavefront_pct"),
+            "ncu_issue_active_pct": ncu.get("issue_active_pct"),
             "executed_flops_per_dof": exec_per_dof,
             "executed_achieved": (exec_per_dof * op.ndofs / kern_t / 1e12) if exec_per_dof else None,
             "executed_frac": (exec_per_dof * op.ndofs / kern_t / 1e12 / peak) if exec_per_dof else None,
@@ -356,10 +389,16 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- CPU baseline: the oracle on the host cores (rank 0, N = 1 only)
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         zn = z.cpu().numpy()
-        rate, cores, text, _ = cpu_oracle_rate(cfg, zn, args.cpu_seconds)
+        rate, cores, text, _, cells, yo = cpu_oracle_rate(cfg, zn, args.cpu_seconds)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": text}
+        # the same oracle blocks double as a parity check of this run's y (reading C-14)
+        yg = y.view(-1, cfg.n3)[torch.from_numpy(cells).to(dev)].cpu().numpy()
+        ymax = float(y.abs().max())
+        parity = {"vs": "O-1 on the cpu_baseline sample (%d cells)" % cells.size,
+                  "max_abs_err_over_max_abs_y": float(np.abs(yg - yo).max() / ymax), "tolerance": 1e-12}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -368,7 +407,9 @@ def run_ours(args, rank, world, local_rank):
                "data": "synthetic (seeded counter-based uniform[-1,1] z, C-13)",
                "config": workload_desc(cfg, world),
                "gflops_model": per_dof * value / 1e9,
-               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+               "roofline": roof, "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "clocks": clk,
+               "step_ms": {"mean": ms_per_step, "min": min(step_ms) if step_ms else None,
+                           "median": float(np.median(step_ms)) if step_ms else None},
                "gpu_launches": args.steps * (info["launches_per_apply"] if world == 1 else
                                              (2 + sum(1 for f in range(6) if op.halo_info(f)[0] >= 0))),
                "kernel_info": info}
