@@ -105,6 +105,17 @@ int dg_apply_ex(dg_ctx* ctx, const double* z, double* y, unsigned terms, void* s
 /* r = f - A z, fused into the final store (f: assembled l_h(phi_i)). */
 int dg_residual(dg_ctx* ctx, const double* z, const double* f, double* r, void* stream);
 
+/* One stage of an explicit strong-stability-preserving Runge-Kutta method in Shu-Osher form
+ * (NEXT-2; M z^(k+1) = M z^(k) + dt (f - A z^(k)), "higher-order Runge-Kutta
+ * methods involve basically the same computations per stage"; Heun = SSP-RK2):
+ *     out = a w + b (z + dt M^-1 (f - A z)),    M = Delta_T I  (orthonormal basis)
+ * fused into the kernel's single store. f == NULL means f = 0; w is read only when a != 0.
+ * Forward Euler: (a, b) = (0, 1). Heun: stage 1 z1 = stage(z = u, a = 0, b = 1);
+ * stage 2 u' = stage(z = z1, w = u, a = 1/2, b = 1/2). out must not alias z or f (it may alias w).
+ * Collective like dg_apply. Errors: DG_EINVAL (aliasing, non-finite a, b, dt, a != 0 without w). */
+int dg_ssp_stage(dg_ctx* ctx, const double* z, const double* f, const double* w, double a, double b, double dt,
+                 double* out, void* stream);
+
 /* End-to-end variant with HOST buffers: z_host, y_host are host pointers (pinned for speed)
    of ndofs doubles; synchronous. Single-rank contexts without z-periodicity run a slab
    pipeline: z-slabs are copied in, applied and copied out on three internal streams, so

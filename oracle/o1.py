@@ -108,3 +108,22 @@ def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL, cells=None, nthreads=0
     if used < 0:
         raise ValueError("o1_apply failed (%d)" % used)
     return y, used
+
+
+def ssp_stage(ncells, lo, hi, k, D, b, c, sigma, z, dt, f=None, w=None, a=0.0, bcoef=1.0, periodic=(0, 0, 0),
+              Dcell=None):
+    """One explicit SSP Runge-Kutta stage in Shu-Osher form, written out from PAPER.md:366-373:
+    M z^(k+1) = M z^(k) + dt (f - A z^(k)) with M = (phi_j, phi_i) = Delta_T I for the orthonormal
+    Legendre basis on cuboid cells, generalised to out = a w + b (z + dt M^-1 (f - A z)).
+    A z by O-1 (naive quadrature)."""
+    n3 = (k + 1) ** 3
+    h = [(hi[q] - lo[q]) / ncells[q] for q in range(3)]
+    dT = h[0] * h[1] * h[2]
+    Az, _ = apply(ncells, lo, hi, k, D, b, c, sigma, z, periodic=periodic, Dcell=Dcell)
+    r = (np.zeros_like(Az) if f is None else np.asarray(f, dtype=np.float64)) - Az
+    znew = np.asarray(z, dtype=np.float64) + (dt / dT) * r
+    out = bcoef * znew
+    if a != 0.0:
+        out = out + a * np.asarray(w, dtype=np.float64)
+    assert out.size == np.asarray(z).size and out.size % n3 == 0
+    return out

@@ -405,7 +405,15 @@ extern "C" int dg_local_layout(const dg_ctx* ctx, int64_t cell_lo[3], int64_t ce
     return DG_OK;
 }
 
-static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, unsigned terms, cudaStream_t s)
+struct Epi {             // store epilogue (KParams::epi)
+    int mode = 0;
+    const double* f = nullptr;
+    const double* w = nullptr;
+    double a = 0.0, b = 1.0, s = 0.0;
+};
+
+static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, unsigned terms, cudaStream_t s,
+                      const Epi* epi = nullptr)
 {
     if (!ctx || !z || !y) return DG_EINVAL;
     if ((const double*)y == z || (f && f == z)) return DG_EINVAL;
@@ -415,6 +423,15 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
     p.z = z;
     p.y = y;
     p.f = f;
+    p.epi = f ? 1 : 0;
+    if (epi) {
+        p.epi = epi->mode;
+        p.f = epi->f;
+        p.w = epi->w;
+        p.ea = epi->a;
+        p.eb = epi->b;
+        p.es = epi->s;
+    }
     p.mask = terms & DG_ALL;
     const bool external = (terms & DG_HALO_EXTERNAL) != 0;
     if (!ctx->partitioned) {
@@ -512,6 +529,7 @@ static int apply_host_pipelined(dg_ctx* ctx, const double* z_host, double* y_hos
             p.z = ctx->hz;
             p.y = ctx->hy;
             p.f = nullptr;
+            p.epi = 0;
             p.mask = DG_ALL;
             p.task_list = nullptr;
             p.task_lo[0] = 0; p.task_lo[1] = 0; p.task_lo[2] = z0;
@@ -527,6 +545,22 @@ static int apply_host_pipelined(dg_ctx* ctx, const double* z_host, double* y_hos
     DG_CUDA(cudaStreamSynchronize(sd));
     DG_CUDA(cudaStreamSynchronize(sc));
     return DG_OK;
+}
+
+extern "C" int dg_ssp_stage(dg_ctx* ctx, const double* z, const double* f, const double* w, double a, double b,
+                            double dt, double* out, void* stream)
+{
+    if (!ctx || !z || !out || out == z || (f && f == out)) return DG_EINVAL;
+    if (!std::isfinite(a) || !std::isfinite(b) || !std::isfinite(dt)) return DG_EINVAL;
+    Epi e;
+    e.mode = 2;
+    e.f = f;
+    e.w = (a != 0.0) ? w : nullptr;
+    if (a != 0.0 && !w) return DG_EINVAL;
+    e.a = a;
+    e.b = b;
+    e.s = dt / ctx->base.dT;     // M^-1 = 1/Delta_T (orthonormal basis, cuboid cells)
+    return apply_impl(ctx, z, nullptr, out, DG_ALL, (cudaStream_t)stream, &e);
 }
 
 extern "C" int dg_apply_host(dg_ctx* ctx, const double* z_host, double* y_host)

@@ -586,6 +586,28 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
     }
 }
 
+// ---------------------------------------------------------------------------------- store epilogue
+// The single store of a cell's y block, with the explicit-step arithmetic of PAPER.md:366-373
+// fused in (M = Delta_T I for the orthonormal basis on cuboid cells, so M^-1 is a scalar):
+//   epi 0: y = A z      epi 1: y = f - A z      epi 2: y = a w + b (z + (dt/Delta_T)(f - A z))
+// (one Shu-Osher stage of an SSP Runge-Kutta method; f or w may be absent = 0). Every value
+// read here belongs to this thread's own x-line of this cell.
+template <int N>
+__device__ __forceinline__ void epilogue(const KParams& p, int64_t off, double (&t)[N])
+{
+    if (p.epi == 1) {
+#pragma unroll
+        for (int e = 0; e < N; ++e) t[e] = __ldg(p.f + off + e) - t[e];
+    } else if (p.epi == 2) {
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            const double r = (p.f ? __ldg(p.f + off + e) : 0.0) - t[e];
+            const double v = fma(p.es, r, __ldg(p.z + off + e));
+            t[e] = p.w ? fma(p.ea, __ldg(p.w + off + e), p.eb * v) : p.eb * v;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------------- kernel
 template <int N>
 __global__ void __launch_bounds__(Cfg<N>::C * Cfg<N>::TPC, Cfg<N>::MINB)
@@ -803,11 +825,7 @@ dg_cell_kernel(const KParams p)
             if (!act[k]) continue;
             const int64_t off = cell * n3 + N * (pa[k] + N * pb[k]);
             double* yc = p.y + off;
-            if (p.f) {
-                const double* fc = p.f + off;
-#pragma unroll
-                for (int e = 0; e < N; ++e) t[k][e] = __ldg(fc + e) - t[k][e];
-            }
+            epilogue<N>(p, off, t[k]);
             if (N % 2 == 0) {
 #pragma unroll
                 for (int e = 0; e < N; e += 2)

@@ -124,7 +124,7 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
     int dev = 0;
     cudaGetDevice(&dev);
 #if DG_N == 8
-    if (use_mma() && !(p.per[0] | p.per[1] | p.per[2])) {   // the DMMA variant has no periodic wrap
+    if (use_mma() && !(p.per[0] | p.per[1] | p.per[2]) && p.epi != 2) {   // DMMA variant: no wrap, no SSP epilogue
         static int done[64];
         constexpr int BYTES = m8::C * m8::PER_CELL * 8;
         if (dev >= 0 && dev < 64 && !done[dev]) {

@@ -479,10 +479,7 @@ dg_gen_kernel(const KParams p)
             if (!act[k]) continue;
             const int64_t off = cell * n3 + N * (pa[k] + N * pb[k]);
             double* yc = p.y + off;
-            if (p.f) {
-#pragma unroll
-                for (int e = 0; e < N; ++e) t[k][e] = __ldg(p.f + off + e) - t[k][e];
-            }
+            epilogue<N>(p, off, t[k]);
 #pragma unroll
             for (int e = 0; e < N; ++e) __stcs(yc + e, t[k][e]);
         }

@@ -27,7 +27,10 @@ int build_tables(int k, HostTables* t);
 struct KParams {
     const double* z;
     double* y;
-    const double* f;          // residual mode: y = f - A z (nullptr -> y = A z)
+    const double* f;          // epi 1: y = f - A z; epi 2: the f of the SSP stage (nullptr = 0)
+    const double* w;          // epi 2: the a w term (nullptr = 0)
+    double ea, eb, es;        // epi 2: y = ea w + eb (z + es (f - A z)), es = dt / Delta_T
+    int epi;                  // store epilogue: 0 y = A z, 1 residual, 2 SSP-RK stage
     const double* ghost[6];   // neighbour-rank boundary layers per face 2q+s (nullptr: none)
     const int64_t* task_list; // local linear cell ids (nullptr -> task box)
     int64_t ntasks;

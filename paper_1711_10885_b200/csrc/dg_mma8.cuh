@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(32 * C, MINB) dg_cell_mma8(const KParams p)
         for (int nt = 0; nt < 8; ++nt) {
             const int64_t off = cell * n3 + 2 * t + 8 * g + 64 * nt;
             double y0 = Fb[nt][0], y1 = Fb[nt][1];
-            if (p.f) {
+            if (p.epi == 1) {
                 const double2 fv = __ldg(reinterpret_cast<const double2*>(p.f + off));
                 y0 = fv.x - y0;
                 y1 = fv.y - y1;

@@ -22,7 +22,7 @@ BC_DIRICHLET, BC_PERIODIC = 0, 1
 EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residual", "dg_apply_host",
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
-            "dg_set_diffusion", "dg_fill_uniform_cells"]
+            "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage"]
 
 
 class DGError(RuntimeError):
@@ -76,6 +76,7 @@ def lib():
         L.dg_partition.argtypes = [ctypes.POINTER(MeshDesc), ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.dg_set_diffusion.argtypes = [vp, vp, ctypes.c_uint, vp]
         L.dg_fill_uniform_cells.argtypes = [vp, vp, ctypes.c_int, u64, vp]
+        L.dg_ssp_stage.argtypes = [vp, vp, vp, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, vp]
         for name in EXPORTED:
             if name != "dg_strerror":
                 getattr(L, name).restype = ctypes.c_int
@@ -187,6 +188,21 @@ class Operator:
             _dev_vec(t, self.ndofs, nm)
         _check(lib().dg_residual(self._h, _ptr(z), _ptr(f), _ptr(r), _stream(stream)), "dg_residual")
         return r
+
+    def ssp_stage(self, z, out, dt, f=None, w=None, a=0.0, b=1.0, stream=None):
+        """out = a w + b (z + dt M^-1 (f - A z)) (dg_ssp_stage; M = Delta_T I)."""
+        for t, nm in ((z, "z"), (out, "out"), (f, "f"), (w, "w")):
+            if t is not None:
+                _dev_vec(t, self.ndofs, nm)
+        _check(lib().dg_ssp_stage(self._h, _ptr(z), _ptr(f), _ptr(w), float(a), float(b), float(dt), _ptr(out),
+                                  _stream(stream)), "dg_ssp_stage")
+        return out
+
+    def heun_step(self, u, dt, tmp, out, f=None, stream=None):
+        """One SSP-RK2 (Heun, Shu-Osher form) step u -> out; tmp holds the first stage."""
+        self.ssp_stage(u, tmp, dt, f=f, stream=stream)
+        self.ssp_stage(tmp, out, dt, f=f, w=u, a=0.5, b=0.5, stream=stream)
+        return out
 
     def apply_host(self, z_host, y_host):
         """End-to-end: host arrays in, host array out (copies inside the call)."""

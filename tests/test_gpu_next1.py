@@ -243,3 +243,54 @@ def test_device_tensor_field_matches_host_recipe():
     own = (gx + cfg.ncells[0] * (gy + cfg.ncells[1] * gz)).reshape(-1)
     assert np.array_equal(D_dev, inputs.tensor_field_cells(own, 6))
     op.close()
+
+
+# ------------------------------------------------------------------ NEXT-2: fused SSP-RK stages
+@pytest.mark.parametrize("general,periodic,k", [(False, (0, 0, 0), 2), (False, (1, 1, 1), 7), (True, (1, 0, 1), 3),
+                                                (True, (0, 0, 0), 7)])
+def test_ssp_stages_vs_oracle(general, periodic, k):
+    """Euler and Heun stages (out = a w + b (z + dt M^-1 (f - A z))) fused into
+    the kernel's store, against O-1 + the same arithmetic written out in oracle/o1.ssp_stage."""
+    from paper_1711_10885_b200 import dg
+    cfg = configs.small(k, ncells=(4, 3, 2), hi=(1.0, 0.75, 0.5), b=(-0.8, 0.4, 0.3), c=0.6)
+    Dc = spd_field(cfg.ncell, 9) if general else None
+    op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma,
+                     bc=dg.bc_from_periodic(periodic))
+    if general:
+        op.set_diffusion(torch.from_numpy(Dc.reshape(-1)).cuda())
+    zn, fn = inputs.uniform(cfg.ndofs, 1), inputs.uniform(cfg.ndofs, 2)
+    z, f = torch.from_numpy(zn).cuda(), torch.from_numpy(fn).cuda()
+    dt = 2e-4
+    e1 = torch.full_like(z, float("nan"))
+    op.ssp_stage(z, e1, dt, f=f)
+    h2 = torch.full_like(z, float("nan"))
+    op.ssp_stage(e1, h2, dt, f=f, w=z, a=0.5, b=0.5)
+    h3 = torch.full_like(z, float("nan"))
+    op.heun_step(z, dt, torch.empty_like(z), h3, f=f)
+    torch.cuda.synchronize()
+    op.close()
+    kw = {"periodic": periodic, "Dcell": Dc}
+    e1r = o1.ssp_stage(*cfg.args(), zn, dt, f=fn, **kw)
+    h2r = o1.ssp_stage(*cfg.args(), e1.cpu().numpy(), dt, f=fn, w=zn, a=0.5, bcoef=0.5, **kw)
+    assert rel(e1.cpu().numpy(), e1r) < TOL
+    assert rel(h2.cpu().numpy(), h2r) < TOL
+    assert np.array_equal(h2.cpu().numpy(), h3.cpu().numpy())
+
+
+def test_ssp_gpu_conserves_mass_periodic():
+    """Periodic, c = 0, f = 0: 100 Heun steps keep sum_e z_(e,0) to rounding."""
+    from paper_1711_10885_b200 import dg
+    cfg = configs.small(5, ncells=(4, 4, 4), hi=(1.0, 1.0, 1.0), b=(1.0, -0.5, 0.25), c=0.0)
+    op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma,
+                     bc=dg.bc_from_periodic((1, 1, 1)))
+    op.set_diffusion(torch.from_numpy(spd_field(cfg.ncell, 4).reshape(-1) * 1e-3).cuda())
+    u = torch.from_numpy(inputs.uniform(cfg.ndofs, 3)).cuda()
+    m0 = float(u.view(cfg.ncell, -1)[:, 0].sum())
+    tmp, nxt = torch.empty_like(u), torch.empty_like(u)
+    for _ in range(100):
+        op.heun_step(u, 1e-4, tmp, nxt)
+        u, nxt = nxt, u
+    torch.cuda.synchronize()
+    op.close()
+    m1 = float(u.view(cfg.ncell, -1)[:, 0].sum())
+    assert np.isfinite(m1) and abs(m1 - m0) < 1e-12 * float(u.abs().sum())

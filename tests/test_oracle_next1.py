@@ -186,3 +186,38 @@ def test_uniform_field_equals_constant_D():
     ya, _ = o1.apply(*args, z, periodic=(0, 1, 0))
     yb, _ = o1.apply(*args, z, periodic=(0, 1, 0), Dcell=np.tile(D, (12, 1, 1)))
     assert np.array_equal(ya, yb)
+
+
+# ------------------------------------------------------------------ NEXT-2: explicit SSP stages
+@pytest.mark.parametrize("k", [1, 3])
+def test_ssp_pure_reaction_closed_form(k):
+    """D = 0, b = 0: A = c Delta_T I, so M^-1 A = c and forward Euler gives z (1 - c dt), Heun
+    z (1 - c dt + (c dt)^2 / 2) -- the textbook stability polynomials of the two methods."""
+    nc, lo, hi = (3, 2, 2), (0, 0, 0), (1.5, 1.0, 0.5)
+    n3 = (k + 1) ** 3
+    z = inputs.uniform(12 * n3, 3)
+    args = (nc, lo, hi, k, np.zeros(9), (0, 0, 0), 0.7, 10.0)
+    dt = 0.3
+    e1 = o1.ssp_stage(*args, z, dt)
+    assert rel(e1, z * (1 - 0.7 * dt)) < 1e-14
+    h2 = o1.ssp_stage(*args, e1, dt, w=z, a=0.5, bcoef=0.5)
+    assert rel(h2, z * (1 - 0.7 * dt + (0.7 * dt) ** 2 / 2)) < 1e-14
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_ssp_conserves_mass_periodic(k):
+    """Periodic box, c = 0, f = 0: a_h(u, 1) = 0 term by term (grad 1 = 0, [[1]] = 0), so every
+    stage conserves the integral of u = Delta_T sum_e z_(e, 0)."""
+    nc, lo, hi = MESH
+    n3 = (k + 1) ** 3
+    z = inputs.uniform(12 * n3, 5)
+    args = (nc, lo, hi, k, np.eye(3), (0.8, -0.4, 0.3), 0.0, 30.0)
+    Dc = spd_field(12, 8)
+    mass = lambda v: v.reshape(12, n3)[:, 0].sum()
+    e1 = o1.ssp_stage(*args, z, 1e-3, periodic=(1, 1, 1), Dcell=Dc)
+    h2 = o1.ssp_stage(*args, e1, 1e-3, w=z, a=0.5, bcoef=0.5, periodic=(1, 1, 1), Dcell=Dc)
+    assert abs(mass(e1) - mass(z)) < 1e-13 * np.abs(z).sum()
+    assert abs(mass(h2) - mass(z)) < 1e-13 * np.abs(z).sum()
+    # control: with Dirichlet faces the boundary fluxes change the mass
+    d1 = o1.ssp_stage(*args, z, 1e-3, Dcell=Dc)
+    assert abs(mass(d1) - mass(z)) > 1e-8
