@@ -21,7 +21,8 @@ class _Problem(ctypes.Structure):
     _fields_ = [("nc", ctypes.c_int64 * 3), ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
                 ("k", ctypes.c_int), ("D", ctypes.c_double * 9), ("b", ctypes.c_double * 3),
                 ("c", ctypes.c_double), ("sigma", ctypes.c_double), ("periodic", ctypes.c_int * 3),
-                ("Dcell", ctypes.c_void_p)]
+                ("Dcell", ctypes.c_void_p), ("m", ctypes.c_int), ("bkind", ctypes.c_int),
+                ("bamp", ctypes.c_double * 3)]
 
 
 def build(force=False):
@@ -49,8 +50,12 @@ def lib():
     return _lib
 
 
-def _problem(ncells, lo, hi, k, D, b, c, sigma, periodic=(0, 0, 0), Dcell=None):
+def _problem(ncells, lo, hi, k, D, b, c, sigma, periodic=(0, 0, 0), Dcell=None, m=0, bkind=0, bamp=(1.0, 1.0, 1.0)):
     P = _Problem()
+    P.m = int(m)
+    P.bkind = int(bkind)
+    for q in range(3):
+        P.bamp[q] = float(bamp[q])
     for q in range(3):
         P.periodic[q] = 1 if periodic[q] else 0
     P.Dcell = None if Dcell is None else Dcell.ctypes.data
@@ -78,13 +83,16 @@ def tables(k):
     return arrs
 
 
-def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL, cells=None, nthreads=0, periodic=(0, 0, 0), Dcell=None):
+def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL, cells=None, nthreads=0, periodic=(0, 0, 0), Dcell=None,
+          m=0, bkind=0, bamp=(1.0, 1.0, 1.0)):
     """y = A z (mask selects volume / interior-face / boundary-face terms).
 
     cells=None: full vector. cells=int64 array: returns the compact blocks of
     those cells only, shape (len(cells), n^3) (sampled mode). Returns (y, threads).
     periodic[q]: glue the two sides normal to q (NEXT-1). Dcell: per-cell diffusion
-    tensors, array [ncells_total, 3, 3] in global cell order (NEXT-1; D is then ignored)."""
+    tensors, array [ncells_total, 3, 3] in global cell order (NEXT-1; D is then ignored).
+    m: Gauss points per direction (0: k+1; NEXT-3 over-integration). bkind: 0 constant b,
+    1 Taylor-Green field, 2 linear test field (x2, x3, x1); times bamp."""
     n3 = (k + 1) ** 3
     ncell_total = int(ncells[0]) * int(ncells[1]) * int(ncells[2])
     z = np.ascontiguousarray(z, dtype=np.float64)
@@ -94,7 +102,7 @@ def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL, cells=None, nthreads=0
         Dcell = np.ascontiguousarray(Dcell, dtype=np.float64).reshape(-1, 9)
         if Dcell.shape[0] != ncell_total:
             raise ValueError("Dcell has %d tensors, expected %d" % (Dcell.shape[0], ncell_total))
-    P = _problem(ncells, lo, hi, k, D, b, c, sigma, periodic, Dcell)
+    P = _problem(ncells, lo, hi, k, D, b, c, sigma, periodic, Dcell, m, bkind, bamp)
     if cells is None:
         y = np.zeros(ncell_total * n3)
         used = lib().o1_apply(ctypes.byref(P), z.ctypes.data, y.ctypes.data, mask, None, 0, 0, nthreads)
@@ -111,7 +119,7 @@ def apply(ncells, lo, hi, k, D, b, c, sigma, z, mask=ALL, cells=None, nthreads=0
 
 
 def ssp_stage(ncells, lo, hi, k, D, b, c, sigma, z, dt, f=None, w=None, a=0.0, bcoef=1.0, periodic=(0, 0, 0),
-              Dcell=None):
+              Dcell=None, **kw):
     """One explicit SSP Runge-Kutta stage in Shu-Osher form, written out from PAPER.md:366-373:
     M z^(k+1) = M z^(k) + dt (f - A z^(k)) with M = (phi_j, phi_i) = Delta_T I for the orthonormal
     Legendre basis on cuboid cells, generalised to out = a w + b (z + dt M^-1 (f - A z)).
@@ -119,7 +127,7 @@ def ssp_stage(ncells, lo, hi, k, D, b, c, sigma, z, dt, f=None, w=None, a=0.0, b
     n3 = (k + 1) ** 3
     h = [(hi[q] - lo[q]) / ncells[q] for q in range(3)]
     dT = h[0] * h[1] * h[2]
-    Az, _ = apply(ncells, lo, hi, k, D, b, c, sigma, z, periodic=periodic, Dcell=Dcell)
+    Az, _ = apply(ncells, lo, hi, k, D, b, c, sigma, z, periodic=periodic, Dcell=Dcell, **kw)
     r = (np.zeros_like(Az) if f is None else np.asarray(f, dtype=np.float64)) - Az
     znew = np.asarray(z, dtype=np.float64) + (dt / dT) * r
     out = bcoef * znew

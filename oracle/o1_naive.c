@@ -50,7 +50,28 @@ typedef struct {
     double sigma;      /* D-independent penalty factor (C-4) */
     int periodic[3];   /* per direction: 0 = both sides weak Dirichlet, 1 = periodic (NEXT-1) */
     const double* Dcell; /* NULL: D above everywhere; else per-cell tensors [cell][9] (NEXT-1) */
+    int m;             /* Gauss points per direction; 0 -> k+1 (NEXT-3 over-integration) */
+    int bkind;         /* 0: constant b above; 1: Taylor-Green; 2: linear test field (NEXT-2) */
+    double bamp[3];    /* per-component amplitude of the field (bkind != 0) */
 } o1_problem;
+
+/* b(x) at a physical point (bkind != 0): the field times bamp (header). */
+static void o1_velocity(const o1_problem* P, const double x[3], double b[3])
+{
+    if (P->bkind == 1) {
+        b[0] = cos(x[0]) * sin(-x[1]) * sin(-x[2]);
+        b[1] = 0.5 * sin(x[0]) * cos(-x[1]) * sin(-x[2]);
+        b[2] = 0.5 * sin(x[0]) * sin(-x[1]) * cos(-x[2]);
+    } else if (P->bkind == 2) {
+        b[0] = x[1];
+        b[1] = x[2];
+        b[2] = x[0];
+    } else {
+        b[0] = P->b[0]; b[1] = P->b[1]; b[2] = P->b[2];
+        return;
+    }
+    for (int r = 0; r < 3; ++r) b[r] *= P->bamp[r];
+}
 
 enum { O1_VOLUME = 1, O1_INTERIOR = 2, O1_BOUNDARY = 4 };
 
@@ -123,7 +144,7 @@ int o1_tables(int k, double* xi, double* w, double* theta_at, double* dtheta_at,
 }
 
 typedef struct {
-    int n;
+    int n, m;
     double h[3];
     double xi[O1_NMAX], w[O1_NMAX];
     double th[O1_NMAX][O1_NMAX], dth[O1_NMAX][O1_NMAX];  /* [point][basis] */
@@ -187,7 +208,7 @@ static double o1_harmonic(double a, double b)
 static void o1_cell(const o1_problem* P, const o1_tab* T, const double* z, int64_t e,
                     unsigned mask, double* yc)
 {
-    int n = T->n, m = T->n;
+    int n = T->n, m = T->m;
     int64_t n3 = (int64_t)n * n * n;
     int64_t ic[3];
     ic[0] = e % P->nc[0];
@@ -208,9 +229,12 @@ static void o1_cell(const o1_problem* P, const o1_tab* T, const double* z, int64
                     double u, g[3];
                     o1_eval(T, zc, p, &u, g);
                     double W = dT * T->w[a1] * T->w[a2] * T->w[a3];
+                    double xp[3], bp[3];
+                    for (int r = 0; r < 3; ++r) xp[r] = P->lo[r] + ((double)ic[r] + T->xi[p[r]]) * T->h[r];
+                    o1_velocity(P, xp, bp);
                     double F[3];
                     for (int r = 0; r < 3; ++r)
-                        F[r] = W * (D[3 * r + 0] * g[0] + D[3 * r + 1] * g[1] + D[3 * r + 2] * g[2] - P->b[r] * u);
+                        F[r] = W * (D[3 * r + 0] * g[0] + D[3 * r + 1] * g[1] + D[3 * r + 2] * g[2] - bp[r] * u);
                     o1_accum(T, yc, p, W * P->c * u, F);
                 }
     }
@@ -242,6 +266,11 @@ static void o1_cell(const o1_problem* P, const o1_tab* T, const double* z, int64
                     double W = dF * T->w[b1] * T->w[b2];
                     double u, g[3];
                     o1_eval(T, zc, pown, &u, g);
+                    double xf[3], bf[3];     /* the face point (own cell's coordinates) and b there */
+                    xf[q] = P->lo[q] + ((double)ic[q] + (double)s) * T->h[q];
+                    xf[t1] = P->lo[t1] + ((double)ic[t1] + T->xi[b1]) * T->h[t1];
+                    xf[t2] = P->lo[t2] + ((double)ic[t2] + T->xi[b2]) * T->h[t2];
+                    o1_velocity(P, xf, bf);
                     if (interior) {
                         /* nu = +e_q oriented from T- (low cell) to T+ (high cell) */
                         double un, gn[3];
@@ -256,7 +285,7 @@ static void o1_cell(const o1_problem* P, const o1_tab* T, const double* z, int64
                         if (dm + dp == 0.0) { wm = 0.5; wp = 0.5; }  /* C-5 */
                         else { wm = dp / (dm + dp); wp = dm / (dm + dp); }
                         double gam = o1_harmonic(dm, dp) * P->sigma;
-                        double bn = P->b[q];
+                        double bn = bf[q];
                         double Phi = (bn >= 0.0) ? bn * um : bn * up;
                         double J = um - up;
                         double Avg = wm * sm + wp * sp;          /* C-1: "+" reading */
@@ -272,7 +301,7 @@ static void o1_cell(const o1_problem* P, const o1_tab* T, const double* z, int64
                     } else {
                         /* Dirichlet boundary face, outward normal nu = (2s-1) e_q */
                         double nu = s ? 1.0 : -1.0;
-                        double bn = nu * P->b[q];
+                        double bn = nu * bf[q];
                         double sn = nu * (D[3 * q + 0] * g[0] + D[3 * q + 1] * g[1] + D[3 * q + 2] * g[2]);
                         double Phi = (bn >= 0.0) ? bn * u : 0.0;   /* Phi(u, 0, b_nu) */
                         double gam = Dqq * P->sigma;               /* C-6 */
@@ -289,10 +318,12 @@ static void o1_cell(const o1_problem* P, const o1_tab* T, const double* z, int64
 static void o1_setup_tab(const o1_problem* P, o1_tab* T)
 {
     int n = P->k + 1;
+    int m = P->m > 0 ? P->m : n;
     T->n = n;
+    T->m = m;
     for (int q = 0; q < 3; ++q) T->h[q] = (P->hi[q] - P->lo[q]) / (double)P->nc[q];
-    o1_gauss(n, T->xi, T->w);
-    for (int i = 0; i < n; ++i) o1_theta(n, T->xi[i], T->th[i], T->dth[i]);
+    o1_gauss(m, T->xi, T->w);
+    for (int i = 0; i < m; ++i) o1_theta(n, T->xi[i], T->th[i], T->dth[i]);
     o1_theta(n, 0.0, T->th_end[0], T->dth_end[0]);
     o1_theta(n, 1.0, T->th_end[1], T->dth_end[1]);
 }
@@ -305,7 +336,7 @@ static void o1_setup_tab(const o1_problem* P, o1_tab* T)
 int o1_apply(const o1_problem* P, const double* z, double* y, unsigned mask,
              const int64_t* cells, int64_t ncell_list, int compact, int nthreads)
 {
-    if (P->k < 0 || P->k + 1 > O1_NMAX) return -1;
+    if (P->k < 0 || P->k + 1 > O1_NMAX || P->m > O1_NMAX || (P->m > 0 && P->m < P->k + 1)) return -1;
     o1_tab T;
     o1_setup_tab(P, &T);
     int64_t n3 = (int64_t)T.n * T.n * T.n;

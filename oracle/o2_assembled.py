@@ -24,6 +24,10 @@ NEXT-1 (the paper's Problem A): `periodic[q]` glues the two bo
 sides normal to q (the wrap face is an interior face, T- = the last cell, nu = +e_q);
 `Dcell[e]` gives cell e its own tensor, so D-, D+, the weights w+- and the harmonic
 penalty <d-, d+> differ per face.
+
+NEXT-2/3 (the Taylor-Green run): `m` Gauss points per direction
+(over-integration, q = 2p+4 -> m = k+3) and a velocity field `bfield(x) -> b` evaluated at
+every quadrature point of volumes and faces.
 """
 import numpy as np
 
@@ -61,7 +65,20 @@ def _basis_on(n, pts_per_dir, h):
     return phi, grad
 
 
-def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic=(0, 0, 0), Dcell=None):
+def taylor_green(x):
+    """eq:2: x of shape (3, npts) -> b of shape (3, npts)."""
+    return np.stack([np.cos(x[0]) * np.sin(-x[1]) * np.sin(-x[2]),
+                     0.5 * np.sin(x[0]) * np.cos(-x[1]) * np.sin(-x[2]),
+                     0.5 * np.sin(x[0]) * np.sin(-x[1]) * np.cos(-x[2])])
+
+
+def linear_field(x):
+    """The linear divergence-free test field b = (x2, x3, x1)."""
+    return np.stack([x[1], x[2], x[0]])
+
+
+def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic=(0, 0, 0), Dcell=None, m=0,
+             bfield=None):
     """Dense A (N x N), N = prod(ncells) * (k+1)^3, cell-major global order (C-3).
 
     avg_sign = -1 selects the weighted average exactly as PAPER.md:271 prints it
@@ -80,15 +97,30 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic
     dT = h[0] * h[1] * h[2]
     ncell = nc[0] * nc[1] * nc[2]
     A = np.zeros((ncell * n3, ncell * n3))
-    xi, w = gauss01(n)
+    m = m if m else n
+    xi, w = gauss01(m)
+
+    def points(ic, pts_per_dir):
+        """physical coordinates (3, npts) of the tensor point set, x fastest (as _tensor orders it)."""
+        X = [lo[q] + (ic[q] + np.asarray(pts_per_dir[q], float)) * h[q] for q in range(3)]
+        gz, gy, gx = np.meshgrid(X[2], X[1], X[0], indexing="ij")
+        return np.stack([gx.ravel(), gy.ravel(), gz.ravel()])
+
+    def velocity(ic, pts_per_dir):
+        npts = np.prod([np.size(v) for v in pts_per_dir])
+        if bfield is None:
+            return np.tile(b[:, None], (1, npts))
+        return bfield(points(ic, pts_per_dir))
 
     # ---- volume blocks (coefficients constant per cell, uniform cells)
     if mask & VOLUME:
         phi, grad = _basis_on(n, [xi, xi, xi], h)
         W = dT * np.einsum("a,b,c->cba", w, w, w).reshape(-1)
         for e in range(ncell):
+            ic = (e % nc[0], (e // nc[0]) % nc[1], e // (nc[0] * nc[1]))
+            bp = velocity(ic, [xi, xi, xi])                       # (3, npts)
             # integrand (D grad u - b u) . grad v + c u v, u = phi_j (columns), v = phi_i (rows)
-            flux = np.einsum("rs,spj->rpj", Dcell[e], grad) - b[:, None, None] * phi[None, :, :]
+            flux = np.einsum("rs,spj->rpj", Dcell[e], grad) - bp[:, :, None] * phi[None, :, :]
             Avol = np.einsum("p,rpi,rpj->ij", W, grad, flux) + c * np.einsum("p,pi,pj->ij", W, phi, phi)
             A[e * n3:(e + 1) * n3, e * n3:(e + 1) * n3] += Avol
 
@@ -134,8 +166,10 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic
                         else:
                             wm, wp = dp / (dm + dp), dm / (dm + dp)
                         gam = (0.0 if dm + dp == 0.0 else 2 * dm * dp / (dm + dp)) * sigma
-                        bnu = b @ nu
-                        Phi = bnu * um if bnu >= 0 else bnu * up          # linear in the trial function
+                        fpts = [None, None, None]
+                        fpts[q], fpts[t[0]], fpts[t[1]] = np.array([1.0]), xi, xi
+                        bnu = velocity(ic, fpts)[q][:, None]              # b . nu per face point
+                        Phi = np.where(bnu >= 0, bnu * um, bnu * up)      # linear in the trial function
                         nDg = (wm * np.einsum("r,rs,spj->pj", nu, Dm, gm)
                                + avg_sign * wp * np.einsum("r,rs,spj->pj", nu, Dp, gp))   # nu.{D grad .}_w
                         jump = um - up
@@ -156,8 +190,10 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic
                                 D = Dcell[e]
                                 phs, grs = (phi1, grad1) if s == 1 else (phi0, grad0)
                                 nuo = nu * (1.0 if s == 1 else -1.0)
-                                bnu = b @ nuo
-                                Phi = bnu * phs if bnu >= 0 else 0.0 * phs      # Phi(u, 0, b_nu)
+                                fpts = [None, None, None]
+                                fpts[q], fpts[t[0]], fpts[t[1]] = np.array([float(s)]), xi, xi
+                                bnu = (velocity(ic, fpts).T @ nuo)[:, None]
+                                Phi = np.where(bnu >= 0, bnu * phs, 0.0)         # Phi(u, 0, b_nu)
                                 sn = np.einsum("r,rs,spj->pj", nuo, D, grs)     # nu.D grad
                                 gam = (nuo @ D @ nuo) * sigma
                                 B = (np.einsum("p,pi,pj->ij", Wf, phs, Phi)

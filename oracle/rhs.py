@@ -76,11 +76,13 @@ class KinkedField:
         return np.broadcast_to(vx[None, None, :], (np.size(z), np.size(y), np.size(x))).copy()
 
 
-def consistency_data(ncells, lo, hi, k, D, b, c, sigma, seed=0, Dcell=None, field=None):
+def consistency_data(ncells, lo, hi, k, D, b, c, sigma, seed=0, Dcell=None, field=None, bfield=None):
     """Return (z_star, F) for a seeded random u* in Q_k (all boundary faces Dirichlet).
 
     Dcell ([ncell, 3, 3], NEXT-1): per-cell tensors for f and the Dirichlet terms of l_h.
-    field: any object with eval(x, y, z, d) (default: PolyField of degree k with `seed`)."""
+    field: any object with eval(x, y, z, d) (default: PolyField of degree k with `seed`).
+    bfield: velocity field b(x) (x: (3, npts) -> (3, npts), NEXT-2); default the constant b.
+    Quadrature: k+1 Gauss points per direction (exact for polynomial data of the tests)."""
     nc = [int(v) for v in ncells]
     n = k + 1
     D0 = np.asarray(D, float).reshape(3, 3)
@@ -108,10 +110,11 @@ def consistency_data(ncells, lo, hi, k, D, b, c, sigma, seed=0, Dcell=None, fiel
                 z[e] = np.einsum("kji,kc,jb,ia->cba", Wv * us, th, th, th) / dT
                 # f = -sum_rs D_rs d_r d_s u* + b . grad u* + c u*
                 f = c * us
+                bv = _velocity(b, bfield, X, Y, Zc)          # [r][z, y, x]
                 for r in range(3):
                     dr = [0, 0, 0]
                     dr[r] += 1
-                    f = f + b[r] * u.eval(X, Y, Zc, tuple(dr))
+                    f = f + bv[r] * u.eval(X, Y, Zc, tuple(dr))
                     for s in range(3):
                         if D[r, s] != 0.0:
                             drs = [0, 0, 0]
@@ -126,11 +129,11 @@ def consistency_data(ncells, lo, hi, k, D, b, c, sigma, seed=0, Dcell=None, fiel
                             continue
                         nu = np.zeros(3)
                         nu[q] = 1.0 if s == 1 else -1.0
-                        bnu = nu @ b
                         gam = (nu @ D @ nu) * sigma
                         pts = [X, Y, Zc]
                         pts[q] = np.array([lo[q] + (ic[q] + s) * h[q]])
                         g = u.eval(*pts)                            # [z,y,x] with size-1 axis q
+                        bnu = nu[q] * _velocity(b, bfield, *pts)[q]  # b . nu per face point
                         Wf = dT / h[q] * np.ones_like(g)
                         for r in range(3):
                             if r != q:
@@ -147,11 +150,20 @@ def consistency_data(ncells, lo, hi, k, D, b, c, sigma, seed=0, Dcell=None, fiel
                                  np.einsum("kc,jb,ia->kjicba", V[2], G[1], V[0]) / h[1],
                                  np.einsum("kc,jb,ia->kjicba", G[2], V[1], V[0]) / h[2]]
                         nDgrad = sum(nu[r2] * D[r2, s2] * grads[s2] for r2 in range(3) for s2 in range(3))
-                        phi_in = 0.0 if bnu >= 0 else bnu       # Phi(0, g, b_nu) = b_nu g on inflow
+                        phi_in = np.where(bnu >= 0, 0.0, bnu)   # Phi(0, g, b_nu) = b_nu g on inflow
                         integrand = (-phi_in * g + gam * g)[..., None, None, None] * phi \
                             - g[..., None, None, None] * nDgrad
                         F[e] += np.einsum("kji,kjicba->cba", Wf, integrand)
     return z.reshape(-1), F.reshape(-1)
+
+
+def _velocity(b, bfield, X, Y, Z):
+    """b at the tensor grid X (fastest) x Y x Z: array [3][z, y, x]."""
+    gz, gy, gx = np.meshgrid(np.atleast_1d(Z), np.atleast_1d(Y), np.atleast_1d(X), indexing="ij")
+    if bfield is None:
+        return np.stack([np.full(gx.shape, float(b[r])) for r in range(3)])
+    pts = np.stack([gx.ravel(), gy.ravel(), gz.ravel()])
+    return bfield(pts).reshape((3,) + gx.shape)
 
 
 def upwind_energy(ncells, lo, hi, k, b, z):
