@@ -142,6 +142,23 @@ const char* dg_strerror(int code);
  * entry, bad flags), DG_ENOMEM, DG_ECUDA, DG_ENCCL. Not timed. */
 int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags, void* stream);
 
+/* Velocity field b(x) evaluated at every quadrature point (NEXT-2: the paper's Taylor-Green
+ * transport run):
+ *   kind 0: the constant b of dg_setup (default);
+ *   kind 1: Taylor-Green, b = (cos x1 sin(-x2) sin(-x3), 1/2 sin x1 cos(-x2) sin(-x3),
+ *           1/2 sin x1 sin(-x2) cos(-x3)) (eq:2), x the physical coordinates;
+ *   kind 2: the linear divergence-free test field b = (x2, x3, x1);
+ * each component times amp[r]. b is continuous, so b.nu is evaluated once per face point
+ * (reading N-4); a periodic box needs a box-periodic field (Taylor-Green on (-pi, pi)^3).
+ * Runs on the variable-velocity kernel (constant diagonal D; k <= 8).
+ * Errors: DG_EINVAL (kind, non-finite amp), DG_EUNSUPPORTED (per-cell / full D set, k > 8). */
+int dg_set_velocity(dg_ctx* ctx, int kind, const double amp[3]);
+
+/* Gauss points per direction m (NEXT-3 over-integration; q = 2p + 4 is m = k + 3, PAPER.md:950-956,
+ * :1102-1104). m = k + 1 (default) or k + 3 with k <= 8. Errors: DG_EINVAL (m < k + 1),
+ * DG_EUNSUPPORTED (other m, per-cell / full D set). */
+int dg_set_quadrature(dg_ctx* ctx, int m);
+
 /* ---- halo plumbing (multi-rank; also used by the single-process loopback test) ----
  * face f = 2q + s (q = direction, s = 0 low / 1 high side of this rank's box).
  * neighbor_rank = -1 when the face lies on the domain boundary. count = doubles in the

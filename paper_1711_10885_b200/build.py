@@ -22,10 +22,18 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.
 NS = list(range(2, 12))
 
 
+# (n, m) pairs of the variable-velocity / over-integrated kernel: m = n (q = 2p) and m = n + 2
+# (q = 2p + 4, the paper's Taylor-Green run), k <= 8
+VB = [(n, m) for n in range(2, 10) for m in (n, n + 2)]
+
+
 def _sources():
     jobs = []
     for n in NS:
         jobs.append((os.path.join(CSRC, "dg_cell_inst.cu"), os.path.join(OBJ, "dg_cell_n%d.o" % n), ["-DDG_N=%d" % n]))
+    for n, m in VB:
+        jobs.append((os.path.join(CSRC, "dg_vb_inst.cu"), os.path.join(OBJ, "dg_vb_n%d_m%d.o" % (n, m)),
+                     ["-DDG_N=%d" % n, "-DDG_M=%d" % m]))
     for name in ("dg_aux.cu", "dg_abi.cpp", "dg_dispatch.cpp", "dg_nccl.cpp", "tables.cpp"):
         base = os.path.splitext(name)[0]
         extra = ["-x", "cu"] if name.endswith(".cpp") else []

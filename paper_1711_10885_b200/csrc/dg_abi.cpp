@@ -42,8 +42,17 @@ struct dg_ctx {
     double* dsend[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     double* drecv[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int* dbad = nullptr;             // validation flag of dg_set_diffusion
+    // variable-velocity / over-integrated path (dg_vb.cuh)
+    int m = 0;                       // Gauss points per direction (k+1 or k+3)
+    bool vb = false;                 // launch dg_vb_kernel
     KParams base;
 };
+
+static cudaError_t launch_any(const dg_ctx* ctx, const KParams& p, cudaStream_t s)
+{
+    if (ctx->vb) return launch_vb(ctx->k, ctx->m, p, s);
+    return ctx->general ? launch_gen(ctx->k, p, s) : launch_cell(ctx->k, p, s);
+}
 
 static std::mutex g_tab_mu;
 static bool g_tab_done[64][KMAX + 1];
@@ -207,8 +216,12 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
         p.per[q] = ctx->per[q];
         p.wrap[q] = ctx->per[q] && ctx->parts[q] == 1;
         p.h[q] = h[q];
+        p.lo[q] = mesh->lo[q];
+        p.bamp[q] = 1.0;
     }
     p.sigma = sigma;
+    p.bkind = 0;
+    ctx->m = k + 1;
     for (int r = 0; r < 3; ++r)
         for (int s = 0; s < 3; ++s) p.Dhat[3 * r + s] = D[3 * r + s] / (h[r] * h[s]);
     p.c = c;
@@ -306,6 +319,60 @@ static int alloc_dfield(dg_ctx* ctx)
     return DG_OK;
 }
 
+static std::mutex g_vb_mu;
+static bool g_vb_done[64][KMAX + 1][NMAX + 1];
+
+// switch between the fast kernels and the variable-velocity / over-integrated kernel
+static int update_vb(dg_ctx* ctx)
+{
+    const bool want = ctx->base.bkind != 0 || ctx->m != ctx->k + 1;
+    if (!want) { ctx->vb = false; return DG_OK; }
+    if (ctx->general) return DG_EUNSUPPORTED;                 // per-cell / full D with b(x): not built
+    if (!vb_available(ctx->k, ctx->m)) return DG_EUNSUPPORTED;
+    std::lock_guard<std::mutex> lk(g_vb_mu);
+    if (!g_vb_done[ctx->device][ctx->k][ctx->m]) {
+        HostTables t;
+        if (build_tables_m(ctx->k, ctx->m, &t) != 0) return DG_EINVAL;
+        if (upload_tables_vb(ctx->k, ctx->m, t) != 0) return DG_ECUDA;
+        g_vb_done[ctx->device][ctx->k][ctx->m] = true;
+    }
+    ctx->vb = true;
+    return DG_OK;
+}
+
+extern "C" int dg_set_velocity(dg_ctx* ctx, int kind, const double amp[3])
+{
+    if (!ctx || kind < 0 || kind > 2 || (kind != 0 && !amp)) return DG_EINVAL;
+    for (int r = 0; r < 3 && kind; ++r)
+        if (!std::isfinite(amp[r])) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    const int old_kind = ctx->base.bkind;
+    double old_amp[3] = {ctx->base.bamp[0], ctx->base.bamp[1], ctx->base.bamp[2]};
+    ctx->base.bkind = kind;
+    for (int r = 0; r < 3; ++r) ctx->base.bamp[r] = kind ? amp[r] : 1.0;
+    const int rc = update_vb(ctx);
+    if (rc != DG_OK) {
+        ctx->base.bkind = old_kind;
+        for (int r = 0; r < 3; ++r) ctx->base.bamp[r] = old_amp[r];
+        update_vb(ctx);
+    }
+    return rc;
+}
+
+extern "C" int dg_set_quadrature(dg_ctx* ctx, int m)
+{
+    if (!ctx || m < ctx->k + 1 || m > NMAX) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    const int old = ctx->m;
+    ctx->m = m;
+    const int rc = update_vb(ctx);
+    if (rc != DG_OK) {
+        ctx->m = old;
+        update_vb(ctx);
+    }
+    return rc;
+}
+
 extern "C" int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags, void* stream)
 {
     if (!ctx || (flags & ~(unsigned)DG_HALO_EXTERNAL)) return DG_EINVAL;
@@ -320,6 +387,7 @@ extern "C" int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags
         ctx->general = false;
         return DG_OK;
     }
+    if (ctx->vb) return DG_EUNSUPPORTED;   // b(x) / over-integration run on constant diagonal D only
     int rc = alloc_dfield(ctx);
     if (rc != DG_OK) return rc;
     if (!Dcell) {
@@ -438,7 +506,7 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         p.task_list = nullptr;
         for (int q = 0; q < 3; ++q) { p.task_lo[q] = 0; p.task_cnt[q] = ctx->nloc[q]; }
         p.ntasks = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2];
-        return cuda_rc(ctx->general ? launch_gen(ctx->k, p, s) : launch_cell(ctx->k, p, s));
+        return cuda_rc(launch_any(ctx, p, s));
     }
     // (iv) of SURVEY.md 3: pack partition layers, exchange on the comm stream, overlap with inner cells
     const bool need_comm = !external && (p.mask & DG_INTERIOR_FACES);
@@ -476,9 +544,7 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
     p.task_list = nullptr;
     for (int q = 0; q < 3; ++q) { p.task_lo[q] = ctx->inner_lo[q]; p.task_cnt[q] = ctx->inner_cnt[q]; }
     p.ntasks = ctx->inner_cnt[0] * ctx->inner_cnt[1] * ctx->inner_cnt[2];
-    auto launch = [&](const KParams& kp) {
-        return ctx->general ? launch_gen(ctx->k, kp, s) : launch_cell(ctx->k, kp, s);
-    };
+    auto launch = [&](const KParams& kp) { return launch_any(ctx, kp, s); };
     DG_CUDA(launch(p));
     if (need_comm) DG_CUDA(cudaStreamWaitEvent(s, ctx->ev_recv, 0));
     p.task_list = ctx->shell;
@@ -535,7 +601,7 @@ static int apply_host_pipelined(dg_ctx* ctx, const double* z_host, double* y_hos
             p.task_lo[0] = 0; p.task_lo[1] = 0; p.task_lo[2] = z0;
             p.task_cnt[0] = ctx->nloc[0]; p.task_cnt[1] = ctx->nloc[1]; p.task_cnt[2] = cnt;
             p.ntasks = ctx->nloc[0] * ctx->nloc[1] * cnt;
-            DG_CUDA(ctx->general ? launch_gen(ctx->k, p, sc) : launch_cell(ctx->k, p, sc));
+            DG_CUDA(launch_any(ctx, p, sc));
             DG_CUDA(cudaEventRecord(ctx->ev_done, sc));
             DG_CUDA(cudaStreamWaitEvent(sd, ctx->ev_done, 0));
             DG_CUDA(cudaMemcpyAsync(y_host + z0 * layer, ctx->hy + z0 * layer, (size_t)(cnt * layer) * sizeof(double),
@@ -666,7 +732,9 @@ extern "C" int dg_get_kernel_info(const dg_ctx* ctx, dg_kernel_info* info)
     if (!ctx || !info) return DG_EINVAL;
     DG_CUDA(cudaSetDevice(ctx->device));
     LaunchInfo li;
-    if ((ctx->general ? gen_launch_info(ctx->k, &li) : cell_launch_info(ctx->k, &li)) != 0) return DG_ECUDA;
+    const int rc = ctx->vb ? vb_launch_info(ctx->k, ctx->m, &li)
+                           : (ctx->general ? gen_launch_info(ctx->k, &li) : cell_launch_info(ctx->k, &li));
+    if (rc != 0) return DG_ECUDA;
     info->launches_per_apply = ctx->partitioned ? 2 : 1;
     info->cells_per_cta = li.cells_per_cta;
     info->threads_per_cta = li.threads;

@@ -55,3 +55,48 @@ int cell_launch_info(int k, LaunchInfo* info)
 }
 
 }  // namespace dg
+
+namespace dg {
+
+#define DG_VDECL(n, m)                                                    \
+    int upload_tables_vb_n##n##_m##m(const HostTables&);                  \
+    cudaError_t launch_vb_n##n##_m##m(const KParams&, cudaStream_t);      \
+    int vb_info_n##n##_m##m(LaunchInfo*);
+#define DG_VPAIR(n, m2) DG_VDECL(n, n) DG_VDECL(n, m2)
+DG_VPAIR(2, 4) DG_VPAIR(3, 5) DG_VPAIR(4, 6) DG_VPAIR(5, 7) DG_VPAIR(6, 8) DG_VPAIR(7, 9) DG_VPAIR(8, 10) DG_VPAIR(9, 11)
+
+#define DG_VCASES(call)                                                                            \
+    switch ((k + 1) * 100 + m) {                                                                   \
+    case 202: return call(2, 2); case 204: return call(2, 4); case 303: return call(3, 3);         \
+    case 305: return call(3, 5); case 404: return call(4, 4); case 406: return call(4, 6);         \
+    case 505: return call(5, 5); case 507: return call(5, 7); case 606: return call(6, 6);         \
+    case 608: return call(6, 8); case 707: return call(7, 7); case 709: return call(7, 9);         \
+    case 808: return call(8, 8); case 810: return call(8, 10); case 909: return call(9, 9);        \
+    case 911: return call(9, 11);                                                                  \
+    default: break;                                                                                \
+    }
+
+bool vb_available(int k, int m) { return k >= 1 && k <= 8 && (m == k + 1 || m == k + 3); }
+
+int upload_tables_vb(int k, int m, const HostTables& t)
+{
+#define DG_VU(n, mm) upload_tables_vb_n##n##_m##mm(t)
+    DG_VCASES(DG_VU)
+    return -1;
+}
+
+cudaError_t launch_vb(int k, int m, const KParams& p, cudaStream_t s)
+{
+#define DG_VL(n, mm) launch_vb_n##n##_m##mm(p, s)
+    DG_VCASES(DG_VL)
+    return cudaErrorInvalidValue;
+}
+
+int vb_launch_info(int k, int m, LaunchInfo* info)
+{
+#define DG_VI(n, mm) vb_info_n##n##_m##mm(info)
+    DG_VCASES(DG_VI)
+    return -1;
+}
+
+}  // namespace dg

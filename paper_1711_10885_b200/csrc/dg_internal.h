@@ -11,7 +11,7 @@ constexpr int NMAX = KMAX + 1;
 
 // 1D tables for one degree (host side, double). Built by tables.cpp.
 struct HostTables {
-    int n;
+    int n, m;                // basis size n = k+1, Gauss points per direction m (>= n)
     double xi[NMAX], w[NMAX];
     double V[NMAX][NMAX];    // V[i][j]  = theta_j(xi_i)                    (A^(q) of eq:evalfe)
     double Dc[NMAX][NMAX];   // Dc[i][l] = L'_l(xi_i): collocation derivative at the Gauss points
@@ -22,6 +22,7 @@ struct HostTables {
     double G[NMAX][NMAX];    // G[i][j]  = theta'_j(xi_i)   (reference derivative, modal -> Gauss points)
 };
 int build_tables(int k, HostTables* t);
+int build_tables_m(int k, int m, HostTables* t);
 
 // Per-launch parameters (passed by value; lands in the kernel parameter constant bank).
 struct KParams {
@@ -56,6 +57,10 @@ struct KParams {
     const double* Dghost[6];  // neighbour-rank layers of Dfield per face (nullptr: none)
     double sigma;
     double h[3];
+    // variable-velocity kernel (NEXT-2/3):
+    int bkind;                // 0 constant b, 1 Taylor-Green field, 2 linear (x2, x3, x1)
+    double bamp[3];           // per-component amplitude of the field
+    double lo[3];             // physical coordinates of the global box's low corner
 };
 
 struct LaunchInfo {
@@ -66,6 +71,11 @@ struct LaunchInfo {
 int upload_tables(int k, const HostTables& t);          // to this device's __constant__ bank
 cudaError_t launch_cell(int k, const KParams& p, cudaStream_t s);
 cudaError_t launch_gen(int k, const KParams& p, cudaStream_t s);      // general-coefficient kernel
+// variable-velocity / over-integrated kernel for (k, m), m in {k+1, k+3}, k <= 8 (dg_vb.cuh)
+bool vb_available(int k, int m);
+int upload_tables_vb(int k, int m, const HostTables& t);
+cudaError_t launch_vb(int k, int m, const KParams& p, cudaStream_t s);
+int vb_launch_info(int k, int m, LaunchInfo* info);
 int cell_launch_info(int k, LaunchInfo* info);
 int gen_launch_info(int k, LaunchInfo* info);
 

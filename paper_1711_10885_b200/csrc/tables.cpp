@@ -35,11 +35,17 @@ static void shifted_legendre(int n, ld x, ld* P, ld* dP)
     }
 }
 
-int build_tables(int k, HostTables* t)
+int build_tables(int k, HostTables* t) { return build_tables_m(k, k + 1, t); }
+
+// m >= k+1 Gauss points (over-integration, NEXT-3): V and G are m x n; the collocation
+// derivative Dc and the Lagrange vectors L, L' live on the m points (interpolation with the
+// first m basis functions, exact for the degree-k traces and lines).
+int build_tables_m(int k, int m, HostTables* t)
 {
-    if (k < 1 || k > KMAX) return -1;
-    const int n = k + 1, m = n;
+    if (k < 1 || k > KMAX || m < k + 1 || m > NMAX) return -1;
+    const int n = k + 1;
     t->n = n;
+    t->m = m;
     ld xi[NMAX], w[NMAX];
     ld P[NMAX + 2], dP[NMAX + 2];
     for (int i = 0; i < m; ++i) {
@@ -56,20 +62,20 @@ int build_tables(int k, HostTables* t)
         // weight on [0,1]: 1 / (x(1-x) Pt'_m(x)^2)
         w[i] = 1.0L / (x * (1.0L - x) * dP[m] * dP[m]);
     }
-    ld th[NMAX][NMAX], dth[NMAX][NMAX];
+    ld th[NMAX][NMAX], dth[NMAX][NMAX];      // theta_j, theta'_j at the m points, j < m
     for (int i = 0; i < m; ++i) {
-        shifted_legendre(n, xi[i], P, dP);
-        for (int j = 0; j < n; ++j) {
+        shifted_legendre(m, xi[i], P, dP);
+        for (int j = 0; j < m; ++j) {
             ld s = sqrtl(2.0L * j + 1.0L);
             th[i][j] = s * P[j];
             dth[i][j] = s * dP[j];
         }
     }
     ld e0[NMAX], e1[NMAX], de0[NMAX], de1[NMAX];
-    shifted_legendre(n, 0.0L, P, dP);
-    for (int j = 0; j < n; ++j) { ld s = sqrtl(2.0L * j + 1.0L); e0[j] = s * P[j]; de0[j] = s * dP[j]; }
-    shifted_legendre(n, 1.0L, P, dP);
-    for (int j = 0; j < n; ++j) { ld s = sqrtl(2.0L * j + 1.0L); e1[j] = s * P[j]; de1[j] = s * dP[j]; }
+    shifted_legendre(m, 0.0L, P, dP);
+    for (int j = 0; j < m; ++j) { ld s = sqrtl(2.0L * j + 1.0L); e0[j] = s * P[j]; de0[j] = s * dP[j]; }
+    shifted_legendre(m, 1.0L, P, dP);
+    for (int j = 0; j < m; ++j) { ld s = sqrtl(2.0L * j + 1.0L); e1[j] = s * P[j]; de1[j] = s * dP[j]; }
 
     for (int i = 0; i < m; ++i) {
         t->xi[i] = (double)xi[i];
@@ -80,13 +86,13 @@ int build_tables(int k, HostTables* t)
         }
         for (int l = 0; l < m; ++l) {
             ld s = 0;
-            for (int j = 0; j < n; ++j) s += dth[i][j] * th[l][j];
+            for (int j = 0; j < m; ++j) s += dth[i][j] * th[l][j];
             t->Dc[i][l] = (double)(s * w[l]);
         }
     }
     for (int l = 0; l < m; ++l) {
         ld a0 = 0, a1 = 0, b0 = 0, b1 = 0;
-        for (int j = 0; j < n; ++j) {
+        for (int j = 0; j < m; ++j) {
             a0 += e0[j] * th[l][j];
             a1 += e1[j] * th[l][j];
             b0 += de0[j] * th[l][j];

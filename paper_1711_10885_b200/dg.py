@@ -22,7 +22,7 @@ BC_DIRICHLET, BC_PERIODIC = 0, 1
 EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residual", "dg_apply_host",
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
-            "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage"]
+            "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage", "dg_set_velocity", "dg_set_quadrature"]
 
 
 class DGError(RuntimeError):
@@ -76,6 +76,8 @@ def lib():
         L.dg_partition.argtypes = [ctypes.POINTER(MeshDesc), ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.dg_set_diffusion.argtypes = [vp, vp, ctypes.c_uint, vp]
         L.dg_fill_uniform_cells.argtypes = [vp, vp, ctypes.c_int, u64, vp]
+        L.dg_set_velocity.argtypes = [vp, ctypes.c_int, vp]
+        L.dg_set_quadrature.argtypes = [vp, ctypes.c_int]
         L.dg_ssp_stage.argtypes = [vp, vp, vp, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, vp]
         for name in EXPORTED:
             if name != "dg_strerror":
@@ -220,6 +222,15 @@ class Operator:
             ncell = self.ndofs // self.n3
             _dev_vec(Dcell, ncell * 9, "Dcell")
         _check(lib().dg_set_diffusion(self._h, _ptr(Dcell), flags, _stream(stream)), "dg_set_diffusion")
+
+    def set_velocity(self, kind, amp=(1.0, 1.0, 1.0)):
+        """Velocity field b(x) at every quadrature point: 0 constant, 1 Taylor-Green, 2 linear (dg_set_velocity)."""
+        a = (ctypes.c_double * 3)(*[float(v) for v in amp])
+        _check(lib().dg_set_velocity(self._h, int(kind), a), "dg_set_velocity")
+
+    def set_quadrature(self, m):
+        """Gauss points per direction (k+1 or k+3; dg_set_quadrature)."""
+        _check(lib().dg_set_quadrature(self._h, int(m)), "dg_set_quadrature")
 
     def fill_uniform_cells(self, t, per_cell, seed, stream=None):
         """t[per_cell * l + i] = U(seed, per_cell * e_global(l) + i) (dg_fill_uniform_cells)."""

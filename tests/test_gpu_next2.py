@@ -1,0 +1,159 @@
+"""NEXT-2/3 on the GPU: the variable-velocity / over-integrated kernel (dg_vb.cuh) against the
+oracle O-1 element by element at 1e-12 (reading C-14): the Taylor-Green field of the paper's
+transport run (eq:2) on (-pi, pi)^3 with q = 2p + 4 (m = k + 3) and q = 2p,
+the linear test field on Dirichlet boxes per term mask, polynomial consistency through
+dg_residual, conservation over Heun steps, and partition invariance (loopback)."""
+import numpy as np
+import pytest
+
+from oracle import o1, o2_assembled as o2, rhs
+from paper_1711_10885_b200 import configs, inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+PI = np.pi
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def tg_cfg(k, ncells=(4, 3, 3), D=5e-6):
+    return configs.Config("TG-k%d" % k, ncells, (-PI,) * 3, (PI,) * 3, k, (D, 0, 0, 0, D, 0, 0, 0, D), (0, 0, 0),
+                          0.0, 3.0 * k * (k + 2) * max(ncells) / (2 * PI), 7, periodic=(1, 1, 1))
+
+
+def run(cfg, z_np, kind, m, amp=(1.0, 1.0, 1.0), terms=7, periodic=None):
+    from paper_1711_10885_b200 import dg
+    per = cfg.periodic if periodic is None else periodic
+    op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, bc=dg.bc_from_periodic(per))
+    op.set_velocity(kind, amp)
+    op.set_quadrature(m)
+    z = torch.from_numpy(z_np).cuda()
+    y = torch.full_like(z, float("nan"))
+    op.apply(z, y, terms=terms)
+    torch.cuda.synchronize()
+    info = op.kernel_info()
+    op.close()
+    return y.cpu().numpy(), info
+
+
+@pytest.mark.parametrize("k", list(range(1, 9)))
+@pytest.mark.parametrize("extra", [0, 2])
+def test_taylor_green_vs_o1(k, extra):
+    cfg = tg_cfg(k, D=0.05)
+    z = inputs.uniform(cfg.ndofs, 40 + k)
+    y, info = run(cfg, z, 1, k + 1 + extra)
+    yref, _ = o1.apply(*cfg.args(), z, m=k + 1 + extra, bkind=1, periodic=(1, 1, 1))
+    assert rel(y, yref) < TOL
+    assert info["threads_per_cta"] >= (k + 1 + extra) ** 2
+
+
+@pytest.mark.parametrize("k", [1, 3, 6])
+def test_linear_field_masks_vs_o1(k):
+    cfg = configs.small(k, ncells=(4, 3, 2), lo=(-0.3, 0.1, 0.2), hi=(1.2, 1.1, 0.7), b=(0, 0, 0), c=0.4)
+    z = inputs.uniform(cfg.ndofs, 7)
+    amp = (0.7, -1.1, 0.4)
+    for mask in (1, 2, 4, 7):
+        y, _ = run(cfg, z, 2, k + 3, amp, terms=mask)
+        yref, _ = o1.apply(*cfg.args(), z, mask=mask, m=k + 3, bkind=2, bamp=amp)
+        assert rel(y, yref) < TOL, mask
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_constant_velocity_over_integrated_equals_fast_kernel(k):
+    """Constant coefficients are integrated exactly with m = k+1 and k+3: the vb kernel with m = k+3
+    reproduces the fast kernel's result."""
+    from paper_1711_10885_b200 import dg
+    cfg = configs.small(k, ncells=(5, 3, 2), b=(1.0, -0.5, 0.25), c=0.3)
+    z = inputs.uniform(cfg.ndofs, 8)
+    y, _ = run(cfg, z, 0, k + 3)
+    op = dg.from_config(cfg)
+    zt = torch.from_numpy(z).cuda()
+    yf = torch.empty_like(zt)
+    op.apply(zt, yf)
+    torch.cuda.synchronize()
+    op.close()
+    assert rel(y, yf.cpu().numpy()) < TOL
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_residual_consistency_linear_velocity(k):
+    from paper_1711_10885_b200 import dg
+    cfg = configs.small(k, ncells=(3, 2, 2), b=(0, 0, 0), c=0.4)
+    amp = np.array([0.8, -0.6, 1.2])
+    zs, F = rhs.consistency_data(*cfg.args(), seed=k, bfield=lambda x: o2.linear_field(x) * amp[:, None])
+    op = dg.from_config(cfg)
+    op.set_velocity(2, tuple(amp))
+    op.set_quadrature(k + 3)
+    zt, ft = torch.from_numpy(zs).cuda(), torch.from_numpy(F).cuda()
+    r = torch.empty_like(zt)
+    op.residual(zt, ft, r)
+    torch.cuda.synchronize()
+    op.close()
+    assert np.abs(r.cpu().numpy()).max() < 1e-12 * np.abs(F).max()
+
+
+def test_taylor_green_heun_conserves_mass():
+    """The paper's transport setting (D = 5e-6 I, c = f = 0, periodic, q = 2p+4, Heun): the cell
+    means' sum is conserved step after step."""
+    from paper_1711_10885_b200 import dg
+    k = 3
+    cfg = tg_cfg(k, ncells=(6, 6, 6))
+    op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma,
+                     bc=dg.bc_from_periodic((1, 1, 1)))
+    op.set_velocity(1)
+    op.set_quadrature(k + 3)
+    u = torch.from_numpy(inputs.uniform(cfg.ndofs, 3)).cuda()
+    m0 = float(u.view(cfg.ncell, -1)[:, 0].sum())
+    tmp, nxt = torch.empty_like(u), torch.empty_like(u)
+    for _ in range(50):
+        op.heun_step(u, 1e-3, tmp, nxt)
+        u, nxt = nxt, u
+    torch.cuda.synchronize()
+    op.close()
+    m1 = float(u.view(cfg.ncell, -1)[:, 0].sum())
+    assert np.isfinite(m1) and abs(m1 - m0) < 1e-12 * float(u.abs().sum())
+
+
+def test_taylor_green_partition_loopback_bitwise():
+    from paper_1711_10885_b200 import dg
+    from test_gpu_loopback import as_tensor, local_cells
+    k = 2
+    cfg = tg_cfg(k, ncells=(4, 4, 2))
+    ys, _ = run(cfg, inputs.uniform(cfg.ndofs, cfg.seed), 1, k + 3)
+    parts = (2, 2, 1)
+    ops, zs = [], []
+    for r in range(4):
+        op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, rank=r, nranks=4,
+                         parts=parts, bc=dg.bc_from_periodic((1, 1, 1)))
+        op.set_velocity(1)
+        op.set_quadrature(k + 3)
+        z = torch.empty(op.ndofs, dtype=torch.float64, device="cuda")
+        op.fill_uniform_local(z, cfg.seed)
+        op.halo_pack(z)
+        ops.append(op)
+        zs.append(z)
+    torch.cuda.synchronize()
+    for op in ops:
+        for f in range(6):
+            nb, cnt = op.halo_info(f)
+            if nb >= 0:
+                as_tensor(op.halo_buffer_ptr(f, 1), cnt).copy_(as_tensor(ops[nb].halo_buffer_ptr(f ^ 1, 0), cnt))
+    torch.cuda.synchronize()
+    yg = np.full(cfg.ndofs, np.nan)
+    for r, op in enumerate(ops):
+        y = torch.full_like(zs[r], float("nan"))
+        op.apply(zs[r], y, terms=dg.ALL | dg.HALO_EXTERNAL)
+        torch.cuda.synchronize()
+        yg.reshape(-1, cfg.n3)[local_cells(cfg, op.cell_lo, op.cell_cnt)] = y.cpu().numpy().reshape(-1, cfg.n3)
+        op.close()
+    assert np.array_equal(yg, ys)
