@@ -57,6 +57,8 @@ def workload(name, world):
         return configs.c5_strong(grid)
     if name.startswith("a-k"):
         return configs.problem_a(int(name[3:]), world)
+    if name.startswith("tg-k") and world == 1:
+        return configs.taylor_green(int(name[4:]))
     cfg = configs.by_name(name)
     if world != 1:
         raise SystemExit("workload %s is single-GPU" % name)
@@ -67,6 +69,10 @@ def workload_desc(cfg, world):
     dtxt = ("per-cell SPD tensor field (inputs.tensor_field_*, seed %d)" % cfg.dfield_seed
             if cfg.dfield_seed >= 0 else str(list(cfg.D)))
     bc = "periodic" if all(cfg.periodic) else ("Dirichlet" if not any(cfg.periodic) else "periodic %s" % (cfg.periodic,))
+    if cfg.bkind:
+        bc += ", b(x) = Taylor-Green field at every quadrature point" if cfg.bkind == 1 else ", b(x) linear field"
+    if cfg.m and cfg.m != cfg.k + 1:
+        bc += ", m = %d Gauss points per direction (q = %d)" % (cfg.m, 2 * cfg.m - 1)
     return {"workload": "%s: %dx%dx%d cells, k=%d, %d DOFs, box %s-%s, D=%s, b=%s, c=%g, sigma=%g, %s, seed %d"
                         % (cfg.name, cfg.ncells[0], cfg.ncells[1], cfg.ncells[2], cfg.k, cfg.ndofs,
                            list(cfg.lo), list(cfg.hi), dtxt, list(cfg.b), cfg.c, cfg.sigma, bc, cfg.seed),
@@ -138,8 +144,8 @@ def sample_cells(cfg, count, seed=0):
 
 
 def oracle_kw(cfg):
-    """periodic / per-cell tensor keywords of the oracle for this workload (host field, global order)."""
-    kw = {"periodic": cfg.periodic}
+    """periodic / per-cell tensor / velocity / quadrature keywords of the oracle for this workload."""
+    kw = {"periodic": cfg.periodic, "bkind": cfg.bkind, "m": cfg.m}
     if cfg.dfield_seed >= 0:
         kw["Dcell"] = inputs.tensor_field_cells(np.arange(cfg.ncell), cfg.dfield_seed)
     return kw
@@ -268,7 +274,13 @@ def run_ours(args, rank, world, local_rank):
                      nranks=world, parts=cfg.parts, nccl_id=nccl_id, bc=dg.bc_from_periodic(cfg.periodic))
     if cfg.dfield_seed >= 0:
         op.set_tensor_field(cfg.dfield_seed)
+    if cfg.bkind:
+        op.set_velocity(cfg.bkind)
+    if cfg.m and cfg.m != cfg.k + 1:
+        op.set_quadrature(cfg.m)
     general = cfg.dfield_seed >= 0 or any(cfg.D[i] != 0 for i in (1, 2, 3, 5, 6, 7))
+    kname = ("dg_vb_kernel<%d,%d>" % (cfg.k + 1, cfg.m or cfg.k + 1) if (cfg.bkind or (cfg.m and cfg.m != cfg.k + 1))
+             else ("dg_gen_kernel<%d>" % (cfg.k + 1) if general else "dg_cell_kernel<%d>" % (cfg.k + 1)))
     info = op.kernel_info()
     z = torch.empty(op.ndofs, dtype=torch.float64, device=dev)
     y = torch.empty_like(z)
@@ -359,7 +371,7 @@ def run_ours(args, rank, world, local_rank):
             "executed_achieved": (exec_per_dof * op.ndofs / kern_t / 1e12) if exec_per_dof else None,
             "executed_frac": (exec_per_dof * op.ndofs / kern_t / 1e12 / peak) if exec_per_dof else None,
             "ncu_source": "profiles/ncu_full_summary.json (ncu --set full, --clock-control none)" if ncu else None,
-            "kernel": "%s<%d> (FP64 DFMA pipe)" % ("dg_gen_kernel" if general else "dg_cell_kernel", cfg.k + 1),
+            "kernel": "%s (FP64 DFMA pipe)" % kname,
             "flops_basis": "paper model FLOPDOF_vol+FLOPDOF_face(3,%d) = %.1f flop/DOF x %d DOFs per launch "
                            "(PAPER.md:675-676); the kernel executes fewer (collocation variant, DESIGN.md)"
                            % (cfg.k, per_dof, op.ndofs),
@@ -428,7 +440,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default=None,
                     help="default: C3 (N=1) / C3-per-GPU weak (N>1); also c1, c2, c4-kK, c5weak, c5strong, "
-                         "a-kK (the paper's Problem A: periodic, per-cell tensor D, ~4e8 DOFs)")
+                         "a-kK (the paper's Problem A: periodic, per-cell tensor D, ~4e8 DOFs), "
+                         "tg-kK (the Taylor-Green transport operator: b(x) at every point, q = 2p+4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -23,6 +23,8 @@ class Config:
     parts: Tuple[int, int, int] = (1, 1, 1)
     periodic: Tuple[int, int, int] = (0, 0, 0)
     dfield_seed: int = -1          # >= 0: per-cell tensor field inputs.tensor_field_* (Problem A)
+    bkind: int = 0                 # velocity field: 0 constant b, 1 Taylor-Green (NEXT-2)
+    m: int = 0                     # Gauss points per direction (0: k+1)
 
     @property
     def n3(self):
@@ -110,6 +112,19 @@ def problem_a(k, P=1):
                   k, I3, B_A, 1.0, sigma_for(k, 1.0 / N), 5, (px, py, pz), (1, 1, 1), 6)
 
 
+def taylor_green(k, N=None):
+    """The paper's transport run as an operator workload: the periodic box
+    (-pi, pi)^3, D = 5e-6 I, c = 0, the Taylor-Green field b(x) (eq:2) at every quadrature point,
+    q = 2p + 4 (m = k + 3). N^3 cells with N = round(736.8 / (k+1)) (~4e8 DOFs) by default; the
+    paper's production mesh is N = 240 at k = 5. sigma = 3k(k+2)/h."""
+    if N is None:
+        N = int(round(736.8 / (k + 1)))
+    h = 2 * np.pi / N
+    d = 5e-6
+    return Config("TG-k%d" % k, (N, N, N), (-np.pi,) * 3, (np.pi,) * 3, k, (d, 0, 0, 0, d, 0, 0, 0, d), (0.0, 0.0, 0.0),
+                  0.0, sigma_for(k, h), 8, (1, 1, 1), (1, 1, 1), -1, 1, k + 3)
+
+
 def by_name(name):
     name = name.lower()
     table = {"c1": c1, "c2": c2, "c3": c3, "c5strong": c5_strong, "c5weak": c5_weak}
@@ -117,6 +132,8 @@ def by_name(name):
         return c4(int(name[4:]))
     if name.startswith("a-k"):
         return problem_a(int(name[3:]))
+    if name.startswith("tg-k"):
+        return taylor_green(int(name[4:]))
     return table[name]()
 
 

@@ -301,6 +301,13 @@ def a_ptr(a):
 
 
 def from_config(cfg, **kw):
+    """Operator for a configs.Config: boundary conditions, velocity field and quadrature applied
+    (a per-cell tensor field is left to set_tensor_field)."""
     if getattr(cfg, "periodic", (0, 0, 0)) != (0, 0, 0) and "bc" not in kw:
         kw["bc"] = bc_from_periodic(cfg.periodic)
-    return Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, **kw)
+    op = Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, **kw)
+    if getattr(cfg, "bkind", 0):
+        op.set_velocity(cfg.bkind)
+    if getattr(cfg, "m", 0) and cfg.m != cfg.k + 1:
+        op.set_quadrature(cfg.m)
+    return op
