@@ -154,7 +154,7 @@ static int g_gen_attr_done[64];
 cudaError_t DG_CAT(launch_gen_n, DG_N)(const KParams& p, cudaStream_t s)
 {
     constexpr int N = DG_N;
-    constexpr int C = Cfg<N>::C;
+    constexpr int C = GCfg<N>::C;
     if (p.ntasks <= 0) return cudaSuccess;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -165,15 +165,15 @@ cudaError_t DG_CAT(launch_gen_n, DG_N)(const KParams& p, cudaStream_t s)
         g_gen_attr_done[dev] = 1;
     }
     const int64_t grid = (p.ntasks + C - 1) / C;
-    dg_gen_kernel<N><<<(unsigned)grid, C * Cfg<N>::TPC, GSmem<N>::BYTES, s>>>(p);
+    dg_gen_kernel<N><<<(unsigned)grid, C * GCfg<N>::TPC, GSmem<N>::BYTES, s>>>(p);
     return cudaGetLastError();
 }
 
 int DG_CAT(gen_info_n, DG_N)(LaunchInfo* info)
 {
     constexpr int N = DG_N;
-    info->cells_per_cta = Cfg<N>::C;
-    info->threads = Cfg<N>::C * Cfg<N>::TPC;
+    info->cells_per_cta = GCfg<N>::C;
+    info->threads = GCfg<N>::C * GCfg<N>::TPC;
     info->smem = GSmem<N>::BYTES;
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, dg_gen_kernel<N>) != cudaSuccess) return -3;

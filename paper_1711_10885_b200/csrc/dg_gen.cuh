@@ -74,6 +74,24 @@ __device__ __forceinline__ const double* nb_dfield(const KParams& p, const int l
     return p.Dfield + 6 * (l[0] + p.nloc[0] * (l[1] + p.nloc[1] * (int64_t)l[2]));
 }
 
+// launch configuration of the general kernel: the fast kernel's unless overridden per degree
+#ifdef DG_GTPC
+#define DG_GOVR(ov, d) (ov)
+#else
+#define DG_GOVR(ov, d) (d)
+#endif
+// (one pencil per thread is better than the fast kernel's 2 for n = 6 and 10: A-k5 18.0 -> 22.8,
+// A-k9 19.5 -> 27.5 GDOF/s, measured with tools/variant.py)
+template <int N> struct GCfgD {
+    static constexpr int TPC = (N == 6) ? 64 : (N == 10) ? 128 : Cfg<N>::TPC;
+    static constexpr int P = (N == 6 || N == 10) ? 1 : Cfg<N>::P;
+    static constexpr int C = (N == 6 || N == 10) ? 1 : Cfg<N>::C;
+};
+template <int N> struct GCfg {
+    static constexpr int TPC = DG_GOVR(DG_GTPC, GCfgD<N>::TPC), P = DG_GOVR(DG_GP, GCfgD<N>::P),
+                         C = DG_GOVR(DG_GC, GCfgD<N>::C);
+};
+
 template <int N>
 struct GSmem {
     static constexpr int PER_CELL = 4 * Lay<N>::SLOT + 2 * FLay<N>::SLOT;
@@ -81,10 +99,10 @@ struct GSmem {
 };
 
 template <int N>
-__global__ void __launch_bounds__(Cfg<N>::C * Cfg<N>::TPC)
+__global__ void __launch_bounds__(GCfg<N>::C * GCfg<N>::TPC)
 dg_gen_kernel(const KParams p)
 {
-    constexpr int TPC = Cfg<N>::TPC, P = Cfg<N>::P, C = Cfg<N>::C;
+    constexpr int TPC = GCfg<N>::TPC, P = GCfg<N>::P, C = GCfg<N>::C;
     constexpr int NN = N * N;
     static_assert(TPC * P >= NN, "pencil slots");
     static_assert(TPC <= 32 || C == 1, "multi-warp cells use CTA barriers: one cell per CTA");
