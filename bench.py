@@ -425,6 +425,10 @@ def run_ours(args, rank, world, local_rank):
                "gpu_launches": args.steps * (info["launches_per_apply"] if world == 1 else
                                              (2 + sum(1 for f in range(6) if op.halo_info(f)[0] >= 0))),
                "kernel_info": info}
+        if world > 1:   # the exchange's cost = t(apply) - t(apply with the halo exchange skipped)
+            out["halo_ablation"] = {"ms_per_apply": t / args.steps * 1e3,
+                                    "ms_per_apply_no_exchange": tk / args.steps * 1e3,
+                                    "what": "same applies with DG_HALO_EXTERNAL (stale receive buffers, timing only)"}
         print(json.dumps(out), flush=True)
     op.close()
     if world > 1:
