@@ -577,7 +577,9 @@ static int apply_host_pipelined(dg_ctx* ctx, const double* z_host, double* y_hos
 {
     const int64_t nz = ctx->nloc[2];
     const int64_t layer = ctx->nloc[0] * ctx->nloc[1] * (int64_t)ctx->n3;   // doubles per z-layer
-    int64_t S = (nz + 15) / 16;                                              // <= 16 slabs
+    int64_t want = 32;                                                        // slabs (pipeline depth)
+    if (const char* e = std::getenv("DG_HOST_SLABS")) want = std::max(1L, std::atol(e));
+    int64_t S = (nz + want - 1) / want;
     if (S < 1) S = 1;
     const int64_t nslab = (nz + S - 1) / S;
     cudaStream_t sc = ctx->host_stream, sh = ctx->h2d_stream, sd = ctx->d2h_stream;
