@@ -45,6 +45,12 @@ struct dg_ctx {
     // variable-velocity / over-integrated path (dg_vb.cuh)
     int m = 0;                       // Gauss points per direction (k+1 or k+3)
     bool vb = false;                 // launch dg_vb_kernel
+    // TMA tensor maps of the last z / y pointers (n = 8 fast kernel)
+    bool no_tma = false;             // DG_NO_TMA=1: per-thread global loads / stores instead
+    const double* tma_z = nullptr;
+    const double* tma_y = nullptr;
+    bool tma_z_ok = false, tma_y_ok = false;
+    CUtensorMap tmz, tmy;
     KParams base;
 };
 
@@ -221,7 +227,9 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
     }
     p.sigma = sigma;
     p.bkind = 0;
+    p.tma = 0;
     ctx->m = k + 1;
+    if (const char* e = std::getenv("DG_NO_TMA")) ctx->no_tma = std::atoi(e) != 0;
     for (int r = 0; r < 3; ++r)
         for (int s = 0; s < 3; ++s) p.Dhat[3 * r + s] = D[3 * r + s] / (h[r] * h[s]);
     p.c = c;
@@ -473,6 +481,29 @@ extern "C" int dg_local_layout(const dg_ctx* ctx, int64_t cell_lo[3], int64_t ce
     return DG_OK;
 }
 
+// TMA staging for the n = 8 fast kernel (dg_cell.cuh): tensor maps over z and y, cached by pointer
+static void set_tma(dg_ctx* ctx, KParams& p, const double* z, double* y)
+{
+    p.tma = 0;
+    if (ctx->k != 7 || ctx->general || ctx->vb || ctx->no_tma) return;
+    const int64_t rows = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2] * 64;
+    if (z != ctx->tma_z) {
+        ctx->tma_z_ok = make_row_map(&ctx->tmz, z, rows);
+        ctx->tma_z = z;
+    }
+    if (y != ctx->tma_y) {
+        ctx->tma_y_ok = make_row_map(&ctx->tmy, y, rows);
+        ctx->tma_y = y;
+    }
+    if (!ctx->tma_z_ok) return;
+    p.tmz = ctx->tmz;
+    p.tma = 1;
+    if (ctx->tma_y_ok) {
+        p.tmy = ctx->tmy;
+        p.tma = 2;
+    }
+}
+
 struct Epi {             // store epilogue (KParams::epi)
     int mode = 0;
     const double* f = nullptr;
@@ -501,6 +532,7 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         p.es = epi->s;
     }
     p.mask = terms & DG_ALL;
+    set_tma(ctx, p, z, y);
     const bool external = (terms & DG_HALO_EXTERNAL) != 0;
     if (!ctx->partitioned) {
         p.task_list = nullptr;
@@ -599,6 +631,7 @@ static int apply_host_pipelined(dg_ctx* ctx, const double* z_host, double* y_hos
             p.f = nullptr;
             p.epi = 0;
             p.mask = DG_ALL;
+            set_tma(ctx, p, ctx->hz, ctx->hy);
             p.task_list = nullptr;
             p.task_lo[0] = 0; p.task_lo[1] = 0; p.task_lo[2] = z0;
             p.task_cnt[0] = ctx->nloc[0]; p.task_cnt[1] = ctx->nloc[1]; p.task_cnt[2] = cnt;

@@ -119,8 +119,55 @@ template <> struct FLay<8> {
 template <int N>
 struct Smem {
     static constexpr int PER_CELL = 2 * Lay<N>::SLOT + FLay<N>::SLOT;
-    static constexpr int BYTES = Cfg<N>::C * PER_CELL * 8;
+    // n = 8: TMA staging of the own block (4 KB, 128-byte aligned) plus the mbarrier; the two
+    // x-neighbour blocks are staged in A1 and face slots 4..11, free during phase 1
+    static constexpr int STAGE = (N == 8) ? 512 + 16 + 16 : 0;
+    static constexpr int BYTES = Cfg<N>::C * PER_CELL * 8 + STAGE * 8;
 };
+
+// ---------------------------------------------------------------------------------- TMA (n = 8)
+// The cell block (64 x-lines of 64 B) moves between HBM and shared memory by the tensor memory
+// accelerator with the 64-byte swizzle: 16-byte chunk c of row L lands at chunk c ^ ((addr >> 7) & 3)
+// of its row, so the LDS.128 / STS.128 of one x-line per thread are bank-conflict free, and the
+// global side is read / written as whole 4 KB blocks (no 4x sector over-fetch of per-thread
+// x-line loads, no load/store instructions on the LSU pipe).
+namespace tma {
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(saddr(b)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void expect_tx(uint64_t* b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void load_rows(double* dst, const CUtensorMap* m, int row, uint64_t* b)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                 ::"r"(saddr(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(0), "r"(row), "r"(saddr(b))
+                 : "memory");
+}
+__device__ __forceinline__ void wait(uint64_t* b, uint32_t phase)
+{
+    asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @!P1 bra WAIT_%=;\n}\n"
+                 ::"r"(saddr(b)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void store_rows(const CUtensorMap* m, int row, const double* src)
+{
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n"
+                 ::"l"(reinterpret_cast<uint64_t>(m)), "r"(0), "r"(row), "r"(saddr(src)) : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// double index of element e of row L in a TMA-swizzled block at S
+__device__ __forceinline__ int at(const double* S, int L, int e)
+{
+    const uint32_t row = saddr(S) + 64u * (uint32_t)L;
+    return 8 * L + 2 * ((e >> 1) ^ (int)((row >> 7) & 3u)) + (e & 1);
+}
+}  // namespace tma
 
 // ---------------------------------------------------------------------------------- 1D stages
 // t[k][i] = sum_j V_ij r[k][j]  (even-odd: V_{n-1-i,j} = (-1)^j V_ij)
@@ -611,7 +658,7 @@ __device__ __forceinline__ void epilogue(const KParams& p, int64_t off, double (
 // ---------------------------------------------------------------------------------- kernel
 template <int N>
 __global__ void __launch_bounds__(Cfg<N>::C * Cfg<N>::TPC, Cfg<N>::MINB)
-dg_cell_kernel(const KParams p)
+dg_cell_kernel(const __grid_constant__ KParams p)
 {
     constexpr int TPC = Cfg<N>::TPC, P = Cfg<N>::P, C = Cfg<N>::C;
     constexpr int NN = N * N;
@@ -686,13 +733,63 @@ dg_cell_kernel(const KParams p)
     }
 
     double r[P][N], t[P][N];
+    // TMA staging (n = 8, one cell per CTA): own block and the local x-neighbours' blocks
+    double* STG = nullptr;
+    bool tma_x = false;
+    if constexpr (N == 8 && C == 1) {
+        if (p.tma) {
+            STG = reinterpret_cast<double*>(
+                (reinterpret_cast<uintptr_t>(smem + Smem<N>::PER_CELL) + 127) & ~(uintptr_t)127);
+            uint64_t* mbar = reinterpret_cast<uint64_t*>(STG + 512);
+            const int nq = (int)p.nloc[0];
+            const bool hl = (nbi & 1u) != 0, hh = (nbi & 2u) != 0;
+            const bool ll = hl && (lc[0] > 0 || p.wrap[0]), lh = hh && (lc[0] + 1 < nq || p.wrap[0]);
+            tma_x = (ll || !hl) && (lh || !hh);      // a ghost x-neighbour (other rank): LDG path for it
+            if (tid == 0) tma::mbar_init(mbar);
+            __syncthreads();
+            if (tid == 0) {
+                const int64_t clo = (lc[0] > 0) ? cell - 1 : cell + (nq - 1);
+                const int64_t chi = (lc[0] + 1 < nq) ? cell + 1 : cell - (nq - 1);
+                const bool xl = tma_x && ll, xh = tma_x && lh;
+                tma::expect_tx(mbar, 4096u * (1u + (xl ? 1u : 0u) + (xh ? 1u : 0u)));
+                tma::load_rows(STG, &p.tmz, (int)(cell * 64), mbar);
+                if (xl) tma::load_rows(A1, &p.tmz, (int)(clo * 64), mbar);
+                if (xh) tma::load_rows(NT + 4 * 64, &p.tmz, (int)(chi * 64), mbar);
+            }
+            tma::wait(mbar, 0);
+        }
+    }
     {
         double rl[P][N], rh[P][N];
         // ---- phase 1: x-pencils (y = a, z = bb) from global, V along x -> A0;
         //      x-neighbour lines loaded alongside and contracted (normal first)
+        if (tma_x) {
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                const int L = pa[k] + N * pb[k];
+#pragma unroll
+                for (int e = 0; e < N; e += 2) {
+                    const double2 a = *reinterpret_cast<const double2*>(STG + tma::at(STG, L, e));
+                    const double2 lo = *reinterpret_cast<const double2*>(A1 + tma::at(A1, L, e));
+                    const double2 hi = *reinterpret_cast<const double2*>(NT + 4 * 64 + tma::at(NT + 4 * 64, L, e));
+                    r[k][e] = a.x; r[k][e + 1] = a.y;
+                    rl[k][e] = lo.x; rl[k][e + 1] = lo.y;
+                    rh[k][e] = hi.x; rh[k][e + 1] = hi.y;
+                }
+            }
+        } else {
         nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
+            if (STG) {
+                const int L = pa[k] + N * pb[k];
+#pragma unroll
+                for (int e = 0; e < N; e += 2) {
+                    const double2 a = *reinterpret_cast<const double2*>(STG + tma::at(STG, L, e));
+                    r[k][e] = a.x; r[k][e + 1] = a.y;
+                }
+                continue;
+            }
             const double* src = zc + N * (pa[k] + N * pb[k]);
             if (N % 2 == 0) {
 #pragma unroll
@@ -705,6 +802,7 @@ dg_cell_kernel(const KParams p)
 #pragma unroll
                 for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
             }
+        }
         }
         v_fwd<N, P>(T.Vh[0], r, t);
 #pragma unroll
@@ -819,6 +917,21 @@ dg_cell_kernel(const KParams p)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
     v_bwd<N, P>(T.Vh[11], r, t);
+    if constexpr (N == 8 && C == 1) {
+        if (STG && p.tma == 2 && p.epi == 0) {   // y through the staging block and one TMA store
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                const int L = pa[k] + N * pb[k];
+#pragma unroll
+                for (int e = 0; e < N; e += 2)
+                    *reinterpret_cast<double2*>(STG + tma::at(STG, L, e)) = make_double2(t[k][e], t[k][e + 1]);
+            }
+            tma::fence_async();
+            __syncthreads();
+            if (tid == 0) tma::store_rows(&p.tmy, (int)(cell * 64), STG);
+            return;
+        }
+    }
     if (valid) {
 #pragma unroll
         for (int k = 0; k < P; ++k) {

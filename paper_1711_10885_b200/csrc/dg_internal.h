@@ -2,6 +2,7 @@
 // (Product path only; nothing here is shared with oracle/.)
 #pragma once
 #include <cstdint>
+#include <cuda.h>            // CUtensorMap (type only; the encoder is fetched through the runtime)
 #include <cuda_runtime.h>
 
 namespace dg {
@@ -61,6 +62,10 @@ struct KParams {
     int bkind;                // 0 constant b, 1 Taylor-Green field, 2 linear (x2, x3, x1)
     double bamp[3];           // per-component amplitude of the field
     double lo[3];             // physical coordinates of the global box's low corner
+    // TMA staging of the x-direction cell blocks (n = 8 fast kernel): z and y viewed as
+    // [cells * 64 rows][8 doubles] with the 64-byte swizzle
+    int tma;                  // 1: tmz (loads) valid; 2: tmy (store) valid too
+    CUtensorMap tmz, tmy;
 };
 
 struct LaunchInfo {
@@ -77,6 +82,8 @@ int upload_tables_vb(int k, int m, const HostTables& t);
 cudaError_t launch_vb(int k, int m, const KParams& p, cudaStream_t s);
 int vb_launch_info(int k, int m, LaunchInfo* info);
 int cell_launch_info(int k, LaunchInfo* info);
+// 2D tensor map [rows][8 doubles] (64-byte rows, box 64 x 8, 64-byte swizzle) over ptr; false if unavailable
+bool make_row_map(CUtensorMap* map, const double* ptr, int64_t rows);
 int gen_launch_info(int k, LaunchInfo* info);
 
 // Halo / inputs kernels (dg_aux.cu).
