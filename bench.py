@@ -447,7 +447,7 @@ def main():
                          "a-kK (the paper's Problem A: periodic, per-cell tensor D, ~4e8 DOFs), "
                          "tg-kK (the Taylor-Green transport operator: b(x) at every point, q = 2p+4)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline sample budget")
     ap.add_argument("--ref-seconds", type=float, default=120.0, help="reference arm total budget")
