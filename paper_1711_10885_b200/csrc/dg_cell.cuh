@@ -167,6 +167,47 @@ __device__ __forceinline__ int at(const double* S, int L, int e)
     const uint32_t row = saddr(S) + 64u * (uint32_t)L;
     return 8 * L + 2 * ((e >> 1) ^ (int)((row >> 7) & 3u)) + (e & 1);
 }
+// Issue the TMA loads of a cell's own block (into STG) and of its local x-neighbours' blocks
+// (into XL, XH) and wait for them; returns whether both x-neighbours are TMA-staged (a ghost
+// neighbour on another rank is read by per-thread loads instead). One cell per CTA.
+__device__ __forceinline__ bool stage_x(const KParams& p, double* STG, double* XL, double* XH, int tid,
+                                       const int (&lc)[3], int64_t cell, unsigned nbi)
+{
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(STG + 512);
+    const int nq = (int)p.nloc[0];
+    const bool hl = (nbi & 1u) != 0, hh = (nbi & 2u) != 0;
+    const bool ll = hl && (lc[0] > 0 || p.wrap[0]), lh = hh && (lc[0] + 1 < nq || p.wrap[0]);
+    const bool tma_x = (ll || !hl) && (lh || !hh);
+    if (tid == 0) mbar_init(mbar);
+    __syncthreads();
+    if (tid == 0) {
+        const int64_t clo = (lc[0] > 0) ? cell - 1 : cell + (nq - 1);
+        const int64_t chi = (lc[0] + 1 < nq) ? cell + 1 : cell - (nq - 1);
+        const bool xl = tma_x && ll, xh = tma_x && lh;
+        expect_tx(mbar, 4096u * (1u + (xl ? 1u : 0u) + (xh ? 1u : 0u)));
+        load_rows(STG, &p.tmz, (int)(cell * 64), mbar);
+        if (xl) load_rows(XL, &p.tmz, (int)(clo * 64), mbar);
+        if (xh) load_rows(XH, &p.tmz, (int)(chi * 64), mbar);
+    }
+    wait(mbar, 0);
+    return tma_x;
+}
+// x-line L (elements e, e+1) of a staged block
+__device__ __forceinline__ double2 line2(const double* S, int L, int e)
+{
+    return *reinterpret_cast<const double2*>(S + at(S, L, e));
+}
+// write the y x-line of row L into the staging block, then (tid 0) one TMA store of the block
+__device__ __forceinline__ void put2(double* S, int L, int e, double a, double b)
+{
+    *reinterpret_cast<double2*>(S + at(S, L, e)) = make_double2(a, b);
+}
+__device__ __forceinline__ void store_block(const KParams& p, const double* S, int tid, int64_t cell)
+{
+    fence_async();
+    __syncthreads();
+    if (tid == 0) store_rows(&p.tmy, (int)(cell * 64), S);
+}
 }  // namespace tma
 
 // ---------------------------------------------------------------------------------- 1D stages
@@ -740,23 +781,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         if (p.tma) {
             STG = reinterpret_cast<double*>(
                 (reinterpret_cast<uintptr_t>(smem + Smem<N>::PER_CELL) + 127) & ~(uintptr_t)127);
-            uint64_t* mbar = reinterpret_cast<uint64_t*>(STG + 512);
-            const int nq = (int)p.nloc[0];
-            const bool hl = (nbi & 1u) != 0, hh = (nbi & 2u) != 0;
-            const bool ll = hl && (lc[0] > 0 || p.wrap[0]), lh = hh && (lc[0] + 1 < nq || p.wrap[0]);
-            tma_x = (ll || !hl) && (lh || !hh);      // a ghost x-neighbour (other rank): LDG path for it
-            if (tid == 0) tma::mbar_init(mbar);
-            __syncthreads();
-            if (tid == 0) {
-                const int64_t clo = (lc[0] > 0) ? cell - 1 : cell + (nq - 1);
-                const int64_t chi = (lc[0] + 1 < nq) ? cell + 1 : cell - (nq - 1);
-                const bool xl = tma_x && ll, xh = tma_x && lh;
-                tma::expect_tx(mbar, 4096u * (1u + (xl ? 1u : 0u) + (xh ? 1u : 0u)));
-                tma::load_rows(STG, &p.tmz, (int)(cell * 64), mbar);
-                if (xl) tma::load_rows(A1, &p.tmz, (int)(clo * 64), mbar);
-                if (xh) tma::load_rows(NT + 4 * 64, &p.tmz, (int)(chi * 64), mbar);
-            }
-            tma::wait(mbar, 0);
+            tma_x = tma::stage_x(p, STG, A1, NT + 4 * 64, tid, lc, cell, nbi);
         }
     }
     {
@@ -769,9 +794,9 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 const int L = pa[k] + N * pb[k];
 #pragma unroll
                 for (int e = 0; e < N; e += 2) {
-                    const double2 a = *reinterpret_cast<const double2*>(STG + tma::at(STG, L, e));
-                    const double2 lo = *reinterpret_cast<const double2*>(A1 + tma::at(A1, L, e));
-                    const double2 hi = *reinterpret_cast<const double2*>(NT + 4 * 64 + tma::at(NT + 4 * 64, L, e));
+                    const double2 a = tma::line2(STG, L, e);
+                    const double2 lo = tma::line2(A1, L, e);
+                    const double2 hi = tma::line2(NT + 4 * 64, L, e);
                     r[k][e] = a.x; r[k][e + 1] = a.y;
                     rl[k][e] = lo.x; rl[k][e + 1] = lo.y;
                     rh[k][e] = hi.x; rh[k][e + 1] = hi.y;
@@ -785,7 +810,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 const int L = pa[k] + N * pb[k];
 #pragma unroll
                 for (int e = 0; e < N; e += 2) {
-                    const double2 a = *reinterpret_cast<const double2*>(STG + tma::at(STG, L, e));
+                    const double2 a = tma::line2(STG, L, e);
                     r[k][e] = a.x; r[k][e + 1] = a.y;
                 }
                 continue;
@@ -923,12 +948,9 @@ dg_cell_kernel(const __grid_constant__ KParams p)
             for (int k = 0; k < P; ++k) {
                 const int L = pa[k] + N * pb[k];
 #pragma unroll
-                for (int e = 0; e < N; e += 2)
-                    *reinterpret_cast<double2*>(STG + tma::at(STG, L, e)) = make_double2(t[k][e], t[k][e + 1]);
+                for (int e = 0; e < N; e += 2) tma::put2(STG, L, e, t[k][e], t[k][e + 1]);
             }
-            tma::fence_async();
-            __syncthreads();
-            if (tid == 0) tma::store_rows(&p.tmy, (int)(cell * 64), STG);
+            tma::store_block(p, STG, tid, cell);
             return;
         }
     }

@@ -95,12 +95,13 @@ template <int N> struct GCfg {
 template <int N>
 struct GSmem {
     static constexpr int PER_CELL = 4 * Lay<N>::SLOT + 2 * FLay<N>::SLOT;
-    static constexpr int BYTES = Cfg<N>::C * PER_CELL * 8;
+    static constexpr int STAGE = (N == 8) ? 512 + 16 + 16 : 0;   // TMA staging of the own block (n = 8)
+    static constexpr int BYTES = GCfg<N>::C * PER_CELL * 8 + STAGE * 8;
 };
 
 template <int N>
 __global__ void __launch_bounds__(GCfg<N>::C * GCfg<N>::TPC)
-dg_gen_kernel(const KParams p)
+dg_gen_kernel(const __grid_constant__ KParams p)
 {
     constexpr int TPC = GCfg<N>::TPC, P = GCfg<N>::P, C = GCfg<N>::C;
     constexpr int NN = N * N;
@@ -178,15 +179,48 @@ dg_gen_kernel(const KParams p)
     }
 
     double r[P][N], t[P][N];
+    // TMA staging (n = 8): own block (STG) and the local x-neighbours' blocks (X1, X2: free in P1)
+    double* STG = nullptr;
+    bool tma_x = false;
+    if constexpr (N == 8 && C == 1) {
+        if (p.tma) {
+            STG = reinterpret_cast<double*>(
+                (reinterpret_cast<uintptr_t>(smem + GSmem<N>::PER_CELL) + 127) & ~(uintptr_t)127);
+            tma_x = tma::stage_x(p, STG, X1, X2, tid, lc, cell, nbi);
+        }
+    }
     // ---------------------------------------------------------------- P1-P3: u at the Gauss points
     {
         double rl[P][N], rh[P][N];
-        nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
+        if (tma_x) {
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-            const double* src = zc + N * (pa[k] + N * pb[k]);
+            for (int k = 0; k < P; ++k) {
+                const int L = pa[k] + N * pb[k];
 #pragma unroll
-            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
+                for (int e = 0; e < N; e += 2) {
+                    const double2 a = tma::line2(STG, L, e), lo = tma::line2(X1, L, e), hi = tma::line2(X2, L, e);
+                    r[k][e] = a.x; r[k][e + 1] = a.y;
+                    rl[k][e] = lo.x; rl[k][e + 1] = lo.y;
+                    rh[k][e] = hi.x; rh[k][e + 1] = hi.y;
+                }
+            }
+        } else {
+            nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                if (STG) {
+                    const int L = pa[k] + N * pb[k];
+#pragma unroll
+                    for (int e = 0; e < N; e += 2) {
+                        const double2 a = tma::line2(STG, L, e);
+                        r[k][e] = a.x; r[k][e + 1] = a.y;
+                    }
+                    continue;
+                }
+                const double* src = zc + N * (pa[k] + N * pb[k]);
+#pragma unroll
+                for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
+            }
         }
         v_fwd<N, P>(T.Vh[0], r, t);
 #pragma unroll
@@ -491,6 +525,18 @@ dg_gen_kernel(const KParams p)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
     v_bwd<N, P>(T.Vh[11], r, t);
+    if constexpr (N == 8 && C == 1) {
+        if (STG && p.tma == 2 && p.epi == 0) {   // y through the staging block and one TMA store
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                const int L = pa[k] + N * pb[k];
+#pragma unroll
+                for (int e = 0; e < N; e += 2) tma::put2(STG, L, e, t[k][e], t[k][e + 1]);
+            }
+            tma::store_block(p, STG, tid, cell);
+            return;
+        }
+    }
     if (valid) {
 #pragma unroll
         for (int k = 0; k < P; ++k) {
