@@ -237,12 +237,7 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
     for (int q = 0; q < 3; ++q) p.dF[q] = p.dT / h[q];
     // Traversal order (L2 reuse of neighbour cells): z fastest inside columns, columns
     // grouped in 4 x 16 tiles, so a cell's neighbours are touched within ~4096 tasks.
-    p.tile[0] = 4;
-    p.tile[1] = 16;
-    if (const char* e = std::getenv("DG_TILE")) {   // experiments: "TX,TY"
-        long tx = 0, ty = 0;
-        if (std::sscanf(e, "%ld,%ld", &tx, &ty) == 2 && tx > 0 && ty > 0) { p.tile[0] = tx; p.tile[1] = ty; }
-    }
+
 
     if (ctx->partitioned) {
         for (int f = 0; f < 6; ++f) {
@@ -504,6 +499,28 @@ static void set_tma(dg_ctx* ctx, KParams& p, const double* z, double* y)
     }
 }
 
+// Magic numbers of decode_task (dg_cell.cuh): q = (umulhi(a, m) + a) >> l equals a / d for
+// every a < 2^31 with l = ceil(log2 d), m = ceil(2^(32+l) / d) - 2^32.
+static void magic_div(uint64_t d, unsigned* m, unsigned* l)
+{
+    if (d < 1) d = 1;
+    unsigned s = 0;
+    while ((1ull << s) < d) ++s;
+    const unsigned __int128 num = ((unsigned __int128)1 << (32 + s));
+    const uint64_t mm = (uint64_t)((num + d - 1) / d) - (1ull << 32);
+    *m = (unsigned)mm;
+    *l = s;
+}
+// the task box of a launch (cells lo .. lo + cnt - 1, traversal order of decode_task)
+static void set_box(KParams& p, const int64_t lo[3], const int64_t cnt[3])
+{
+    p.task_list = nullptr;
+    for (int q = 0; q < 3; ++q) { p.task_lo[q] = lo[q]; p.task_cnt[q] = cnt[q]; }
+    p.ntasks = cnt[0] * cnt[1] * cnt[2];
+    magic_div((uint64_t)cnt[2], &p.dmag[0], &p.dsh[0]);
+    magic_div((uint64_t)cnt[0] * 16u, &p.dmag[1], &p.dsh[1]);
+}
+
 struct Epi {             // store epilogue (KParams::epi)
     int mode = 0;
     const double* f = nullptr;
@@ -535,9 +552,8 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
     set_tma(ctx, p, z, y);
     const bool external = (terms & DG_HALO_EXTERNAL) != 0;
     if (!ctx->partitioned) {
-        p.task_list = nullptr;
-        for (int q = 0; q < 3; ++q) { p.task_lo[q] = 0; p.task_cnt[q] = ctx->nloc[q]; }
-        p.ntasks = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2];
+        const int64_t zero[3] = {0, 0, 0};
+        set_box(p, zero, ctx->nloc);
         return cuda_rc(launch_any(ctx, p, s));
     }
     // (iv) of SURVEY.md 3: pack partition layers, exchange on the comm stream, overlap with inner cells
@@ -573,9 +589,7 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         DG_CUDA(cudaEventRecord(ctx->ev_recv, ctx->comm_stream));
     }
     // inner cells: no remote data
-    p.task_list = nullptr;
-    for (int q = 0; q < 3; ++q) { p.task_lo[q] = ctx->inner_lo[q]; p.task_cnt[q] = ctx->inner_cnt[q]; }
-    p.ntasks = ctx->inner_cnt[0] * ctx->inner_cnt[1] * ctx->inner_cnt[2];
+    set_box(p, ctx->inner_lo, ctx->inner_cnt);
     auto launch = [&](const KParams& kp) { return launch_any(ctx, kp, s); };
     DG_CUDA(launch(p));
     if (need_comm) DG_CUDA(cudaStreamWaitEvent(s, ctx->ev_recv, 0));
@@ -632,10 +646,8 @@ static int apply_host_pipelined(dg_ctx* ctx, const double* z_host, double* y_hos
             p.epi = 0;
             p.mask = DG_ALL;
             set_tma(ctx, p, ctx->hz, ctx->hy);
-            p.task_list = nullptr;
-            p.task_lo[0] = 0; p.task_lo[1] = 0; p.task_lo[2] = z0;
-            p.task_cnt[0] = ctx->nloc[0]; p.task_cnt[1] = ctx->nloc[1]; p.task_cnt[2] = cnt;
-            p.ntasks = ctx->nloc[0] * ctx->nloc[1] * cnt;
+            const int64_t blo[3] = {0, 0, z0}, bcnt[3] = {ctx->nloc[0], ctx->nloc[1], cnt};
+            set_box(p, blo, bcnt);
             DG_CUDA(launch_any(ctx, p, sc));
             DG_CUDA(cudaEventRecord(ctx->ev_done, sc));
             DG_CUDA(cudaStreamWaitEvent(sd, ctx->ev_done, 0));

@@ -674,6 +674,37 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
     }
 }
 
+// ---------------------------------------------------------------------------------- task -> cell
+// z fastest within a column; columns in tiles of TX x TY (ragged at the box edge). The two
+// runtime divisors (column height nz, tile-row size TY nx) use host-precomputed magic numbers
+// (q = (umulhi(a, m) + a) >> l, exact for a < 2^31); full tiles divide by the compile-time
+// TX TY, TX.
+constexpr unsigned TRAV_TX = 4, TRAV_TY = 16;
+__device__ __forceinline__ unsigned fdiv(unsigned a, unsigned m, unsigned l) { return (__umulhi(a, m) + a) >> l; }
+__device__ __forceinline__ void decode_task(const KParams& p, unsigned task, int (&lc)[3])
+{
+    const unsigned nz = (unsigned)p.task_cnt[2], nx = (unsigned)p.task_cnt[0], ny = (unsigned)p.task_cnt[1];
+    const unsigned col = fdiv(task, p.dmag[0], p.dsh[0]);                 // task / nz
+    const unsigned ty = fdiv(col, p.dmag[1], p.dsh[1]);                   // col / (TY nx)
+    const unsigned wy = min(TRAV_TY, ny - ty * TRAV_TY);
+    const unsigned cr = col - ty * TRAV_TY * nx;
+    unsigned tx, wx, ci;
+    if (wy == TRAV_TY) {
+        tx = cr / (TRAV_TX * TRAV_TY);
+        wx = min(TRAV_TX, nx - tx * TRAV_TX);
+        ci = cr - tx * TRAV_TX * TRAV_TY;
+    } else {
+        tx = cr / (TRAV_TX * wy);
+        wx = min(TRAV_TX, nx - tx * TRAV_TX);
+        ci = cr - tx * TRAV_TX * wy;
+    }
+    const unsigned cy = (wx == TRAV_TX) ? ci / TRAV_TX : ci / wx;
+    const unsigned cx = ci - cy * wx;
+    lc[0] = (int)(p.task_lo[0] + tx * TRAV_TX + cx);
+    lc[1] = (int)(p.task_lo[1] + ty * TRAV_TY + cy);
+    lc[2] = (int)(p.task_lo[2] + (task - col * nz));
+}
+
 // ---------------------------------------------------------------------------------- store epilogue
 // The single store of a cell's y block, with the explicit-step arithmetic of PAPER.md:366-373
 // fused in (M = Delta_T I for the orthonormal basis on cuboid cells, so M^-1 is a scalar):
@@ -733,19 +764,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         lc[1] = (int)((e / nx) % ny);
         lc[2] = (int)(e / (nx * ny));
     } else {
-        // z fastest within a column; columns in tiles of TX x TY (ragged at the box edge)
-        const unsigned nz = (unsigned)p.task_cnt[2], nx = (unsigned)p.task_cnt[0], ny = (unsigned)p.task_cnt[1];
-        const unsigned TX = (unsigned)p.tile[0], TY = (unsigned)p.tile[1];
-        const unsigned col = task / nz;
-        const unsigned ty = col / (TY * nx);
-        const unsigned wy = min(TY, ny - ty * TY);
-        const unsigned cr = col - ty * TY * nx;
-        const unsigned tx = cr / (TX * wy);
-        const unsigned wx = min(TX, nx - tx * TX);
-        const unsigned ci = cr - tx * TX * wy;
-        lc[0] = (int)(p.task_lo[0] + tx * TX + ci % wx);
-        lc[1] = (int)(p.task_lo[1] + ty * TY + ci / wx);
-        lc[2] = (int)(p.task_lo[2] + (task - col * nz));
+        decode_task(p, task, lc);
     }
     const int64_t n3 = (int64_t)NN * N;
     const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * (int64_t)lc[2]);

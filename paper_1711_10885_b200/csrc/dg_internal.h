@@ -37,7 +37,7 @@ struct KParams {
     const int64_t* task_list; // local linear cell ids (nullptr -> task box)
     int64_t ntasks;
     int64_t task_lo[3], task_cnt[3];
-    int64_t tile[2];          // traversal: z fastest within tiles of tile[0] x tile[1] (x, y) columns
+    unsigned dmag[2], dsh[2]; // magic division by task_cnt[2] and by TRAV_TY * task_cnt[0] (decode_task)
     int64_t nloc[3];          // local cell counts
     int64_t gofs[3];          // global index of local cell (0,0,0)
     int64_t gcells[3];        // global cell counts

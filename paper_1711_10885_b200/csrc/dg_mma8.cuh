@@ -277,18 +277,7 @@ __global__ void __launch_bounds__(32 * C, MINB) dg_cell_mma8(const KParams p)
         lc[1] = (int)((e / nx) % ny);
         lc[2] = (int)(e / (nx * ny));
     } else {
-        const unsigned nz = (unsigned)p.task_cnt[2], nx = (unsigned)p.task_cnt[0], ny = (unsigned)p.task_cnt[1];
-        const unsigned TX = (unsigned)p.tile[0], TY = (unsigned)p.tile[1];
-        const unsigned col = task / nz;
-        const unsigned ty = col / (TY * nx);
-        const unsigned wy = min(TY, ny - ty * TY);
-        const unsigned cr = col - ty * TY * nx;
-        const unsigned tx = cr / (TX * wy);
-        const unsigned wx = min(TX, nx - tx * TX);
-        const unsigned ci = cr - tx * TX * wy;
-        lc[0] = (int)(p.task_lo[0] + tx * TX + ci % wx);
-        lc[1] = (int)(p.task_lo[1] + ty * TY + ci / wx);
-        lc[2] = (int)(p.task_lo[2] + (task - col * nz));
+        decode_task(p, task, lc);
     }
     const int64_t n3 = 512;
     const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * (int64_t)lc[2]);
