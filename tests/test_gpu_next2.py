@@ -157,3 +157,35 @@ def test_taylor_green_partition_loopback_bitwise():
         yg.reshape(-1, cfg.n3)[local_cells(cfg, op.cell_lo, op.cell_cnt)] = y.cpu().numpy().reshape(-1, cfg.n3)
         op.close()
     assert np.array_equal(yg, ys)
+
+
+def test_mode_switching_and_errors():
+    """Velocity / quadrature / diffusion modes switch kernels and refuse unsupported combinations."""
+    from paper_1711_10885_b200 import dg
+    cfg = configs.small(3, ncells=(4, 3, 2), b=(1.0, -0.5, 0.25), c=0.3)
+    z = torch.from_numpy(inputs.uniform(cfg.ndofs, 2)).cuda()
+    op = dg.from_config(cfg)
+    y0, y1, y2 = (torch.empty_like(z) for _ in range(3))
+    op.apply(z, y0)
+    op.set_velocity(1)
+    op.apply(z, y1)                               # Taylor-Green field: different operator
+    op.set_velocity(0)
+    op.apply(z, y2)                               # back to the constant b: the fast kernel again
+    torch.cuda.synchronize()
+    assert np.array_equal(y0.cpu().numpy(), y2.cpu().numpy())
+    assert rel(y1.cpu().numpy(), y0.cpu().numpy()) > 1e-3
+    for bad, code in (((lambda: op.set_quadrature(3)), dg.DG_EINVAL),          # m < k + 1
+                      ((lambda: op.set_quadrature(5)), dg.DG_EUNSUPPORTED),    # only k+1, k+3
+                      ((lambda: op.set_velocity(3)), dg.DG_EINVAL)):
+        with pytest.raises(dg.DGError) as ei:
+            bad()
+        assert ei.value.code == code
+    op.set_diffusion(torch.from_numpy(np.tile(np.eye(3).ravel(), cfg.ncell)).cuda())
+    with pytest.raises(dg.DGError) as ei:
+        op.set_velocity(1)                        # per-cell tensors with b(x): not built
+    assert ei.value.code == dg.DG_EUNSUPPORTED
+    op.close()
+    op9 = dg.Operator((2, 2, 2), (0, 0, 0), (1, 1, 1), 9, cfg.D, cfg.b, cfg.c, 100.0)
+    with pytest.raises(dg.DGError):
+        op9.set_quadrature(12)                    # k = 9: m = k + 3 > 11 points
+    op9.close()
