@@ -54,24 +54,29 @@ __device__ __forceinline__ void g_fwd(const double (&Gh)[(N + 1) / 2][N], const 
     }
 }
 
+// select among three / six register values by a runtime index (no local-memory array indexing)
+__device__ __forceinline__ double sel3(double a0, double a1, double a2, int i) { return i == 0 ? a0 : (i == 1 ? a1 : a2); }
+__device__ __forceinline__ int sel3i(int a0, int a1, int a2, int i) { return i == 0 ? a0 : (i == 1 ? a1 : a2); }
+__device__ __forceinline__ double dsel(const double (&D)[6], int i)
+{
+    return i == 0 ? D[0] : i == 1 ? D[1] : i == 2 ? D[2] : i == 3 ? D[3] : i == 4 ? D[4] : D[5];
+}
+
 // pointer to the 6-vector D of the neighbour across face f (nullptr: no neighbour)
-__device__ __forceinline__ const double* nb_dfield(const KParams& p, const int lc[3], int f, unsigned nbmask)
+__device__ __forceinline__ const double* nb_dfield(const KParams& p, const int (&lc)[3], int64_t cell, int f,
+                                                   unsigned nbmask)
 {
     if (!((nbmask >> f) & 1u)) return nullptr;
     const int q = f >> 1, s = f & 1;
-    const int nq = (int)p.nloc[q];
-    int l[3] = {lc[0], lc[1], lc[2]};
-    const int lq = lc[q] + (s ? 1 : -1);
-    if (lq >= 0 && lq < nq) {
-        l[q] = lq;
-    } else if (p.wrap[q]) {
-        l[q] = (lq < 0) ? nq - 1 : 0;
-    } else {
-        const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
-                                                                            : (lc[0] + p.nloc[0] * lc[1]);
-        return p.Dghost[f] + 6 * gi;
-    }
-    return p.Dfield + 6 * (l[0] + p.nloc[0] * (l[1] + p.nloc[1] * (int64_t)l[2]));
+    const int nq = (int)sel3(p.nloc[0], p.nloc[1], p.nloc[2], q);
+    const int lcq = sel3i(lc[0], lc[1], lc[2], q);
+    const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
+    const int lq = lcq + (s ? 1 : -1);
+    if (lq >= 0 && lq < nq) return p.Dfield + 6 * (cell + (s ? st : -st));
+    if (p.wrap[q]) return p.Dfield + 6 * (cell + (s ? -(int64_t)(nq - 1) * st : (int64_t)(nq - 1) * st));
+    const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
+                                                                        : (lc[0] + p.nloc[0] * lc[1]);
+    return p.Dghost[f] + 6 * gi;
 }
 
 // launch configuration of the general kernel: the fast kernel's unless overridden per degree
@@ -100,7 +105,10 @@ struct GSmem {
 };
 
 template <int N>
-__global__ void __launch_bounds__(GCfg<N>::C * GCfg<N>::TPC)
+#ifndef DG_GMB
+#define DG_GMB 1
+#endif
+__global__ void __launch_bounds__(GCfg<N>::C * GCfg<N>::TPC, DG_GMB)
 dg_gen_kernel(const __grid_constant__ KParams p)
 {
     constexpr int TPC = GCfg<N>::TPC, P = GCfg<N>::P, C = GCfg<N>::C;
@@ -292,8 +300,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         const int f = tk / N, line = tk - f * N, q = f >> 1;
         if (!((nbi >> f) & 1u)) continue;
         const int t1 = (q == 0) ? 1 : 0;
-        const double* Dn = nb_dfield(p, lc, f, nbmask);
-        const double cqq = __ldg(Dn + q) / p.h[q], cq1 = __ldg(Dn + dsym(q, t1)) / p.h[t1];
+        const double* Dn = nb_dfield(p, lc, cell, f, nbmask);
+        const double cqq = __ldg(Dn + q) * p.hinv[q], cq1 = __ldg(Dn + dsym(q, t1)) * p.hinv[t1];
         double rr[1][N], tt[1][N], ga[N];
 #pragma unroll
         for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(2 * f, e, line)];
@@ -319,8 +327,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         if (tk < 6 * N) {
             // neighbour stage 2 (lines along i2): u+ = V Va, s+ = V E + D+_qt2/h_t2 G Va
             if (!((nbi >> f) & 1u)) continue;
-            const double* Dn = nb_dfield(p, lc, f, nbmask);
-            const double cq2 = __ldg(Dn + dsym(q, t2)) / p.h[t2];
+            const double* Dn = nb_dfield(p, lc, cell, f, nbmask);
+            const double cq2 = __ldg(Dn + dsym(q, t2)) * p.hinv[t2];
             double rr[1][N], tt[1][N], va[N], gv[N];
 #pragma unroll
             for (int e = 0; e < N; ++e) va[e] = NT[FLay<N>::at(2 * f, line, e)];
@@ -339,7 +347,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         } else {
             // own pass A (lines along i1): s_part = D_qq/h_q d_n u + D_qt1/h_t1 Dc u-
             if (!((fact >> f) & 1u)) continue;
-            const double cqq = Dw[q] / p.h[q], cq1 = Dw[dsym(q, t1)] / p.h[t1];
+            const double cqq = Dw[q] * p.hinv[q], cq1 = Dw[dsym(q, t1)] * p.hinv[t1];
             double rr[1][N], tt[1][N];
 #pragma unroll
             for (int e = 0; e < N; ++e) rr[0][e] = OT[FLay<N>::at(2 * f, e, line)];
@@ -357,7 +365,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
 #pragma unroll
         for (int rr = 0; rr < 3; ++rr)
 #pragma unroll
-            for (int ss = 0; ss < 3; ++ss) Dh[rr][ss] = Dw[dsym(rr, ss)] / (p.h[rr] * p.h[ss]);
+            for (int ss = 0; ss < 3; ++ss) Dh[rr][ss] = Dw[dsym(rr, ss)] * (p.hinv[rr] * p.hinv[ss]);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
             if (!act[k]) continue;
@@ -383,8 +391,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
         const bool interior = (nbmask >> f) & 1u;
         const double dme = Dw[q];
-        const double cq2 = Dw[dsym(q, t2)] / p.h[t2];
-        const double cn = dme / p.h[q], c1 = Dw[dsym(q, t1)] / p.h[t1];
+        const double cq2 = Dw[dsym(q, t2)] * p.hinv[t2];
+        const double cn = dme * p.hinv[q], c1 = Dw[dsym(q, t1)] * p.hinv[t1];
         double uo[N], so[N], cv[N];
         {
             double rr[1][N], tt[1][N];
@@ -395,11 +403,12 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             for (int e = 0; e < N; ++e) so[e] = fma(cq2, tt[0][e], OT[FLay<N>::at(2 * f + 1, line, e)]);
         }
         double dnb = 0.0;
-        if (interior) dnb = __ldg(nb_dfield(p, lc, f, nbmask) + q);
+        if (interior) dnb = __ldg(nb_dfield(p, lc, cell, f, nbmask) + q);
         const double dm = sd ? dme : dnb, dp = sd ? dnb : dme;     // delta of T-, T+
         const double dsum = dm + dp;
-        const double wm = dsum == 0.0 ? 0.5 : dp / dsum, wp = dsum == 0.0 ? 0.5 : dm / dsum;   // C-5
-        const double gam = interior ? (dsum == 0.0 ? 0.0 : 2.0 * dm * dp / dsum) * p.sigma : dme * p.sigma;
+        const double rsum = dsum == 0.0 ? 0.0 : 1.0 / dsum;
+        const double wm = dsum == 0.0 ? 0.5 : dp * rsum, wp = dsum == 0.0 ? 0.5 : dm * rsum;   // C-5
+        const double gam = interior ? (2.0 * dm * dp * rsum) * p.sigma : dme * p.sigma;
         const double wself = sd ? wm : wp;
         const double bq = p.bq[q];
         double c2[N];
