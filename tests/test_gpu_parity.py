@@ -125,7 +125,7 @@ def test_upwind_energy_identity():
     assert abs(z @ y - E) < 1e-12 * E
 
 
-@pytest.mark.parametrize("k", [1, 3, 6])
+@pytest.mark.parametrize("k", [1, 3, 6, 7])
 def test_residual_polynomial_consistency(k):
     """dg_residual(z*, F) ~ 0 for u* in Q_k (reading C-1)."""
     dg = dgmod()
