@@ -175,11 +175,7 @@ dg_vb_kernel(const KParams p)
         lc[1] = (int)((e / nx) % ny);
         lc[2] = (int)(e / (nx * ny));
     } else {
-        const unsigned nz = (unsigned)p.task_cnt[2], nx = (unsigned)p.task_cnt[0];
-        const unsigned col = task / nz;
-        lc[0] = (int)(p.task_lo[0] + col % nx);
-        lc[1] = (int)(p.task_lo[1] + col / nx);
-        lc[2] = (int)(p.task_lo[2] + (task - col * nz));
+        decode_task(p, task, lc);   // the tiled traversal of the fast kernel (L2 reuse of neighbours)
     }
     const int64_t n3 = (int64_t)NN * N;
     const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * (int64_t)lc[2]);

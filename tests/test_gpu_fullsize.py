@@ -90,6 +90,16 @@ def test_c5_strong_max_size_slab():
     torch.cuda.empty_cache()
 
 
+def test_c5_weak_block_slab():
+    cfg = configs.c5_weak(1)
+    z, y = run_full(cfg)
+    ymax = float(y.abs().max())
+    for z0, seed in ((1, 3), (cfg.ncells[2] // 2, 4), (cfg.ncells[2] - 2, 5)):
+        assert slab_check(cfg, z, y, z0, 120, seed) <= TOL * ymax
+    del z, y
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("k", [2, 7])
 def test_problem_a_full_size_slab(k):
     """The paper's Problem A at ~4e8 DOFs (periodic, per-cell tensor field) on the general kernel;
