@@ -41,8 +41,12 @@ struct TabV {
 };
 __constant__ TabV<DG_N, DG_M> g_tabv;
 
+// one thread per quadrature-space pencil (CW = m^2 threads per cell); small m packs C cells per
+// CTA (all phases are CTA barriers), so the widest phase keeps most threads busy
 template <int M> struct VCfg {
-    static constexpr int TPC = ((M * M + 31) / 32) * 32;   // one thread per quadrature-space pencil
+    static constexpr int CW = M * M;
+    static constexpr int C = (M * M <= 64) ? 128 / (M * M) : 1;
+    static constexpr int TPC = ((C * CW + 31) / 32) * 32;
 };
 
 template <int N, int M> struct VLay {
@@ -58,7 +62,7 @@ template <int M> struct VFL {                               // 12 face arrays of
 template <int N, int M> struct VSmem {
     static constexpr int BT = 3 * 4 * (M + 2);               // 1D velocity tables: [dir][fn][point]
     static constexpr int PER_CELL = 2 * VLay<N, M>::SLOT + VFL<M>::SLOT + BT;
-    static constexpr int BYTES = PER_CELL * 8;
+    static constexpr int BYTES = VCfg<M>::C * PER_CELL * 8;
 };
 
 // r (n modal values) -> t (m points): t_i = sum_j V_ij r_j, even-odd over the symmetric rule
@@ -153,20 +157,24 @@ template <int N, int M>
 __global__ void __launch_bounds__(VCfg<M>::TPC)
 dg_vb_kernel(const KParams p)
 {
-    constexpr int TPC = VCfg<M>::TPC;
+    constexpr int TPC = VCfg<M>::CW;                   // stride of the per-cell loops below
+    constexpr int CC = VCfg<M>::C;
     constexpr int NN = N * N, MM = M * M;
     static_assert(N == DG_N && M == DG_M, "one (n, m) per translation unit");
     using LY = VLay<N, M>;
     using FL = VFL<M>;
     extern __shared__ double smem[];
     const TabV<N, M>& T = g_tabv;
-    const int lane = threadIdx.x;
-    double* A = smem;
+    const int slot = threadIdx.x / TPC;
+    const int lane = (slot < CC) ? threadIdx.x - slot * TPC : (1 << 20);   // padding threads: no work
+    double* A = smem + (slot < CC ? slot : 0) * VSmem<N, M>::PER_CELL;
     double* B = A + LY::SLOT;
     double* NT = B + LY::SLOT;
     double* BT = NT + FL::SLOT;                        // [dir][fn][M + 2]
 
-    unsigned task = blockIdx.x;
+    unsigned task = blockIdx.x * (unsigned)CC + (unsigned)(slot < CC ? slot : 0);
+    const bool valid = task < (unsigned)p.ntasks && slot < CC;
+    if (task >= (unsigned)p.ntasks) task = (unsigned)p.ntasks - 1u;
     int lc[3];
     if (p.task_list) {
         const unsigned e = (unsigned)p.task_list[task];
@@ -411,7 +419,7 @@ dg_vb_kernel(const KParams p)
     }
     __syncthreads();
     // phase 8: V^T along x on modal pencils (y, z < n); the single store of y (+ epilogue)
-    if (lane < NN) {
+    if (lane < NN && valid) {
         const int ya = lane % N, zb = lane / N;
         double t[M], r[N];
 #pragma unroll

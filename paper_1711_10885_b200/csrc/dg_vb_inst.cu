@@ -68,14 +68,15 @@ cudaError_t DG_CAT3(launch_vb_n, DG_N, m, DG_M)(const KParams& p, cudaStream_t s
         if (e != cudaSuccess) return e;
         g_attr[dev] = 1;
     }
-    vb::dg_vb_kernel<N, M><<<(unsigned)p.ntasks, vb::VCfg<M>::TPC, vb::VSmem<N, M>::BYTES, s>>>(p);
+    constexpr int C = vb::VCfg<M>::C;
+    vb::dg_vb_kernel<N, M><<<(unsigned)((p.ntasks + C - 1) / C), vb::VCfg<M>::TPC, vb::VSmem<N, M>::BYTES, s>>>(p);
     return cudaGetLastError();
 }
 
 int DG_CAT3(vb_info_n, DG_N, m, DG_M)(LaunchInfo* info)
 {
     constexpr int N = DG_N, M = DG_M;
-    info->cells_per_cta = 1;
+    info->cells_per_cta = vb::VCfg<M>::C;
     info->threads = vb::VCfg<M>::TPC;
     info->smem = vb::VSmem<N, M>::BYTES;
     cudaFuncAttributes fa;
