@@ -114,3 +114,18 @@ def test_problem_a_full_size_slab(k):
         assert err <= TOL * ymax
     del z, y
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("k", list(range(1, 11)))
+def test_c4_full_vector_vs_o3(k):
+    """Every element of the C4 vectors (~1e8 DOFs) against the Kronecker closed form O-3 (SURVEY.md 4:
+    "O-3: full on every config")."""
+    from oracle import o3_kron as o3
+    cfg = configs.c4(k)
+    z, y = run_full(cfg)
+    zn = z.cpu().numpy()
+    yn = y.cpu().numpy()
+    del z, y
+    torch.cuda.empty_cache()
+    y3 = o3.apply(*cfg.args(), zn)
+    assert np.abs(yn - y3).max() <= TOL * np.abs(y3).max()
