@@ -28,6 +28,12 @@ penalty <d-, d+> differ per face.
 NEXT-2/3 (the Taylor-Green run): `m` Gauss points per direction
 (over-integration, q = 2p+4 -> m = k+3) and a velocity field `bfield(x) -> b` evaluated at
 every quadrature point of volumes and faces.
+
+NEXT-3 affine geometry (Problem B's "affine geometries"): `J` maps the
+axis-aligned reference mesh on [lo, hi] to the physical mesh x = lo + J (xhat - lo). Every
+integral is evaluated in PHYSICAL terms: gradients J^-T grad_hat, volume element |J| dxhat,
+face normals nu = cof(J) e_q / |cof(J) e_q| and surface element |cof(J) e_q| dShat (cof(J) =
+|J| J^-T), delta = nu^T D nu and b.nu with the physical normal, the penalty sigma as given.
 """
 import numpy as np
 
@@ -78,7 +84,7 @@ def linear_field(x):
 
 
 def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic=(0, 0, 0), Dcell=None, m=0,
-             bfield=None):
+             bfield=None, J=None):
     """Dense A (N x N), N = prod(ncells) * (k+1)^3, cell-major global order (C-3).
 
     avg_sign = -1 selects the weighted average exactly as PAPER.md:271 prints it
@@ -99,12 +105,24 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic
     A = np.zeros((ncell * n3, ncell * n3))
     m = m if m else n
     xi, w = gauss01(m)
+    Jm = np.eye(3) if J is None else np.asarray(J, dtype=np.float64).reshape(3, 3)
+    detJ = float(np.linalg.det(Jm))
+    if detJ <= 0:
+        raise ValueError("the affine map must preserve orientation")
+    JinvT = np.linalg.inv(Jm).T
+    cof = detJ * JinvT
+    lo_v = np.asarray(lo, dtype=np.float64)
+
+    def phys_grad(grad):
+        """reference-mesh gradients (3, p, j) -> physical gradients J^-T grad_hat."""
+        return np.einsum("rs,spj->rpj", JinvT, grad)
 
     def points(ic, pts_per_dir):
         """physical coordinates (3, npts) of the tensor point set, x fastest (as _tensor orders it)."""
         X = [lo[q] + (ic[q] + np.asarray(pts_per_dir[q], float)) * h[q] for q in range(3)]
         gz, gy, gx = np.meshgrid(X[2], X[1], X[0], indexing="ij")
-        return np.stack([gx.ravel(), gy.ravel(), gz.ravel()])
+        xhat = np.stack([gx.ravel(), gy.ravel(), gz.ravel()])
+        return lo_v[:, None] + Jm @ (xhat - lo_v[:, None])     # physical points
 
     def velocity(ic, pts_per_dir):
         npts = np.prod([np.size(v) for v in pts_per_dir])
@@ -115,7 +133,8 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic
     # ---- volume blocks (coefficients constant per cell, uniform cells)
     if mask & VOLUME:
         phi, grad = _basis_on(n, [xi, xi, xi], h)
-        W = dT * np.einsum("a,b,c->cba", w, w, w).reshape(-1)
+        grad = phys_grad(grad)
+        W = detJ * dT * np.einsum("a,b,c->cba", w, w, w).reshape(-1)
         for e in range(ncell):
             ic = (e % nc[0], (e // nc[0]) % nc[1], e // (nc[0] * nc[1]))
             bp = velocity(ic, [xi, xi, xi])                       # (3, npts)
@@ -128,9 +147,11 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic
     for q in range(3):
         t = [r for r in range(3) if r != q]
         dF = dT / h[q]
-        Wf = dF * np.einsum("a,b->ba", w, w).reshape(-1)   # tangential point p = pt1 + m*pt2
-        nu = np.zeros(3)
-        nu[q] = 1.0
+        eq = np.zeros(3)
+        eq[q] = 1.0
+        area = float(np.linalg.norm(cof @ eq))              # |cof(J) e_q|: physical / reference face measure
+        Wf = area * dF * np.einsum("a,b->ba", w, w).reshape(-1)   # tangential point p = pt1 + m*pt2
+        nu = (cof @ eq) / area                              # physical unit normal of a reference q-face
 
         def face_basis(s):
             pts = [None, None, None]
@@ -138,7 +159,7 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic
             pts[t[0]] = xi
             pts[t[1]] = xi
             phi, grad = _basis_on(n, pts, h)
-            return phi, grad   # point ordering x-fastest over the three dirs = t1-fastest over the face
+            return phi, phys_grad(grad)   # point ordering x-fastest over the three dirs = t1-fastest over the face
 
         phi1, grad1 = face_basis(1)   # face x_q = 1 of a cell
         phi0, grad0 = face_basis(0)   # face x_q = 0 of a cell
@@ -168,7 +189,7 @@ def assemble(ncells, lo, hi, k, D, b, c, sigma, mask=ALL, avg_sign=1.0, periodic
                         gam = (0.0 if dm + dp == 0.0 else 2 * dm * dp / (dm + dp)) * sigma
                         fpts = [None, None, None]
                         fpts[q], fpts[t[0]], fpts[t[1]] = np.array([1.0]), xi, xi
-                        bnu = velocity(ic, fpts)[q][:, None]              # b . nu per face point
+                        bnu = (velocity(ic, fpts).T @ nu)[:, None]        # b . nu per face point
                         Phi = np.where(bnu >= 0, bnu * um, bnu * up)      # linear in the trial function
                         nDg = (wm * np.einsum("r,rs,spj->pj", nu, Dm, gm)
                                + avg_sign * wp * np.einsum("r,rs,spj->pj", nu, Dp, gp))   # nu.{D grad .}_w

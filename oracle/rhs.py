@@ -206,3 +206,93 @@ def upwind_energy(ncells, lo, hi, k, b, z):
         E += 0.5 * abs(b[q]) * np.sum(wt * tr0[tuple(first)] ** 2)
         E += 0.5 * abs(b[q]) * np.sum(wt * tr1[tuple(last)] ** 2)
     return E
+
+
+def consistency_data_affine(ncells, lo, hi, k, D, b, c, sigma, J, seed=0):
+    """(z*, F) on the affinely mapped mesh x = lo + J (xhat - lo) (NEXT-3) for a seeded polynomial u*
+    of TOTAL degree min(k, 2) in the physical coordinates (P_k is invariant under affine maps and
+    lies in the mapped Q_k, so SIPG reproduces it): u* = a0 + g.x (+ x^T H x for k >= 2).
+    Every integral physical: volume |J| dxhat, faces |cof(J) e_q| dShat with nu = cof(J) e_q / |.|,
+    l_h of PAPER.md:316-325 on the Dirichlet faces (gamma = nu^T D nu sigma, reading C-6)."""
+    nc = [int(v) for v in ncells]
+    n = k + 1
+    D = np.asarray(D, float).reshape(3, 3)
+    b = np.asarray(b, float)
+    Jm = np.asarray(J, float).reshape(3, 3)
+    detJ = float(np.linalg.det(Jm))
+    JinvT = np.linalg.inv(Jm).T
+    cof = detJ * JinvT
+    lo_v = np.asarray(lo, float)
+    rng = np.random.default_rng(seed)
+    a0 = rng.uniform(-1, 1)
+    g = rng.uniform(-1, 1, 3)
+    H = np.zeros((3, 3))
+    if k >= 2:
+        H = rng.uniform(-1, 1, (3, 3))
+        H = 0.5 * (H + H.T)
+
+    def u_star(x):                     # x: (3, npts)
+        return a0 + g @ x + np.einsum("ip,ij,jp->p", x, H, x)
+
+    def grad_u(x):
+        return g[:, None] + 2.0 * H @ x
+
+    f_const = -2.0 * np.trace(D @ H)   # -div(D grad u*)
+    h = [(hi[q] - lo[q]) / nc[q] for q in range(3)]
+    dT = h[0] * h[1] * h[2]
+    xi, w = gauss01(n)
+    th, dth = theta(n, xi)
+    t0, d0 = theta(n, [0.0])
+    t1, d1 = theta(n, [1.0])
+    ncell = nc[0] * nc[1] * nc[2]
+    z = np.zeros((ncell, n ** 3))
+    F = np.zeros((ncell, n ** 3))
+
+    def phys(ic, pts):                 # tensor points (x fastest) of reference cell ic -> physical (3, npts)
+        X = [lo[q] + (ic[q] + np.asarray(pts[q], float)) * h[q] for q in range(3)]
+        gz, gy, gx = np.meshgrid(X[2], X[1], X[0], indexing="ij")
+        xh = np.stack([gx.ravel(), gy.ravel(), gz.ravel()])
+        return lo_v[:, None] + Jm @ (xh - lo_v[:, None])
+
+    def tens(vx, vy, vz):              # [point (z slow, x fast), basis j = jx + n(jy + n jz)]
+        return np.einsum("ai,bj,ck->cbakji", vx, vy, vz).reshape(vz.shape[0] * vy.shape[0] * vx.shape[0], -1)
+
+    Wv = dT * np.einsum("k,j,i->kji", w, w, w).reshape(-1)
+    phi_v = tens(th, th, th)
+    for iz in range(nc[2]):
+        for iy in range(nc[1]):
+            for ix in range(nc[0]):
+                ic = (ix, iy, iz)
+                e = ix + nc[0] * (iy + nc[1] * iz)
+                x = phys(ic, [xi, xi, xi])
+                us = u_star(x)
+                z[e] = (Wv * us) @ phi_v / dT                    # (1/(|J| dT)) int u* phi |J| dxhat
+                fv = f_const + b @ grad_u(x) + c * us
+                F[e] += detJ * (Wv * fv) @ phi_v
+                for q in range(3):
+                    for s in (0, 1):
+                        if not ((s == 0 and ic[q] == 0) or (s == 1 and ic[q] == nc[q] - 1)):
+                            continue
+                        eq = np.zeros(3)
+                        eq[q] = 1.0
+                        area = float(np.linalg.norm(cof @ eq))
+                        nu = (cof @ eq) / area * (1.0 if s == 1 else -1.0)      # outward physical normal
+                        pts = [xi, xi, xi]
+                        pts[q] = np.array([float(s)])
+                        xf = phys(ic, pts)
+                        gval = u_star(xf)
+                        V = [th, th, th]
+                        G = [dth, dth, dth]
+                        V[q] = t1 if s == 1 else t0
+                        G[q] = d1 if s == 1 else d0
+                        phi = tens(V[0], V[1], V[2])
+                        grads = np.stack([tens(G[0], V[1], V[2]) / h[0], tens(V[0], G[1], V[2]) / h[1],
+                                          tens(V[0], V[1], G[2]) / h[2]])   # reference-mesh gradients
+                        pg = np.einsum("rs,spj->rpj", JinvT, grads)         # physical gradients
+                        nDg = np.einsum("r,rs,spj->pj", nu, D, pg)
+                        Wf = area * dT / h[q] * np.einsum("a,b->ba", w, w).reshape(-1)
+                        bnu = b @ nu
+                        gam = (nu @ D @ nu) * sigma
+                        phi_in = 0.0 if bnu >= 0 else bnu                  # Phi(0, g, b_nu)
+                        F[e] += ((-phi_in + gam) * Wf * gval) @ phi - (Wf * gval) @ nDg
+    return z.reshape(-1), F.reshape(-1)
