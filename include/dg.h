@@ -142,6 +142,18 @@ const char* dg_strerror(int code);
  * entry, bad flags), DG_ENOMEM, DG_ECUDA, DG_ENCCL. Not timed. */
 int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags, void* stream);
 
+/* Affine geometry (NEXT-3: the paper's Problem B has "affine geometries"): the
+ * physical mesh is the image x = lo + J (xhat - lo) of the axis-aligned box mesh of dg_setup
+ * (J row-major 3x3, det J > 0); D, b, c, sigma (dg_setup) and per-cell tensors (dg_set_diffusion)
+ * are physical. The kernels integrate on the reference mesh with Dhat = |J| J^-1 D J^-T,
+ * bhat = |J| J^-1 b, chat = |J| c and the penalty sigma / |J^-T e_q| per face direction (the
+ * exact change of variables of eq:blf for a constant J: volume element |J|, face element
+ * |cof(J) e_q|, normal cof(J) e_q / |cof(J) e_q|); the SSP mass is |J| Delta_T. J = I restores the
+ * axis-aligned mesh. Call before dg_set_diffusion with per-cell tensors.
+ * Errors: DG_EINVAL (det J <= 0, non-finite), DG_EUNSUPPORTED (velocity field / over-integration
+ * set, or per-cell tensors already set). */
+int dg_set_affine(dg_ctx* ctx, const double J[9]);
+
 /* Velocity field b(x) evaluated at every quadrature point (NEXT-2: the paper's Taylor-Green
  * transport run):
  *   kind 0: the constant b of dg_setup (default);

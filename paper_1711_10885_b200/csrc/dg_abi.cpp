@@ -37,6 +37,7 @@ struct dg_ctx {
     double* hy = nullptr;
     // general-coefficient path (full / per-cell D, dg_gen.cuh)
     bool general = false;            // launch dg_gen_kernel instead of dg_cell_kernel
+    bool dfield_const = false;       // the field is the constant tensor of dg_setup (not the caller's)
     double Dconst[9] = {0};          // the tensor given to dg_setup
     double* dfield = nullptr;        // [local cell][6]
     double* dsend[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -45,6 +46,12 @@ struct dg_ctx {
     // variable-velocity / over-integrated path (dg_vb.cuh)
     int m = 0;                       // Gauss points per direction (k+1 or k+3)
     bool vb = false;                 // launch dg_vb_kernel
+    // physical coefficients (dg_setup) and the affine map of the mesh (dg_set_affine; NEXT-3)
+    double Dphys[9] = {0}, bphys[3] = {0}, cphys = 0.0, sigma = 0.0;
+    double J[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    double Jinv[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    double detJ = 1.0;
+    bool affine = false;
     // TMA tensor maps of the last z / y pointers (n = 8 fast kernel)
     bool no_tma = false;             // DG_NO_TMA=1: per-thread global loads / stores instead
     const double* tma_z = nullptr;
@@ -126,6 +133,63 @@ extern "C" int dg_nccl_unique_id(void* out128)
     if (api->ncclGetUniqueId(&id) != 0) return DG_ENCCL;
     std::memcpy(out128, &id, sizeof(id));
     return DG_OK;
+}
+
+// Kernel coefficients from the physical D, b, c, sigma and the affine map x = lo + J (xhat - lo)
+// of the mesh (identity unless dg_set_affine): the kernels integrate on the axis-aligned
+// reference mesh, and for a constant J the weak form there is the same with
+//   Dhat = |J| J^-1 D J^-T,  bhat = |J| J^-1 b,  chat = |J| c,  sigma_q = sigma / |J^-T e_q|
+// (volume element |J| dxhat; face element |cof(J) e_q| dShat with nu = cof(J) e_q / |cof(J) e_q|,
+// cof(J) = |J| J^-T; delta = nu^T D nu = (|J| / |cof(J) e_q|^2) e_q^T Dhat e_q, so the weights
+// w+- are unchanged and the harmonic-mean penalty scales by |J| / |cof(J) e_q|).
+static void transform_D(const dg_ctx* ctx, const double* D, double* Dh)
+{
+    double T[9];                       // J^-1 D
+    for (int r = 0; r < 3; ++r)
+        for (int s = 0; s < 3; ++s) {
+            double a = 0.0;
+            for (int t = 0; t < 3; ++t) a += ctx->Jinv[3 * r + t] * D[3 * t + s];
+            T[3 * r + s] = a;
+        }
+    for (int r = 0; r < 3; ++r)
+        for (int s = 0; s < 3; ++s) {
+            double a = 0.0;
+            for (int t = 0; t < 3; ++t) a += T[3 * r + t] * ctx->Jinv[3 * s + t];
+            Dh[3 * r + s] = ctx->detJ * a;
+        }
+    for (int r = 0; r < 3; ++r)        // exact symmetry
+        for (int s = r + 1; s < 3; ++s) Dh[3 * s + r] = Dh[3 * r + s];
+}
+
+static void set_coefficients(dg_ctx* ctx)
+{
+    KParams& p = ctx->base;
+    double Dh[9], bh[3];
+    if (ctx->affine) {
+        transform_D(ctx, ctx->Dphys, Dh);
+        for (int r = 0; r < 3; ++r) {
+            double a = 0.0;
+            for (int t = 0; t < 3; ++t) a += ctx->Jinv[3 * r + t] * ctx->bphys[t];
+            bh[r] = ctx->detJ * a;
+        }
+    } else {
+        for (int i = 0; i < 9; ++i) Dh[i] = ctx->Dphys[i];
+        for (int r = 0; r < 3; ++r) bh[r] = ctx->bphys[r];
+    }
+    for (int q = 0; q < 3; ++q) {
+        double nrm = 0.0;              // |J^-T e_q| = norm of row q of J^-1 ... column q of J^-T
+        for (int t = 0; t < 3; ++t) nrm += ctx->Jinv[3 * q + t] * ctx->Jinv[3 * q + t];
+        p.sigq[q] = ctx->affine ? ctx->sigma / std::sqrt(nrm) : ctx->sigma;
+        p.kb[q] = bh[q] * p.hinv[q];
+        p.bq[q] = bh[q];
+        p.Dqq_h[q] = Dh[4 * q] * p.hinv[q];
+        p.gam[q] = Dh[4 * q] * p.sigq[q];  // <delta, delta> = delta for constant D
+    }
+    for (int r = 0; r < 3; ++r)
+        for (int s = 0; s < 3; ++s) p.Dhat[3 * r + s] = Dh[3 * r + s] * p.hinv[r] * p.hinv[s];
+    p.sigma = ctx->sigma;
+    p.c = ctx->detJ * ctx->cphys;
+    for (int i = 0; i < 9; ++i) ctx->Dconst[i] = Dh[i];
 }
 
 extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const double D[9], const double b[3],
@@ -215,26 +279,23 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
         p.nloc[q] = ctx->nloc[q];
         p.gofs[q] = ctx->gofs[q];
         p.gcells[q] = ctx->gcells[q];
-        p.kb[q] = b[q] / h[q];
-        p.bq[q] = b[q];
-        p.Dqq_h[q] = D[4 * q] / h[q];
-        p.gam[q] = D[4 * q] * sigma;     // <delta, delta> = delta for constant D
         p.per[q] = ctx->per[q];
         p.wrap[q] = ctx->per[q] && ctx->parts[q] == 1;
         p.h[q] = h[q];
         p.lo[q] = mesh->lo[q];
         p.bamp[q] = 1.0;
     }
-    p.sigma = sigma;
     p.bkind = 0;
     p.tma = 0;
     ctx->m = k + 1;
     if (const char* e = std::getenv("DG_NO_TMA")) ctx->no_tma = std::atoi(e) != 0;
-    for (int r = 0; r < 3; ++r)
-        for (int s = 0; s < 3; ++s) p.Dhat[3 * r + s] = D[3 * r + s] / (h[r] * h[s]);
-    p.c = c;
     p.dT = h[0] * h[1] * h[2];
     for (int q = 0; q < 3; ++q) p.dF[q] = p.dT / h[q];
+    for (int i = 0; i < 9; ++i) ctx->Dphys[i] = D[i];
+    for (int q = 0; q < 3; ++q) ctx->bphys[q] = b[q];
+    ctx->cphys = c;
+    ctx->sigma = sigma;
+    set_coefficients(ctx);
     // Traversal order (L2 reuse of neighbour cells): z fastest inside columns, columns
     // grouped in 4 x 16 tiles, so a cell's neighbours are touched within ~4096 tasks.
 
@@ -289,7 +350,6 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
         for (int q = 0; q < 3; ++q) { ctx->inner_lo[q] = 0; ctx->inner_cnt[q] = ctx->nloc[q]; }
     }
     for (int f = 0; f < 6; ++f) p.ghost[f] = ctx->recvbuf[f];
-    for (int i = 0; i < 9; ++i) ctx->Dconst[i] = D[i];
     // a full (off-diagonal) constant tensor runs on the general-coefficient kernel with a
     // constant per-cell field; a diagonal one on the fast kernel
     bool offdiag = false;
@@ -330,7 +390,7 @@ static int update_vb(dg_ctx* ctx)
 {
     const bool want = ctx->base.bkind != 0 || ctx->m != ctx->k + 1;
     if (!want) { ctx->vb = false; return DG_OK; }
-    if (ctx->general) return DG_EUNSUPPORTED;                 // per-cell / full D with b(x): not built
+    if (ctx->general || ctx->affine) return DG_EUNSUPPORTED;  // per-cell / full D / affine with b(x): not built
     if (!vb_available(ctx->k, ctx->m)) return DG_EUNSUPPORTED;
     std::lock_guard<std::mutex> lk(g_vb_mu);
     if (!g_vb_done[ctx->device][ctx->k][ctx->m]) {
@@ -341,6 +401,38 @@ static int update_vb(dg_ctx* ctx)
     }
     ctx->vb = true;
     return DG_OK;
+}
+
+extern "C" int dg_set_affine(dg_ctx* ctx, const double J[9])
+{
+    if (!ctx || !J) return DG_EINVAL;
+    for (int i = 0; i < 9; ++i)
+        if (!std::isfinite(J[i])) return DG_EINVAL;
+    const double det = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
+                       J[2] * (J[3] * J[7] - J[4] * J[6]);
+    if (!(det > 0.0)) return DG_EINVAL;                   // orientation preserving, non-degenerate
+    if (ctx->vb) return DG_EUNSUPPORTED;                  // b(x) / over-integration: axis-aligned only
+    if (ctx->general && !ctx->dfield_const) return DG_EUNSUPPORTED;   // set the map before per-cell tensors
+    DG_CUDA(cudaSetDevice(ctx->device));
+    for (int i = 0; i < 9; ++i) ctx->J[i] = J[i];
+    ctx->detJ = det;
+    // J^-1 = adj(J) / det
+    ctx->Jinv[0] = (J[4] * J[8] - J[5] * J[7]) / det;
+    ctx->Jinv[1] = (J[2] * J[7] - J[1] * J[8]) / det;
+    ctx->Jinv[2] = (J[1] * J[5] - J[2] * J[4]) / det;
+    ctx->Jinv[3] = (J[5] * J[6] - J[3] * J[8]) / det;
+    ctx->Jinv[4] = (J[0] * J[8] - J[2] * J[6]) / det;
+    ctx->Jinv[5] = (J[2] * J[3] - J[0] * J[5]) / det;
+    ctx->Jinv[6] = (J[3] * J[7] - J[4] * J[6]) / det;
+    ctx->Jinv[7] = (J[1] * J[6] - J[0] * J[7]) / det;
+    ctx->Jinv[8] = (J[0] * J[4] - J[1] * J[3]) / det;
+    bool ident = true;
+    for (int i = 0; i < 9; ++i) ident = ident && J[i] == ((i % 4 == 0) ? 1.0 : 0.0);
+    ctx->affine = !ident;
+    set_coefficients(ctx);
+    // the transformed tensor may be full: the general kernel with a constant field, else the fast kernel
+    ctx->general = false;
+    return dg_set_diffusion(ctx, nullptr, 0, nullptr) == DG_OK ? cuda_rc(cudaStreamSynchronize(nullptr)) : DG_ECUDA;
 }
 
 extern "C" int dg_set_velocity(dg_ctx* ctx, int kind, const double amp[3])
@@ -400,10 +492,13 @@ extern "C" int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags
             if (ctx->drecv[f])
                 DG_CUDA(launch_dfield_const(ctx->drecv[f], ctx->Dconst, ctx->halo_count[f] / ctx->n3, s));
         ctx->general = true;
+        ctx->dfield_const = true;
         return DG_OK;
     }
     DG_CUDA(cudaMemsetAsync(ctx->dbad, 0, sizeof(int), s));
-    DG_CUDA(launch_dfield_pack(Dcell, ctx->dfield, ctx->dbad, ncell, s));
+    // physical tensors; on an affine mesh each is mapped to |J| J^-1 D J^-T on the fly
+    DG_CUDA(launch_dfield_pack(Dcell, ctx->dfield, ctx->dbad, ncell, ctx->affine ? ctx->Jinv : nullptr, ctx->detJ, s));
+    ctx->dfield_const = false;
     int bad = 0;
     DG_CUDA(cudaMemcpyAsync(&bad, ctx->dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
     DG_CUDA(cudaStreamSynchronize(s));
@@ -672,7 +767,7 @@ extern "C" int dg_ssp_stage(dg_ctx* ctx, const double* z, const double* f, const
     if (a != 0.0 && !w) return DG_EINVAL;
     e.a = a;
     e.b = b;
-    e.s = dt / ctx->base.dT;     // M^-1 = 1/Delta_T (orthonormal basis, cuboid cells)
+    e.s = dt / (ctx->base.dT * ctx->detJ);   // M^-1 = 1/(|J| Delta_T) (orthonormal basis)
     return apply_impl(ctx, z, nullptr, out, DG_ALL, (cudaStream_t)stream, &e);
 }
 

@@ -84,7 +84,10 @@ namespace dg {
 // Per-cell tensors [cell][9] (row-major) -> [cell][6] = D00 D11 D22 D01 D02 D12 with
 // validation: symmetric, finite, nonnegative diagonal (PSD necessary conditions); *bad != 0
 // on violation (dg_set_diffusion returns DG_EINVAL).
-__global__ void dfield_pack_kernel(const double* __restrict__ D9, double* __restrict__ D6, int* bad, int64_t ncell)
+struct Mat3 { double a[9]; };
+
+__global__ void dfield_pack_kernel(const double* __restrict__ D9, double* __restrict__ D6, int* bad, int64_t ncell,
+                                   int affine, Mat3 Ji, double det)
 {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncell; e += (int64_t)gridDim.x * blockDim.x) {
         const double* d = D9 + 9 * e;
@@ -92,8 +95,20 @@ __global__ void dfield_pack_kernel(const double* __restrict__ D9, double* __rest
         for (int i = 0; i < 9; ++i) ok = ok && isfinite(d[i]);
         ok = ok && d[1] == d[3] && d[2] == d[6] && d[5] == d[7] && d[0] >= 0.0 && d[4] >= 0.0 && d[8] >= 0.0;
         if (!ok) atomicOr(bad, 1);
+        double m[9];
+        for (int i = 0; i < 9; ++i) m[i] = d[i];
+        if (affine) {                  // Dhat = |J| J^-1 D J^-T (reference-mesh tensor of an affine mesh)
+            double t[9];
+            for (int r = 0; r < 3; ++r)
+                for (int s = 0; s < 3; ++s)
+                    t[3 * r + s] = Ji.a[3 * r] * d[s] + Ji.a[3 * r + 1] * d[3 + s] + Ji.a[3 * r + 2] * d[6 + s];
+            for (int r = 0; r < 3; ++r)
+                for (int s = 0; s < 3; ++s)
+                    m[3 * r + s] = det * (t[3 * r] * Ji.a[3 * s] + t[3 * r + 1] * Ji.a[3 * s + 1] +
+                                          t[3 * r + 2] * Ji.a[3 * s + 2]);
+        }
         double* o = D6 + 6 * e;
-        o[0] = d[0]; o[1] = d[4]; o[2] = d[8]; o[3] = d[1]; o[4] = d[2]; o[5] = d[5];
+        o[0] = m[0]; o[1] = m[4]; o[2] = m[8]; o[3] = m[1]; o[4] = m[2]; o[5] = m[5];
     }
 }
 
@@ -113,10 +128,13 @@ static unsigned blocks_for(int64_t n)
     return (unsigned)(b > 0 ? b : 1);
 }
 
-cudaError_t launch_dfield_pack(const double* D9, double* D6, int* bad, int64_t ncell, cudaStream_t s)
+cudaError_t launch_dfield_pack(const double* D9, double* D6, int* bad, int64_t ncell, const double* Jinv,
+                               double det, cudaStream_t s)
 {
     if (ncell == 0) return cudaSuccess;
-    dfield_pack_kernel<<<blocks_for(ncell), 256, 0, s>>>(D9, D6, bad, ncell);
+    Mat3 Ji;
+    for (int i = 0; i < 9; ++i) Ji.a[i] = Jinv ? Jinv[i] : (i % 4 == 0 ? 1.0 : 0.0);
+    dfield_pack_kernel<<<blocks_for(ncell), 256, 0, s>>>(D9, D6, bad, ncell, Jinv ? 1 : 0, Ji, det);
     return cudaGetLastError();
 }
 

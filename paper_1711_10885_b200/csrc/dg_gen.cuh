@@ -408,7 +408,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         const double dsum = dm + dp;
         const double rsum = dsum == 0.0 ? 0.0 : 1.0 / dsum;
         const double wm = dsum == 0.0 ? 0.5 : dp * rsum, wp = dsum == 0.0 ? 0.5 : dm * rsum;   // C-5
-        const double gam = interior ? (2.0 * dm * dp * rsum) * p.sigma : dme * p.sigma;
+        const double gam = (interior ? 2.0 * dm * dp * rsum : dme) * p.sigq[q];
         const double wself = sd ? wm : wp;
         const double bq = p.bq[q];
         double c2[N];

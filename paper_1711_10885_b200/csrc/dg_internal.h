@@ -57,6 +57,7 @@ struct KParams {
     const double* Dfield;     // [local cell][6] = D00 D11 D22 D01 D02 D12
     const double* Dghost[6];  // neighbour-rank layers of Dfield per face (nullptr: none)
     double sigma;
+    double sigq[3];           // penalty factor per face direction (sigma / |J^-T e_q| on an affine mesh)
     double h[3];
     // variable-velocity kernel (NEXT-2/3):
     int bkind;                // 0 constant b, 1 Taylor-Green field, 2 linear (x2, x3, x1)
@@ -88,7 +89,8 @@ int gen_launch_info(int k, LaunchInfo* info);
 
 // Halo / inputs kernels (dg_aux.cu).
 cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc[3], int face, cudaStream_t s);
-cudaError_t launch_dfield_pack(const double* D9, double* D6, int* bad, int64_t ncell, cudaStream_t s);
+cudaError_t launch_dfield_pack(const double* D9, double* D6, int* bad, int64_t ncell, const double* Jinv,
+                               double det, cudaStream_t s);
 cudaError_t launch_dfield_const(double* D6, const double D9[9], int64_t ncell, cudaStream_t s);
 cudaError_t launch_fill_uniform(double* dst, int64_t count, uint64_t seed, int64_t offset, cudaStream_t s);
 cudaError_t launch_fill_uniform_local(double* dst, int n3, const int64_t nloc[3], const int64_t gofs[3],

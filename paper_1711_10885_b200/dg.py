@@ -22,7 +22,8 @@ BC_DIRICHLET, BC_PERIODIC = 0, 1
 EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residual", "dg_apply_host",
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
-            "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage", "dg_set_velocity", "dg_set_quadrature"]
+            "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage", "dg_set_velocity", "dg_set_quadrature",
+            "dg_set_affine"]
 
 
 class DGError(RuntimeError):
@@ -77,6 +78,7 @@ def lib():
         L.dg_set_diffusion.argtypes = [vp, vp, ctypes.c_uint, vp]
         L.dg_fill_uniform_cells.argtypes = [vp, vp, ctypes.c_int, u64, vp]
         L.dg_set_velocity.argtypes = [vp, ctypes.c_int, vp]
+        L.dg_set_affine.argtypes = [vp, vp]
         L.dg_set_quadrature.argtypes = [vp, ctypes.c_int]
         L.dg_ssp_stage.argtypes = [vp, vp, vp, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, vp]
         for name in EXPORTED:
@@ -222,6 +224,11 @@ class Operator:
             ncell = self.ndofs // self.n3
             _dev_vec(Dcell, ncell * 9, "Dcell")
         _check(lib().dg_set_diffusion(self._h, _ptr(Dcell), flags, _stream(stream)), "dg_set_diffusion")
+
+    def set_affine(self, J):
+        """Physical mesh x = lo + J (xhat - lo) of the axis-aligned box (dg_set_affine; NEXT-3)."""
+        a = (ctypes.c_double * 9)(*[float(v) for v in np.asarray(J, dtype=np.float64).ravel()])
+        _check(lib().dg_set_affine(self._h, a), "dg_set_affine")
 
     def set_velocity(self, kind, amp=(1.0, 1.0, 1.0)):
         """Velocity field b(x) at every quadrature point: 0 constant, 1 Taylor-Green, 2 linear (dg_set_velocity)."""
