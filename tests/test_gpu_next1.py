@@ -294,3 +294,30 @@ def test_ssp_gpu_conserves_mass_periodic():
     op.close()
     m1 = float(u.view(cfg.ncell, -1)[:, 0].sum())
     assert np.isfinite(m1) and abs(m1 - m0) < 1e-12 * float(u.abs().sum())
+
+
+def test_general_kernel_symmetry_and_energy():
+    """Invariants on the general kernel: SIPG symmetry for b = 0 with per-cell tensors on a periodic
+    box (w^T A z = z^T A w), and for D = 0, c = 0 the pure-upwind energy z^T A z (positive: the
+    upwind flux only dissipates) equal to O-1's."""
+    from paper_1711_10885_b200 import dg
+    cfg = configs.small(4, ncells=(4, 3, 3), hi=(1.0, 0.75, 0.75), b=(0, 0, 0), c=0.5)
+    Dc = spd_field(cfg.ncell, 12)
+    z = inputs.uniform(cfg.ndofs, 1)
+    w = inputs.uniform(cfg.ndofs, 2)
+    yz = run(cfg, z, (1, 1, 1), Dcell=Dc)
+    yw = run(cfg, w, (1, 1, 1), Dcell=Dc)
+    assert abs(w @ yz - z @ yw) < 1e-13 * abs(w @ yz)
+    cfg2 = configs.small(3, ncells=(4, 3, 2), hi=(1.0, 0.75, 0.5), D=(0,) * 9, b=(1.0, -0.5, 0.25), c=0.0)
+    op = dg.Operator(cfg2.ncells, cfg2.lo, cfg2.hi, cfg2.k, (0, 0.1, 0, 0.1, 0, 0, 0, 0, 0), cfg2.b, 0.0,
+                     cfg2.sigma, bc=dg.bc_from_periodic((1, 1, 1)))   # off-diagonal D: the general kernel
+    op.set_diffusion(torch.zeros(cfg2.ncell * 9, dtype=torch.float64, device="cuda"))
+    zz = inputs.uniform(cfg2.ndofs, 3)
+    zt = torch.from_numpy(zz).cuda()
+    y = torch.empty_like(zt)
+    op.apply(zt, y)
+    torch.cuda.synchronize()
+    op.close()
+    yref, _ = o1.apply(*cfg2.args(), zz, periodic=(1, 1, 1))
+    E = zz @ yref
+    assert E > 0 and abs(zz @ y.cpu().numpy() - E) < 1e-12 * E
