@@ -183,6 +183,8 @@ __device__ __forceinline__ bool stage_x(const KParams& p, double* STG, double* X
     if (tid == 0) {
         const int64_t clo = (lc[0] > 0) ? cell - 1 : cell + (nq - 1);
         const int64_t chi = (lc[0] + 1 < nq) ? cell + 1 : cell - (nq - 1);
+        const int64_t ncell = p.nloc[0] * p.nloc[1] * p.nloc[2];
+        DG_ASSERT(cell >= 0 && cell < ncell && clo >= 0 && clo < ncell && chi >= 0 && chi < ncell);
         const bool xl = tma_x && ll, xh = tma_x && lh;
         expect_tx(mbar, 4096u * (1u + (xl ? 1u : 0u) + (xh ? 1u : 0u)));
         load_rows(STG, &p.tmz, (int)(cell * 64), mbar);
@@ -378,6 +380,18 @@ __device__ __forceinline__ void nb_load(const KParams& p, const double* zc, cons
     const int64_t wst = (int64_t)(nq - 1) * st * n3;   // periodic wrap inside this rank's box
     const double* zl = (lq > 0) ? zc - st * n3 : (p.wrap[q] ? zc + wst : (hl ? p.ghost[2 * q] + gi * n3 : zc));
     const double* zh = (lq + 1 < nq) ? zc + st * n3 : (p.wrap[q] ? zc - wst : (hh ? p.ghost[2 * q + 1] + gi * n3 : zc));
+#ifdef DG_CHECK
+    {
+        const int64_t nall = p.nloc[0] * p.nloc[1] * p.nloc[2] * n3;
+        const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+        const int64_t nlay = p.nloc[t1] * p.nloc[t2];
+        DG_ASSERT(gi >= 0 && gi < nlay);
+        if (lq > 0 || p.wrap[q] || !hl) DG_ASSERT(zl >= p.z && zl + n3 <= p.z + nall);
+        else DG_ASSERT(p.ghost[2 * q] != nullptr);
+        if (lq + 1 < nq || p.wrap[q] || !hh) DG_ASSERT(zh >= p.z && zh + n3 <= p.z + nall);
+        else DG_ASSERT(p.ghost[2 * q + 1] != nullptr);
+    }
+#endif
 #pragma unroll
     for (int k = 0; k < P; ++k) {
         if (q == 0 && N % 2 == 0) {
@@ -768,6 +782,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     }
     const int64_t n3 = (int64_t)NN * N;
     const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * (int64_t)lc[2]);
+    DG_ASSERT(lc[0] >= 0 && lc[0] < p.nloc[0] && lc[1] >= 0 && lc[1] < p.nloc[1] && lc[2] >= 0 && lc[2] < p.nloc[2]);
     const double* zc = p.z + cell * n3;
     const bool do_int = (p.mask & 2u) != 0, do_bnd = (p.mask & 4u) != 0, do_vol = (p.mask & 1u) != 0;
 

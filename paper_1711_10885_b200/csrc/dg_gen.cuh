@@ -72,10 +72,12 @@ __device__ __forceinline__ const double* nb_dfield(const KParams& p, const int (
     const int lcq = sel3i(lc[0], lc[1], lc[2], q);
     const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
     const int lq = lcq + (s ? 1 : -1);
+    DG_ASSERT(lq >= -1 && lq <= nq);
     if (lq >= 0 && lq < nq) return p.Dfield + 6 * (cell + (s ? st : -st));
     if (p.wrap[q]) return p.Dfield + 6 * (cell + (s ? -(int64_t)(nq - 1) * st : (int64_t)(nq - 1) * st));
     const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
                                                                         : (lc[0] + p.nloc[0] * lc[1]);
+    DG_ASSERT(p.Dghost[f] != nullptr);
     return p.Dghost[f] + 6 * gi;
 }
 
@@ -148,6 +150,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     }
     const int64_t n3 = (int64_t)NN * N;
     const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * (int64_t)lc[2]);
+    DG_ASSERT(lc[0] >= 0 && lc[0] < p.nloc[0] && lc[1] >= 0 && lc[1] < p.nloc[1] && lc[2] >= 0 && lc[2] < p.nloc[2]);
     const double* zc = p.z + cell * n3;
     const bool do_int = (p.mask & 2u) != 0, do_bnd = (p.mask & 4u) != 0, do_vol = (p.mask & 1u) != 0;
 

@@ -7,6 +7,15 @@
 
 namespace dg {
 
+// Device-side bounds checks of the debug build (-DDG_CHECK; tools/check_build.py): a violated
+// index traps the kernel, so the GPU test suite run against that build is a memcheck of the
+// cell / neighbour / ghost / TMA indexing (compute-sanitizer is unavailable on the GPU pool).
+#ifdef DG_CHECK
+#define DG_ASSERT(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define DG_ASSERT(c) do { } while (0)
+#endif
+
 constexpr int KMAX = 10;
 constexpr int NMAX = KMAX + 1;
 

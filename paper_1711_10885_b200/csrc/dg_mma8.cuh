@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(32 * C, MINB) dg_cell_mma8(const KParams p)
     }
     const int64_t n3 = 512;
     const int64_t cell = lc[0] + p.nloc[0] * (lc[1] + p.nloc[1] * (int64_t)lc[2]);
+    DG_ASSERT(lc[0] >= 0 && lc[0] < p.nloc[0] && lc[1] >= 0 && lc[1] < p.nloc[1] && lc[2] >= 0 && lc[2] < p.nloc[2]);
     const double* zc = p.z + cell * n3;
     const bool do_int = (p.mask & 2u) != 0, do_bnd = (p.mask & 4u) != 0, do_vol = (p.mask & 1u) != 0;
     unsigned nbmask = 0;
