@@ -1,13 +1,14 @@
 // Fused cell kernel: y = A z for the SIPG/WSIPG operator of arXiv 1711.10885,
 // FP64, sm_100a.
 //
-// Work decomposition: a cell is processed by TPC threads (one warp for n = 7..9, a
-// fraction of a warp for small n, two warps for n >= 10); each thread owns P
-// "pencils" (lines of n points along one direction) in each of the three roles
-// (x-, y- and z-pencil), so one uniform-register load of a 1D matrix entry feeds P
-// DFMAs and the cell's phases synchronise with __syncwarp only (no CTA barrier for
-// TPC <= 32). The 1D matrices live in __constant__ memory (one copy per use site so
-// the compiler reloads per stage instead of hoisting whole matrices into registers).
+// Work decomposition (Cfg<N>, measured per degree): a cell is processed by TPC threads
+// (a fraction of a warp for small n, with several cells per CTA; 1-4 warps for n >= 5, one
+// cell per CTA; k = 7: two warps, one pencil per thread); each thread owns P "pencils" (lines
+// of n points along one direction) in each of the three roles (x-, y- and z-pencil). Phases
+// synchronise with __syncwarp when a cell fits a warp, else with CTA barriers. The 1D
+// matrices live in __constant__ memory (one copy per use site so the compiler reloads per
+// stage instead of hoisting whole matrices into registers). At n = 8 the own and x-neighbour
+// blocks arrive by TMA and y leaves by a TMA store (namespace tma below).
 //
 // Per cell (Algorithm 1, reorganised owner-computes):
 //   (1) u at the n^3 Gauss points by sum factorization u_q = (V x V x V) z
