@@ -49,6 +49,10 @@ struct Tab {
     double L[6][4][N];       // per use site: L_l(0), L_l(1), L'_l(0), L'_l(1)
     double th0[N], th1[N], dth0[N], dth1[N];
     double Gh[HC][N];        // G_ij = theta'_j(xi_i), rows i < ceil(n/2) (general kernel, even-odd)
+    // sigma/delta form of the fast kernel (n = 8, SDF below): doubled forward V and doubled even-odd
+    // Dc, Dc^T diag(w), one copy per use site
+    double Vs[9][HC][N];
+    EO<N> Dcs[3], DcTws[3];
     // even-odd forms used by the roles (one copy per direction):
     EO<N> DcTw[3];                         // Dc^T diag(w): Gauss weights folded into the transposed stage
     double Le[3][4][(N / 2) > 0 ? N / 2 : 1];  // (L0_i +- L0_{n-1-i})/2, (L'0_i +- L'0_{n-1-i})/2, i < n/2
@@ -329,6 +333,88 @@ __device__ __forceinline__ double dot(const double* a, const double* v)
     return s;
 }
 
+// ---------------------------------------------------------------------------------- sigma/delta form
+// For even n every array of the n = 8 fast kernel is kept in "sigma/delta form" along each of
+// its three directions: position i < n/2 holds t_i + t_(n-1-i), position n-1-i holds
+// t_i - t_(n-1-i). All pointwise operations (Gauss weights w_i = w_(n-1-i), constant
+// coefficients, the face fluxes, the traces and lifts) are linear with symmetric weights, so
+// they commute with this change of basis along every direction, and the 1D stages consume and
+// produce it directly with doubled even-odd tables: no sum / difference instructions around
+// the forward stages, the Dc and Dc^T diag(w) stages, or before the backward stages.
+__host__ __device__ constexpr bool sdf(int n) { return n == 8; }
+
+template <int N, int P>
+__device__ __forceinline__ void v_fwd_sd(const double (&Vs)[(N + 1) / 2][N], const double (&r)[P][N], double (&t)[P][N])
+{
+    constexpr int H = N / 2;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        double E[P], O[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) { E[k] = 0.0; O[k] = 0.0; }
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                if (j & 1) O[k] = fma(Vs[i][j], r[k][j], O[k]);
+                else E[k] = fma(Vs[i][j], r[k][j], E[k]);
+            }
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            t[k][i] = E[k];
+            t[k][N - 1 - i] = O[k];
+        }
+    }
+}
+
+template <int N, int P>
+__device__ __forceinline__ void v_bwd_sd(const double (&Vh)[(N + 1) / 2][N], const double (&r)[P][N], double (&t)[P][N])
+{
+    constexpr int H = N / 2;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        double acc[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) acc[k] = 0.0;
+#pragma unroll
+        for (int i = 0; i < H; ++i)
+#pragma unroll
+            for (int k = 0; k < P; ++k) acc[k] = fma(Vh[i][j], (j & 1) ? r[k][N - 1 - i] : r[k][i], acc[k]);
+#pragma unroll
+        for (int k = 0; k < P; ++k) t[k][j] = acc[k];
+    }
+}
+
+// out = A2 r with A2 the doubled even-odd form, r and out in sigma/delta form; optional addends
+template <int N, int P, bool ADD>
+__device__ __forceinline__ void c_apply_s(const EO<N>& A2, const double (&r)[P][N], double (&t)[P][N],
+                                          const double (&qa)[P][(N / 2) > 0 ? N / 2 : 1],
+                                          const double (&pb)[P][(N / 2) > 0 ? N / 2 : 1])
+{
+    constexpr int H = N / 2;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        double Pp[P], Q[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            Pp[k] = ADD ? pb[k][i] : 0.0;
+            Q[k] = ADD ? qa[k][i] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < H; ++j)
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                Pp[k] = fma(A2.p[i][j], r[k][j], Pp[k]);
+                Q[k] = fma(A2.m[i][j], r[k][N - 1 - j], Q[k]);
+            }
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            t[k][i] = Q[k];
+            t[k][N - 1 - i] = Pp[k];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------------- face terms
 // Contribution cv * phi_i + cg_phys * d_q phi_i of one face point, returned as
 // (cv, cg = cg_phys / h_q, the coefficient of the REFERENCE normal derivative).
@@ -460,7 +546,8 @@ __device__ __forceinline__ void nb_tangential(const double (&Vh)[(N + 1) / 2][N]
             double rr[1][N], tt[1][N];
 #pragma unroll
             for (int e = 0; e < N; ++e) rr[0][e] = NT[dim ? FLay<N>::at(arr, line, e) : FLay<N>::at(arr, e, line)];
-            v_fwd<N, 1>(Vh, rr, tt);
+            if constexpr (sdf(N)) v_fwd_sd<N, 1>(Vh, rr, tt);   // Vh is a doubled copy (Tab::Vs)
+            else v_fwd<N, 1>(Vh, rr, tt);
 #pragma unroll
             for (int e = 0; e < N; ++e) NT[dim ? FLay<N>::at(arr, line, e) : FLay<N>::at(arr, e, line)] = tt[0][e];
         }
@@ -625,8 +712,21 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
 {
     constexpr int H = N / 2;
     constexpr int HH = H > 0 ? H : 1;
+    constexpr bool SD = sdf(N);
     double g[P][N], s[P][HH], d[P][HH];
-    c_apply_sd<N, P>(T.Dc[q], r, g, s, d);
+    if constexpr (SD) {                         // r in sigma/delta form: the sums are the input itself
+        double z0[P][HH];
+        c_apply_s<N, P, false>(T.Dcs[q], r, g, z0, z0);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int j = 0; j < H; ++j) {
+                s[k][j] = r[k][j];
+                d[k][j] = r[k][N - 1 - j];
+            }
+    } else {
+        c_apply_sd<N, P>(T.Dc[q], r, g, s, d);
+    }
     const double* Lp = T.Le[q][0];
     const double* Lm = T.Le[q][1];
     const double* LDp = T.Le[q][2];
@@ -646,7 +746,7 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
             Bd = fma(LDm[i], d[k][i], Bd);
         }
         const double tr_u[2] = {A + B, A - B}, tr_d[2] = {Ad + Bd, Bd - Ad};
-        const double Wf = p.dF[q] * wab;
+        const double Wf = (SD ? 2.0 : 1.0) * p.dF[q] * wab;   // SD: the lift addends enter doubled
         FaceOut fo[2];
 #pragma unroll
         for (int sd = 0; sd < 2; ++sd) {
@@ -678,7 +778,8 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
 #pragma unroll
         for (int e = 0; e < N; ++e) g[k][e] = fma(kd, g[k][e], -kb * r[k][e]);
     }
-    c_apply_add<N, P>(T.DcTw[q], g, out, qa, pbv, mid);
+    if constexpr (SD) c_apply_s<N, P, true>(T.DcTws[q], g, out, qa, pbv);
+    else c_apply_add<N, P>(T.DcTw[q], g, out, qa, pbv, mid);
     if (with_reaction && do_vol) {
 #pragma unroll
         for (int k = 0; k < P; ++k) {
@@ -864,7 +965,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
             }
         }
         }
-        v_fwd<N, P>(T.Vh[0], r, t);
+        if constexpr (sdf(N)) v_fwd_sd<N, P>(T.Vs[0], r, t); else v_fwd<N, P>(T.Vh[0], r, t);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k])
@@ -879,13 +980,13 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         for (int k = 0; k < P; ++k)
 #pragma unroll
             for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-        v_fwd<N, P>(T.Vh[1], r, t);
+        if constexpr (sdf(N)) v_fwd_sd<N, P>(T.Vs[1], r, t); else v_fwd<N, P>(T.Vh[1], r, t);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) A1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
-        nb_tangential<N, TPC>(T.Vh[2], NT, 0, 0, nbi, (lane + TPC / 2) % TPC);
+        nb_tangential<N, TPC>(sdf(N) ? T.Vs[2] : T.Vh[2], NT, 0, 0, nbi, (lane + TPC / 2) % TPC);
         nb_contract<N, P>(T, NT, 1, nbi, pa, pb, act, rl, rh);
         csync();
 
@@ -896,14 +997,14 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         for (int k = 0; k < P; ++k)
 #pragma unroll
             for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
-        v_fwd<N, P>(T.Vh[3], r, t);
+        if constexpr (sdf(N)) v_fwd_sd<N, P>(T.Vs[3], r, t); else v_fwd<N, P>(T.Vh[3], r, t);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
-        nb_tangential<N, TPC>(T.Vh[4], NT, 1, 0, nbi, lane);
-        nb_tangential<N, TPC>(T.Vh[5], NT, 0, 1, nbi, (lane + TPC / 2) % TPC);
+        nb_tangential<N, TPC>(sdf(N) ? T.Vs[4] : T.Vh[4], NT, 1, 0, nbi, lane);
+        nb_tangential<N, TPC>(sdf(N) ? T.Vs[5] : T.Vh[5], NT, 0, 1, nbi, (lane + TPC / 2) % TPC);
         nb_contract<N, P>(T, NT, 2, nbi, pa, pb, act, rl, rh);
         csync();
     }
@@ -919,8 +1020,8 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         if (act[k])
 #pragma unroll
             for (int e = 0; e < N; ++e) A1[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
-    nb_tangential<N, TPC>(T.Vh[6], NT, 2, 0, nbi, lane);
-    nb_tangential<N, TPC>(T.Vh[7], NT, 1, 1, nbi, (lane + TPC / 2) % TPC);
+    nb_tangential<N, TPC>(sdf(N) ? T.Vs[6] : T.Vh[6], NT, 2, 0, nbi, lane);
+    nb_tangential<N, TPC>(sdf(N) ? T.Vs[7] : T.Vh[7], NT, 1, 1, nbi, (lane + TPC / 2) % TPC);
     csync();
 
     // ---- phase 5: y role -> A1 += T2; z-arrays step C
@@ -937,7 +1038,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 const int ie = Lay<N>::at(pa[k], e, pb[k]);
                 A1[ie] = A1[ie] + t[k][e];
             }
-    nb_tangential<N, TPC>(T.Vh[8], NT, 2, 1, nbi, lane);
+    nb_tangential<N, TPC>(sdf(N) ? T.Vs[8] : T.Vh[8], NT, 2, 1, nbi, lane);
     csync();
 
     // ---- phase 6: z role (+ reaction) -> X = T1 + T2 + T3; V^T along z -> A0
@@ -950,7 +1051,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) t[k][e] += act[k] ? A1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
-    v_bwd<N, P>(T.Vh[9], t, r);   // in place: A0 z-positions of this pencil are read only by this thread
+    if constexpr (sdf(N)) v_bwd_sd<N, P>(T.Vh[9], t, r); else v_bwd<N, P>(T.Vh[9], t, r);   // in place: A0 z-positions of this pencil are read only by this thread
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
@@ -963,7 +1064,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-    v_bwd<N, P>(T.Vh[10], r, t);
+    if constexpr (sdf(N)) v_bwd_sd<N, P>(T.Vh[10], r, t); else v_bwd<N, P>(T.Vh[10], r, t);
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
@@ -976,7 +1077,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
-    v_bwd<N, P>(T.Vh[11], r, t);
+    if constexpr (sdf(N)) v_bwd_sd<N, P>(T.Vh[11], r, t); else v_bwd<N, P>(T.Vh[11], r, t);
     if constexpr (N == 8 && C == 1) {
         if (STG && p.tma == 2 && p.epi == 0) {   // y through the staging block and one TMA store
 #pragma unroll

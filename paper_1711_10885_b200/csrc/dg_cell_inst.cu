@@ -40,6 +40,21 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
             for (int j = 0; j < N; ++j) h.Vh[c][i][j] = t.V[i][j];
     for (int i = 0; i < Tab<N>::HC; ++i)
         for (int j = 0; j < N; ++j) h.Gh[i][j] = t.G[i][j];
+    {   // sigma/delta form (dg_cell.cuh, sdf): doubled forward V, doubled Dc and Dc^T diag(w)
+        static double D2[NMAX][NMAX], A2[NMAX][NMAX];
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) {
+                D2[i][j] = 2.0 * t.Dc[i][j];
+                A2[i][j] = 2.0 * t.Dc[j][i] * t.w[j];
+            }
+        for (int c = 0; c < 9; ++c)
+            for (int i = 0; i < Tab<N>::HC; ++i)
+                for (int j = 0; j < N; ++j) h.Vs[c][i][j] = 2.0 * t.V[i][j];
+        for (int c = 0; c < 3; ++c) {
+            fill_eo<N>(h.Dcs[c], D2, false);
+            fill_eo<N>(h.DcTws[c], A2, false);
+        }
+    }
     for (int c = 0; c < 6; ++c) {
         fill_eo<N>(h.Dc[c], t.Dc, false);
         fill_eo<N>(h.DcT[c], t.Dc, true);
