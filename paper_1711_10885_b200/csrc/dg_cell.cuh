@@ -341,7 +341,7 @@ __device__ __forceinline__ double dot(const double* a, const double* v)
 // they commute with this change of basis along every direction, and the 1D stages consume and
 // produce it directly with doubled even-odd tables: no sum / difference instructions around
 // the forward stages, the Dc and Dc^T diag(w) stages, or before the backward stages.
-__host__ __device__ constexpr bool sdf(int n) { return n == 8; }
+__host__ __device__ constexpr bool sdf(int n) { return (n % 2) == 0; }
 
 template <int N, int P>
 __device__ __forceinline__ void v_fwd_sd(const double (&Vs)[(N + 1) / 2][N], const double (&r)[P][N], double (&t)[P][N])
