@@ -341,11 +341,13 @@ __device__ __forceinline__ double dot(const double* a, const double* v)
 // they commute with this change of basis along every direction, and the 1D stages consume and
 // produce it directly with doubled even-odd tables: no sum / difference instructions around
 // the forward stages, the Dc and Dc^T diag(w) stages, or before the backward stages.
-__host__ __device__ constexpr bool sdf(int n) { return (n % 2) == 0; }
+__host__ __device__ constexpr bool sdf(int n) { return n >= 2; }
 
 template <int N, int P>
 __device__ __forceinline__ void v_fwd_sd(const double (&Vs)[(N + 1) / 2][N], const double (&r)[P][N], double (&t)[P][N])
 {
+    // Vs: rows i < n/2 doubled; for odd n the middle row is the plain V_Hj (the middle entry
+    // of the sigma/delta form is the plain value t_H)
     constexpr int H = N / 2;
 #pragma unroll
     for (int i = 0; i < H; ++i) {
@@ -365,6 +367,15 @@ __device__ __forceinline__ void v_fwd_sd(const double (&Vs)[(N + 1) / 2][N], con
             t[k][N - 1 - i] = O[k];
         }
     }
+    if (N & 1) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            double E = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; j += 2) E = fma(Vs[H][j], r[k][j], E);
+            t[k][H] = E;
+        }
+    }
 }
 
 template <int N, int P>
@@ -375,7 +386,7 @@ __device__ __forceinline__ void v_bwd_sd(const double (&Vh)[(N + 1) / 2][N], con
     for (int j = 0; j < N; ++j) {
         double acc[P];
 #pragma unroll
-        for (int k = 0; k < P; ++k) acc[k] = 0.0;
+        for (int k = 0; k < P; ++k) acc[k] = ((N & 1) && !(j & 1)) ? Vh[H][j] * r[k][H] : 0.0;
 #pragma unroll
         for (int i = 0; i < H; ++i)
 #pragma unroll
@@ -385,11 +396,12 @@ __device__ __forceinline__ void v_bwd_sd(const double (&Vh)[(N + 1) / 2][N], con
     }
 }
 
-// out = A2 r with A2 the doubled even-odd form, r and out in sigma/delta form; optional addends
+// out = A r for a centro-antisymmetric A, r and out in sigma/delta form: A2 is the even-odd form
+// with p, m and (odd n) col doubled, row plain; optional addends (pairs doubled, middle plain)
 template <int N, int P, bool ADD>
 __device__ __forceinline__ void c_apply_s(const EO<N>& A2, const double (&r)[P][N], double (&t)[P][N],
                                           const double (&qa)[P][(N / 2) > 0 ? N / 2 : 1],
-                                          const double (&pb)[P][(N / 2) > 0 ? N / 2 : 1])
+                                          const double (&pb)[P][(N / 2) > 0 ? N / 2 : 1], const double (&mid)[P])
 {
     constexpr int H = N / 2;
 #pragma unroll
@@ -398,6 +410,7 @@ __device__ __forceinline__ void c_apply_s(const EO<N>& A2, const double (&r)[P][
 #pragma unroll
         for (int k = 0; k < P; ++k) {
             Pp[k] = ADD ? pb[k][i] : 0.0;
+            if (N & 1) Pp[k] = fma(A2.col[i], r[k][H], Pp[k]);
             Q[k] = ADD ? qa[k][i] : 0.0;
         }
 #pragma unroll
@@ -411,6 +424,15 @@ __device__ __forceinline__ void c_apply_s(const EO<N>& A2, const double (&r)[P][
         for (int k = 0; k < P; ++k) {
             t[k][i] = Q[k];
             t[k][N - 1 - i] = Pp[k];
+        }
+    }
+    if (N & 1) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            double acc = ADD ? mid[k] : 0.0;
+#pragma unroll
+            for (int j = 0; j < H; ++j) acc = fma(A2.row[j], r[k][N - 1 - j], acc);
+            t[k][H] = acc;
         }
     }
 }
@@ -715,8 +737,8 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
     constexpr bool SD = sdf(N);
     double g[P][N], s[P][HH], d[P][HH];
     if constexpr (SD) {                         // r in sigma/delta form: the sums are the input itself
-        double z0[P][HH];
-        c_apply_s<N, P, false>(T.Dcs[q], r, g, z0, z0);
+        double z0[P][HH], zm[P];
+        c_apply_s<N, P, false>(T.Dcs[q], r, g, z0, z0, zm);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -746,7 +768,7 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
             Bd = fma(LDm[i], d[k][i], Bd);
         }
         const double tr_u[2] = {A + B, A - B}, tr_d[2] = {Ad + Bd, Bd - Ad};
-        const double Wf = (SD ? 2.0 : 1.0) * p.dF[q] * wab;   // SD: the lift addends enter doubled
+        const double Wf = p.dF[q] * wab;
         FaceOut fo[2];
 #pragma unroll
         for (int sd = 0; sd < 2; ++sd) {
@@ -763,13 +785,16 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
                 fo[sd] = flux_boundary(p, q, sd, Wf, tr_u[sd], tr_d[sd]);
             }
         }
-        // lift (normal direction LAST) as even/odd addends of the Dc^T stage
+        // lift (normal direction LAST) as even/odd addends of the Dc^T stage (SD: the pair addends
+        // enter the sigma/delta output doubled, the middle one plain)
         const double Pc = fo[0].cv + fo[1].cv, Mc = fo[0].cv - fo[1].cv;
         const double Qc = fo[0].cg - fo[1].cg, Rc = fo[0].cg + fo[1].cg;
+        const double two = SD ? 2.0 : 1.0;
+        const double Pc2 = two * Pc, Mc2 = two * Mc, Qc2 = two * Qc, Rc2 = two * Rc;
 #pragma unroll
         for (int i = 0; i < H; ++i) {
-            qa[k][i] = fma(Pc, Lp[i], Qc * LDp[i]);
-            pbv[k][i] = fma(Mc, Lm[i], Rc * LDm[i]);
+            qa[k][i] = fma(Pc2, Lp[i], Qc2 * LDp[i]);
+            pbv[k][i] = fma(Mc2, Lm[i], Rc2 * LDm[i]);
         }
         mid[k] = (N & 1) ? fma(Pc, T.Lmid[q][0], Qc * T.Lmid[q][1]) : 0.0;
         // quadrature-point data with the weights folded into Dc^T diag(w) (eq:gauss_points)
@@ -778,7 +803,7 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
 #pragma unroll
         for (int e = 0; e < N; ++e) g[k][e] = fma(kd, g[k][e], -kb * r[k][e]);
     }
-    if constexpr (SD) c_apply_s<N, P, true>(T.DcTws[q], g, out, qa, pbv);
+    if constexpr (SD) c_apply_s<N, P, true>(T.DcTws[q], g, out, qa, pbv, mid);
     else c_apply_add<N, P>(T.DcTw[q], g, out, qa, pbv, mid);
     if (with_reaction && do_vol) {
 #pragma unroll

@@ -49,10 +49,14 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
             }
         for (int c = 0; c < 9; ++c)
             for (int i = 0; i < Tab<N>::HC; ++i)
-                for (int j = 0; j < N; ++j) h.Vs[c][i][j] = 2.0 * t.V[i][j];
+                for (int j = 0; j < N; ++j) h.Vs[c][i][j] = ((N & 1) && i == N / 2 ? 1.0 : 2.0) * t.V[i][j];
         for (int c = 0; c < 3; ++c) {
             fill_eo<N>(h.Dcs[c], D2, false);
             fill_eo<N>(h.DcTws[c], A2, false);
+            for (int i = 0; i < N / 2; ++i) {     // the middle row (odd n) stays plain
+                h.Dcs[c].row[i] *= 0.5;
+                h.DcTws[c].row[i] *= 0.5;
+            }
         }
     }
     for (int c = 0; c < 6; ++c) {
