@@ -171,6 +171,32 @@ int dg_set_velocity(dg_ctx* ctx, int kind, const double amp[3]);
  * DG_EUNSUPPORTED (other m, per-cell / full D set). */
 int dg_set_quadrature(dg_ctx* ctx, int m);
 
+/* ---- matrix-based comparison (the paper's "matrix-based" columns of
+ * Table 1: "we also assemble the matrix of the operator (again using our sum-factorized
+ * implementation) and apply the resulting matrix to a vector") ----
+ * Single-rank contexts only (DG_EUNSUPPORTED otherwise).
+ *
+ * Layout (block stencil, caller-owned DEVICE array of dg_matrix_size doubles): for every local
+ * cell S in cell-major order 7 blocks of n^3 x n^3 doubles; slot 0 = A_{S,S}, slot 1 + f =
+ * A_{S,T_f}, T_f the face-f neighbour (f = 2q + s as for the halo faces, wrapped on periodic
+ * directions); each block COLUMN-major with leading dimension ld = n^3 rounded up to even:
+ * A[((S * 7 + slot) * n^3 + j) * ld + i] is the entry of row (S, i) and column (T_slot, j); for
+ * odd n^3 row i = n^3 is a zero pad (16-byte aligned columns). Slots with no neighbour (Dirichlet
+ * side) and slots whose neighbour already occurs in an earlier slot (1 or 2 cells along a
+ * periodic direction) are zero. 7 n^3 ld doubles per cell: 14.7 MB at k = 7. */
+int dg_matrix_size(const dg_ctx* ctx, int64_t* ndoubles);
+/* Assemble the operator the next dg_apply would apply (constant or per-cell D, velocity field,
+ * quadrature, affine map) into A: every column is a probe of the fused sum-factorized kernel
+ * with unit vectors on a colour class of cells whose closed face neighbourhoods are disjoint
+ * (27 to 125 classes x n^3 probes). Allocates two ndofs scratch vectors; synchronous on stream.
+ * Errors: DG_EINVAL, DG_ENOMEM, DG_ECUDA, DG_EUNSUPPORTED (nranks > 1). */
+int dg_assemble(dg_ctx* ctx, double* A, void* stream);
+/* y = A z with an assembled A (the matrix-based operator application): per cell
+ * y_S = sum_slot A_{S,T_slot} z_{T_slot}; enqueued on stream (meshes with few row blocks use a
+ * library-owned scratch of 7 x rows doubles, allocated at the first call). Errors: DG_EINVAL
+ * (null, y == z), DG_ENOMEM, DG_ECUDA, DG_EUNSUPPORTED (nranks > 1). */
+int dg_matrix_apply(dg_ctx* ctx, const double* A, const double* z, double* y, void* stream);
+
 /* ---- halo plumbing (multi-rank; also used by the single-process loopback test) ----
  * face f = 2q + s (q = direction, s = 0 low / 1 high side of this rank's box).
  * neighbor_rank = -1 when the face lies on the domain boundary. count = doubles in the

@@ -112,6 +112,16 @@ def problem_a(k, P=1):
                   k, I3, B_A, 1.0, sigma_for(k, 1.0 / N), 5, (px, py, pz), (1, 1, 1), 6)
 
 
+def problem_a_matrix(k, budget_bytes=24e9):
+    """Problem A (as problem_a) on the mesh the matrix-based comparison can hold (NEXT-4; the paper
+    also scales its matrix-based runs down): N^3 cells with the assembled
+    block-stencil matrix (7 n^6 doubles per cell, include/dg.h) within budget_bytes, N >= 3."""
+    n = k + 1
+    N = max(3, int((budget_bytes / (56.0 * n ** 6)) ** (1.0 / 3.0)))
+    return Config("MB-k%d" % k, (N, N, N), (0, 0, 0), (1.0, 1.0, 1.0), k, I3, B_A, 1.0, sigma_for(k, 1.0 / N), 5,
+                  (1, 1, 1), (1, 1, 1), 6)
+
+
 def taylor_green(k, N=None):
     """The paper's transport run as an operator workload: the periodic box
     (-pi, pi)^3, D = 5e-6 I, c = 0, the Taylor-Green field b(x) (eq:2) at every quadrature point,
@@ -134,6 +144,8 @@ def by_name(name):
         return problem_a(int(name[3:]))
     if name.startswith("tg-k"):
         return taylor_green(int(name[4:]))
+    if name.startswith("mb-k"):
+        return problem_a_matrix(int(name[4:]))
     return table[name]()
 
 

@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <array>
 #include <mutex>
 #include <new>
 #include <vector>
@@ -58,6 +59,8 @@ struct dg_ctx {
     const double* tma_y = nullptr;
     bool tma_z_ok = false, tma_y_ok = false;
     CUtensorMap tmz, tmy;
+    double* mscratch = nullptr;      // dg_matrix_apply slot-split partial sums
+    int64_t mscratch_n = 0;
     KParams base;
 };
 
@@ -108,6 +111,7 @@ static void free_ctx(dg_ctx* c)
     }
     if (c->hz) cudaFree(c->hz);
     if (c->hy) cudaFree(c->hy);
+    if (c->mscratch) cudaFree(c->mscratch);
     if (c->comm) {
         const NcclApi* api = nccl_api();
         if (api) api->ncclCommDestroy(c->comm);
@@ -624,7 +628,7 @@ struct Epi {             // store epilogue (KParams::epi)
 };
 
 static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, unsigned terms, cudaStream_t s,
-                      const Epi* epi = nullptr)
+                      const Epi* epi = nullptr, const int64_t* tasks = nullptr, int64_t ntasks = 0)
 {
     if (!ctx || !z || !y) return DG_EINVAL;
     if ((const double*)y == z || (f && f == z)) return DG_EINVAL;
@@ -649,6 +653,11 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
     if (!ctx->partitioned) {
         const int64_t zero[3] = {0, 0, 0};
         set_box(p, zero, ctx->nloc);
+        if (tasks) {                 // only the listed local cells (dg_assemble's probes)
+            if (ntasks == 0) return DG_OK;
+            p.task_list = tasks;
+            p.ntasks = ntasks;
+        }
         return cuda_rc(launch_any(ctx, p, s));
     }
     // (iv) of SURVEY.md 3: pack partition layers, exchange on the comm stream, overlap with inner cells
@@ -798,6 +807,137 @@ extern "C" int dg_apply_host(dg_ctx* ctx, const double* z_host, double* y_host)
     DG_CUDA(cudaMemcpyAsync(y_host, ctx->hy, bytes, cudaMemcpyDeviceToHost, ctx->host_stream));
     DG_CUDA(cudaStreamSynchronize(ctx->host_stream));
     return DG_OK;
+}
+
+// ---- matrix-based comparison (NEXT-4; dg_matrix.cu) ----
+extern "C" int dg_matrix_size(const dg_ctx* ctx, int64_t* ndoubles)
+{
+    if (!ctx || !ndoubles) return DG_EINVAL;
+    const int64_t ncell = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2];
+    *ndoubles = ncell * 7 * (int64_t)ctx->n3 * (ctx->n3 + (ctx->n3 & 1));
+    return DG_OK;
+}
+
+// Probes of different colours are independent (separate z / y, disjoint matrix columns): they
+// run on up to 8 streams ("lanes"), each with its own probe vectors, so the small per-probe
+// launches (a task list of ~7/27 of the cells) overlap and fill the GPU.
+extern "C" int dg_assemble(dg_ctx* ctx, double* A, void* stream)
+{
+    if (!ctx || !A) return DG_EINVAL;
+    if (ctx->nranks != 1) return DG_EUNSUPPORTED;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t nA = 0;
+    dg_matrix_size(ctx, &nA);
+    const size_t vbytes = (size_t)ctx->ndofs * sizeof(double);
+    const int64_t ncell = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2];
+    const int n3 = ctx->n3;
+    int ncol[3];
+    bool present[3][5];
+    matrix_colours(ctx->nloc, ctx->per, ncol, present);
+    std::vector<std::array<int, 3>> cols;
+    for (int c2 = 0; c2 < ncol[2]; ++c2)
+        for (int c1 = 0; c1 < ncol[1]; ++c1)
+            for (int c0 = 0; c0 < ncol[0]; ++c0)
+                if (present[0][c0] && present[1][c1] && present[2][c2]) cols.push_back({c0, c1, c2});
+    // task lists of all colours, back to back (a cell is next to at most 7 colour classes)
+    int64_t* tasks = nullptr;
+    unsigned long long* count = nullptr;
+    if (cudaMalloc(&tasks, (size_t)(7 * ncell + 1) * sizeof(int64_t)) != cudaSuccess) return DG_ENOMEM;
+    if (cudaMalloc(&count, sizeof(unsigned long long)) != cudaSuccess) { cudaFree(tasks); return DG_ENOMEM; }
+    int rc = DG_OK;
+    std::vector<int64_t> off(cols.size() + 1, 0);
+    for (size_t ci = 0; ci < cols.size() && rc == DG_OK; ++ci) {
+        unsigned long long nt = 0;
+        if (launch_probe_tasks(ctx->nloc, ctx->per, cols[ci].data(), tasks + off[ci], count, s) != cudaSuccess ||
+            cudaMemcpyAsync(&nt, count, sizeof(nt), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            rc = DG_ECUDA;
+        off[ci + 1] = off[ci] + (int64_t)nt;
+    }
+    struct Lane {
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev = nullptr;
+        double* z = nullptr;
+        double* y = nullptr;
+    };
+    std::vector<Lane> lanes;
+    const int want = (int)std::min<size_t>(8, cols.size());
+    for (int l = 0; l < want && rc == DG_OK; ++l) {
+        Lane ln;
+        if (cudaMalloc(&ln.z, vbytes) != cudaSuccess) break;
+        if (cudaMalloc(&ln.y, vbytes) != cudaSuccess) { cudaFree(ln.z); break; }
+        if (cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ln.ev, cudaEventDisableTiming) != cudaSuccess) {
+            rc = DG_ECUDA;
+            lanes.push_back(ln);
+            break;
+        }
+        lanes.push_back(ln);
+    }
+    cudaGetLastError();                       // a failed optional lane allocation is not an error
+    if (rc == DG_OK && lanes.empty() && !cols.empty()) rc = DG_ENOMEM;
+    cudaEvent_t ev0 = nullptr;
+    if (rc == DG_OK && (cudaMemsetAsync(A, 0, (size_t)nA * sizeof(double), s) != cudaSuccess ||
+                        cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming) != cudaSuccess ||
+                        cudaEventRecord(ev0, s) != cudaSuccess))
+        rc = DG_ECUDA;
+    for (auto& ln : lanes)
+        if (rc == DG_OK && (cudaStreamWaitEvent(ln.st, ev0, 0) != cudaSuccess ||
+                            cudaMemsetAsync(ln.z, 0, vbytes, ln.st) != cudaSuccess))
+            rc = DG_ECUDA;
+    for (size_t ci = 0; ci < cols.size() && rc == DG_OK; ++ci) {
+        Lane& ln = lanes[ci % lanes.size()];
+        const int* col = cols[ci].data();
+        const int64_t* tl = tasks + off[ci];
+        const int64_t nt = off[ci + 1] - off[ci];
+        if (launch_probe_set(ln.z, n3, ctx->nloc, ctx->per, col, 0, 1.0, ln.st) != cudaSuccess) {
+            rc = DG_ECUDA;
+            break;
+        }
+        // probe (col, j): z = sum of e_(T, j) over the cells T of colour col; y on the cells next to
+        // them (the task list); the scatter also moves the probe to (col, j + 1) and, after the
+        // last j, leaves z zero for the lane's next colour
+        for (int j = 0; j < n3 && rc == DG_OK; ++j) {
+            rc = apply_impl(ctx, ln.z, nullptr, ln.y, DG_ALL, ln.st, nullptr, tl, nt);
+            if (rc != DG_OK) break;
+            if (launch_probe_scatter(A, ln.y, ln.z, tl, nt, n3, ctx->nloc, ctx->per, col, j, j + 1 < n3 ? j + 1 : -1,
+                                     ln.st) != cudaSuccess)
+                rc = DG_ECUDA;
+        }
+    }
+    for (auto& ln : lanes) {
+        if (ln.ev && ln.st && (cudaEventRecord(ln.ev, ln.st) != cudaSuccess || cudaStreamWaitEvent(s, ln.ev, 0) != cudaSuccess))
+            rc = rc == DG_OK ? DG_ECUDA : rc;
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess && rc == DG_OK) rc = DG_ECUDA;
+    for (auto& ln : lanes) {
+        if (ln.st) { cudaStreamSynchronize(ln.st); cudaStreamDestroy(ln.st); }
+        if (ln.ev) cudaEventDestroy(ln.ev);
+        cudaFree(ln.z);
+        cudaFree(ln.y);
+    }
+    if (ev0) cudaEventDestroy(ev0);
+    cudaFree(tasks);
+    cudaFree(count);
+    return rc;
+}
+
+extern "C" int dg_matrix_apply(dg_ctx* ctx, const double* A, const double* z, double* y, void* stream)
+{
+    if (!ctx || !A || !z || !y || (const double*)y == z) return DG_EINVAL;
+    if (ctx->nranks != 1) return DG_EUNSUPPORTED;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    const int64_t ns = matrix_scratch_doubles(ctx->n3, ctx->ndofs / ctx->n3);
+    if (ns > ctx->mscratch_n) {
+        if (ctx->mscratch) cudaFree(ctx->mscratch);
+        ctx->mscratch = nullptr;
+        ctx->mscratch_n = 0;
+        if (cudaMalloc(&ctx->mscratch, (size_t)ns * sizeof(double)) != cudaSuccess) return DG_ENOMEM;
+        ctx->mscratch_n = ns;
+    }
+    return cuda_rc(launch_matrix_apply(A, z, y, ns ? ctx->mscratch : nullptr, ctx->n3, ctx->nloc, ctx->per,
+                                       (cudaStream_t)stream));
 }
 
 extern "C" int dg_sync(dg_ctx* ctx)

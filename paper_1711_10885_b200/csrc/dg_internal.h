@@ -101,6 +101,18 @@ cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc
 cudaError_t launch_dfield_pack(const double* D9, double* D6, int* bad, int64_t ncell, const double* Jinv,
                                double det, cudaStream_t s);
 cudaError_t launch_dfield_const(double* D6, const double D9[9], int64_t ncell, cudaStream_t s);
+// matrix-based comparison (dg_matrix.cu, NEXT-4)
+void matrix_colours(const int64_t nloc[3], const int per[3], int ncol[3], bool present[3][5]);
+cudaError_t launch_probe_set(double* z, int n3, const int64_t nloc[3], const int per[3], const int col[3], int j,
+                             double val, cudaStream_t s);
+cudaError_t launch_probe_tasks(const int64_t nloc[3], const int per[3], const int col[3], int64_t* list,
+                               unsigned long long* count, cudaStream_t s);
+cudaError_t launch_probe_scatter(double* A, const double* y, double* z, const int64_t* tasks, int64_t ntask, int n3,
+                                 const int64_t nloc[3], const int per[3], const int col[3], int j, int nj,
+                                 cudaStream_t s);
+int64_t matrix_scratch_doubles(int n3, int64_t ncell);
+cudaError_t launch_matrix_apply(const double* A, const double* z, double* y, double* scratch, int n3,
+                                const int64_t nloc[3], const int per[3], cudaStream_t s);
 cudaError_t launch_fill_uniform(double* dst, int64_t count, uint64_t seed, int64_t offset, cudaStream_t s);
 cudaError_t launch_fill_uniform_local(double* dst, int n3, const int64_t nloc[3], const int64_t gofs[3],
                                       const int64_t gcells[3], uint64_t seed, cudaStream_t s);

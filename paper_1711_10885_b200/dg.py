@@ -23,7 +23,7 @@ EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residu
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
             "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage", "dg_set_velocity", "dg_set_quadrature",
-            "dg_set_affine"]
+            "dg_set_affine", "dg_matrix_size", "dg_assemble", "dg_matrix_apply"]
 
 
 class DGError(RuntimeError):
@@ -80,6 +80,9 @@ def lib():
         L.dg_set_velocity.argtypes = [vp, ctypes.c_int, vp]
         L.dg_set_affine.argtypes = [vp, vp]
         L.dg_set_quadrature.argtypes = [vp, ctypes.c_int]
+        L.dg_matrix_size.argtypes = [vp, vp]
+        L.dg_assemble.argtypes = [vp, vp, vp]
+        L.dg_matrix_apply.argtypes = [vp, vp, vp, vp, vp]
         L.dg_ssp_stage.argtypes = [vp, vp, vp, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, vp, vp]
         for name in EXPORTED:
             if name != "dg_strerror":
@@ -216,6 +219,25 @@ class Operator:
                 raise TypeError("host vectors must be contiguous float64 numpy arrays of ndofs entries")
         _check(lib().dg_apply_host(self._h, a_ptr(z_host), a_ptr(y_host)), "dg_apply_host")
         return y_host
+
+    def matrix_size(self):
+        """dg_matrix_size: doubles of the assembled block-stencil matrix (7 n^6 per cell)."""
+        n = ctypes.c_int64()
+        _check(lib().dg_matrix_size(self._h, ctypes.byref(n)), "dg_matrix_size")
+        return n.value
+
+    def assemble(self, A, stream=None):
+        """dg_assemble: the operator of the next apply into the caller's device matrix A."""
+        _dev_vec(A, self.matrix_size(), "A")
+        _check(lib().dg_assemble(self._h, _ptr(A), _stream(stream)), "dg_assemble")
+
+    def matrix_apply(self, A, z, y, stream=None):
+        """dg_matrix_apply: y = A z with the assembled matrix."""
+        _dev_vec(A, self.matrix_size(), "A")
+        _dev_vec(z, self.ndofs, "z")
+        _dev_vec(y, self.ndofs, "y")
+        _check(lib().dg_matrix_apply(self._h, _ptr(A), _ptr(z), _ptr(y), _stream(stream)), "dg_matrix_apply")
+        return y
 
     def set_diffusion(self, Dcell, flags=0, stream=None):
         """Per-cell tensors: CUDA float64 tensor of local cells x 9 (row-major), or None to

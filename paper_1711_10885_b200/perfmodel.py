@@ -56,3 +56,18 @@ def fp64_peak_tflops(sm_mhz=1965.0):
 # bench workload (configs.problem_a), not the target.
 PAPER_TABLE1_A_MDOFS = {1: 170.2, 2: 393.0, 3: 537.8, 4: 595.0, 5: 617.2, 6: 599.0, 7: 570.1, 8: 540.6,
                         9: 504.8, 10: 471.3}
+
+# Table 1's matrix-based columns (PETSc BAIJ matvec on meshes scaled down to fit, and the
+# sum-factorized assembly), MDOF/s on the same node.
+PAPER_TABLE1_MATRIX_MDOFS = {1: 206.45, 2: 64.20, 3: 26.85, 4: 9.544, 5: 4.585, 6: 2.311, 7: 1.462, 8: 0.614,
+                             9: 0.298}
+PAPER_TABLE1_ASSEMBLY_MDOFS = {1: 16.04, 2: 8.71, 3: 4.66, 4: 2.57, 5: 1.93, 6: 1.21, 7: 0.665, 8: 0.874, 9: 0.701}
+
+
+def matrix_bytes_per_dof(k):
+    """HBM bytes per DOF of one block-stencil matvec: the row's 7 n^3 matrix entries (x ld / n^3
+    for the even leading dimension ld of the layout, include/dg.h) plus reading z and writing y
+    once (8 + 8)."""
+    n3 = (k + 1) ** 3
+    ld = n3 + (n3 & 1)
+    return 8.0 * 7 * ld + 16.0

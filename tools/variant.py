@@ -1,8 +1,9 @@
 """Build an experiment variant of one degree's translation unit (development aid).
 
     python tools/variant.py NAME N [-DFLAG[=V] ...]
+    python tools/variant.py NAME matrix [-DFLAG[=V] ...]
 
-Recompiles dg_cell_inst.cu for n = N with the extra flags, links it with the standard
+Recompiles dg_cell_inst.cu for n = N (or dg_matrix.cu) with the extra flags, links it with the standard
 objects into variants/NAME.so (select at run time with DG_LIB=$PWD/variants/NAME.so).
 """
 import os
@@ -15,12 +16,16 @@ from paper_1711_10885_b200 import build as B  # noqa: E402
 
 
 def main():
-    name, n, flags = sys.argv[1], int(sys.argv[2]), sys.argv[3:]
+    name, flags = sys.argv[1], sys.argv[3:]
+    matrix = sys.argv[2] == "matrix"
+    n = 0 if matrix else int(sys.argv[2])
     B.build()
     obj = os.path.join(ROOT, "build", "var", name + ".o")
     os.makedirs(os.path.dirname(obj), exist_ok=True)
-    cmd = [B.NVCC] + B.ARCH + B.FLAGS + ["-DDG_N=%d" % n] + flags + ["-Xptxas", "-v", "-c",
-                                                                    os.path.join(B.CSRC, "dg_cell_inst.cu"), "-o", obj]
+    src = os.path.join(B.CSRC, "dg_matrix.cu" if matrix else "dg_cell_inst.cu")
+    replaced = "dg_matrix.o" if matrix else "dg_cell_n%d.o" % n
+    cmd = [B.NVCC] + B.ARCH + B.FLAGS + ([] if matrix else ["-DDG_N=%d" % n]) + flags + ["-Xptxas", "-v", "-c", src,
+                                                                                       "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         sys.exit("compile failed:\n" + r.stderr[-2000:])
@@ -28,7 +33,7 @@ def main():
     for i, l in enumerate(lines):
         if "dg_cell_kernel" in l and "Compiling" in l:
             print(name, " | ".join(x.strip() for x in lines[i + 1:i + 4] if "Used" in x or "spill" in x))
-    objs = [os.path.join(B.OBJ, f) for f in sorted(os.listdir(B.OBJ)) if f.endswith(".o") and f != "dg_cell_n%d.o" % n]
+    objs = [os.path.join(B.OBJ, f) for f in sorted(os.listdir(B.OBJ)) if f.endswith(".o") and f != replaced]
     out = os.path.join(ROOT, "variants", name + ".so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     r = subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-o", out, obj] + objs + ["-ldl", "-lpthread"],
