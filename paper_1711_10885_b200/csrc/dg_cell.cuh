@@ -52,7 +52,14 @@ struct Tab {
     // sigma/delta form of the fast kernel (n = 8, SDF below): doubled forward V and doubled even-odd
     // Dc, Dc^T diag(w), one copy per use site
     double Vs[9][HC][N];
-    EO<N> Dcs[3], DcTws[3];
+    EO<N> Dcs[5], DcTws[3];
+    // sigma/delta form of the general kernel (dg_gen.cuh): doubled Dc^T, doubled G (its odd rows
+    // first), trace rows acting on sigma/delta arrays (value / derivative at 0, 1), lift rows
+    // adding a plain vector to a sigma/delta array
+    EO<N> DcTs[5];
+    double Gs[HC][N];
+    double Ls[2][4][N];
+    double Lsl[4][N];
     // even-odd forms used by the roles (one copy per direction):
     EO<N> DcTw[3];                         // Dc^T diag(w): Gauss weights folded into the transposed stage
     double Le[3][4][(N / 2) > 0 ? N / 2 : 1];  // (L0_i +- L0_{n-1-i})/2, (L'0_i +- L'0_{n-1-i})/2, i < n/2

@@ -51,11 +51,34 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
             for (int i = 0; i < Tab<N>::HC; ++i)
                 for (int j = 0; j < N; ++j) h.Vs[c][i][j] = ((N & 1) && i == N / 2 ? 1.0 : 2.0) * t.V[i][j];
         for (int c = 0; c < 3; ++c) {
-            fill_eo<N>(h.Dcs[c], D2, false);
             fill_eo<N>(h.DcTws[c], A2, false);
-            for (int i = 0; i < N / 2; ++i) {     // the middle row (odd n) stays plain
+            for (int i = 0; i < N / 2; ++i) h.DcTws[c].row[i] *= 0.5;   // the middle row (odd n) stays plain
+        }
+        for (int c = 0; c < 5; ++c) {
+            fill_eo<N>(h.Dcs[c], D2, false);
+            fill_eo<N>(h.DcTs[c], D2, true);
+            for (int i = 0; i < N / 2; ++i) {
                 h.Dcs[c].row[i] *= 0.5;
-                h.DcTws[c].row[i] *= 0.5;
+                h.DcTs[c].row[i] *= 0.5;
+            }
+        }
+        constexpr int H = N / 2;
+        for (int i = 0; i < Tab<N>::HC; ++i)
+            for (int j = 0; j < N; ++j) h.Gs[i][j] = ((N & 1) && i == H ? 1.0 : 2.0) * t.G[i][j];
+        const double* rows[4] = {t.L0, t.L1, t.LD0, t.LD1};
+        for (int r = 0; r < 4; ++r) {
+            const double* l = rows[r];
+            for (int i = 0; i < H; ++i) {
+                for (int c = 0; c < 2; ++c) {
+                    h.Ls[c][r][i] = 0.5 * (l[i] + l[N - 1 - i]);
+                    h.Ls[c][r][N - 1 - i] = 0.5 * (l[i] - l[N - 1 - i]);
+                }
+                h.Lsl[r][i] = l[i] + l[N - 1 - i];
+                h.Lsl[r][N - 1 - i] = l[i] - l[N - 1 - i];
+            }
+            if (N & 1) {
+                h.Ls[0][r][H] = h.Ls[1][r][H] = l[H];
+                h.Lsl[r][H] = l[H];
             }
         }
     }

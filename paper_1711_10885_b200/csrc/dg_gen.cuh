@@ -19,6 +19,10 @@
 //     L'(s) along the normal and its tangential parts with Dc^T along the face lines, into
 //     the quadrature-space accumulator before the V^T stages (normal direction LAST).
 // Each cell still writes only its own y block once (owner computes, no atomics).
+// Every array between stages is in sigma/delta form along each direction it has been evaluated
+// in (dg_cell.cuh): the pointwise flux, the face fluxes and the lifts are linear with weights
+// symmetric about the cell centre and the upwind / weight choices are per face, so they commute
+// with the form; traces and lifts use rows built for it (Tab::Ls, Tab::Lsl).
 #pragma once
 #include "dg_cell.cuh"
 
@@ -50,6 +54,31 @@ __device__ __forceinline__ void g_fwd(const double (&Gh)[(N + 1) / 2][N], const 
         double O = 0.0;
 #pragma unroll
         for (int j = 1; j < N; j += 2) O = fma(Gh[H][j], r[j], O);
+        t[H] = O;
+    }
+}
+
+// the same in sigma/delta form (position i < n/2: t_i + t_{n-1-i} = 2 O_i, position n-1-i:
+// t_i - t_{n-1-i} = 2 E_i; Gs doubled, its middle row plain)
+template <int N>
+__device__ __forceinline__ void g_fwd_sd(const double (&Gs)[(N + 1) / 2][N], const double (&r)[N], double (&t)[N])
+{
+    constexpr int H = N / 2;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        double E = 0.0, O = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (j & 1) O = fma(Gs[i][j], r[j], O);
+            else E = fma(Gs[i][j], r[j], E);
+        }
+        t[i] = O;
+        t[N - 1 - i] = E;
+    }
+    if (N & 1) {
+        double O = 0.0;
+#pragma unroll
+        for (int j = 1; j < N; j += 2) O = fma(Gs[H][j], r[j], O);
         t[H] = O;
     }
 }
@@ -222,7 +251,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
             }
         }
-        v_fwd<N, P>(T.Vh[0], r, t);
+        v_fwd_sd<N, P>(T.Vs[0], r, t);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k])
@@ -236,7 +265,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         for (int k = 0; k < P; ++k)
 #pragma unroll
             for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-        v_fwd<N, P>(T.Vh[1], r, t);
+        v_fwd_sd<N, P>(T.Vs[1], r, t);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k])
@@ -252,10 +281,10 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
         nb_contract<N, P>(T, NT, 2, nbi, pa, pb, act, rl, rh);
     }
-    v_fwd<N, P>(T.Vh[2], r, t);                                  // t = u on this thread's z-pencils
+    v_fwd_sd<N, P>(T.Vs[2], r, t);                               // t = u on this thread's z-pencils
     {
-        double g[P][N];
-        c_apply<N, P>(T.Dc[0], t, g);
+        double g[P][N], z0[P][(N / 2) > 0 ? N / 2 : 1], zm[P];
+        c_apply_s<N, P, false>(T.Dcs[0], t, g, z0, z0, zm);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k]) {
@@ -267,8 +296,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 // own z-face traces: u and the reference normal derivative at z = 0, 1
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
-                    OT[FLay<N>::at(2 * (4 + s), pa[k], pb[k])] = dot<N>(T.L[0][s], t[k]);
-                    OT[FLay<N>::at(2 * (4 + s) + 1, pa[k], pb[k])] = dot<N>(T.L[0][2 + s], t[k]);
+                    OT[FLay<N>::at(2 * (4 + s), pa[k], pb[k])] = dot<N>(T.Ls[0][s], t[k]);
+                    OT[FLay<N>::at(2 * (4 + s) + 1, pa[k], pb[k])] = dot<N>(T.Ls[0][2 + s], t[k]);
                 }
             }
     }
@@ -283,7 +312,10 @@ dg_gen_kernel(const __grid_constant__ KParams p)
 #pragma unroll
             for (int e = 0; e < N; ++e)
                 r[k][e] = act[k] ? A0[q == 0 ? Lay<N>::at(e, pa[k], pb[k]) : Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-        c_apply<N, P>(T.Dc[1 + q], r, t);
+        {
+            double z0[P][(N / 2) > 0 ? N / 2 : 1], zm[P];
+            c_apply_s<N, P, false>(T.Dcs[1 + q], r, t, z0, z0, zm);
+        }
         double* X = q == 0 ? X0 : X1;
 #pragma unroll
         for (int k = 0; k < P; ++k)
@@ -293,8 +325,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                     X[q == 0 ? Lay<N>::at(e, pa[k], pb[k]) : Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
-                    OT[FLay<N>::at(2 * (2 * q + s), pa[k], pb[k])] = dot<N>(T.L[1][s], r[k]);
-                    OT[FLay<N>::at(2 * (2 * q + s) + 1, pa[k], pb[k])] = dot<N>(T.L[1][2 + s], r[k]);
+                    OT[FLay<N>::at(2 * (2 * q + s), pa[k], pb[k])] = dot<N>(T.Ls[1][s], r[k]);
+                    OT[FLay<N>::at(2 * (2 * q + s) + 1, pa[k], pb[k])] = dot<N>(T.Ls[1][2 + s], r[k]);
                 }
             }
     }
@@ -308,14 +340,14 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         double rr[1][N], tt[1][N], ga[N];
 #pragma unroll
         for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(2 * f, e, line)];
-        g_fwd<N>(T.Gh, rr[0], ga);
-        v_fwd<N, 1>(T.Vh[3], rr, tt);
+        g_fwd_sd<N>(T.Gs, rr[0], ga);
+        v_fwd_sd<N, 1>(T.Vs[3], rr, tt);
 #pragma unroll
         for (int e = 0; e < N; ++e) {
             NT[FLay<N>::at(2 * f, e, line)] = tt[0][e];
             rr[0][e] = NT[FLay<N>::at(2 * f + 1, e, line)];
         }
-        v_fwd<N, 1>(T.Vh[4], rr, tt);
+        v_fwd_sd<N, 1>(T.Vs[4], rr, tt);
 #pragma unroll
         for (int e = 0; e < N; ++e) NT[FLay<N>::at(2 * f + 1, e, line)] = fma(cqq, tt[0][e], cq1 * ga[e]);
     }
@@ -337,14 +369,14 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             for (int e = 0; e < N; ++e) va[e] = NT[FLay<N>::at(2 * f, line, e)];
 #pragma unroll
             for (int e = 0; e < N; ++e) rr[0][e] = va[e];
-            v_fwd<N, 1>(T.Vh[5], rr, tt);
+            v_fwd_sd<N, 1>(T.Vs[5], rr, tt);
 #pragma unroll
             for (int e = 0; e < N; ++e) {
                 NT[FLay<N>::at(2 * f, line, e)] = tt[0][e];
                 rr[0][e] = NT[FLay<N>::at(2 * f + 1, line, e)];
             }
-            v_fwd<N, 1>(T.Vh[6], rr, tt);
-            g_fwd<N>(T.Gh, va, gv);
+            v_fwd_sd<N, 1>(T.Vs[6], rr, tt);
+            g_fwd_sd<N>(T.Gs, va, gv);
 #pragma unroll
             for (int e = 0; e < N; ++e) NT[FLay<N>::at(2 * f + 1, line, e)] = fma(cq2, gv[e], tt[0][e]);
         } else {
@@ -354,7 +386,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             double rr[1][N], tt[1][N];
 #pragma unroll
             for (int e = 0; e < N; ++e) rr[0][e] = OT[FLay<N>::at(2 * f, e, line)];
-            c_apply<N, 1>(T.Dc[3], rr, tt);
+            double z0[1][(N / 2) > 0 ? N / 2 : 1], zm[1];
+            c_apply_s<N, 1, false>(T.Dcs[3], rr, tt, z0, z0, zm);
 #pragma unroll
             for (int e = 0; e < N; ++e) {
                 const int ix = FLay<N>::at(2 * f + 1, e, line);
@@ -401,7 +434,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             double rr[1][N], tt[1][N];
 #pragma unroll
             for (int e = 0; e < N; ++e) uo[e] = rr[0][e] = OT[FLay<N>::at(2 * f, line, e)];
-            c_apply<N, 1>(T.Dc[4], rr, tt);
+            double z0[1][(N / 2) > 0 ? N / 2 : 1], zm[1];
+            c_apply_s<N, 1, false>(T.Dcs[4], rr, tt, z0, z0, zm);
 #pragma unroll
             for (int e = 0; e < N; ++e) so[e] = fma(cq2, tt[0][e], OT[FLay<N>::at(2 * f + 1, line, e)]);
         }
@@ -443,7 +477,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             double rr[1][N], tt[1][N];
 #pragma unroll
             for (int e = 0; e < N; ++e) rr[0][e] = c2[e];
-            c_apply<N, 1>(T.DcT[0], rr, tt);                          // tangential test derivative along i2
+            double z0[1][(N / 2) > 0 ? N / 2 : 1], zm[1];
+            c_apply_s<N, 1, false>(T.DcTs[0], rr, tt, z0, z0, zm);   // tangential test derivative along i2
 #pragma unroll
             for (int e = 0; e < N; ++e) OT[FLay<N>::at(2 * f, line, e)] = cv[e] + tt[0][e];
         }
@@ -457,7 +492,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         double rr[1][N], tt[1][N];
 #pragma unroll
         for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(2 * f, e, line)];
-        c_apply<N, 1>(T.DcT[1], rr, tt);
+        double z0[1][(N / 2) > 0 ? N / 2 : 1], zm[1];
+        c_apply_s<N, 1, false>(T.DcTs[1], rr, tt, z0, z0, zm);
 #pragma unroll
         for (int e = 0; e < N; ++e) OT[FLay<N>::at(2 * f, e, line)] += tt[0][e];
     }
@@ -474,7 +510,10 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         for (int k = 0; k < P; ++k)
 #pragma unroll
             for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X[at(k, e)] : 0.0;
-        c_apply<N, P>(T.DcT[2 + q], r, t);
+        {
+            double z0[P][(N / 2) > 0 ? N / 2 : 1], zm[P];
+            c_apply_s<N, P, false>(T.DcTs[2 + q], r, t, z0, z0, zm);
+        }
 #pragma unroll
         for (int k = 0; k < P; ++k) {
             if (!act[k]) continue;
@@ -485,7 +524,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 const double cv = OT[FLay<N>::at(2 * f, pa[k], pb[k])];
                 const double cg = OT[FLay<N>::at(2 * f + 1, pa[k], pb[k])];
 #pragma unroll
-                for (int e = 0; e < N; ++e) t[k][e] = fma(cv, T.L[2][s][e], fma(cg, T.L[2][2 + s][e], t[k][e]));
+                for (int e = 0; e < N; ++e) t[k][e] = fma(cv, T.Lsl[s][e], fma(cg, T.Lsl[2 + s][e], t[k][e]));
             }
         }
         if (q < 2) {
@@ -503,7 +542,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         }
     }
     // ---------------------------------------------------------------- P10-P12: V^T along z, y, x; store
-    v_bwd<N, P>(T.Vh[9], t, r);
+    v_bwd_sd<N, P>(T.Vh[9], t, r);
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
@@ -514,7 +553,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-    v_bwd<N, P>(T.Vh[10], r, t);
+    v_bwd_sd<N, P>(T.Vh[10], r, t);
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
@@ -525,7 +564,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
-    v_bwd<N, P>(T.Vh[11], r, t);
+    v_bwd_sd<N, P>(T.Vh[11], r, t);
     if constexpr (N == 8 && C == 1) {
         if (STG && p.tma == 2 && p.epi == 0) {   // y through the staging block and one TMA store
 #pragma unroll
