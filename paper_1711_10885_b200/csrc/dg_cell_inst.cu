@@ -2,6 +2,7 @@
 // fused cell kernel instantiation, its __constant__ table upload and launcher.
 #include "dg_cell.cuh"
 #include "dg_gen.cuh"
+#include "dg_reg.cuh"
 #if DG_N == 8
 #include "dg_mma8.cuh"
 #endif
@@ -117,6 +118,25 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
         h.dth1[i] = t.dth1[i];
     }
     if (cudaMemcpyToSymbol(g_tab, &h, sizeof(h)) != cudaSuccess) return -3;
+    {
+        static RTab<N> rt;
+        for (int i = 0; i < N; ++i) {
+            for (int j = 0; j < N; ++j) {
+                rt.V[i][j] = t.V[i][j];
+                rt.Dc[i][j] = t.Dc[i][j];
+            }
+            rt.w[i] = t.w[i];
+            rt.L[0][i] = t.L0[i];
+            rt.L[1][i] = t.L1[i];
+            rt.L[2][i] = t.LD0[i];
+            rt.L[3][i] = t.LD1[i];
+            rt.th0[i] = t.th0[i];
+            rt.th1[i] = t.th1[i];
+            rt.dth0[i] = t.dth0[i];
+            rt.dth1[i] = t.dth1[i];
+        }
+        if (cudaMemcpyToSymbol(g_rtab, &rt, sizeof(rt)) != cudaSuccess) return -3;
+    }
 #if DG_N == 8
     // per-lane DMMA fragments (dg_mma8.cuh): lane l -> g = l >> 2, t = l & 3
     static double fr[32][16];
@@ -157,12 +177,32 @@ static bool use_mma()
 
 static int g_attr_done[64];
 
+// n <= DG_REG_NMAX: the register-resident kernel (dg_reg.cuh) unless DG_CELL_KERNEL=pencil
+static bool use_reg()
+{
+    if (DG_N > DG_REG_NMAX) return false;
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("DG_CELL_KERNEL");
+        v = (e && std::strcmp(e, "pencil") == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+constexpr int REG_THREADS = 128;
+
 cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
 {
     constexpr int N = DG_N;
     constexpr int C = Cfg<N>::C;
     constexpr int THREADS = C * Cfg<N>::TPC;
     if (p.ntasks <= 0) return cudaSuccess;
+    if constexpr (N <= DG_REG_NMAX) {
+        if (use_reg()) {
+            const int64_t grid = (p.ntasks + REG_THREADS - 1) / REG_THREADS;
+            dg_reg_kernel<N><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
+            return cudaGetLastError();
+        }
+    }
     int dev = 0;
     cudaGetDevice(&dev);
 #if DG_N == 8
@@ -234,6 +274,19 @@ int DG_CAT(gen_info_n, DG_N)(LaunchInfo* info)
 int DG_CAT(cell_info_n, DG_N)(LaunchInfo* info)
 {
     constexpr int N = DG_N;
+    if constexpr (N <= DG_REG_NMAX) if (use_reg()) {
+        info->cells_per_cta = REG_THREADS;
+        info->threads = REG_THREADS;
+        info->smem = 0;
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, dg_reg_kernel<N>) != cudaSuccess) return -3;
+        info->regs = fa.numRegs;
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_reg_kernel<N>, REG_THREADS, 0) != cudaSuccess)
+            return -3;
+        info->ctas_per_sm = blocks;
+        return 0;
+    }
 #if DG_N == 8
     if (use_mma()) {
         constexpr int BYTES = m8::C * m8::PER_CELL * 8;

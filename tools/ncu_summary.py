@@ -95,7 +95,7 @@ def main():
     ap.add_argument("--json", default=None, help="merge {name: summary} into this JSON file")
     args = ap.parse_args()
     launches = raw(args.rep)
-    cell = [d for d in launches if "dg_cell" in d.get("Kernel Name", ("", ""))[0]] or launches
+    cell = [d for d in launches if any(k in d.get("Kernel Name", ("", ""))[0] for k in ("dg_cell", "dg_reg", "dg_gen", "dg_vb"))] or launches
     s = summarize(cell[0])
     if args.ndofs:
         s["ndofs"] = args.ndofs
