@@ -123,6 +123,7 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
         for (int i = 0; i < N; ++i) {
             for (int j = 0; j < N; ++j) {
                 rt.V[i][j] = t.V[i][j];
+                rt.G[i][j] = t.G[i][j];
                 rt.Dc[i][j] = t.Dc[i][j];
             }
             rt.w[i] = t.w[i];
@@ -199,7 +200,7 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
     if constexpr (N <= DG_REG_NMAX) {
         if (use_reg()) {
             const int64_t grid = (p.ntasks + REG_THREADS - 1) / REG_THREADS;
-            dg_reg_kernel<N><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
+            dg_reg_kernel<N, false><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
             return cudaGetLastError();
         }
     }
@@ -238,6 +239,13 @@ cudaError_t DG_CAT(launch_gen_n, DG_N)(const KParams& p, cudaStream_t s)
     constexpr int N = DG_N;
     constexpr int C = GCfg<N>::C;
     if (p.ntasks <= 0) return cudaSuccess;
+    if constexpr (N <= DG_REG_GMAX) {
+        if (use_reg()) {
+            const int64_t grid = (p.ntasks + REG_THREADS - 1) / REG_THREADS;
+            dg_reg_kernel<N, true><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
+            return cudaGetLastError();
+        }
+    }
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !g_gen_attr_done[dev]) {
@@ -254,6 +262,20 @@ cudaError_t DG_CAT(launch_gen_n, DG_N)(const KParams& p, cudaStream_t s)
 int DG_CAT(gen_info_n, DG_N)(LaunchInfo* info)
 {
     constexpr int N = DG_N;
+    if constexpr (N <= DG_REG_GMAX) if (use_reg()) {
+        info->cells_per_cta = REG_THREADS;
+        info->threads = REG_THREADS;
+        info->smem = 0;
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, dg_reg_kernel<N, true>) != cudaSuccess) return -3;
+        info->regs = fa.numRegs;
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_reg_kernel<N, true>, REG_THREADS, 0) !=
+            cudaSuccess)
+            return -3;
+        info->ctas_per_sm = blocks;
+        return 0;
+    }
     info->cells_per_cta = GCfg<N>::C;
     info->threads = GCfg<N>::C * GCfg<N>::TPC;
     info->smem = GSmem<N>::BYTES;
@@ -279,10 +301,10 @@ int DG_CAT(cell_info_n, DG_N)(LaunchInfo* info)
         info->threads = REG_THREADS;
         info->smem = 0;
         cudaFuncAttributes fa;
-        if (cudaFuncGetAttributes(&fa, dg_reg_kernel<N>) != cudaSuccess) return -3;
+        if (cudaFuncGetAttributes(&fa, dg_reg_kernel<N, false>) != cudaSuccess) return -3;
         info->regs = fa.numRegs;
         int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_reg_kernel<N>, REG_THREADS, 0) != cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_reg_kernel<N, false>, REG_THREADS, 0) != cudaSuccess)
             return -3;
         info->ctas_per_sm = blocks;
         return 0;

@@ -1,5 +1,6 @@
-// Register-resident cell kernel for the smallest bases (constant diagonal D; the fast path of
-// dg_cell.cuh for n <= DG_REG_NMAX): one THREAD per cell, the whole n^3 block and every
+// Register-resident cell kernel for the smallest bases: one THREAD per cell (constant diagonal D,
+// the fast path of dg_cell.cuh, for n <= DG_REG_NMAX; GEN = true: full / per-cell tensors, the
+// general path of dg_gen.cuh, for n <= DG_REG_GMAX), the whole n^3 block and every
 // intermediate array in registers, no shared memory and no barriers.
 //
 // Why: at n = 2 a pencil is 2 points, so the pencil kernel spends most of its issue slots on
@@ -19,19 +20,24 @@
 // Each thread writes only its own cell's y block (owner computes).
 #pragma once
 #include "dg_cell.cuh"
+#include "dg_gen.cuh"
 
 namespace dg {
 
 #ifndef DG_REG_NMAX
-#define DG_REG_NMAX 3
+#define DG_REG_NMAX 3      // constant diagonal D (fast path)
+#endif
+#ifndef DG_REG_GMAX
+#define DG_REG_GMAX 2      // full / per-cell tensors (general path; n = 3 would need ~320 registers)
 #endif
 
-// full 1D tables of the register kernel (tables.cpp): V_ij = theta_j(xi_i), Dc = G V^-1 (the
+// full 1D tables of the register kernel (tables.cpp): V_ij = theta_j(xi_i), G_ij = theta'_j(xi_i),
+// Dc = G V^-1 (the
 // collocation derivative), Gauss weights, the Lagrange rows L_l(0), L_l(1), L'_l(0), L'_l(1)
 // and theta_j(0), theta_j(1), theta'_j(0), theta'_j(1)
 template <int N>
 struct RTab {
-    double V[N][N], Dc[N][N], w[N], L[4][N], th0[N], th1[N], dth0[N], dth1[N];
+    double V[N][N], G[N][N], Dc[N][N], w[N], L[4][N], th0[N], th1[N], dth0[N], dth1[N];
 };
 __constant__ RTab<DG_N> g_rtab;
 
@@ -109,17 +115,41 @@ __device__ __forceinline__ void reg_load(const double* src, double (&a)[N * N * 
     }
 }
 
-// the faces of direction Q: own traces, neighbour traces, fluxes, lifts into X (quadrature space)
-template <int N, int Q>
-__device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, const double* zc, int64_t n3,
-                                          const int (&lc)[3], unsigned nbmask, bool do_int, bool do_bnd,
-                                          const double (&u)[N * N * N], double (&X)[N * N * N])
+// 2D face-array stages: o(i, b) = sum_j M[i][j] a(j, b) (AX = 0) or o(a, i) = sum_j M[i][j] a(a, j)
+template <int N, int AX, bool TR>
+__device__ __forceinline__ void fstage(const double (&M)[N][N], const double (&a)[N][N], double (&o)[N][N])
 {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double m = TR ? M[j][i] : M[i][j];
+                acc = fma(m, AX == 0 ? a[j][c] : a[c][j], acc);
+            }
+            if (AX == 0) o[i][c] = acc;
+            else o[c][i] = acc;
+        }
+}
+
+// the faces of direction Q: own traces, neighbour traces, fluxes, lifts into X (quadrature space).
+// GEN: full per-cell tensors (dg_gen.cuh semantics): nu.D grad u with the tangential derivatives
+// of both traces (own: Dc along the face lines; neighbour: G in its tangential stages), weights
+// w-+ = d+-/(d- + d+), penalty <d-, d+> sigma_q (C-5), tangential test-derivative lifts with Dc^T.
+template <int N, int Q, bool GEN>
+__device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, const double* zc, int64_t n3,
+                                          const int (&lc)[3], int64_t cell, unsigned nbmask, bool do_int, bool do_bnd,
+                                          const double (&Dw)[6], const double (&u)[N * N * N], double (&X)[N * N * N])
+{
+    constexpr int T1 = (Q == 0) ? 1 : 0, T2 = (Q == 2) ? 1 : 2;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
         const bool interior = (nbmask >> (2 * Q + s)) & 1u;
         if (interior ? !do_int : !do_bnd) continue;
-        double un[N][N], dn[N][N];
+        double un[N][N], sn[N][N];                 // neighbour u+ and nu.D+ grad u+ (physical)
+        double dnb = 0.0;                          // neighbour D_qq (GEN)
         if (interior) {
             double zn[N * N * N];
             reg_load<N>(reg_nb<N>(p, zc, n3, lc, Q, s, nbmask), zn);
@@ -139,56 +169,118 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
                     cu[a][b] = su;
                     cd[a][b] = sd;
                 }
-            // V along the first, then the second tangential axis
-            double tu[N][N], td[N][N];
+            // tangential stages: V along the first, then the second tangential axis
+            double t0[N][N], t1[N][N], dn[N][N];
+            fstage<N, 0, false>(R.V, cu, t0);
+            fstage<N, 1, false>(R.V, t0, un);
+            fstage<N, 0, false>(R.V, cd, t1);
+            fstage<N, 1, false>(R.V, t1, dn);
+            if constexpr (GEN) {
+                const double* Dn = nb_dfield(p, lc, cell, 2 * Q + s, nbmask);
+                dnb = __ldg(Dn + Q);
+                const double cqq = dnb * p.hinv[Q], cq1 = __ldg(Dn + dsym(Q, T1)) * p.hinv[T1],
+                             cq2 = __ldg(Dn + dsym(Q, T2)) * p.hinv[T2];
+                double g1[N][N], g2[N][N];
+                fstage<N, 0, false>(R.G, cu, t1);          // d/dt1: G along the first axis, V along the second
+                fstage<N, 1, false>(R.V, t1, g1);
+                fstage<N, 1, false>(R.G, t0, g2);          // d/dt2: V along the first, G along the second
 #pragma unroll
-            for (int i = 0; i < N; ++i)
+                for (int a = 0; a < N; ++a)
 #pragma unroll
-                for (int b = 0; b < N; ++b) {
-                    double su = 0.0, sd = 0.0;
+                    for (int b = 0; b < N; ++b) sn[a][b] = fma(cqq, dn[a][b], fma(cq1, g1[a][b], cq2 * g2[a][b]));
+            } else {
 #pragma unroll
-                    for (int j = 0; j < N; ++j) {
-                        su = fma(R.V[i][j], cu[j][b], su);
-                        sd = fma(R.V[i][j], cd[j][b], sd);
-                    }
-                    tu[i][b] = su;
-                    td[i][b] = sd;
-                }
+                for (int a = 0; a < N; ++a)
 #pragma unroll
-            for (int a = 0; a < N; ++a)
-#pragma unroll
-                for (int i = 0; i < N; ++i) {
-                    double su = 0.0, sd = 0.0;
-#pragma unroll
-                    for (int j = 0; j < N; ++j) {
-                        su = fma(R.V[i][j], tu[a][j], su);
-                        sd = fma(R.V[i][j], td[a][j], sd);
-                    }
-                    un[a][i] = su;
-                    dn[a][i] = sd;
-                }
+                    for (int b = 0; b < N; ++b) sn[a][b] = p.Dqq_h[Q] * dn[a][b];
+            }
         }
+        // own traces by extrapolation of the Gauss-point values along the normal
+        double uo[N][N], dref[N][N];
 #pragma unroll
         for (int a = 0; a < N; ++a)
 #pragma unroll
             for (int b = 0; b < N; ++b) {
-                // own traces by extrapolation of the Gauss-point values along the normal
-                double uo = 0.0, dref = 0.0;
+                double su = 0.0, sd = 0.0;
 #pragma unroll
                 for (int e = 0; e < N; ++e) {
                     const double v = u[rat<N, Q>(e, a, b)];
-                    uo = fma(R.L[s][e], v, uo);
-                    dref = fma(R.L[2 + s][e], v, dref);
+                    su = fma(R.L[s][e], v, su);
+                    sd = fma(R.L[2 + s][e], v, sd);
                 }
-                const double Wf = p.dF[Q] * R.w[a] * R.w[b];
-                const FaceOut fo = interior ? flux_interior(p, Q, s, Wf, uo, dref, un[a][b], p.Dqq_h[Q] * dn[a][b])
-                                            : flux_boundary(p, Q, s, Wf, uo, dref);
+                uo[a][b] = su;
+                dref[a][b] = sd;
+            }
+        double cvf[N][N], cgf[N][N];               // value and normal-derivative lift coefficients
+        if constexpr (GEN) {
+            const double dme = Dw[Q];
+            const double cn = dme * p.hinv[Q], c1 = Dw[dsym(Q, T1)] * p.hinv[T1], c2 = Dw[dsym(Q, T2)] * p.hinv[T2];
+            double d1[N][N], d2[N][N];
+            fstage<N, 0, false>(R.Dc, uo, d1);           // tangential derivatives of the own trace
+            fstage<N, 1, false>(R.Dc, uo, d2);
+            const double dm = s ? dme : dnb, dp = s ? dnb : dme;      // delta of T-, T+
+            const double dsum = dm + dp;
+            const double rsum = dsum == 0.0 ? 0.0 : 1.0 / dsum;
+            const double wm = dsum == 0.0 ? 0.5 : dp * rsum, wp = dsum == 0.0 ? 0.5 : dm * rsum;   // C-5
+            const double gam = (interior ? 2.0 * dm * dp * rsum : dme) * p.sigq[Q];
+            const double wself = s ? wm : wp;
+            const double bq = p.bq[Q];
+            double f1[N][N], f2[N][N];
+#pragma unroll
+            for (int a = 0; a < N; ++a)
+#pragma unroll
+                for (int b = 0; b < N; ++b) {
+                    const double Wf = p.dF[Q] * R.w[a] * R.w[b];
+                    const double so = fma(cn, dref[a][b], fma(c1, d1[a][b], c2 * d2[a][b]));
+                    double coef;
+                    if (interior) {
+                        const double um = s ? uo[a][b] : un[a][b], up = s ? un[a][b] : uo[a][b];
+                        const double sm = s ? so : sn[a][b], sp = s ? sn[a][b] : so;
+                        const double Phi = (bq >= 0.0) ? bq * um : bq * up;   // upwind flux
+                        const double J = um - up;
+                        const double com = Phi - (wm * sm + wp * sp) + gam * J;
+                        cvf[a][b] = s ? Wf * com : -Wf * com;
+                        coef = -Wf * wself * J;
+                    } else {
+                        const double nu = s ? 1.0 : -1.0;                      // outward normal
+                        const double bn = nu * bq;
+                        const double Phi = (bn >= 0.0) ? bn * uo[a][b] : 0.0;
+                        cvf[a][b] = Wf * (Phi - nu * so + gam * uo[a][b]);
+                        coef = -Wf * uo[a][b] * nu;
+                    }
+                    cgf[a][b] = coef * cn;                                     // normal part (L')
+                    f1[a][b] = coef * c1;                                      // tangential parts (Dc^T)
+                    f2[a][b] = coef * c2;
+                }
+            double l1[N][N], l2[N][N];
+            fstage<N, 0, true>(R.Dc, f1, l1);
+            fstage<N, 1, true>(R.Dc, f2, l2);
+#pragma unroll
+            for (int a = 0; a < N; ++a)
+#pragma unroll
+                for (int b = 0; b < N; ++b) cvf[a][b] += l1[a][b] + l2[a][b];
+        } else {
+#pragma unroll
+            for (int a = 0; a < N; ++a)
+#pragma unroll
+                for (int b = 0; b < N; ++b) {
+                    const double Wf = p.dF[Q] * R.w[a] * R.w[b];
+                    const FaceOut fo = interior ? flux_interior(p, Q, s, Wf, uo[a][b], dref[a][b], un[a][b], sn[a][b])
+                                                : flux_boundary(p, Q, s, Wf, uo[a][b], dref[a][b]);
+                    cvf[a][b] = fo.cv;
+                    cgf[a][b] = fo.cg;
+                }
+        }
+        // lift (normal direction LAST) into the quadrature-space accumulator
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+#pragma unroll
+            for (int b = 0; b < N; ++b)
 #pragma unroll
                 for (int e = 0; e < N; ++e) {
                     const int ix = rat<N, Q>(e, a, b);
-                    X[ix] = fma(fo.cv, R.L[s][e], fma(fo.cg, R.L[2 + s][e], X[ix]));
+                    X[ix] = fma(cvf[a][b], R.L[s][e], fma(cgf[a][b], R.L[2 + s][e], X[ix]));
                 }
-            }
     }
 }
 
@@ -197,7 +289,7 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
 #else
 #define DG_REG_BOUNDS __launch_bounds__(128)
 #endif
-template <int N>
+template <int N, bool GEN>
 __global__ void DG_REG_BOUNDS dg_reg_kernel(const __grid_constant__ KParams p)
 {
     constexpr int N3 = N * N * N;
@@ -236,32 +328,70 @@ __global__ void DG_REG_BOUNDS dg_reg_kernel(const __grid_constant__ KParams p)
     rcontract<N, 2>(R.V, t, u);                     // u at the Gauss points
 #pragma unroll
     for (int i = 0; i < N3; ++i) X[i] = 0.0;
+    double Dw[6] = {0, 0, 0, 0, 0, 0};
+    if constexpr (GEN) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) Dw[i] = __ldg(p.Dfield + 6 * cell + i);
+    }
     if (do_vol) {
-        // roles: X += Dc_q^T x^(q), x^(q) = W (D_qq/h_q^2 d_q u - b_q/h_q u); reaction W c u
+        if constexpr (GEN) {
+            // x^(r) = W (sum_s D_rs/(h_r h_s) d_s u - b_r/h_r u), X += Dc_r^T x^(r)   (eq:gauss_points)
+            double g0[N3], g1[N3], g2[N3];
+            rcontract<N, 0>(R.Dc, u, g0);
+            rcontract<N, 1>(R.Dc, u, g1);
+            rcontract<N, 2>(R.Dc, u, g2);
+            double Dh[3][3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            if (q == 0) rcontract<N, 0>(R.Dc, u, t);
-            else if (q == 1) rcontract<N, 1>(R.Dc, u, t);
-            else rcontract<N, 2>(R.Dc, u, t);
-            const double kd = p.dT * p.Dhat[4 * q], kb = p.dT * p.kb[q];
+            for (int rr = 0; rr < 3; ++rr)
 #pragma unroll
-            for (int iz = 0; iz < N; ++iz)
+                for (int ss = 0; ss < 3; ++ss) Dh[rr][ss] = p.dT * Dw[dsym(rr, ss)] * (p.hinv[rr] * p.hinv[ss]);
 #pragma unroll
-                for (int iy = 0; iy < N; ++iy)
+            for (int q = 0; q < 3; ++q) {
+                const double kb = p.dT * p.kb[q];
 #pragma unroll
-                    for (int ix = 0; ix < N; ++ix) {
-                        const int i = ix + N * (iy + N * iz);
-                        const double W = R.w[ix] * R.w[iy] * R.w[iz];
-                        t[i] = W * fma(kd, t[i], -kb * u[i]);
-                    }
-            double o[N3];
-            if (q == 0) rcontract_t<N, 0>(R.Dc, t, o);
-            else if (q == 1) rcontract_t<N, 1>(R.Dc, t, o);
-            else rcontract_t<N, 2>(R.Dc, t, o);
+                for (int iz = 0; iz < N; ++iz)
 #pragma unroll
-            for (int i = 0; i < N3; ++i) X[i] += o[i];
+                    for (int iy = 0; iy < N; ++iy)
+#pragma unroll
+                        for (int ix = 0; ix < N; ++ix) {
+                            const int i = ix + N * (iy + N * iz);
+                            const double W = R.w[ix] * R.w[iy] * R.w[iz];
+                            t[i] = W * (Dh[q][0] * g0[i] + Dh[q][1] * g1[i] + Dh[q][2] * g2[i] - kb * u[i]);
+                        }
+                double o[N3];
+                if (q == 0) rcontract_t<N, 0>(R.Dc, t, o);
+                else if (q == 1) rcontract_t<N, 1>(R.Dc, t, o);
+                else rcontract_t<N, 2>(R.Dc, t, o);
+#pragma unroll
+                for (int i = 0; i < N3; ++i) X[i] += o[i];
+            }
+        } else {
+            // roles: X += Dc_q^T x^(q), x^(q) = W (D_qq/h_q^2 d_q u - b_q/h_q u)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (q == 0) rcontract<N, 0>(R.Dc, u, t);
+                else if (q == 1) rcontract<N, 1>(R.Dc, u, t);
+                else rcontract<N, 2>(R.Dc, u, t);
+                const double kd = p.dT * p.Dhat[4 * q], kb = p.dT * p.kb[q];
+#pragma unroll
+                for (int iz = 0; iz < N; ++iz)
+#pragma unroll
+                    for (int iy = 0; iy < N; ++iy)
+#pragma unroll
+                        for (int ix = 0; ix < N; ++ix) {
+                            const int i = ix + N * (iy + N * iz);
+                            const double W = R.w[ix] * R.w[iy] * R.w[iz];
+                            t[i] = W * fma(kd, t[i], -kb * u[i]);
+                        }
+                double o[N3];
+                if (q == 0) rcontract_t<N, 0>(R.Dc, t, o);
+                else if (q == 1) rcontract_t<N, 1>(R.Dc, t, o);
+                else rcontract_t<N, 2>(R.Dc, t, o);
+#pragma unroll
+                for (int i = 0; i < N3; ++i) X[i] += o[i];
+            }
         }
-        const double wc = p.dT * p.c;
+        const double wc = p.dT * p.c;          // reaction W c u
 #pragma unroll
         for (int iz = 0; iz < N; ++iz)
 #pragma unroll
@@ -272,9 +402,9 @@ __global__ void DG_REG_BOUNDS dg_reg_kernel(const __grid_constant__ KParams p)
                     X[i] = fma(wc * R.w[ix] * R.w[iy] * R.w[iz], u[i], X[i]);
                 }
     }
-    reg_faces<N, 0>(p, R, zc, n3, lc, nbmask, do_int, do_bnd, u, X);
-    reg_faces<N, 1>(p, R, zc, n3, lc, nbmask, do_int, do_bnd, u, X);
-    reg_faces<N, 2>(p, R, zc, n3, lc, nbmask, do_int, do_bnd, u, X);
+    reg_faces<N, 0, GEN>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
+    reg_faces<N, 1, GEN>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
+    reg_faces<N, 2, GEN>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
     rcontract_t<N, 2>(R.V, X, t);
     rcontract_t<N, 1>(R.V, t, u);
     rcontract_t<N, 0>(R.V, u, t);                   // y block

@@ -1,9 +1,8 @@
-# register-resident kernel (dg_reg.cuh, n <= 3): GPU suite, C4 k = 1, 2 against the pencil kernel, ncu capture
+# register-resident kernels (dg_reg.cuh): GPU suite, C4 / Problem A at k = 1, 2 against the pencil kernels
 export PYTHONPATH=$PWD
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-for k in 1 2; do
-echo "reg k$k $(python tools/quick_time.py c4-k$k 5 | tail -1)"
-echo "pencil k$k $(DG_CELL_KERNEL=pencil python tools/quick_time.py c4-k$k 5 | tail -1)"
-ncu --set full --clock-control none --import-source on -k regex:dg_reg_kernel -s 2 -c 1 -o gpurun_out/reg_k${k}_full python tools/quick_time.py c4-k$k 2 > gpurun_out/ncu_reg_k$k.log 2>&1; echo "ncu k$k rc=$?"
+for c in c4-k1 c4-k2 a-k1 a-k2; do
+echo "reg $c $(python tools/quick_time.py $c 5 | tail -1)"
+echo "pencil $c $(DG_CELL_KERNEL=pencil python tools/quick_time.py $c 5 | tail -1)"
 done
