@@ -115,9 +115,11 @@ def problem_a(k, P=1):
 def problem_a_matrix(k, budget_bytes=24e9):
     """Problem A (as problem_a) on the mesh the matrix-based comparison can hold (NEXT-4; the paper
     also scales its matrix-based runs down): N^3 cells with the assembled
-    block-stencil matrix (7 n^6 doubles per cell, include/dg.h) within budget_bytes, N >= 3."""
+    block-stencil matrix (7 n^6 doubles per cell, include/dg.h) within budget_bytes, N >= 3 and a
+    multiple of 3."""
     n = k + 1
     N = max(3, int((budget_bytes / (56.0 * n ** 6)) ** (1.0 / 3.0)))
+    N -= N % 3          # 27 colour classes for dg_assemble's probes (a periodic tail adds classes)
     return Config("MB-k%d" % k, (N, N, N), (0, 0, 0), (1.0, 1.0, 1.0), k, I3, B_A, 1.0, sigma_for(k, 1.0 / N), 5,
                   (1, 1, 1), (1, 1, 1), 6)
 

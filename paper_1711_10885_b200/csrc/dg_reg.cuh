@@ -28,7 +28,7 @@ namespace dg {
 #define DG_REG_NMAX 3      // constant diagonal D (fast path)
 #endif
 #ifndef DG_REG_GMAX
-#define DG_REG_GMAX 2      // full / per-cell tensors (general path; n = 3 would need ~320 registers)
+#define DG_REG_GMAX 3      // full / per-cell tensors (general path; n = 3 spills ~0.5 KB and still wins 1.7x)
 #endif
 
 // full 1D tables of the register kernel (tables.cpp): V_ij = theta_j(xi_i), G_ij = theta'_j(xi_i),
@@ -334,7 +334,41 @@ __global__ void DG_REG_BOUNDS dg_reg_kernel(const __grid_constant__ KParams p)
         for (int i = 0; i < 6; ++i) Dw[i] = __ldg(p.Dfield + 6 * cell + i);
     }
     if (do_vol) {
-        if constexpr (GEN) {
+        if constexpr (GEN && N >= 3) {
+            // as below, with the reference derivatives recomputed per role (two arrays live instead
+            // of four: registers)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double kb = p.dT * p.kb[q];
+#pragma unroll
+                for (int i = 0; i < N3; ++i) t[i] = -kb * u[i];
+#pragma unroll
+                for (int sd = 0; sd < 3; ++sd) {
+                    double g[N3];
+                    if (sd == 0) rcontract<N, 0>(R.Dc, u, g);
+                    else if (sd == 1) rcontract<N, 1>(R.Dc, u, g);
+                    else rcontract<N, 2>(R.Dc, u, g);
+                    const double dh = p.dT * Dw[dsym(q, sd)] * (p.hinv[q] * p.hinv[sd]);
+#pragma unroll
+                    for (int i = 0; i < N3; ++i) t[i] = fma(dh, g[i], t[i]);
+                }
+#pragma unroll
+                for (int iz = 0; iz < N; ++iz)
+#pragma unroll
+                    for (int iy = 0; iy < N; ++iy)
+#pragma unroll
+                        for (int ix = 0; ix < N; ++ix) {
+                            const int i = ix + N * (iy + N * iz);
+                            t[i] *= R.w[ix] * R.w[iy] * R.w[iz];
+                        }
+                double o[N3];
+                if (q == 0) rcontract_t<N, 0>(R.Dc, t, o);
+                else if (q == 1) rcontract_t<N, 1>(R.Dc, t, o);
+                else rcontract_t<N, 2>(R.Dc, t, o);
+#pragma unroll
+                for (int i = 0; i < N3; ++i) X[i] += o[i];
+            }
+        } else if constexpr (GEN) {
             // x^(r) = W (sum_s D_rs/(h_r h_s) d_s u - b_r/h_r u), X += Dc_r^T x^(r)   (eq:gauss_points)
             double g0[N3], g1[N3], g2[N3];
             rcontract<N, 0>(R.Dc, u, g0);

@@ -3,6 +3,8 @@
 * The k = 7 FP64 tensor-core kernel (dg_mma8.cuh, opt-in DG_CELL_KERNEL=mma) against the
   oracle O-1 per term mask, on meshes with every boundary type (run in a subprocess: the
   kernel choice is read once per process).
+* k = 1, 2: the register-resident kernels (dg_reg.cuh, the default for n <= 3) and the pencil kernels (DG_CELL_KERNEL=pencil) against O-1, per mask, constant and
+  per-cell tensors, Dirichlet and periodic (subprocess per kernel choice).
 * Determinism: repeated applies are bit-identical (no atomics, no races: each cell is
   computed by one CTA and written once). compute-sanitizer is closed on this pool, so this
   plus NaN-initialised outputs in every parity test stand in for racecheck/initcheck.
@@ -58,6 +60,62 @@ def test_k7_kernel_variants_vs_o1(kernel):
             assert err == 0.0
         else:
             assert err < 1e-12, (name, mask, err)
+
+
+SCRIPT_LOWK = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, %r)
+from oracle import o1
+from paper_1711_10885_b200 import configs, dg, inputs
+out = []
+rng = np.random.default_rng(3)
+for k in (1, 2):
+    for cfg, per, tensors in ((configs.small(k, ncells=(5, 3, 4)), (0, 0, 0), False),
+                              (configs.small(k, ncells=(4, 3, 2), b=(-1.0, 0.5, -0.25)), (1, 0, 1), False),
+                              (configs.small(k, ncells=(3, 4, 2), b=(0.3, -0.2, 0.1)), (1, 1, 1), True),
+                              (configs.small(k, ncells=(4, 2, 3)), (0, 1, 0), True)):
+        ncell = cfg.ncells[0] * cfg.ncells[1] * cfg.ncells[2]
+        op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, k, cfg.D, cfg.b, cfg.c, cfg.sigma, bc=dg.bc_from_periodic(per))
+        Dc = None
+        if tensors:
+            M = rng.normal(size=(ncell, 3, 3))
+            Dc = np.einsum("eij,ekj->eik", M, M) + 0.5 * np.eye(3)[None]
+            op.set_diffusion(torch.from_numpy(Dc.reshape(-1).copy()).cuda())
+        z = inputs.uniform(cfg.ndofs, 5 + k)
+        zt = torch.from_numpy(z).cuda()
+        info = op.kernel_info()
+        for mask in (1, 2, 4, 7):
+            y = torch.full_like(zt, float("nan"))
+            op.apply(zt, y, terms=mask)
+            torch.cuda.synchronize()
+            yref, _ = o1.apply(*cfg.args(), z, mask=mask, periodic=per, Dcell=Dc)
+            den = max(np.abs(yref).max(), 1e-300)
+            out.append([k, str(per), tensors, mask, float(np.abs(y.cpu().numpy() - yref).max() / den),
+                        float(np.abs(yref).max()), info["smem_bytes"]])
+        op.close()
+print(json.dumps({"rows": out}))
+"""
+
+
+@pytest.mark.parametrize("kernel", ["reg", "pencil"])
+def test_low_degree_kernels_vs_o1(kernel):
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    env.pop("DG_CELL_KERNEL", None)
+    if kernel == "pencil":
+        env["DG_CELL_KERNEL"] = "pencil"
+    r = subprocess.run([sys.executable, "-c", SCRIPT_LOWK % ROOT], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert len(res["rows"]) == 2 * 4 * 4
+    for k, per, tensors, mask, err, scale, smem in res["rows"]:
+        # the register kernels use no shared memory: shows which kernel ran
+        reg_expected = kernel == "reg"
+        assert (smem == 0) == reg_expected, (k, per, tensors, smem)
+        if scale == 0.0:
+            assert err == 0.0
+        else:
+            assert err < 1e-12, (k, per, tensors, mask, err)
 
 
 def test_repeat_applies_bit_identical():
