@@ -43,14 +43,17 @@ template <int N>
 struct Tab {
     static constexpr int HC = (N + 1) / 2;
     double Vh[12][HC][N];    // V_ij = theta_j(xi_i), rows i < ceil(n/2); one copy per use site
-    EO<N> Dc[6];             // collocation derivative Dc_il (row = point, col = value)
-    EO<N> DcT[6];            // its transpose
+    // pad0..pad3: unused. They keep the constant-bank offsets of the tables below where an
+    // earlier table set put them; the packed layout measured 0.9 % slower at C3 (82.5 -> 81.8
+    // GDOF/s, A/B on one box), i.e. the placement of each stage's tables in constant-cache lines
+    // matters at this level.
+    EO<N> pad0[12];
     double w[N];
-    double L[6][4][N];       // per use site: L_l(0), L_l(1), L'_l(0), L'_l(1)
+    double pad1[6][4][N];
     double th0[N], th1[N], dth0[N], dth1[N];
-    double Gh[HC][N];        // G_ij = theta'_j(xi_i), rows i < ceil(n/2) (general kernel, even-odd)
-    // sigma/delta form of the fast kernel (n = 8, SDF below): doubled forward V and doubled even-odd
-    // Dc, Dc^T diag(w), one copy per use site
+    double pad2[HC][N];
+    // sigma/delta form (below): doubled forward V, doubled even-odd Dc and Dc^T diag(w), one copy
+    // per use site (the middle row of an odd n plain)
     double Vs[9][HC][N];
     EO<N> Dcs[5], DcTws[3];
     // sigma/delta form of the general kernel (dg_gen.cuh): doubled Dc^T, doubled G (its odd rows
@@ -60,8 +63,8 @@ struct Tab {
     double Gs[HC][N];
     double Ls[2][4][N];
     double Lsl[4][N];
-    // even-odd forms used by the roles (one copy per direction):
-    EO<N> DcTw[3];                         // Dc^T diag(w): Gauss weights folded into the transposed stage
+    EO<N> pad3[3];
+    // the roles' own traces from the even/odd sums (one copy per direction):
     double Le[3][4][(N / 2) > 0 ? N / 2 : 1];  // (L0_i +- L0_{n-1-i})/2, (L'0_i +- L'0_{n-1-i})/2, i < n/2
     double Lmid[3][2];                     // L0_H, L'0_H (odd n)
 };
@@ -227,67 +230,6 @@ __device__ __forceinline__ void store_block(const KParams& p, const double* S, i
 // ---------------------------------------------------------------------------------- 1D stages
 // t[k][i] = sum_j V_ij r[k][j]  (even-odd: V_{n-1-i,j} = (-1)^j V_ij)
 template <int N, int P>
-__device__ __forceinline__ void v_fwd(const double (&Vh)[(N + 1) / 2][N], const double (&r)[P][N], double (&t)[P][N])
-{
-    constexpr int H = N / 2;
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-        double E[P], O[P];
-#pragma unroll
-        for (int k = 0; k < P; ++k) { E[k] = 0.0; O[k] = 0.0; }
-#pragma unroll
-        for (int j = 0; j < N; ++j)
-#pragma unroll
-            for (int k = 0; k < P; ++k) {
-                if (j & 1) O[k] = fma(Vh[i][j], r[k][j], O[k]);
-                else E[k] = fma(Vh[i][j], r[k][j], E[k]);
-            }
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            t[k][i] = E[k] + O[k];
-            t[k][N - 1 - i] = E[k] - O[k];
-        }
-    }
-    if (N & 1) {
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            double E = 0.0;
-#pragma unroll
-            for (int j = 0; j < N; j += 2) E = fma(Vh[H][j], r[k][j], E);
-            t[k][H] = E;
-        }
-    }
-}
-
-// t[k][j] = sum_i V_ij r[k][i]
-template <int N, int P>
-__device__ __forceinline__ void v_bwd(const double (&Vh)[(N + 1) / 2][N], const double (&r)[P][N], double (&t)[P][N])
-{
-    constexpr int H = N / 2;
-    double s[P][H > 0 ? H : 1], d[P][H > 0 ? H : 1];
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-#pragma unroll
-        for (int i = 0; i < H; ++i) {
-            s[k][i] = r[k][i] + r[k][N - 1 - i];
-            d[k][i] = r[k][i] - r[k][N - 1 - i];
-        }
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-        double acc[P];
-#pragma unroll
-        for (int k = 0; k < P; ++k) acc[k] = ((N & 1) && !(j & 1)) ? Vh[H][j] * r[k][H] : 0.0;
-#pragma unroll
-        for (int i = 0; i < H; ++i)
-#pragma unroll
-            for (int k = 0; k < P; ++k) acc[k] = fma(Vh[i][j], (j & 1) ? d[k][i] : s[k][i], acc[k]);
-#pragma unroll
-        for (int k = 0; k < P; ++k) t[k][j] = acc[k];
-    }
-}
-
-// t[k] = A r[k] for a centro-antisymmetric A (A_{n-1-i,n-1-j} = -A_ij) in even-odd form
-template <int N, int P>
 __device__ __forceinline__ void c_apply(const EO<N>& A, const double (&r)[P][N], double (&t)[P][N])
 {
     constexpr int H = N / 2;
@@ -341,14 +283,13 @@ __device__ __forceinline__ double dot(const double* a, const double* v)
 }
 
 // ---------------------------------------------------------------------------------- sigma/delta form
-// For even n every array of the n = 8 fast kernel is kept in "sigma/delta form" along each of
-// its three directions: position i < n/2 holds t_i + t_(n-1-i), position n-1-i holds
-// t_i - t_(n-1-i). All pointwise operations (Gauss weights w_i = w_(n-1-i), constant
+// Every array of the pencil kernels is kept in "sigma/delta form" along each of its three
+// directions: position i < n/2 holds t_i + t_(n-1-i), position n-1-i holds t_i - t_(n-1-i)
+// (odd n: the middle entry plain). All pointwise operations (Gauss weights w_i = w_(n-1-i), constant
 // coefficients, the face fluxes, the traces and lifts) are linear with symmetric weights, so
 // they commute with this change of basis along every direction, and the 1D stages consume and
 // produce it directly with doubled even-odd tables: no sum / difference instructions around
 // the forward stages, the Dc and Dc^T diag(w) stages, or before the backward stages.
-__host__ __device__ constexpr bool sdf(int n) { return n >= 2; }
 
 template <int N, int P>
 __device__ __forceinline__ void v_fwd_sd(const double (&Vs)[(N + 1) / 2][N], const double (&r)[P][N], double (&t)[P][N])
@@ -575,158 +516,9 @@ __device__ __forceinline__ void nb_tangential(const double (&Vh)[(N + 1) / 2][N]
             double rr[1][N], tt[1][N];
 #pragma unroll
             for (int e = 0; e < N; ++e) rr[0][e] = NT[dim ? FLay<N>::at(arr, line, e) : FLay<N>::at(arr, e, line)];
-            if constexpr (sdf(N)) v_fwd_sd<N, 1>(Vh, rr, tt);   // Vh is a doubled copy (Tab::Vs)
-            else v_fwd<N, 1>(Vh, rr, tt);
+            v_fwd_sd<N, 1>(Vh, rr, tt);   // Vh is a doubled copy (Tab::Vs)
 #pragma unroll
             for (int e = 0; e < N; ++e) NT[dim ? FLay<N>::at(arr, line, e) : FLay<N>::at(arr, e, line)] = tt[0][e];
-        }
-    }
-}
-
-// Role phase for normal direction q on this thread's q-pencils of u (r[k][e], e along q):
-//   g = Dc u (reference d/dx_hat_q), own traces, face fluxes with the neighbour traces,
-//   x^(q) = W (D_qq/h_q^2 g - b_q/h_q u) [+ x^(0) = W c u for the z role], and
-//   out = Dc^T x^(q) [+ x^(0)] + lifts of the two q-faces (normal direction LAST).
-// W = Delta_T w_a w_b w_e at the pencil's points; Wf = Delta_F,q w_a w_b at its face point.
-template <int N, int P>
-__device__ __forceinline__ void role_q(const KParams& p, const Tab<N>& T, const EO<N>& Dq, const EO<N>& DqT,
-                                      const double (&Ls)[4][N], const double* NT, int q, unsigned nbmask,
-                                      bool do_int, bool do_bnd, bool do_vol, bool with_reaction, const int (&pa)[P],
-                                      const int (&pb)[P], const double (&r)[P][N], double (&out)[P][N])
-{
-    double g[P][N];
-    c_apply<N, P>(Dq, r, g);
-    const double kd = p.Dhat[4 * q], kb = p.kb[q];
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const double wab = T.w[pa[k]] * T.w[pb[k]];
-        const double wv = do_vol ? p.dT * wab : 0.0;
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-            const double W = wv * T.w[e];
-            g[k][e] = W * (kd * g[k][e] - kb * r[k][e]);       // x^(q) / h_q   (eq:gauss_points)
-        }
-    }
-    c_apply<N, P>(DqT, g, out);
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const double Wf = p.dF[q] * T.w[pa[k]] * T.w[pb[k]];
-        FaceOut fo[2];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const int f = 2 * q + s;
-            const double uo = dot<N>(Ls[s], r[k]);            // own trace u(x_q = s)
-            const double dref = dot<N>(Ls[2 + s], r[k]);      // own d u / d x_hat_q at x_q = s
-            fo[s].cv = 0.0;
-            fo[s].cg = 0.0;
-            if ((nbmask >> f) & 1u) {
-                if (do_int) {
-                    const double un = NT[FLay<N>::at(2 * f, pa[k], pb[k])];
-                    const double sn = p.Dqq_h[q] * NT[FLay<N>::at(2 * f + 1, pa[k], pb[k])];
-                    fo[s] = flux_interior(p, q, s, Wf, uo, dref, un, sn);
-                }
-            } else if (do_bnd) {
-                fo[s] = flux_boundary(p, q, s, Wf, uo, dref);
-            }
-        }
-        const double wc = (with_reaction && do_vol) ? p.dT * T.w[pa[k]] * T.w[pb[k]] * p.c : 0.0;
-#pragma unroll
-        for (int e = 0; e < N; ++e)
-            out[k][e] += wc * T.w[e] * r[k][e] + fo[0].cv * Ls[0][e] + fo[0].cg * Ls[2][e] + fo[1].cv * Ls[1][e] +
-                         fo[1].cg * Ls[3][e];
-    }
-}
-
-// c_apply that also returns the even/odd sums s_j = r_j + r_{n-1-j}, d_j = r_j - r_{n-1-j}
-template <int N, int P>
-__device__ __forceinline__ void c_apply_sd(const EO<N>& A, const double (&r)[P][N], double (&t)[P][N],
-                                           double (&s)[P][(N / 2) > 0 ? N / 2 : 1],
-                                           double (&d)[P][(N / 2) > 0 ? N / 2 : 1])
-{
-    constexpr int H = N / 2;
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-#pragma unroll
-        for (int j = 0; j < H; ++j) {
-            s[k][j] = r[k][j] + r[k][N - 1 - j];
-            d[k][j] = r[k][j] - r[k][N - 1 - j];
-        }
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-        double Pp[P], Q[P];
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            Pp[k] = (N & 1) ? A.col[i] * r[k][H] : 0.0;
-            Q[k] = 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < H; ++j)
-#pragma unroll
-            for (int k = 0; k < P; ++k) {
-                Pp[k] = fma(A.p[i][j], s[k][j], Pp[k]);
-                Q[k] = fma(A.m[i][j], d[k][j], Q[k]);
-            }
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            t[k][i] = Pp[k] + Q[k];
-            t[k][N - 1 - i] = Q[k] - Pp[k];
-        }
-    }
-    if (N & 1) {
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < H; ++j) acc = fma(A.row[j], d[k][j], acc);
-            t[k][H] = acc;
-        }
-    }
-}
-
-// c_apply with an even/odd-paired addend merged into the accumulators:
-// t_i += qa_i + pb_i, t_{n-1-i} += qa_i - pb_i (i < n/2), t_H += mid (odd n)
-template <int N, int P>
-__device__ __forceinline__ void c_apply_add(const EO<N>& A, const double (&r)[P][N], double (&t)[P][N],
-                                            const double (&qa)[P][(N / 2) > 0 ? N / 2 : 1],
-                                            const double (&pb)[P][(N / 2) > 0 ? N / 2 : 1], const double (&mid)[P])
-{
-    constexpr int H = N / 2;
-    double s[P][H > 0 ? H : 1], d[P][H > 0 ? H : 1];
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-#pragma unroll
-        for (int j = 0; j < H; ++j) {
-            s[k][j] = r[k][j] + r[k][N - 1 - j];
-            d[k][j] = r[k][j] - r[k][N - 1 - j];
-        }
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-        double Pp[P], Q[P];
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            Pp[k] = (N & 1) ? fma(A.col[i], r[k][H], pb[k][i]) : pb[k][i];
-            Q[k] = qa[k][i];
-        }
-#pragma unroll
-        for (int j = 0; j < H; ++j)
-#pragma unroll
-            for (int k = 0; k < P; ++k) {
-                Pp[k] = fma(A.p[i][j], s[k][j], Pp[k]);
-                Q[k] = fma(A.m[i][j], d[k][j], Q[k]);
-            }
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            t[k][i] = Pp[k] + Q[k];
-            t[k][N - 1 - i] = Q[k] - Pp[k];
-        }
-    }
-    if (N & 1) {
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            double acc = mid[k];
-#pragma unroll
-            for (int j = 0; j < H; ++j) acc = fma(A.row[j], d[k][j], acc);
-            t[k][H] = acc;
         }
     }
 }
@@ -741,9 +533,8 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
 {
     constexpr int H = N / 2;
     constexpr int HH = H > 0 ? H : 1;
-    constexpr bool SD = sdf(N);
     double g[P][N], s[P][HH], d[P][HH];
-    if constexpr (SD) {                         // r in sigma/delta form: the sums are the input itself
+    {                                           // r in sigma/delta form: the sums are the input itself
         double z0[P][HH], zm[P];
         c_apply_s<N, P, false>(T.Dcs[q], r, g, z0, z0, zm);
 #pragma unroll
@@ -753,8 +544,6 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
                 s[k][j] = r[k][j];
                 d[k][j] = r[k][N - 1 - j];
             }
-    } else {
-        c_apply_sd<N, P>(T.Dc[q], r, g, s, d);
     }
     const double* Lp = T.Le[q][0];
     const double* Lm = T.Le[q][1];
@@ -792,12 +581,11 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
                 fo[sd] = flux_boundary(p, q, sd, Wf, tr_u[sd], tr_d[sd]);
             }
         }
-        // lift (normal direction LAST) as even/odd addends of the Dc^T stage (SD: the pair addends
-        // enter the sigma/delta output doubled, the middle one plain)
+        // lift (normal direction LAST) as even/odd addends of the Dc^T stage: the pair addends
+        // enter the sigma/delta output doubled, the middle one plain
         const double Pc = fo[0].cv + fo[1].cv, Mc = fo[0].cv - fo[1].cv;
         const double Qc = fo[0].cg - fo[1].cg, Rc = fo[0].cg + fo[1].cg;
-        const double two = SD ? 2.0 : 1.0;
-        const double Pc2 = two * Pc, Mc2 = two * Mc, Qc2 = two * Qc, Rc2 = two * Rc;
+        const double Pc2 = 2.0 * Pc, Mc2 = 2.0 * Mc, Qc2 = 2.0 * Qc, Rc2 = 2.0 * Rc;
 #pragma unroll
         for (int i = 0; i < H; ++i) {
             qa[k][i] = fma(Pc2, Lp[i], Qc2 * LDp[i]);
@@ -810,8 +598,7 @@ __device__ __forceinline__ void role_eo(const KParams& p, const Tab<N>& T, const
 #pragma unroll
         for (int e = 0; e < N; ++e) g[k][e] = fma(kd, g[k][e], -kb * r[k][e]);
     }
-    if constexpr (SD) c_apply_s<N, P, true>(T.DcTws[q], g, out, qa, pbv, mid);
-    else c_apply_add<N, P>(T.DcTw[q], g, out, qa, pbv, mid);
+    c_apply_s<N, P, true>(T.DcTws[q], g, out, qa, pbv, mid);
     if (with_reaction && do_vol) {
 #pragma unroll
         for (int k = 0; k < P; ++k) {
@@ -997,7 +784,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
             }
         }
         }
-        if constexpr (sdf(N)) v_fwd_sd<N, P>(T.Vs[0], r, t); else v_fwd<N, P>(T.Vh[0], r, t);
+        v_fwd_sd<N, P>(T.Vs[0], r, t);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k])
@@ -1012,13 +799,13 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         for (int k = 0; k < P; ++k)
 #pragma unroll
             for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-        if constexpr (sdf(N)) v_fwd_sd<N, P>(T.Vs[1], r, t); else v_fwd<N, P>(T.Vh[1], r, t);
+        v_fwd_sd<N, P>(T.Vs[1], r, t);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) A1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
-        nb_tangential<N, TPC>(sdf(N) ? T.Vs[2] : T.Vh[2], NT, 0, 0, nbi, (lane + TPC / 2) % TPC);
+        nb_tangential<N, TPC>(T.Vs[2], NT, 0, 0, nbi, (lane + TPC / 2) % TPC);
         nb_contract<N, P>(T, NT, 1, nbi, pa, pb, act, rl, rh);
         csync();
 
@@ -1029,14 +816,14 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         for (int k = 0; k < P; ++k)
 #pragma unroll
             for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
-        if constexpr (sdf(N)) v_fwd_sd<N, P>(T.Vs[3], r, t); else v_fwd<N, P>(T.Vh[3], r, t);
+        v_fwd_sd<N, P>(T.Vs[3], r, t);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
-        nb_tangential<N, TPC>(sdf(N) ? T.Vs[4] : T.Vh[4], NT, 1, 0, nbi, lane);
-        nb_tangential<N, TPC>(sdf(N) ? T.Vs[5] : T.Vh[5], NT, 0, 1, nbi, (lane + TPC / 2) % TPC);
+        nb_tangential<N, TPC>(T.Vs[4], NT, 1, 0, nbi, lane);
+        nb_tangential<N, TPC>(T.Vs[5], NT, 0, 1, nbi, (lane + TPC / 2) % TPC);
         nb_contract<N, P>(T, NT, 2, nbi, pa, pb, act, rl, rh);
         csync();
     }
@@ -1052,8 +839,8 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         if (act[k])
 #pragma unroll
             for (int e = 0; e < N; ++e) A1[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
-    nb_tangential<N, TPC>(sdf(N) ? T.Vs[6] : T.Vh[6], NT, 2, 0, nbi, lane);
-    nb_tangential<N, TPC>(sdf(N) ? T.Vs[7] : T.Vh[7], NT, 1, 1, nbi, (lane + TPC / 2) % TPC);
+    nb_tangential<N, TPC>(T.Vs[6], NT, 2, 0, nbi, lane);
+    nb_tangential<N, TPC>(T.Vs[7], NT, 1, 1, nbi, (lane + TPC / 2) % TPC);
     csync();
 
     // ---- phase 5: y role -> A1 += T2; z-arrays step C
@@ -1070,7 +857,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 const int ie = Lay<N>::at(pa[k], e, pb[k]);
                 A1[ie] = A1[ie] + t[k][e];
             }
-    nb_tangential<N, TPC>(sdf(N) ? T.Vs[8] : T.Vh[8], NT, 2, 1, nbi, lane);
+    nb_tangential<N, TPC>(T.Vs[8], NT, 2, 1, nbi, lane);
     csync();
 
     // ---- phase 6: z role (+ reaction) -> X = T1 + T2 + T3; V^T along z -> A0
@@ -1083,7 +870,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) t[k][e] += act[k] ? A1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
-    if constexpr (sdf(N)) v_bwd_sd<N, P>(T.Vh[9], t, r); else v_bwd<N, P>(T.Vh[9], t, r);   // in place: A0 z-positions of this pencil are read only by this thread
+    v_bwd_sd<N, P>(T.Vh[9], t, r);   // in place: A0 z-positions of this pencil are read only by this thread
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
@@ -1096,7 +883,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(pa[k], e, pb[k])] : 0.0;
-    if constexpr (sdf(N)) v_bwd_sd<N, P>(T.Vh[10], r, t); else v_bwd<N, P>(T.Vh[10], r, t);
+    v_bwd_sd<N, P>(T.Vh[10], r, t);
 #pragma unroll
     for (int k = 0; k < P; ++k)
         if (act[k])
@@ -1109,7 +896,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
-    if constexpr (sdf(N)) v_bwd_sd<N, P>(T.Vh[11], r, t); else v_bwd<N, P>(T.Vh[11], r, t);
+    v_bwd_sd<N, P>(T.Vh[11], r, t);
     if constexpr (N == 8 && C == 1) {
         if (STG && p.tma == 2 && p.epi == 0) {   // y through the staging block and one TMA store
 #pragma unroll

@@ -39,9 +39,7 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
     for (int c = 0; c < 12; ++c)
         for (int i = 0; i < Tab<N>::HC; ++i)
             for (int j = 0; j < N; ++j) h.Vh[c][i][j] = t.V[i][j];
-    for (int i = 0; i < Tab<N>::HC; ++i)
-        for (int j = 0; j < N; ++j) h.Gh[i][j] = t.G[i][j];
-    {   // sigma/delta form (dg_cell.cuh, sdf): doubled forward V, doubled Dc and Dc^T diag(w)
+    {   // sigma/delta form (dg_cell.cuh): doubled forward V, doubled Dc and Dc^T diag(w)
         static double D2[NMAX][NMAX], A2[NMAX][NMAX];
         for (int i = 0; i < N; ++i)
             for (int j = 0; j < N; ++j) {
@@ -83,17 +81,9 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
             }
         }
     }
-    for (int c = 0; c < 6; ++c) {
-        fill_eo<N>(h.Dc[c], t.Dc, false);
-        fill_eo<N>(h.DcT[c], t.Dc, true);
-    }
     {
-        static double Aw[NMAX][NMAX];   // Dc^T diag(w)
-        for (int i = 0; i < N; ++i)
-            for (int j = 0; j < N; ++j) Aw[i][j] = t.Dc[j][i] * t.w[j];
         constexpr int H = N / 2;
         for (int c = 0; c < 3; ++c) {
-            fill_eo<N>(h.DcTw[c], Aw, false);
             for (int i = 0; i < H; ++i) {
                 h.Le[c][0][i] = 0.5 * (t.L0[i] + t.L0[N - 1 - i]);
                 h.Le[c][1][i] = 0.5 * (t.L0[i] - t.L0[N - 1 - i]);
@@ -106,12 +96,6 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
     }
     for (int i = 0; i < N; ++i) {
         h.w[i] = t.w[i];
-        for (int c = 0; c < 6; ++c) {
-            h.L[c][0][i] = t.L0[i];
-            h.L[c][1][i] = t.L1[i];
-            h.L[c][2][i] = t.LD0[i];
-            h.L[c][3][i] = t.LD1[i];
-        }
         h.th0[i] = t.th0[i];
         h.th1[i] = t.th1[i];
         h.dth0[i] = t.dth0[i];
