@@ -39,8 +39,20 @@ struct EO {                        // even-odd form of a centro-antisymmetric ma
     double row[H > 0 ? H : 1];                // A_Hj            (odd N)
 };
 
+// Leading pad of the table block: the constant-bank placement of the per-stage tables changes
+// the fast kernel's speed by a few per cent (C3, one box, A/B: shifts of 0 / 16 / 32 / 48 / 64 /
+// 80 / 96 / 192 / 320 / 384 / 512 / 1024 bytes gave 82.5 / 83.3 / 83.4 / 83.4 / 84.0 / 83.7 / 83.6
+// / 83.6 / 83.5 / 82.7 / 82.3 / 81.4 GDOF/s, an 8-byte shift 78.1; Problem A k = 7 lost 0.9 %
+// with it), so n = 8 keeps the best one
+// (one table per translation unit: DG_PADX doubles, per degree below, overridable for sweeps)
+#ifndef DG_PADX
+#define DG_PADX ((DG_N) == 8 ? 8 : 0)
+#endif
+template <int P> struct TabHead { double head[P]; };
+template <> struct TabHead<0> {};
+
 template <int N>
-struct Tab {
+struct Tab : TabHead<DG_PADX> {
     static constexpr int HC = (N + 1) / 2;
     double Vh[12][HC][N];    // V_ij = theta_j(xi_i), rows i < ceil(n/2); one copy per use site
     // pad0..pad3: unused. They keep the constant-bank offsets of the tables below where an
