@@ -98,7 +98,7 @@ template <> struct Cfg<2> { static constexpr int TPC = DG_OVR(2, DG_TPC, 8), P =
 template <> struct Cfg<3> { static constexpr int TPC = DG_OVR(3, DG_TPC, 16), P = DG_OVR(3, DG_P, 1), C = DG_OVR(3, DG_C, 8), MINB = DG_OVR(3, DG_MINB, 8); };
 template <> struct Cfg<4> { static constexpr int TPC = DG_OVR(4, DG_TPC, 16), P = DG_OVR(4, DG_P, 1), C = DG_OVR(4, DG_C, 4), MINB = DG_OVR(4, DG_MINB, 8); };
 template <> struct Cfg<5> { static constexpr int TPC = DG_OVR(5, DG_TPC, 32), P = DG_OVR(5, DG_P, 1), C = DG_OVR(5, DG_C, 1), MINB = DG_OVR(5, DG_MINB, 16); };
-template <> struct Cfg<6> { static constexpr int TPC = DG_OVR(6, DG_TPC, 32), P = DG_OVR(6, DG_P, 2), C = DG_OVR(6, DG_C, 1), MINB = DG_OVR(6, DG_MINB, 16); };
+template <> struct Cfg<6> { static constexpr int TPC = DG_OVR(6, DG_TPC, 36), P = DG_OVR(6, DG_P, 1), C = DG_OVR(6, DG_C, 4), MINB = DG_OVR(6, DG_MINB, 6); };
 template <> struct Cfg<7> { static constexpr int TPC = DG_OVR(7, DG_TPC, 64), P = DG_OVR(7, DG_P, 1), C = DG_OVR(7, DG_C, 1), MINB = DG_OVR(7, DG_MINB, 10); };
 template <> struct Cfg<8> { static constexpr int TPC = DG_OVR(8, DG_TPC, 64), P = DG_OVR(8, DG_P, 1), C = DG_OVR(8, DG_C, 1), MINB = DG_OVR(8, DG_MINB, 10); };
 template <> struct Cfg<9> { static constexpr int TPC = DG_OVR(9, DG_TPC, 96), P = DG_OVR(9, DG_P, 1), C = DG_OVR(9, DG_C, 1), MINB = DG_OVR(9, DG_MINB, 5); };
@@ -683,7 +683,6 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     constexpr int NN = N * N;
     static_assert(N == DG_N, "one degree per translation unit");
     static_assert(TPC * P >= NN, "pencil slots");
-    static_assert(TPC <= 32 || C == 1, "multi-warp cells use CTA barriers: one cell per CTA");
     extern __shared__ double smem[];
     const Tab<N>& T = g_tab;
 
@@ -696,7 +695,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     double* NT = A1 + Lay<N>::SLOT;
 
     auto csync = [&]() {
-        if (TPC <= 32) __syncwarp(); else __syncthreads();
+        if (32 % TPC == 0) __syncwarp(); else __syncthreads();   // a cell within one warp, else CTA-wide
     };
 
     // ---- cell of this slot (32-bit index math: at most 2^31 cells per rank)

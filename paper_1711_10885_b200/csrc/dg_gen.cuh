@@ -116,12 +116,13 @@ __device__ __forceinline__ const double* nb_dfield(const KParams& p, const int (
 #else
 #define DG_GOVR(ov, d) (d)
 #endif
-// (one pencil per thread is better than the fast kernel's 2 for n = 6 and 10: A-k5 18.0 -> 22.8,
-// A-k9 19.5 -> 27.5 GDOF/s, measured with tools/variant.py)
+// (one pencil per thread is better than the fast kernel's 2 for n = 10: A-k9 19.5 -> 27.5 GDOF/s;
+// n = 6: 36 threads per cell (every thread a pencil), 2 cells per CTA straddling warps: A-k5
+// 26.6 -> 28.5; measured with tools/variant.py)
 template <int N> struct GCfgD {
-    static constexpr int TPC = (N == 6) ? 64 : (N == 10) ? 128 : Cfg<N>::TPC;
+    static constexpr int TPC = (N == 6) ? 36 : (N == 10) ? 128 : Cfg<N>::TPC;
     static constexpr int P = (N == 6 || N == 10) ? 1 : Cfg<N>::P;
-    static constexpr int C = (N == 6 || N == 10) ? 1 : Cfg<N>::C;
+    static constexpr int C = (N == 6) ? 2 : (N == 10) ? 1 : Cfg<N>::C;
 };
 template <int N> struct GCfg {
     static constexpr int TPC = DG_GOVR(DG_GTPC, GCfgD<N>::TPC), P = DG_GOVR(DG_GP, GCfgD<N>::P),
@@ -145,7 +146,6 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     constexpr int TPC = GCfg<N>::TPC, P = GCfg<N>::P, C = GCfg<N>::C;
     constexpr int NN = N * N;
     static_assert(TPC * P >= NN, "pencil slots");
-    static_assert(TPC <= 32 || C == 1, "multi-warp cells use CTA barriers: one cell per CTA");
     extern __shared__ double smem[];
     const Tab<N>& T = g_tab;
 
@@ -159,7 +159,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     double* NT = X2 + Lay<N>::SLOT;                  // neighbour face arrays (2 per face)
     double* OT = NT + FLay<N>::SLOT;                 // own face arrays (2 per face)
     auto csync = [&]() {
-        if (TPC <= 32) __syncwarp(); else __syncthreads();
+        if (32 % TPC == 0) __syncwarp(); else __syncthreads();   // a cell within one warp, else CTA-wide
     };
 
     unsigned task = blockIdx.x * (unsigned)C + (unsigned)slot;
