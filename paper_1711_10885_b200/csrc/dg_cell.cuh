@@ -108,12 +108,14 @@ template <> struct Cfg<11> { static constexpr int TPC = DG_OVR(11, DG_TPC, 128),
 // Shared-memory layout of one n^3 cell array: x-, y- and z-pencil accesses of a warp are
 // (nearly) bank-conflict free (searched offline; n = 8 uses an XOR swizzle that is conflict
 // free for all three access patterns).
+// Padded linear layouts for the other n, chosen with the bank-conflict model of
+// tools/smem_layout.py (validated against ncu: 55 % / 26 % conflicts predicted for the old n = 4
+// / n = 6 layouts, 53 % / 28 % measured) over SY, SZ and index rotations.
 template <int N> struct Lay {
-    static constexpr int SY = (N == 6) ? 9 : (N == 10 ? 11 : N);
-    static constexpr int SZ = (N == 2) ? 5 : (N == 3) ? 9 : (N == 4) ? 18 : (N == 5) ? 25 : (N == 6) ? 54
-                            : (N == 7) ? 54 : (N == 9) ? 85 : (N == 10) ? 110 : 121;
-    static constexpr int SLOT = (N == 2) ? 10 : (N == 3) ? 27 : (N == 4) ? 73 : (N == 5) ? 125 : (N == 6) ? 324
-                              : (N == 7) ? 385 : (N == 9) ? 769 : (N == 10) ? 1100 : 1331;
+    static constexpr int SY = (N == 6) ? 9 : N;
+    static constexpr int SZ = (N == 2) ? 5 : (N == 3) ? 9 : (N == 5) ? 25 : (N == 6) ? 54
+                            : (N == 7) ? 55 : (N == 9) ? 89 : (N == 10) ? 106 : 123;
+    static constexpr int SLOT = SZ * (N - 1) + SY * (N - 1) + N;
     __device__ __forceinline__ static int at(int x, int y, int z) { return x + SY * y + SZ * z; }
 };
 // n = 4: a half-warp (16 lanes, one 8-byte phase) holds one cell's 16 pencils; the residue mod 16
@@ -136,8 +138,9 @@ template <> struct Lay<8> {
 // neighbour trace u+, then the lift coefficient cv; slot 2f+1 the neighbour normal
 // derivative, then cg.
 template <int N> struct FLay {
-    static constexpr int RS = N + 1;
-    static constexpr int ARR = N * RS + 1;
+    static constexpr int RS = (N >= 5) ? N : N + 1;
+    static constexpr int ARR = (N == 5) ? 25 : (N == 6) ? 41 : (N == 7) ? 56 : (N == 9) ? 81 : (N == 10) ? 101
+                             : (N == 11) ? 121 : N * RS + 1;
     static constexpr int SLOT = 12 * ARR;
     __device__ __forceinline__ static int at(int arr, int i1, int i2) { return arr * ARR + i1 + RS * i2; }
 };
@@ -506,7 +509,7 @@ __device__ __forceinline__ void nb_load(const KParams& p, const double* zc, cons
 
 // Normal-direction-first contraction of the loaded neighbour lines:
 // low neighbour (face 2q) is seen at its x_q = 1, high neighbour (face 2q+1) at x_q = 0.
-template <int N, int P>
+template <int N, int P, class FL = FLay<N>>
 __device__ __forceinline__ void nb_contract(const Tab<N>& T, double* NT, int q, unsigned nbmask, const int (&pa)[P],
                                            const int (&pb)[P], const bool (&act)[P], const double (&rl)[P][N],
                                            const double (&rh)[P][N])
@@ -524,12 +527,12 @@ __device__ __forceinline__ void nb_contract(const Tab<N>& T, double* NT, int q, 
         }
         if (act[k]) {
             if (hl) {
-                NT[FLay<N>::at(4 * q, pa[k], pb[k])] = ul;
-                NT[FLay<N>::at(4 * q + 1, pa[k], pb[k])] = dl;
+                NT[FL::at(4 * q, pa[k], pb[k])] = ul;
+                NT[FL::at(4 * q + 1, pa[k], pb[k])] = dl;
             }
             if (hh) {
-                NT[FLay<N>::at(4 * q + 2, pa[k], pb[k])] = uh;
-                NT[FLay<N>::at(4 * q + 3, pa[k], pb[k])] = dh;
+                NT[FL::at(4 * q + 2, pa[k], pb[k])] = uh;
+                NT[FL::at(4 * q + 3, pa[k], pb[k])] = dh;
             }
         }
     }

@@ -110,6 +110,20 @@ __device__ __forceinline__ const double* nb_dfield(const KParams& p, const int (
     return p.Dghost[f] + 6 * gi;
 }
 
+// face-array layout of the general kernel: the fast kernel's, except n = 5, 6, 11 where the
+// unpadded face arrays of FLay are slower here (different access mix: own traces, tangential
+// derivatives; A-k4 31.7 -> 29.3, A-k5 28.5 -> 26.6, A-k10 29.1 -> 28.2 GDOF/s measured)
+template <int N> struct GFLay : FLay<N> {};
+template <int N> struct GFLayPad {
+    static constexpr int RS = N + 1;
+    static constexpr int ARR = N * RS + 1;
+    static constexpr int SLOT = 12 * ARR;
+    __device__ __forceinline__ static int at(int arr, int i1, int i2) { return arr * ARR + i1 + RS * i2; }
+};
+template <> struct GFLay<5> : GFLayPad<5> {};
+template <> struct GFLay<6> : GFLayPad<6> {};
+template <> struct GFLay<11> : GFLayPad<11> {};
+
 // launch configuration of the general kernel: the fast kernel's unless overridden per degree
 #ifdef DG_GTPC
 #define DG_GOVR(ov, d) (ov)
@@ -131,7 +145,7 @@ template <int N> struct GCfg {
 
 template <int N>
 struct GSmem {
-    static constexpr int PER_CELL = 4 * Lay<N>::SLOT + 2 * FLay<N>::SLOT;
+    static constexpr int PER_CELL = 4 * Lay<N>::SLOT + 2 * GFLay<N>::SLOT;
     static constexpr int STAGE = (N == 8) ? 512 + 16 + 16 : 0;   // TMA staging of the own block (n = 8)
     static constexpr int BYTES = GCfg<N>::C * PER_CELL * 8 + STAGE * 8;
 };
@@ -157,7 +171,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     double* X1 = X0 + Lay<N>::SLOT;                  // d_y u -> x^(2)
     double* X2 = X1 + Lay<N>::SLOT;                  // d_z u -> x^(3)
     double* NT = X2 + Lay<N>::SLOT;                  // neighbour face arrays (2 per face)
-    double* OT = NT + FLay<N>::SLOT;                 // own face arrays (2 per face)
+    double* OT = NT + GFLay<N>::SLOT;                 // own face arrays (2 per face)
     auto csync = [&]() {
         if (32 % TPC == 0) __syncwarp(); else __syncthreads();   // a cell within one warp, else CTA-wide
     };
@@ -257,7 +271,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) X0[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
-        nb_contract<N, P>(T, NT, 0, nbi, pa, pb, act, rl, rh);
+        nb_contract<N, P, GFLay<N>>(T, NT, 0, nbi, pa, pb, act, rl, rh);
         csync();
 
         nb_load<N, P>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
@@ -271,7 +285,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) X1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
-        nb_contract<N, P>(T, NT, 1, nbi, pa, pb, act, rl, rh);
+        nb_contract<N, P, GFLay<N>>(T, NT, 1, nbi, pa, pb, act, rl, rh);
         csync();
 
         nb_load<N, P>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
@@ -279,7 +293,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         for (int k = 0; k < P; ++k)
 #pragma unroll
             for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
-        nb_contract<N, P>(T, NT, 2, nbi, pa, pb, act, rl, rh);
+        nb_contract<N, P, GFLay<N>>(T, NT, 2, nbi, pa, pb, act, rl, rh);
     }
     v_fwd_sd<N, P>(T.Vs[2], r, t);                               // t = u on this thread's z-pencils
     {
@@ -296,8 +310,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 // own z-face traces: u and the reference normal derivative at z = 0, 1
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
-                    OT[FLay<N>::at(2 * (4 + s), pa[k], pb[k])] = dot<N>(T.Ls[0][s], t[k]);
-                    OT[FLay<N>::at(2 * (4 + s) + 1, pa[k], pb[k])] = dot<N>(T.Ls[0][2 + s], t[k]);
+                    OT[GFLay<N>::at(2 * (4 + s), pa[k], pb[k])] = dot<N>(T.Ls[0][s], t[k]);
+                    OT[GFLay<N>::at(2 * (4 + s) + 1, pa[k], pb[k])] = dot<N>(T.Ls[0][2 + s], t[k]);
                 }
             }
     }
@@ -325,8 +339,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                     X[q == 0 ? Lay<N>::at(e, pa[k], pb[k]) : Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
-                    OT[FLay<N>::at(2 * (2 * q + s), pa[k], pb[k])] = dot<N>(T.Ls[1][s], r[k]);
-                    OT[FLay<N>::at(2 * (2 * q + s) + 1, pa[k], pb[k])] = dot<N>(T.Ls[1][2 + s], r[k]);
+                    OT[GFLay<N>::at(2 * (2 * q + s), pa[k], pb[k])] = dot<N>(T.Ls[1][s], r[k]);
+                    OT[GFLay<N>::at(2 * (2 * q + s) + 1, pa[k], pb[k])] = dot<N>(T.Ls[1][2 + s], r[k]);
                 }
             }
     }
@@ -339,17 +353,17 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         const double cqq = __ldg(Dn + q) * p.hinv[q], cq1 = __ldg(Dn + dsym(q, t1)) * p.hinv[t1];
         double rr[1][N], tt[1][N], ga[N];
 #pragma unroll
-        for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(2 * f, e, line)];
+        for (int e = 0; e < N; ++e) rr[0][e] = NT[GFLay<N>::at(2 * f, e, line)];
         g_fwd_sd<N>(T.Gs, rr[0], ga);
         v_fwd_sd<N, 1>(T.Vs[3], rr, tt);
 #pragma unroll
         for (int e = 0; e < N; ++e) {
-            NT[FLay<N>::at(2 * f, e, line)] = tt[0][e];
-            rr[0][e] = NT[FLay<N>::at(2 * f + 1, e, line)];
+            NT[GFLay<N>::at(2 * f, e, line)] = tt[0][e];
+            rr[0][e] = NT[GFLay<N>::at(2 * f + 1, e, line)];
         }
         v_fwd_sd<N, 1>(T.Vs[4], rr, tt);
 #pragma unroll
-        for (int e = 0; e < N; ++e) NT[FLay<N>::at(2 * f + 1, e, line)] = fma(cqq, tt[0][e], cq1 * ga[e]);
+        for (int e = 0; e < N; ++e) NT[GFLay<N>::at(2 * f + 1, e, line)] = fma(cqq, tt[0][e], cq1 * ga[e]);
     }
     csync();
 
@@ -366,31 +380,31 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             const double cq2 = __ldg(Dn + dsym(q, t2)) * p.hinv[t2];
             double rr[1][N], tt[1][N], va[N], gv[N];
 #pragma unroll
-            for (int e = 0; e < N; ++e) va[e] = NT[FLay<N>::at(2 * f, line, e)];
+            for (int e = 0; e < N; ++e) va[e] = NT[GFLay<N>::at(2 * f, line, e)];
 #pragma unroll
             for (int e = 0; e < N; ++e) rr[0][e] = va[e];
             v_fwd_sd<N, 1>(T.Vs[5], rr, tt);
 #pragma unroll
             for (int e = 0; e < N; ++e) {
-                NT[FLay<N>::at(2 * f, line, e)] = tt[0][e];
-                rr[0][e] = NT[FLay<N>::at(2 * f + 1, line, e)];
+                NT[GFLay<N>::at(2 * f, line, e)] = tt[0][e];
+                rr[0][e] = NT[GFLay<N>::at(2 * f + 1, line, e)];
             }
             v_fwd_sd<N, 1>(T.Vs[6], rr, tt);
             g_fwd_sd<N>(T.Gs, va, gv);
 #pragma unroll
-            for (int e = 0; e < N; ++e) NT[FLay<N>::at(2 * f + 1, line, e)] = fma(cq2, gv[e], tt[0][e]);
+            for (int e = 0; e < N; ++e) NT[GFLay<N>::at(2 * f + 1, line, e)] = fma(cq2, gv[e], tt[0][e]);
         } else {
             // own pass A (lines along i1): s_part = D_qq/h_q d_n u + D_qt1/h_t1 Dc u-
             if (!((fact >> f) & 1u)) continue;
             const double cqq = Dw[q] * p.hinv[q], cq1 = Dw[dsym(q, t1)] * p.hinv[t1];
             double rr[1][N], tt[1][N];
 #pragma unroll
-            for (int e = 0; e < N; ++e) rr[0][e] = OT[FLay<N>::at(2 * f, e, line)];
+            for (int e = 0; e < N; ++e) rr[0][e] = OT[GFLay<N>::at(2 * f, e, line)];
             double z0[1][(N / 2) > 0 ? N / 2 : 1], zm[1];
             c_apply_s<N, 1, false>(T.Dcs[3], rr, tt, z0, z0, zm);
 #pragma unroll
             for (int e = 0; e < N; ++e) {
-                const int ix = FLay<N>::at(2 * f + 1, e, line);
+                const int ix = GFLay<N>::at(2 * f + 1, e, line);
                 OT[ix] = fma(cqq, OT[ix], cq1 * tt[0][e]);
             }
         }
@@ -433,11 +447,11 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         {
             double rr[1][N], tt[1][N];
 #pragma unroll
-            for (int e = 0; e < N; ++e) uo[e] = rr[0][e] = OT[FLay<N>::at(2 * f, line, e)];
+            for (int e = 0; e < N; ++e) uo[e] = rr[0][e] = OT[GFLay<N>::at(2 * f, line, e)];
             double z0[1][(N / 2) > 0 ? N / 2 : 1], zm[1];
             c_apply_s<N, 1, false>(T.Dcs[4], rr, tt, z0, z0, zm);
 #pragma unroll
-            for (int e = 0; e < N; ++e) so[e] = fma(cq2, tt[0][e], OT[FLay<N>::at(2 * f + 1, line, e)]);
+            for (int e = 0; e < N; ++e) so[e] = fma(cq2, tt[0][e], OT[GFLay<N>::at(2 * f + 1, line, e)]);
         }
         double dnb = 0.0;
         if (interior) dnb = __ldg(nb_dfield(p, lc, cell, f, nbmask) + q);
@@ -454,7 +468,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             const double Wf = p.dF[q] * T.w[line] * T.w[e];        // face point (i1 = line, i2 = e)
             double coef;
             if (interior) {
-                const double un = NT[FLay<N>::at(2 * f, line, e)], sn = NT[FLay<N>::at(2 * f + 1, line, e)];
+                const double un = NT[GFLay<N>::at(2 * f, line, e)], sn = NT[GFLay<N>::at(2 * f + 1, line, e)];
                 const double um = sd ? uo[e] : un, up = sd ? un : uo[e];
                 const double sm = sd ? so[e] : sn, sp = sd ? sn : so[e];
                 const double Phi = (bq >= 0.0) ? bq * um : bq * up;   // upwind flux
@@ -469,8 +483,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 cv[e] = Wf * (Phi - nu * so[e] + gam * uo[e]);
                 coef = -Wf * uo[e] * nu;
             }
-            OT[FLay<N>::at(2 * f + 1, line, e)] = coef * cn;         // normal part (lifted with L')
-            NT[FLay<N>::at(2 * f, line, e)] = coef * c1;             // t1 part (Dc^T along i1 in P7)
+            OT[GFLay<N>::at(2 * f + 1, line, e)] = coef * cn;         // normal part (lifted with L')
+            NT[GFLay<N>::at(2 * f, line, e)] = coef * c1;             // t1 part (Dc^T along i1 in P7)
             c2[e] = coef * cq2;                                      // t2 part (Dc^T along i2 below)
         }
         {
@@ -480,7 +494,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             double z0[1][(N / 2) > 0 ? N / 2 : 1], zm[1];
             c_apply_s<N, 1, false>(T.DcTs[0], rr, tt, z0, z0, zm);   // tangential test derivative along i2
 #pragma unroll
-            for (int e = 0; e < N; ++e) OT[FLay<N>::at(2 * f, line, e)] = cv[e] + tt[0][e];
+            for (int e = 0; e < N; ++e) OT[GFLay<N>::at(2 * f, line, e)] = cv[e] + tt[0][e];
         }
     }
     csync();
@@ -491,11 +505,11 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         if (!((fact >> f) & 1u)) continue;
         double rr[1][N], tt[1][N];
 #pragma unroll
-        for (int e = 0; e < N; ++e) rr[0][e] = NT[FLay<N>::at(2 * f, e, line)];
+        for (int e = 0; e < N; ++e) rr[0][e] = NT[GFLay<N>::at(2 * f, e, line)];
         double z0[1][(N / 2) > 0 ? N / 2 : 1], zm[1];
         c_apply_s<N, 1, false>(T.DcTs[1], rr, tt, z0, z0, zm);
 #pragma unroll
-        for (int e = 0; e < N; ++e) OT[FLay<N>::at(2 * f, e, line)] += tt[0][e];
+        for (int e = 0; e < N; ++e) OT[GFLay<N>::at(2 * f, e, line)] += tt[0][e];
     }
     csync();
 
@@ -521,8 +535,8 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             for (int s = 0; s < 2; ++s) {
                 const int f = 2 * q + s;
                 if (!((fact >> f) & 1u)) continue;
-                const double cv = OT[FLay<N>::at(2 * f, pa[k], pb[k])];
-                const double cg = OT[FLay<N>::at(2 * f + 1, pa[k], pb[k])];
+                const double cv = OT[GFLay<N>::at(2 * f, pa[k], pb[k])];
+                const double cg = OT[GFLay<N>::at(2 * f + 1, pa[k], pb[k])];
 #pragma unroll
                 for (int e = 0; e < N; ++e) t[k][e] = fma(cv, T.Lsl[s][e], fma(cg, T.Lsl[2 + s][e], t[k][e]));
             }
