@@ -18,8 +18,9 @@ import itertools
 
 CFG = {2: (8, 1, 16), 3: (16, 1, 8), 4: (16, 1, 4), 5: (32, 1, 1), 6: (36, 1, 4), 7: (64, 1, 1), 8: (64, 1, 1),
        9: (96, 1, 1), 10: (64, 2, 1), 11: (128, 1, 1)}
-GEN_LAY = {2: (2, 5, 10), 3: (3, 9, 27), 4: (4, 18, 73), 5: (5, 25, 125), 6: (9, 54, 324), 7: (7, 54, 385),
-           9: (9, 85, 769), 10: (11, 110, 1100), 11: (11, 121, 1331)}
+GEN_LAY = {2: (2, 5, 9), 3: (3, 9, 27), 5: (5, 25, 125), 6: (9, 54, 321), 7: (7, 55, 379),
+           9: (9, 89, 793), 10: (10, 106, 1054), 11: (11, 123, 1351)}
+GEN_FLAY = {5: (5, 25), 6: (6, 41), 7: (7, 56), 9: (9, 81), 10: (10, 101), 11: (11, 121)}
 
 
 def lay_source(n):
@@ -36,13 +37,16 @@ def flay_source(n):
         return (lambda a, i1, i2: 16 * a + (i1 ^ (a & 3)) + 4 * (i2 ^ (a & 3))), 12 * 16
     if n == 8:
         return (lambda a, i1, i2: 64 * a + 8 * (i2 ^ (a & 1)) + (i1 ^ ((i2 >> 1) | ((a & 1) << 2)))), 12 * 64
-    rs = n + 1
-    arr = n * rs + 1
+    rs, arr = GEN_FLAY.get(n, (n + 1, n * (n + 1) + 1))
     return (lambda a, i1, i2: a * arr + i1 + rs * i2), 12 * arr
 
 
-def accesses(n, tpc, p, c, lay, lslot, flay, fslot):
-    """Yield, per warp instruction, the list of (lane, word address) of the active lanes."""
+def accesses(n, tpc, p, c, lay, lslot, flay, fslot, pw=None, tw=None):
+    """Yield, per warp instruction, the list of (lane, word address) of the active lanes.
+    pw: width of the pencil grid (pencil pc = a + pw b; lanes with a or b >= n idle), tw: lines per
+    face array in the tangential-stage lane mapping (both n by default, as in the kernel)."""
+    pw = pw or n
+    tw = tw or n
     per_cell = 2 * lslot + fslot
     threads = c * tpc
     warps = (threads + 31) // 32
@@ -66,9 +70,9 @@ def accesses(n, tpc, p, c, lay, lslot, flay, fslot):
                 acc = []
                 for l, slot, lane in info:
                     pc = lane + k * tpc
-                    if pc >= nn:
+                    pa, pb = pc % pw, pc // pw
+                    if pa >= n or pb >= n:
                         continue
-                    pa, pb = pc % n, pc // n
                     acc.append((l, slot * per_cell + base_of + lay(*coords(e, pa, pb))))
                 yield acc
 
@@ -78,23 +82,25 @@ def accesses(n, tpc, p, c, lay, lslot, flay, fslot):
             acc = []
             for l, slot, lane in info:
                 pc = lane + k * tpc
-                if pc >= nn:
+                pa, pb = pc % pw, pc // pw
+                if pa >= n or pb >= n:
                     continue
-                pa, pb = pc % n, pc // n
                 acc.append((l, slot * per_cell + 2 * lslot + flay(arr, pa, pb)))
             yield acc
 
     def tangential_acc(w, q, dim):
         info = lanes_info(w)
-        rounds = (4 * n + tpc - 1) // tpc
+        rounds = (4 * tw + tpc - 1) // tpc
         for rr in range(rounds):
             for e in range(n):
                 acc = []
                 for l, slot, lane in info:
                     tk = lane + rr * tpc
-                    if tk >= 4 * n:
+                    if tk >= 4 * tw:
                         continue
-                    arr, line = 4 * q + tk // n, tk % n
+                    arr, line = 4 * q + tk // tw, tk % tw
+                    if line >= n:
+                        continue
                     a = flay(arr, e, line) if dim == 0 else flay(arr, line, e)
                     acc.append((l, slot * per_cell + 2 * lslot + a))
                 yield acc   # read
@@ -157,9 +163,9 @@ def wavefronts(acc):
     return tot, ideal
 
 
-def evaluate(n, tpc, p, c, lay, lslot, flay, fslot):
+def evaluate(n, tpc, p, c, lay, lslot, flay, fslot, pw=None, tw=None):
     tot = ideal = 0
-    for acc in accesses(n, tpc, p, c, lay, lslot, flay, fslot):
+    for acc in accesses(n, tpc, p, c, lay, lslot, flay, fslot, pw, tw):
         t, i = wavefronts(acc)
         tot += t
         ideal += i
