@@ -54,11 +54,19 @@ template <int N, int M> struct VLay {
     static constexpr int SLOT = M * SZ;
     __device__ __forceinline__ static int at(int x, int y, int z) { return x + SY * y + SZ * z; }
 };
+// m = 4, 8: the fast kernel's XOR swizzles (dg_cell.cuh Lay / FLay), defined on the whole m^3
+// box, so the mixed modal / point shapes of the forward stages index them too (n <= m). With the
+// padded linear layout the m = 8 roles' x-pencil reads were 8-way bank conflicts (ncu TG-k5:
+// 49 % of the shared-memory wavefronts were conflicts).
+template <int N> struct VLay<N, 8> : Lay<8> {};
+template <int N> struct VLay<N, 4> : Lay<4> {};
 template <int M> struct VFL {                               // 12 face arrays of m x m (+1 pad)
     static constexpr int FS = M * M + 1;
     static constexpr int SLOT = 12 * FS;
     __device__ __forceinline__ static int at(int arr, int i1, int i2) { return arr * FS + i1 + M * i2; }
 };
+template <> struct VFL<8> : FLay<8> {};
+template <> struct VFL<4> : FLay<4> {};
 template <int N, int M> struct VSmem {
     static constexpr int BT = 3 * 4 * (M + 2);               // 1D velocity tables: [dir][fn][point]
     static constexpr int PER_CELL = 2 * VLay<N, M>::SLOT + VFL<M>::SLOT + BT;
