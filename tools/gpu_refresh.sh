@@ -10,3 +10,4 @@ ncu --set full --clock-control none --import-source on -k regex:dg_reg_kernel -s
 python tools/sweep.py --out gpurun_out/sweep.json > gpurun_out/sweep.log 2>&1; echo "sweep rc=$?"
 for k in 1 2 3 4 5 6 7 8 9 10; do echo "a-k$k $(python tools/quick_time.py a-k$k 5 | tail -1)"; done | tee gpurun_out/problemA.log
 python tools/matrix_based.py --big --out gpurun_out/matrix_based.json > gpurun_out/matrix.log 2>&1; echo "matrix rc=$?"
+for k in 1 2 3 4 5 6 7 8; do echo "tg-k$k $(python tools/quick_time.py tg-k$k 3 | tail -1)"; done | tee gpurun_out/tg.log
