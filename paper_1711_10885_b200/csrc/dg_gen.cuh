@@ -146,9 +146,8 @@ template <int N> struct GCfg {
 template <int N>
 struct GSmem {
     static constexpr int PER_CELL = 4 * Lay<N>::SLOT + 2 * GFLay<N>::SLOT;
-    // n = 8: the own block is TMA-staged in A0 (free until P3) and y leaves through A0 as well,
-    // so no separate staging area: 28.7 instead of 33 KB per CTA, 7 instead of 6 CTAs per SM
-    static constexpr int BYTES = GCfg<N>::C * PER_CELL * 8;
+    static constexpr int STAGE = (N == 8) ? 512 + 16 + 16 : 0;   // TMA staging of the own block (n = 8)
+    static constexpr int BYTES = GCfg<N>::C * PER_CELL * 8 + STAGE * 8;
 };
 
 template <int N>
@@ -161,7 +160,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     constexpr int TPC = GCfg<N>::TPC, P = GCfg<N>::P, C = GCfg<N>::C;
     constexpr int NN = N * N;
     static_assert(TPC * P >= NN, "pencil slots");
-    extern __shared__ __align__(1024) double smem[];
+    extern __shared__ double smem[];
     const Tab<N>& T = g_tab;
 
     const int tid = threadIdx.x;
@@ -223,15 +222,14 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     }
 
     double r[P][N], t[P][N];
-    // TMA staging (n = 8): own block in A0 (free until P3; 1024-byte aligned as the first array of
-    // the CTA's shared memory), the local x-neighbours' blocks in X1, X2 (free in P1), the
-    // mbarrier in OT (first written in P3, after several barriers)
+    // TMA staging (n = 8): own block (STG) and the local x-neighbours' blocks (X1, X2: free in P1)
     double* STG = nullptr;
     bool tma_x = false;
     if constexpr (N == 8 && C == 1) {
         if (p.tma) {
-            STG = A0;
-            tma_x = tma::stage_x(p, STG, X1, X2, tid, lc, cell, nbi, OT);
+            STG = reinterpret_cast<double*>(
+                (reinterpret_cast<uintptr_t>(smem + GSmem<N>::PER_CELL) + 127) & ~(uintptr_t)127);
+            tma_x = tma::stage_x(p, STG, X1, X2, tid, lc, cell, nbi);
         }
     }
     // ---------------------------------------------------------------- P1-P3: u at the Gauss points
@@ -583,7 +581,6 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     v_bwd_sd<N, P>(T.Vh[11], r, t);
     if constexpr (N == 8 && C == 1) {
         if (STG && p.tma == 2 && p.epi == 0) {   // y through the staging block and one TMA store
-            csync();                             // every thread has read its A0 x-pencils
 #pragma unroll
             for (int k = 0; k < P; ++k) {
                 const int L = pa[k] + N * pb[k];

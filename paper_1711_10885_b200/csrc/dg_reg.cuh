@@ -94,8 +94,18 @@ __device__ __forceinline__ const double* reg_nb(const KParams& p, const double* 
     const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
                                                                         : (lc[0] + p.nloc[0] * lc[1]);
     const int64_t wst = (int64_t)(nq - 1) * st * n3;
-    if (s == 0) return (lq > 0) ? zc - st * n3 : (p.wrap[q] ? zc + wst : p.ghost[2 * q] + gi * n3);
-    return (lq + 1 < nq) ? zc + st * n3 : (p.wrap[q] ? zc - wst : p.ghost[2 * q + 1] + gi * n3);
+    const bool local = s == 0 ? (lq > 0 || p.wrap[q]) : (lq + 1 < nq || p.wrap[q]);
+    const double* zn = s == 0 ? ((lq > 0) ? zc - st * n3 : (p.wrap[q] ? zc + wst : p.ghost[2 * q] + gi * n3))
+                              : ((lq + 1 < nq) ? zc + st * n3 : (p.wrap[q] ? zc - wst : p.ghost[2 * q + 1] + gi * n3));
+#ifdef DG_CHECK
+    {
+        const int64_t nall = p.nloc[0] * p.nloc[1] * p.nloc[2] * n3;
+        if (local) DG_ASSERT(zn >= p.z && zn + n3 <= p.z + nall);
+        else DG_ASSERT(p.ghost[2 * q + s] != nullptr);
+    }
+#endif
+    (void)local;
+    return zn;
 }
 
 template <int N>
