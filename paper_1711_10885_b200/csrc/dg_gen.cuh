@@ -152,7 +152,7 @@ struct GSmem {
 
 template <int N>
 #ifndef DG_GMB
-#define DG_GMB 1
+#define DG_GMB ((DG_N) == 4 ? 12 : 1)   // minimum CTAs per SM (n = 4: 80 registers, A-k3 30.5 -> 31.0)
 #endif
 __global__ void __launch_bounds__(GCfg<N>::C * GCfg<N>::TPC, DG_GMB)
 dg_gen_kernel(const __grid_constant__ KParams p)
