@@ -130,13 +130,14 @@ template <> struct GFLay<11> : GFLayPad<11> {};
 #else
 #define DG_GOVR(ov, d) (d)
 #endif
-// (one pencil per thread is better than the fast kernel's 2 for n = 10: A-k9 19.5 -> 27.5 GDOF/s;
+// (one pencil per thread is better than the fast kernel's 2 for n = 9, 10: A-k8 14.7 -> 31.4,
+// A-k9 19.5 -> 27.5 GDOF/s;
 // n = 6: 36 threads per cell (every thread a pencil), 2 cells per CTA straddling warps: A-k5
 // 26.6 -> 28.5; measured with tools/variant.py)
 template <int N> struct GCfgD {
-    static constexpr int TPC = (N == 6) ? 36 : (N == 10) ? 128 : Cfg<N>::TPC;
-    static constexpr int P = (N == 6 || N == 10) ? 1 : Cfg<N>::P;
-    static constexpr int C = (N == 6) ? 2 : (N == 10) ? 1 : Cfg<N>::C;
+    static constexpr int TPC = (N == 6) ? 36 : (N == 9) ? 96 : (N == 10) ? 128 : Cfg<N>::TPC;
+    static constexpr int P = (N == 6 || N == 9 || N == 10) ? 1 : Cfg<N>::P;
+    static constexpr int C = (N == 6) ? 2 : (N == 9 || N == 10) ? 1 : Cfg<N>::C;
 };
 template <int N> struct GCfg {
     static constexpr int TPC = DG_GOVR(DG_GTPC, GCfgD<N>::TPC), P = DG_GOVR(DG_GP, GCfgD<N>::P),
