@@ -123,6 +123,17 @@ template <int N> struct GFLayPad {
 template <> struct GFLay<5> : GFLayPad<5> {};
 template <> struct GFLay<6> : GFLayPad<6> {};
 template <> struct GFLay<11> : GFLayPad<11> {};
+// n = 4: the face passes give one lane per line of faces f .. f + 3 on arrays 2f (+1): swizzle by
+// the face index (arr >> 1) instead of the array index, so those 4 arrays take 4 different
+// swizzles (with FLay<4>'s arr & 3, arrays 2f and 2f + 4 collided: ncu A-k3 24 % conflicts)
+template <> struct GFLay<4> {
+    static constexpr int SLOT = 12 * 16;
+    __device__ __forceinline__ static int at(int arr, int i1, int i2)
+    {
+        const int s = (arr >> 1) & 3;
+        return 16 * arr + (i1 ^ s) + 4 * (i2 ^ s);
+    }
+};
 
 // launch configuration of the general kernel: the fast kernel's unless overridden per degree
 #ifdef DG_GTPC
