@@ -120,8 +120,20 @@ template <int N> struct GFLayPad {
     static constexpr int SLOT = 12 * ARR;
     __device__ __forceinline__ static int at(int arr, int i1, int i2) { return arr * ARR + i1 + RS * i2; }
 };
-template <> struct GFLay<5> : GFLayPad<5> {};
 template <> struct GFLay<6> : GFLayPad<6> {};
+// n = 7: i1 rotated by the face index (arr >> 1): the face passes' lines of consecutive faces
+// land on different banks (bank-conflict model over those passes: 224 -> 134 wavefronts per
+// cell; A-k6 27.8 -> 28.6 GDOF/s; the same idea measured slower at n = 5, 9 and neutral at 11,
+// where the runtime mod costs more than the conflicts)
+template <int N, int ARR, int CR> struct GFLayRot {
+    static constexpr int SLOT = 12 * ARR;
+    __device__ __forceinline__ static int at(int arr, int i1, int i2)
+    {
+        return arr * ARR + (i1 + CR * (arr >> 1)) % N + N * i2;
+    }
+};
+template <> struct GFLay<7> : GFLayRot<7, 49, 6> {};
+template <> struct GFLay<5> : GFLayPad<5> {};
 template <> struct GFLay<11> : GFLayPad<11> {};
 // n = 4: the face passes give one lane per line of faces f .. f + 3 on arrays 2f (+1): swizzle by
 // the face index (arr >> 1) instead of the array index, so those 4 arrays take 4 different
