@@ -294,13 +294,13 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
     }
 }
 
-#ifdef DG_RMINB
-#define DG_REG_BOUNDS __launch_bounds__(128, DG_RMINB)
-#else
-#define DG_REG_BOUNDS __launch_bounds__(128)
+// minimum CTAs per SM: n = 2 with constant D at 5 (96 registers: C4-k1 83.3 -> 84.7 GDOF/s; the
+// general variant measured slower so)
+#ifndef DG_RMINB
+#define DG_RMINB(n, gen) ((n) == 2 && !(gen) ? 5 : 1)
 #endif
 template <int N, bool GEN>
-__global__ void DG_REG_BOUNDS dg_reg_kernel(const __grid_constant__ KParams p)
+__global__ void __launch_bounds__(128, DG_RMINB(N, GEN)) dg_reg_kernel(const __grid_constant__ KParams p)
 {
     constexpr int N3 = N * N * N;
     const RTab<N>& R = g_rtab;
