@@ -129,3 +129,32 @@ def test_partitioned_periodic_percell_equals_single_bitwise(k, ncells, parts, pe
         ys = run_single(cfg, terms, periodic, Dc)
         yp = run_partitioned(cfg, parts, terms, periodic, Dc)
         assert np.array_equal(yp, ys)
+
+
+@pytest.mark.parametrize("seed", list(range(30)))
+def test_random_partitions_equal_single_bitwise(seed):
+    """Seeded random partitions (1-2 ranks per direction, 1-3 cells per rank and direction),
+    periodic sides, per-cell tensors and degrees: the partitioned result equals the single-rank
+    one bit for bit (partition invariance)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rng = np.random.default_rng(500 + seed)
+    while True:
+        parts = tuple(int(v) for v in rng.integers(1, 3, size=3))
+        if parts[0] * parts[1] * parts[2] >= 2:
+            break
+    ncells = tuple(parts[q] * int(rng.integers(1, 4)) for q in range(3))
+    k = int(rng.integers(1, 11))
+    if k >= 8:
+        ncells = tuple(min(v, 2 * parts[q]) for q, v in enumerate(ncells))
+    periodic = tuple(int(v) for v in rng.integers(0, 2, size=3))
+    percell = bool(rng.integers(0, 2))
+    cfg = configs.small(k, ncells=ncells, hi=(1.5, 1.0, 0.75), b=tuple(rng.uniform(-1, 1, size=3)), c=0.3)
+    Dc = None
+    if percell:
+        M = rng.normal(size=(cfg.ncells[0] * cfg.ncells[1] * cfg.ncells[2], 3, 3))
+        Dc = np.einsum("eij,ekj->eik", M, M) + 0.5 * np.eye(3)[None]
+    terms = int(rng.choice([7, 7, 2]))
+    ys = run_single(cfg, terms, periodic, Dc)
+    yp = run_partitioned(cfg, parts, terms, periodic, Dc)
+    assert np.array_equal(yp, ys), (k, ncells, parts, periodic, percell, terms)
