@@ -118,3 +118,36 @@ def test_affine_ssp_mass_matrix():
     torch.cuda.synchronize()
     op.close()
     assert rel(out.cpu().numpy(), z.cpu().numpy() * (1 - c * dt)) < 1e-14
+
+
+@pytest.mark.parametrize("seed", list(range(15)))
+def test_random_affine_vs_o2(seed):
+    """Seeded random orientation-preserving affine maps, meshes, boundary kinds and coefficients
+    (k <= 3, O-2 assembled on the physical mesh)."""
+    rng = np.random.default_rng(900 + seed)
+    k = int(rng.integers(1, 4))
+    nc = tuple(int(v) for v in rng.integers(1, 4, size=3))
+    lo = (0.0, 0.0, 0.0)
+    hi = tuple(float(v) for v in rng.uniform(0.5, 1.5, size=3))
+    while True:
+        J = np.eye(3) + 0.4 * rng.normal(size=(3, 3))
+        if np.linalg.det(J) > 0.2:
+            break
+    M = rng.normal(size=(3, 3))
+    D = M @ M.T + 0.3 * np.eye(3)
+    b = tuple(float(v) for v in rng.uniform(-1, 1, size=3))
+    c = float(rng.uniform(0, 1))
+    periodic = tuple(int(v) for v in rng.integers(0, 2, size=3))
+    sigma = 3.0 * k * (k + 2) / min((hi[q] - lo[q]) / nc[q] for q in range(3))
+    from paper_1711_10885_b200 import dg
+    op = dg.Operator(nc, lo, hi, k, D.ravel(), b, c, sigma, bc=dg.bc_from_periodic(periodic))
+    op.set_affine(J.ravel())
+    n = nc[0] * nc[1] * nc[2] * (k + 1) ** 3
+    z = inputs.uniform(n, 40 + seed)
+    zt = torch.from_numpy(z).cuda()
+    y = torch.full_like(zt, float("nan"))
+    op.apply(zt, y)
+    torch.cuda.synchronize()
+    op.close()
+    A = o2.assemble(nc, lo, hi, k, D, b, c, sigma, periodic=periodic, J=J)
+    assert rel(y.cpu().numpy(), A @ z) < TOL, (k, nc, periodic)
