@@ -80,3 +80,39 @@ def test_random_case_vs_o1(seed):
         assert np.abs(yg).max() == 0.0
     else:
         assert np.abs(yg - yref).max() / scale < TOL, (k, nc, periodic, kindD, velocity, m, mask)
+
+
+@pytest.mark.parametrize("seed", list(range(40)))
+def test_random_epilogues_vs_o1(seed):
+    """The fused store epilogues on random cases: dg_residual r = f - A z and the SSP-RK stage
+    out = a w + b (z + dt / Delta_T (f - A z)), from O-1's A z."""
+    from paper_1711_10885_b200 import dg
+    k, nc, lo, hi, periodic, kindD, D, b, c, velocity, m, mask, rng = case(5000 + seed)
+    h = [(hi[q] - lo[q]) / nc[q] for q in range(3)]
+    sigma = configs.sigma_for(k, min(h))
+    ncell = nc[0] * nc[1] * nc[2]
+    op = dg.Operator(nc, lo, hi, k, D.ravel(), b, c, sigma, bc=dg.bc_from_periodic(periodic))
+    Dcell = None
+    if kindD == 2:
+        Dcell = np.stack([spd(rng) for _ in range(ncell)])
+        op.set_diffusion(torch.from_numpy(np.ascontiguousarray(Dcell).reshape(-1)).cuda())
+    if velocity:
+        op.set_velocity(2)
+        op.set_quadrature(m)
+    n = ncell * (k + 1) ** 3
+    z, f, w = inputs.uniform(n, 1 + seed), inputs.uniform(n, 2 + seed), inputs.uniform(n, 3 + seed)
+    zt, ft, wt = (torch.from_numpy(v).cuda() for v in (z, f, w))
+    r = torch.full_like(zt, float("nan"))
+    op.residual(zt, ft, r)
+    dt, a_, b_ = 1e-3 * float(rng.uniform(0.5, 2)), float(rng.uniform(0, 1)), float(rng.uniform(0.5, 1))
+    out = torch.full_like(zt, float("nan"))
+    op.ssp_stage(zt, out, dt, f=ft, w=wt, a=a_, b=b_)
+    torch.cuda.synchronize()
+    op.close()
+    Az, _ = o1.apply(nc, lo, hi, k, D.ravel(), b, c, sigma, z, periodic=periodic, Dcell=Dcell, m=m,
+                     bkind=2 if velocity else 0)
+    rref = f - Az
+    assert np.abs(r.cpu().numpy() - rref).max() <= TOL * np.abs(Az).max() + 1e-15
+    dT = h[0] * h[1] * h[2]
+    oref = a_ * w + b_ * (z + dt / dT * rref)
+    assert np.abs(out.cpu().numpy() - oref).max() <= TOL * b_ * dt / dT * np.abs(Az).max() + 1e-14
