@@ -176,7 +176,7 @@ struct GSmem {
 
 template <int N>
 #ifndef DG_GMB
-#define DG_GMB ((DG_N) == 4 ? 12 : 1)   // minimum CTAs per SM (n = 4: 80 registers, A-k3 30.5 -> 31.0)
+#define DG_GMB ((DG_N) == 4 ? 12 : (DG_N) == 10 ? 5 : 1)   // min CTAs per SM (n = 4: A-k3 30.5 -> 31.0; n = 10: A-k9 29.7 -> 31.0)
 #endif
 __global__ void __launch_bounds__(GCfg<N>::C * GCfg<N>::TPC, DG_GMB)
 dg_gen_kernel(const __grid_constant__ KParams p)
