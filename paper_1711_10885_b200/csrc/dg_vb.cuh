@@ -162,7 +162,16 @@ __device__ __forceinline__ Flux vflux_boundary(const KParams& p, int q, int s, d
 }
 
 template <int N, int M>
-__global__ void __launch_bounds__(VCfg<M>::TPC)
+// minimum CTAs per SM: (n, m) = (4, 6) at 8 (TG-k3 17.5 -> 18.4 GDOF/s); elsewhere the
+// compiler's choice (an explicit minimum of 1 already changed the allocation for the worse)
+#if defined(DG_VMB)
+#define DG_VB_BOUNDS __launch_bounds__(VCfg<M>::TPC, DG_VMB)
+#elif DG_N == 4 && DG_M == 6
+#define DG_VB_BOUNDS __launch_bounds__(VCfg<M>::TPC, 8)
+#else
+#define DG_VB_BOUNDS __launch_bounds__(VCfg<M>::TPC)
+#endif
+__global__ void DG_VB_BOUNDS
 dg_vb_kernel(const KParams p)
 {
     constexpr int TPC = VCfg<M>::CW;                   // stride of the per-cell loops below
