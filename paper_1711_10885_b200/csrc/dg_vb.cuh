@@ -162,12 +162,16 @@ __device__ __forceinline__ Flux vflux_boundary(const KParams& p, int q, int s, d
 }
 
 template <int N, int M>
-// minimum CTAs per SM: (n, m) = (4, 6) at 8 (TG-k3 17.5 -> 18.4 GDOF/s); elsewhere the
-// compiler's choice (an explicit minimum of 1 already changed the allocation for the worse)
+// minimum CTAs per SM, measured per (n, m) of the Taylor-Green runs (q = 2p + 4): (3, 5) 8
+// (TG-k2 13.3 -> 13.6 GDOF/s), (4, 6) 8 (k3 17.5 -> 18.4), (5, 7) 6 (k4 19.2 -> 19.5), (7, 9) 6
+// (k6 25.8 -> 27.3); elsewhere the compiler's choice (an explicit minimum of 1 already changed
+// the allocation for the worse)
 #if defined(DG_VMB)
 #define DG_VB_BOUNDS __launch_bounds__(VCfg<M>::TPC, DG_VMB)
-#elif DG_N == 4 && DG_M == 6
+#elif (DG_N == 3 && DG_M == 5) || (DG_N == 4 && DG_M == 6)
 #define DG_VB_BOUNDS __launch_bounds__(VCfg<M>::TPC, 8)
+#elif (DG_N == 5 && DG_M == 7) || (DG_N == 7 && DG_M == 9)
+#define DG_VB_BOUNDS __launch_bounds__(VCfg<M>::TPC, 6)
 #else
 #define DG_VB_BOUNDS __launch_bounds__(VCfg<M>::TPC)
 #endif
