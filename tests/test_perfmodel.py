@@ -24,3 +24,23 @@ def test_crossover_degree():
 
 def test_fp64_peak():
     assert abs(pm.fp64_peak_tflops() - 37.22) < 0.01
+
+
+def test_table1_columns_and_matrix_bytes():
+    """Table 1's matrix-based columns: the paper's 'A / matrix
+    based' ratio at p = 7 is 390x; the block-stencil matvec moves 7 n^3 matrix entries per row
+    (leading dimension padded to even) plus z and y."""
+    assert abs(pm.PAPER_TABLE1_A_MDOFS[7] / pm.PAPER_TABLE1_MATRIX_MDOFS[7] - 390.0) < 0.5
+    assert pm.matrix_bytes_per_dof(7) == 8 * 7 * 512 + 16
+    assert pm.matrix_bytes_per_dof(2) == 8 * 7 * 28 + 16      # n^3 = 27 -> ld 28
+
+
+def test_matrix_meshes_fit_and_use_27_colour_classes():
+    from paper_1711_10885_b200 import configs
+    for k in range(1, 11):
+        cfg = configs.problem_a_matrix(k)
+        N = cfg.ncells[0]
+        n3 = (k + 1) ** 3
+        assert N % 3 == 0 and cfg.ncells == (N, N, N)
+        assert cfg.ndofs * 7 * (n3 + (n3 & 1)) * 8 <= 24e9
+        assert cfg.periodic == (1, 1, 1) and cfg.dfield_seed >= 0
