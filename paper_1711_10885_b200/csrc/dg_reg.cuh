@@ -294,10 +294,10 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
     }
 }
 
-// minimum CTAs per SM: n = 2 with constant D at 5 (96 registers: C4-k1 83.3 -> 84.7 GDOF/s; the
-// general variant measured slower so)
+// minimum CTAs per SM: n = 2 at 5 with constant D (96 registers: C4-k1 83.3 -> 84.7 GDOF/s) and
+// at 4 with tensors (128 registers, a few spills instead of 150: Problem A k = 1 47.2 -> 50.9)
 #ifndef DG_RMINB
-#define DG_RMINB(n, gen) ((n) == 2 && !(gen) ? 5 : 1)
+#define DG_RMINB(n, gen) ((n) == 2 ? ((gen) ? 4 : 5) : 1)
 #endif
 template <int N, bool GEN>
 __global__ void __launch_bounds__(128, DG_RMINB(N, GEN)) dg_reg_kernel(const __grid_constant__ KParams p)
