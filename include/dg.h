@@ -22,8 +22,9 @@
  *   - all six box sides weak Dirichlet with g = 0 inside A             (C-9, C-10)
  *
  * Vectors are caller-owned DEVICE pointers to FP64 arrays of dg_local_layout()
- * ndofs entries (unless stated otherwise). The library never allocates or
- * frees them. z must not alias y, r or f. y / r are fully overwritten.
+ * ndofs entries (unless stated otherwise), 16-byte aligned (the kernels move x-lines with
+ * 16-byte vector accesses and TMA; a misaligned pointer returns DG_EINVAL). The library never
+ * allocates or frees them. z must not alias y, r or f. y / r are fully overwritten.
  *
  * Every call returns an int status (DG_OK = 0 or a negative DG_E* code); no
  * C++ exception crosses the ABI. dg_apply* / dg_residual are enqueued on the
@@ -76,10 +77,14 @@ enum { DG_BC_DIRICHLET = 0, DG_BC_PERIODIC = 1 };
  *          constant-coefficient kernel; a full D (off-diagonal entries, PAPER.md:202-205, :436;
  *          reading C-16) on the general-coefficient kernel (dg_set_diffusion)
  *   b      constant velocity (div b = 0), c reaction coefficient, sigma >= 0 penalty factor
- *   nccl_unique_id  128-byte ncclUniqueId broadcast by the caller; NULL iff nranks == 1
- *                   or iff the caller drives the halo itself (DG_HALO_EXTERNAL)
- * Errors: DG_EINVAL (k, mesh, D not symmetric / negative diagonal, sigma < 0, parts, periodic
- *         on one side of a direction only), DG_EUNSUPPORTED (unknown bc),
+ *   nccl_unique_id  128-byte ncclUniqueId broadcast by the caller (halo over NCCL, one process
+ *                   per GPU), or an id from dg_fabric_id shared by the ranks as THREADS of one
+ *                   process (the in-process fabric: same exchange semantics, stream-ordered
+ *                   copies; single-GPU tests of the partitioned path); NULL iff nranks == 1 or
+ *                   iff the caller drives the halo itself (DG_HALO_EXTERNAL)
+ * Errors: DG_EINVAL (k, mesh, D not symmetric positive semi-definite -- all principal minors of
+ *         D / max|D_ij| >= -1e-13 --, sigma < 0, parts, periodic on one side of a direction
+ *         only), DG_EUNSUPPORTED (unknown bc),
  *         DG_ECUDA, DG_ENCCL, DG_ENOMEM.
  * Not timed; uploads tables and allocates the halo buffers.
  */
@@ -199,14 +204,21 @@ int dg_matrix_apply(dg_ctx* ctx, const double* A, const double* z, double* y, vo
 
 /* ---- halo plumbing (multi-rank; also used by the single-process loopback test) ----
  * face f = 2q + s (q = direction, s = 0 low / 1 high side of this rank's box).
- * neighbor_rank = -1 when the face lies on the domain boundary. count = doubles in the
- * layer (cells of the face layer x n^3). */
+ * neighbor_rank = -1 when the face lies on the domain boundary. The halo is the face traces of
+ * for every cell of the face layer, the normal-first
+ * contraction of its block u(a,b) = sum_e theta_e(s) z(e; a,b) and
+ * d(a,b) = sum_e theta'_e(s) z(e; a,b) over the tangential modal indices (a along the lower
+ * tangential direction t1, b along t2): [cell t1 + N_t1 t2][u | d][a + n b], 2 n^2 doubles per
+ * cell (1/4 of the block at k = 7); the receiving rank runs the tangential stages.
+ * count = doubles per face = cells of the face layer x 2 n^2. */
 int dg_halo_info(const dg_ctx* ctx, int face, int* neighbor_rank, int64_t* count);
 /* which = 0: send buffer (this rank's own boundary layer, filled by dg_halo_pack),
    which = 1: receive buffer (the neighbour's layer adjacent to this face, read by the kernel),
    which = 2 / 3: the same for the per-cell diffusion field (6 doubles per layer cell;
    count / n^3 * 6 doubles; allocated by dg_set_diffusion, NULL before). */
 int dg_halo_buffer(dg_ctx* ctx, int face, int which, double** ptr);
+/* Fill the send buffers (which = 0) with the face traces of z (the kernel dg_apply runs on its
+   comm stream before the exchange). */
 int dg_halo_pack(dg_ctx* ctx, const double* z, void* stream);
 
 /* ---- seeded inputs (reading C-13; identical to paper_1711_10885_b200/inputs.py) ----
@@ -222,6 +234,11 @@ int dg_fill_uniform_cells(dg_ctx* ctx, double* dst, int per_cell, uint64_t seed,
 
 /* Create a 128-byte ncclUniqueId (rank 0 calls this and broadcasts it). */
 int dg_nccl_unique_id(void* out128);
+/* Create a 128-byte id of an in-process fabric group: pass the same id to dg_setup of every
+   rank (threads of this process, one context each; each rank's applies on its own thread).
+   A rank's exchange blocks its thread until its neighbours reach the same exchange (120 s
+   timeout -> DG_ENCCL). */
+int dg_fabric_id(void* out128);
 
 /* Library / kernel facts for the harness: kernel launches per dg_apply, threads and
    cells per CTA, dynamic shared memory per CTA, registers per thread, of the kernel the

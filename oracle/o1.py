@@ -47,7 +47,21 @@ def lib():
                                   ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int]
         _lib.o1_tables.restype = ctypes.c_int
         _lib.o1_tables.argtypes = [ctypes.c_int] + [ctypes.c_void_p] * 8
+        _lib.o1_velocity_at.restype = ctypes.c_int
+        _lib.o1_velocity_at.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_int64]
     return _lib
+
+
+def velocity(bkind, x, bamp=(1.0, 1.0, 1.0)):
+    """The velocity field O-1 evaluates at its quadrature points (bkind as in apply) at points
+    x of shape (npts, 3); returns b of shape (npts, 3)."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1, 3))
+    b = np.zeros_like(x)
+    amp = np.ascontiguousarray(bamp, dtype=np.float64)
+    if lib().o1_velocity_at(int(bkind), amp.ctypes.data, x.ctypes.data, b.ctypes.data, x.shape[0]) != 0:
+        raise ValueError("o1_velocity_at: bad kind %d" % bkind)
+    return b
 
 
 def _problem(ncells, lo, hi, k, D, b, c, sigma, periodic=(0, 0, 0), Dcell=None, m=0, bkind=0, bamp=(1.0, 1.0, 1.0)):

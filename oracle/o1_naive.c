@@ -143,6 +143,20 @@ int o1_tables(int k, double* xi, double* w, double* theta_at, double* dtheta_at,
     return 0;
 }
 
+/* Exported so tests can pin the velocity field O-1 evaluates at its quadrature points
+ * (o1_velocity above; eq:2) against hand values and div b = 0.
+ * x: npts points (x1, x2, x3) interleaved; b: npts velocities, same layout. */
+int o1_velocity_at(int bkind, const double* bamp, const double* x, double* b, int64_t npts)
+{
+    if (bkind < 0 || bkind > 2 || npts < 0) return -1;
+    o1_problem P;
+    memset(&P, 0, sizeof(P));
+    P.bkind = bkind;
+    for (int r = 0; r < 3; ++r) P.bamp[r] = bamp ? bamp[r] : 1.0;
+    for (int64_t i = 0; i < npts; ++i) o1_velocity(&P, x + 3 * i, b + 3 * i);
+    return 0;
+}
+
 typedef struct {
     int n, m;
     double h[3];

@@ -34,7 +34,7 @@ def _sources():
     for n, m in VB:
         jobs.append((os.path.join(CSRC, "dg_vb_inst.cu"), os.path.join(OBJ, "dg_vb_n%d_m%d.o" % (n, m)),
                      ["-DDG_N=%d" % n, "-DDG_M=%d" % m]))
-    for name in ("dg_aux.cu", "dg_matrix.cu", "dg_abi.cpp", "dg_dispatch.cpp", "dg_nccl.cpp", "tables.cpp"):
+    for name in ("dg_aux.cu", "dg_matrix.cu", "dg_abi.cpp", "dg_dispatch.cpp", "dg_nccl.cpp", "dg_fabric.cpp", "tables.cpp"):
         base = os.path.splitext(name)[0]
         extra = ["-x", "cu"] if name.endswith(".cpp") else []
         jobs.append((os.path.join(CSRC, name), os.path.join(OBJ, base + ".o"), extra))

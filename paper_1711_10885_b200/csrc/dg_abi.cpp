@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "dg_internal.h"
+#include "dg_fabric.h"
 #include "dg_nccl.h"
 
 using namespace dg;
@@ -32,8 +33,10 @@ struct dg_ctx {
     int64_t nshell = 0;
     cudaStream_t comm_stream = nullptr, host_stream = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t ev_slab[2] = {nullptr, nullptr}, ev_done = nullptr;   // dg_apply_host pipeline
-    cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
-    ncclComm_t comm = nullptr;
+    cudaEvent_t ev_z = nullptr, ev_recv = nullptr;   // z ready on the caller's stream; halo received
+    ncclComm_t comm = nullptr;       // the halo transport: NCCL (one process per GPU) ...
+    Fabric* fabric = nullptr;        // ... or the in-process fabric (ranks as threads; dg_fabric.h)
+    TraceArgs targs;                 // trace pack of the partition faces (dg_aux.cu)
     double* hz = nullptr;            // device staging for dg_apply_host
     double* hy = nullptr;
     // general-coefficient path (full / per-cell D, dg_gen.cuh)
@@ -43,6 +46,8 @@ struct dg_ctx {
     double* dfield = nullptr;        // [local cell][6]
     double* dsend[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     double* drecv[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    double* dfield_next = nullptr;   // dg_set_diffusion builds here, then swaps (validate first)
+    double* drecv_next[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int* dbad = nullptr;             // validation flag of dg_set_diffusion
     // variable-velocity / over-integrated path (dg_vb.cuh)
     int m = 0;                       // Gauss points per direction (k+1 or k+3)
@@ -75,6 +80,11 @@ static bool g_tab_done[64][KMAX + 1];
 
 static int cuda_rc(cudaError_t e) { return e == cudaSuccess ? DG_OK : DG_ECUDA; }
 
+// The kernels move x-lines with 16-byte vector loads / stores (and TMA): every vector the
+// library reads or writes must be 16-byte aligned (include/dg.h); a misaligned view would
+// raise a sticky misaligned-address fault that poisons the whole CUDA context.
+static bool misaligned(const void* p) { return p && ((uintptr_t)p & 15u) != 0; }
+
 #define DG_CUDA(x)                                   \
     do {                                             \
         cudaError_t e__ = (x);                       \
@@ -104,6 +114,9 @@ static void free_ctx(dg_ctx* c)
     }
     if (c->shell) cudaFree(c->shell);
     if (c->dfield) cudaFree(c->dfield);
+    if (c->dfield_next) cudaFree(c->dfield_next);
+    for (int f = 0; f < 6; ++f)
+        if (c->drecv_next[f]) cudaFree(c->drecv_next[f]);
     if (c->dbad) cudaFree(c->dbad);
     for (int f = 0; f < 6; ++f) {
         if (c->dsend[f]) cudaFree(c->dsend[f]);
@@ -116,6 +129,7 @@ static void free_ctx(dg_ctx* c)
         const NcclApi* api = nccl_api();
         if (api) api->ncclCommDestroy(c->comm);
     }
+    if (c->fabric) fabric_leave(c->fabric, c->rank);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->host_stream) cudaStreamDestroy(c->host_stream);
     if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
@@ -123,7 +137,7 @@ static void free_ctx(dg_ctx* c)
     for (int i = 0; i < 2; ++i)
         if (c->ev_slab[i]) cudaEventDestroy(c->ev_slab[i]);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
-    if (c->ev_packed) cudaEventDestroy(c->ev_packed);
+    if (c->ev_z) cudaEventDestroy(c->ev_z);
     if (c->ev_recv) cudaEventDestroy(c->ev_recv);
     delete c;
 }
@@ -137,6 +151,52 @@ extern "C" int dg_nccl_unique_id(void* out128)
     if (api->ncclGetUniqueId(&id) != 0) return DG_ENCCL;
     std::memcpy(out128, &id, sizeof(id));
     return DG_OK;
+}
+
+extern "C" int dg_fabric_id(void* out128)
+{
+    if (!out128) return DG_EINVAL;
+    fabric_make_id(out128);
+    return DG_OK;
+}
+
+// ---- halo transport: one exchange = every partition face's send buffer to the
+// neighbour rank across it, every receive buffer from that rank; enqueued on stream s after
+// the producer of the send buffers. NCCL: one group of point-to-point calls. Per peer, NCCL
+// matches sends and receives in issue order; my buffer of face fc lands in the peer's receive
+// buffer of face fc^1, so receives are issued in the order fc^1: with two ranks along a
+// periodic direction both faces talk to the same peer and this keeps them paired. The
+// in-process fabric (dg_fabric.h) implements the same matching rule.
+static int exchange(dg_ctx* ctx, double* const send[6], double* const recv[6], const size_t cnt[6], cudaStream_t s)
+{
+    if (ctx->fabric) {
+        const int r = fabric_exchange(ctx->fabric, ctx->rank, ctx->nbr, send, recv, cnt, s);
+        return r == 0 ? DG_OK : (r == -2 ? DG_ECUDA : DG_ENCCL);
+    }
+    if (!ctx->comm) return DG_ENCCL;
+    const NcclApi* api = nccl_api();
+    if (!api) return DG_ENCCL;
+    if (api->ncclGroupStart() != 0) return DG_ENCCL;
+    for (int fc = 0; fc < 6; ++fc) {
+        const int fr = fc ^ 1;
+        if (ctx->nbr[fc] >= 0 && api->ncclSend(send[fc], cnt[fc], dgNcclFloat64, ctx->nbr[fc], ctx->comm, s) != 0) {
+            api->ncclGroupEnd();
+            return DG_ENCCL;
+        }
+        if (ctx->nbr[fr] >= 0 && api->ncclRecv(recv[fr], cnt[fr], dgNcclFloat64, ctx->nbr[fr], ctx->comm, s) != 0) {
+            api->ncclGroupEnd();
+            return DG_ENCCL;
+        }
+    }
+    return api->ncclGroupEnd() == 0 ? DG_OK : DG_ENCCL;
+}
+// Before the send buffers are overwritten (stream s): NCCL orders its sends on the comm stream
+// itself; the fabric waits for the peers' copies of the previous round.
+static int exchange_prepare(dg_ctx* ctx, cudaStream_t s)
+{
+    if (!ctx->fabric) return DG_OK;
+    const int r = fabric_prepare(ctx->fabric, ctx->rank, ctx->nbr, s);
+    return r == 0 ? DG_OK : (r == -2 ? DG_ECUDA : DG_ENCCL);
 }
 
 // Kernel coefficients from the physical D, b, c, sigma and the affine map x = lo + J (xhat - lo)
@@ -209,14 +269,9 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
         if (mesh->parts[q] < 1 || mesh->ncells[q] % mesh->parts[q] != 0) return DG_EINVAL;
     }
     if ((int64_t)mesh->parts[0] * mesh->parts[1] * mesh->parts[2] != nranks) return DG_EINVAL;
-    for (int i = 0; i < 9; ++i)
-        if (!std::isfinite(D[i])) return DG_EINVAL;
-    for (int r = 0; r < 3; ++r) {
-        if (D[4 * r] < 0.0) return DG_EINVAL;                  // PSD => nonnegative diagonal
-        for (int s = 0; s < 3; ++s)
-            if (D[3 * r + s] != D[3 * s + r]) return DG_EINVAL;    // symmetric
+    if (!psd3(D)) return DG_EINVAL;                            // symmetric PSD
+    for (int r = 0; r < 3; ++r)
         if (!std::isfinite(b[r])) return DG_EINVAL;
-    }
     if (!std::isfinite(c) || !std::isfinite(sigma) || sigma < 0.0) return DG_EINVAL;
     for (int f = 0; f < 6; ++f)
         if (mesh->bc[f] != DG_BC_DIRICHLET && mesh->bc[f] != DG_BC_PERIODIC) return DG_EUNSUPPORTED;
@@ -270,7 +325,7 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
                 ctx->partitioned = true;
             }
             const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
-            ctx->halo_count[f] = ctx->nloc[t1] * ctx->nloc[t2] * ctx->n3;
+            ctx->halo_count[f] = ctx->nloc[t1] * ctx->nloc[t2] * 2 * ctx->n * ctx->n;   // face traces
         }
 
     // kernel constants (eq:gauss_points; penalty reading C-4)
@@ -338,12 +393,29 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
                 cudaSuccess) { free_ctx(ctx); return DG_ECUDA; }
         }
         if (cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_z, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->ev_recv, cudaEventDisableTiming) != cudaSuccess) {
             free_ctx(ctx);
             return DG_ECUDA;
         }
-        if (nccl_unique_id) {
+        {   // trace pack arguments: send buffers, work prefix sums, theta(s), theta'(s)
+            HostTables t;
+            if (build_tables(k, &t) != 0) { free_ctx(ctx); return DG_EINVAL; }
+            TraceArgs& a = ctx->targs;
+            std::memset(&a, 0, sizeof(a));
+            a.start[0] = 0;
+            for (int f = 0; f < 6; ++f) {
+                a.dst[f] = ctx->sendbuf[f];
+                a.start[f + 1] = a.start[f] + (ctx->nbr[f] >= 0 ? ctx->halo_count[f] / 2 : 0);
+            }
+            for (int j = 0; j < ctx->n; ++j) {
+                a.th[0][j] = t.th0[j]; a.th[1][j] = t.th1[j];
+                a.dth[0][j] = t.dth0[j]; a.dth[1][j] = t.dth1[j];
+            }
+        }
+        if (nccl_unique_id && fabric_id_is(nccl_unique_id)) {
+            if (fabric_join(nccl_unique_id, rank, nranks, &ctx->fabric) != 0) { ctx->fabric = nullptr; free_ctx(ctx); return DG_ENCCL; }
+        } else if (nccl_unique_id) {
             const NcclApi* api = nccl_api();
             if (!api) { free_ctx(ctx); return DG_ENCCL; }
             ncclUniqueId id;
@@ -372,18 +444,25 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
 static int alloc_dfield(dg_ctx* ctx)
 {
     const int64_t ncell = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2];
-    if (!ctx->dfield && cudaMalloc(&ctx->dfield, (size_t)ncell * 6 * sizeof(double)) != cudaSuccess) return DG_ENOMEM;
+    const size_t fb = (size_t)ncell * 6 * sizeof(double);
+    if (!ctx->dfield && cudaMalloc(&ctx->dfield, fb) != cudaSuccess) return DG_ENOMEM;
+    if (!ctx->dfield_next && cudaMalloc(&ctx->dfield_next, fb) != cudaSuccess) return DG_ENOMEM;
     if (!ctx->dbad && cudaMalloc(&ctx->dbad, sizeof(int)) != cudaSuccess) return DG_ENOMEM;
     for (int f = 0; f < 6; ++f) {
         if (ctx->nbr[f] < 0 || ctx->dsend[f]) continue;
         const size_t bytes = (size_t)(ctx->halo_count[f] / ctx->n3) * 6 * sizeof(double);
-        if (cudaMalloc(&ctx->dsend[f], bytes) != cudaSuccess || cudaMalloc(&ctx->drecv[f], bytes) != cudaSuccess)
+        if (cudaMalloc(&ctx->dsend[f], bytes) != cudaSuccess || cudaMalloc(&ctx->drecv[f], bytes) != cudaSuccess ||
+            cudaMalloc(&ctx->drecv_next[f], bytes) != cudaSuccess)
             return DG_ENOMEM;
     }
+    return DG_OK;
+}
+
+static void bind_dfield(dg_ctx* ctx)
+{
     KParams& p = ctx->base;
     p.Dfield = ctx->dfield;
     for (int f = 0; f < 6; ++f) p.Dghost[f] = ctx->drecv[f];
-    return DG_OK;
 }
 
 static std::mutex g_vb_mu;
@@ -489,50 +568,46 @@ extern "C" int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags
     if (ctx->vb) return DG_EUNSUPPORTED;   // b(x) / over-integration run on constant diagonal D only
     int rc = alloc_dfield(ctx);
     if (rc != DG_OK) return rc;
+    // Everything is built in the *_next buffers and committed (pointer swap) only when it is
+    // complete: a rejected field or a failed exchange leaves the previous operator intact.
     if (!Dcell) {
         // constant tensor: field and neighbour layers are the same constant (no exchange)
-        DG_CUDA(launch_dfield_const(ctx->dfield, ctx->Dconst, ncell, s));
+        DG_CUDA(launch_dfield_const(ctx->dfield_next, ctx->Dconst, ncell, s));
         for (int f = 0; f < 6; ++f)
-            if (ctx->drecv[f])
-                DG_CUDA(launch_dfield_const(ctx->drecv[f], ctx->Dconst, ctx->halo_count[f] / ctx->n3, s));
-        ctx->general = true;
-        ctx->dfield_const = true;
-        return DG_OK;
-    }
-    DG_CUDA(cudaMemsetAsync(ctx->dbad, 0, sizeof(int), s));
-    // physical tensors; on an affine mesh each is mapped to |J| J^-1 D J^-T on the fly
-    DG_CUDA(launch_dfield_pack(Dcell, ctx->dfield, ctx->dbad, ncell, ctx->affine ? ctx->Jinv : nullptr, ctx->detJ, s));
-    ctx->dfield_const = false;
-    int bad = 0;
-    DG_CUDA(cudaMemcpyAsync(&bad, ctx->dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-    DG_CUDA(cudaStreamSynchronize(s));
-    if (bad) return DG_EINVAL;
-    if (ctx->partitioned) {
-        // the neighbour ranks' boundary layers of the field (setup-time, synchronous)
-        for (int f = 0; f < 6; ++f)
-            if (ctx->nbr[f] >= 0) DG_CUDA(launch_pack(ctx->dfield, ctx->dsend[f], 6, ctx->nloc, f, s));
-        if (!(flags & DG_HALO_EXTERNAL)) {
-            if (!ctx->comm) return DG_ENCCL;
-            const NcclApi* api = nccl_api();
-            if (!api) return DG_ENCCL;
-            if (api->ncclGroupStart() != 0) return DG_ENCCL;
-            for (int f = 0; f < 6; ++f) {   // same pairing rule as the z halo (send f, receive f^1)
-                const int fr = f ^ 1;
-                if (ctx->nbr[f] >= 0 && api->ncclSend(ctx->dsend[f], (size_t)(ctx->halo_count[f] / ctx->n3) * 6,
-                                                      dgNcclFloat64, ctx->nbr[f], ctx->comm, s) != 0) {
-                    api->ncclGroupEnd();
-                    return DG_ENCCL;
-                }
-                if (ctx->nbr[fr] >= 0 && api->ncclRecv(ctx->drecv[fr], (size_t)(ctx->halo_count[fr] / ctx->n3) * 6,
-                                                       dgNcclFloat64, ctx->nbr[fr], ctx->comm, s) != 0) {
-                    api->ncclGroupEnd();
-                    return DG_ENCCL;
-                }
-            }
-            if (api->ncclGroupEnd() != 0) return DG_ENCCL;
-        }
+            if (ctx->drecv_next[f])
+                DG_CUDA(launch_dfield_const(ctx->drecv_next[f], ctx->Dconst, ctx->halo_count[f] / ctx->n3, s));
+    } else {
+        DG_CUDA(cudaMemsetAsync(ctx->dbad, 0, sizeof(int), s));
+        // physical tensors; on an affine mesh each is mapped to |J| J^-1 D J^-T on the fly
+        DG_CUDA(launch_dfield_pack(Dcell, ctx->dfield_next, ctx->dbad, ncell, ctx->affine ? ctx->Jinv : nullptr,
+                                   ctx->detJ, s));
+        int bad = 0;
+        DG_CUDA(cudaMemcpyAsync(&bad, ctx->dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
         DG_CUDA(cudaStreamSynchronize(s));
+        if (bad) return DG_EINVAL;
+        if (ctx->partitioned) {
+            // the neighbour ranks' boundary layers of the field (setup-time, synchronous)
+            if (!(flags & DG_HALO_EXTERNAL)) {
+                rc = exchange_prepare(ctx, s);
+                if (rc != DG_OK) return rc;
+            }
+            for (int f = 0; f < 6; ++f)
+                if (ctx->nbr[f] >= 0) DG_CUDA(launch_pack(ctx->dfield_next, ctx->dsend[f], 6, ctx->nloc, f, s));
+            if (!(flags & DG_HALO_EXTERNAL)) {
+                size_t cnt[6];
+                for (int f = 0; f < 6; ++f) cnt[f] = (size_t)(ctx->halo_count[f] / ctx->n3) * 6;
+                rc = exchange(ctx, ctx->dsend, ctx->drecv_next, cnt, s);
+                if (rc != DG_OK) return rc;
+            }
+            // with DG_HALO_EXTERNAL the caller fills the committed receive layers
+            // (dg_halo_buffer which = 3) after this call
+            DG_CUDA(cudaStreamSynchronize(s));
+        }
     }
+    std::swap(ctx->dfield, ctx->dfield_next);
+    for (int f = 0; f < 6; ++f) std::swap(ctx->drecv[f], ctx->drecv_next[f]);
+    bind_dfield(ctx);
+    ctx->dfield_const = Dcell == nullptr;
     ctx->general = true;
     return DG_OK;
 }
@@ -632,6 +707,8 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
 {
     if (!ctx || !z || !y) return DG_EINVAL;
     if ((const double*)y == z || (f && f == z)) return DG_EINVAL;
+    if (misaligned(z) || misaligned(y) || misaligned(f)) return DG_EINVAL;
+    if (epi && (misaligned(epi->f) || misaligned(epi->w))) return DG_EINVAL;
     if (terms & ~(unsigned)(DG_ALL | DG_HALO_EXTERNAL)) return DG_EINVAL;
     DG_CUDA(cudaSetDevice(ctx->device));
     KParams p = ctx->base;
@@ -660,36 +737,21 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         }
         return cuda_rc(launch_any(ctx, p, s));
     }
-    // (iv) of SURVEY.md 3: pack partition layers, exchange on the comm stream, overlap with inner cells
+    // (iv) of SURVEY.md 3 / 8(e): the partition faces' traces are packed and exchanged on the comm
+    // stream while the inner-box cells (no remote data) run on s; the shell cells follow the
+    // receive. The pack is off s: it is launched first, so its few CTAs start ahead of the
+    // inner kernel's wave, and nothing on s waits for it.
     const bool need_comm = !external && (p.mask & DG_INTERIOR_FACES);
     if (need_comm) {
-        if (!ctx->comm) return DG_ENCCL;
-        const NcclApi* api = nccl_api();
-        if (!api) return DG_ENCCL;
-        for (int fc = 0; fc < 6; ++fc)
-            if (ctx->nbr[fc] >= 0) DG_CUDA(launch_pack(z, ctx->sendbuf[fc], ctx->n3, ctx->nloc, fc, s));
-        DG_CUDA(cudaEventRecord(ctx->ev_packed, s));
-        DG_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
-        if (api->ncclGroupStart() != 0) return DG_ENCCL;
-        // Per peer, NCCL matches sends and receives in issue order. My layer of face fc lands in the
-        // peer's receive buffer of face fc^1, so receives are issued in the order fc^1: with two ranks
-        // along a periodic direction both faces talk to the same peer and this keeps them paired.
-        for (int fc = 0; fc < 6; ++fc) {
-            const int fr = fc ^ 1;
-            if (ctx->nbr[fc] >= 0 &&
-                api->ncclSend(ctx->sendbuf[fc], (size_t)ctx->halo_count[fc], dgNcclFloat64, ctx->nbr[fc], ctx->comm,
-                              ctx->comm_stream) != 0) {
-                api->ncclGroupEnd();
-                return DG_ENCCL;
-            }
-            if (ctx->nbr[fr] >= 0 &&
-                api->ncclRecv(ctx->recvbuf[fr], (size_t)ctx->halo_count[fr], dgNcclFloat64, ctx->nbr[fr], ctx->comm,
-                              ctx->comm_stream) != 0) {
-                api->ncclGroupEnd();
-                return DG_ENCCL;
-            }
-        }
-        if (api->ncclGroupEnd() != 0) return DG_ENCCL;
+        DG_CUDA(cudaEventRecord(ctx->ev_z, s));
+        DG_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_z, 0));
+        int rc = exchange_prepare(ctx, ctx->comm_stream);
+        if (rc != DG_OK) return rc;
+        DG_CUDA(launch_trace_pack(z, ctx->targs, ctx->n, ctx->nloc, ctx->comm_stream));
+        size_t cnt[6];
+        for (int f = 0; f < 6; ++f) cnt[f] = (size_t)ctx->halo_count[f];
+        rc = exchange(ctx, ctx->sendbuf, ctx->recvbuf, cnt, ctx->comm_stream);
+        if (rc != DG_OK) return rc;
         DG_CUDA(cudaEventRecord(ctx->ev_recv, ctx->comm_stream));
     }
     // inner cells: no remote data
@@ -823,7 +885,7 @@ extern "C" int dg_matrix_size(const dg_ctx* ctx, int64_t* ndoubles)
 // launches (a task list of ~7/27 of the cells) overlap and fill the GPU.
 extern "C" int dg_assemble(dg_ctx* ctx, double* A, void* stream)
 {
-    if (!ctx || !A) return DG_EINVAL;
+    if (!ctx || !A || misaligned(A)) return DG_EINVAL;
     if (ctx->nranks != 1) return DG_EUNSUPPORTED;
     DG_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = (cudaStream_t)stream;
@@ -926,6 +988,7 @@ extern "C" int dg_assemble(dg_ctx* ctx, double* A, void* stream)
 extern "C" int dg_matrix_apply(dg_ctx* ctx, const double* A, const double* z, double* y, void* stream)
 {
     if (!ctx || !A || !z || !y || (const double*)y == z) return DG_EINVAL;
+    if (misaligned(A) || misaligned(z) || misaligned(y)) return DG_EINVAL;
     if (ctx->nranks != 1) return DG_EUNSUPPORTED;
     DG_CUDA(cudaSetDevice(ctx->device));
     const int64_t ns = matrix_scratch_doubles(ctx->n3, ctx->ndofs / ctx->n3);
@@ -982,11 +1045,9 @@ extern "C" int dg_halo_buffer(dg_ctx* ctx, int face, int which, double** ptr)
 
 extern "C" int dg_halo_pack(dg_ctx* ctx, const double* z, void* stream)
 {
-    if (!ctx || !z) return DG_EINVAL;
+    if (!ctx || !z || misaligned(z)) return DG_EINVAL;
     DG_CUDA(cudaSetDevice(ctx->device));
-    for (int fc = 0; fc < 6; ++fc)
-        if (ctx->nbr[fc] >= 0) DG_CUDA(launch_pack(z, ctx->sendbuf[fc], ctx->n3, ctx->nloc, fc, (cudaStream_t)stream));
-    return DG_OK;
+    return cuda_rc(launch_trace_pack(z, ctx->targs, ctx->n, ctx->nloc, (cudaStream_t)stream));
 }
 
 extern "C" int dg_fill_uniform(double* dst, int64_t count, uint64_t seed, int64_t offset, void* stream)

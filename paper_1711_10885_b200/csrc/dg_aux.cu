@@ -1,11 +1,12 @@
-// Auxiliary kernels: halo packing (partition-layer cells -> contiguous send buffer)
+// Auxiliary kernels: halo packing (face traces of the partition layers; per-cell field layers)
 // and the counter-based input generator (reading C-13; identical to inputs.py).
 #include "dg_internal.h"
 
 namespace dg {
 
+// Per-cell data of a boundary layer (the diffusion-tensor field, n3 = 6 doubles per cell):
 // face f = 2q + s: the layer lc[q] = (s ? nloc[q]-1 : 0); cells ordered by the two
-// tangential local coordinates (t1 fastest), t1 < t2, each a contiguous n^3 block.
+// tangential local coordinates (t1 fastest), t1 < t2, each a contiguous n3-block.
 __global__ void pack_kernel(const double* __restrict__ z, double* __restrict__ dst, int n3, int64_t n0, int64_t n1,
                             int64_t n2, int q, int s, int64_t total)
 {
@@ -31,6 +32,58 @@ cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     pack_kernel<<<(unsigned)blocks, 256, 0, s>>>(z, dst, n3, nloc[0], nloc[1], nloc[2], q, sd, total);
+    return cudaGetLastError();
+}
+
+// Face-trace halo: for every partition face f = 2q + s with a
+// neighbour rank, the normal-first contraction of this rank's boundary layer
+//     u(a, b) = sum_e theta_e(s) z(e along q; a, b),   d(a, b) = sum_e theta'_e(s) z(...)
+// for each layer cell (ordered t1 fastest, t1 < t2 the tangential directions) and tangential
+// modal pair (a along t1, b along t2): 2 n^2 doubles per cell, [u | d] at a + n b, 1/4 of the
+// block at k = 7. The receiving rank sees this cell across its face f^1 at x_q = s and runs the
+// tangential stages itself (nb_load / nb_traces in dg_cell.cuh). The chain order (e = 0..n-1,
+// fma) is the kernels' own, so a partitioned apply equals the single-rank one bit for bit.
+__global__ void trace_pack_kernel(const double* __restrict__ z, TraceArgs a, int n, int64_t n0, int64_t n1, int64_t n2)
+{
+    const int64_t nl[3] = {n0, n1, n2};
+    const int nn = n * n;
+    const int64_t n3 = (int64_t)nn * n;
+    const int64_t total = a.start[6];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int f = 0;
+        while (i >= a.start[f + 1]) ++f;
+        const int q = f >> 1, s = f & 1;
+        const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+        const int64_t li = i - a.start[f];
+        const int64_t cellk = li / nn;
+        const int t = (int)(li - cellk * nn);
+        const int ta = t % n, tb = t / n;
+        int64_t lc[3];
+        lc[t1] = cellk % nl[t1];
+        lc[t2] = cellk / nl[t1];
+        lc[q] = s ? nl[q] - 1 : 0;
+        const double* blk = z + (lc[0] + n0 * (lc[1] + n1 * lc[2])) * n3;
+        const int se = (q == 0) ? 1 : (q == 1) ? n : nn;
+        const int base = (q == 0) ? n * ta + nn * tb : (q == 1) ? ta + nn * tb : ta + n * tb;
+        double u = 0.0, d = 0.0;
+        for (int e = 0; e < n; ++e) {
+            const double v = __ldg(blk + base + e * se);
+            u = fma(a.th[s][e], v, u);
+            d = fma(a.dth[s][e], v, d);
+        }
+        double* o = a.dst[f] + cellk * 2 * nn;
+        o[t] = u;
+        o[nn + t] = d;
+    }
+}
+
+cudaError_t launch_trace_pack(const double* z, const TraceArgs& a, int n, const int64_t nloc[3], cudaStream_t s)
+{
+    const int64_t total = a.start[6];
+    if (total == 0) return cudaSuccess;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    trace_pack_kernel<<<(unsigned)blocks, 256, 0, s>>>(z, a, n, nloc[0], nloc[1], nloc[2]);
     return cudaGetLastError();
 }
 
@@ -91,10 +144,7 @@ __global__ void dfield_pack_kernel(const double* __restrict__ D9, double* __rest
 {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ncell; e += (int64_t)gridDim.x * blockDim.x) {
         const double* d = D9 + 9 * e;
-        bool ok = true;
-        for (int i = 0; i < 9; ++i) ok = ok && isfinite(d[i]);
-        ok = ok && d[1] == d[3] && d[2] == d[6] && d[5] == d[7] && d[0] >= 0.0 && d[4] >= 0.0 && d[8] >= 0.0;
-        if (!ok) atomicOr(bad, 1);
+        if (!psd3(d)) atomicOr(bad, 1);   // symmetric PSD
         double m[9];
         for (int i = 0; i < 9; ++i) m[i] = d[i];
         if (affine) {                  // Dhat = |J| J^-1 D J^-T (reference-mesh tensor of an affine mesh)

@@ -455,10 +455,15 @@ __device__ __forceinline__ FaceOut flux_boundary(const KParams& p, int q, int s,
 // ---------------------------------------------------------------------------------- kernel pieces
 // Load the lines of the two neighbours across direction q that this thread's pencils need
 // (tangential modal indices (a, bb) fixed, normal index e = 0..n-1).
+// A neighbour on another rank (the partition face of this rank's box) is not loaded as a block:
+// its rank sent the normal-first contraction of its boundary layer (the face traces of SURVEY
+// 8(e), dg_trace_pack in dg_aux.cu: 2 n^2 doubles per face cell, [u | d] at a + n bb). For such
+// a "ghost" side the two values land in rl/rh[k][0..1] and bit 0 (low) / 1 (high) of the
+// returned mask tells nb_traces to take them as they are.
 template <int N, int P>
-__device__ __forceinline__ void nb_load(const KParams& p, const double* zc, const int64_t n3, int q, const int lc[3],
-                                        unsigned nbmask, const int (&pa)[P], const int (&pb)[P], const bool (&act)[P],
-                                        double (&rl)[P][N], double (&rh)[P][N])
+__device__ __forceinline__ unsigned nb_load(const KParams& p, const double* zc, const int64_t n3, int q, const int lc[3],
+                                            unsigned nbmask, const int (&pa)[P], const int (&pb)[P], const bool (&act)[P],
+                                            double (&rl)[P][N], double (&rh)[P][N])
 {
     constexpr int NN = N * N;
     const int lq = lc[q];
@@ -467,19 +472,24 @@ __device__ __forceinline__ void nb_load(const KParams& p, const double* zc, cons
     const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
                                                                         : (lc[0] + p.nloc[0] * lc[1]);
     const bool hl = (nbmask >> (2 * q)) & 1u, hh = (nbmask >> (2 * q + 1)) & 1u;
+    const bool gl = hl && lq == 0 && !p.wrap[q];           // the low neighbour lives on another rank
+    const bool gh = hh && lq + 1 == nq && !p.wrap[q];
     const int64_t wst = (int64_t)(nq - 1) * st * n3;   // periodic wrap inside this rank's box
-    const double* zl = (lq > 0) ? zc - st * n3 : (p.wrap[q] ? zc + wst : (hl ? p.ghost[2 * q] + gi * n3 : zc));
-    const double* zh = (lq + 1 < nq) ? zc + st * n3 : (p.wrap[q] ? zc - wst : (hh ? p.ghost[2 * q + 1] + gi * n3 : zc));
+    const double* zl = (lq > 0) ? zc - st * n3 : (p.wrap[q] ? zc + wst : zc);
+    const double* zh = (lq + 1 < nq) ? zc + st * n3 : (p.wrap[q] ? zc - wst : zc);
+    const double* tl = gl ? p.ghost[2 * q] + gi * 2 * NN : nullptr;
+    const double* th = gh ? p.ghost[2 * q + 1] + gi * 2 * NN : nullptr;
+    const bool ll = hl && !gl, lh = hh && !gh;
 #ifdef DG_CHECK
     {
         const int64_t nall = p.nloc[0] * p.nloc[1] * p.nloc[2] * n3;
         const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
         const int64_t nlay = p.nloc[t1] * p.nloc[t2];
         DG_ASSERT(gi >= 0 && gi < nlay);
-        if (lq > 0 || p.wrap[q] || !hl) DG_ASSERT(zl >= p.z && zl + n3 <= p.z + nall);
-        else DG_ASSERT(p.ghost[2 * q] != nullptr);
-        if (lq + 1 < nq || p.wrap[q] || !hh) DG_ASSERT(zh >= p.z && zh + n3 <= p.z + nall);
-        else DG_ASSERT(p.ghost[2 * q + 1] != nullptr);
+        DG_ASSERT(zl >= p.z && zl + n3 <= p.z + nall);
+        DG_ASSERT(zh >= p.z && zh + n3 <= p.z + nall);
+        if (gl) DG_ASSERT(p.ghost[2 * q] != nullptr);
+        if (gh) DG_ASSERT(p.ghost[2 * q + 1] != nullptr);
     }
 #endif
 #pragma unroll
@@ -488,9 +498,9 @@ __device__ __forceinline__ void nb_load(const KParams& p, const double* zc, cons
             const int base = N * pa[k] + NN * pb[k];
 #pragma unroll
             for (int e = 0; e < N; e += 2) {
-                const double2 vl = (act[k] && hl) ? __ldg(reinterpret_cast<const double2*>(zl + base + e))
+                const double2 vl = (act[k] && ll) ? __ldg(reinterpret_cast<const double2*>(zl + base + e))
                                                   : make_double2(0.0, 0.0);
-                const double2 vh = (act[k] && hh) ? __ldg(reinterpret_cast<const double2*>(zh + base + e))
+                const double2 vh = (act[k] && lh) ? __ldg(reinterpret_cast<const double2*>(zh + base + e))
                                                   : make_double2(0.0, 0.0);
                 rl[k][e] = vl.x; rl[k][e + 1] = vl.y;
                 rh[k][e] = vh.x; rh[k][e + 1] = vh.y;
@@ -500,31 +510,56 @@ __device__ __forceinline__ void nb_load(const KParams& p, const double* zc, cons
             const int base = (q == 0) ? N * pa[k] + NN * pb[k] : (q == 1) ? pa[k] + NN * pb[k] : pa[k] + N * pb[k];
 #pragma unroll
             for (int e = 0; e < N; ++e) {
-                rl[k][e] = (act[k] && hl) ? __ldg(zl + base + e * se) : 0.0;
-                rh[k][e] = (act[k] && hh) ? __ldg(zh + base + e * se) : 0.0;
+                rl[k][e] = (act[k] && ll) ? __ldg(zl + base + e * se) : 0.0;
+                rh[k][e] = (act[k] && lh) ? __ldg(zh + base + e * se) : 0.0;
+            }
+        }
+        if (gl || gh) {
+            const int t = pa[k] + N * pb[k];
+            if (gl) {
+                rl[k][0] = act[k] ? __ldg(tl + t) : 0.0;
+                rl[k][1] = act[k] ? __ldg(tl + NN + t) : 0.0;
+            }
+            if (gh) {
+                rh[k][0] = act[k] ? __ldg(th + t) : 0.0;
+                rh[k][1] = act[k] ? __ldg(th + NN + t) : 0.0;
             }
         }
     }
+    return (gl ? 1u : 0u) | (gh ? 2u : 0u);
 }
 
-// Normal-direction-first contraction of the loaded neighbour lines:
-// low neighbour (face 2q) is seen at its x_q = 1, high neighbour (face 2q+1) at x_q = 0.
+// The neighbour traces of one pencil, normal direction FIRST: the low
+// neighbour (face 2q) is seen at its x_q = 1 (theta(1), theta'(1)), the high one (face 2q+1) at
+// x_q = 0; ghost sides (bit 0 / 1 of gm) arrive contracted.
+template <int N>
+__device__ __forceinline__ void nb_traces(const double* th0, const double* th1, const double* dth0, const double* dth1,
+                                          const double (&rl)[N], const double (&rh)[N], unsigned gm, double& ul,
+                                          double& dl, double& uh, double& dh)
+{
+    ul = 0.0; dl = 0.0; uh = 0.0; dh = 0.0;
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+        ul = fma(th1[e], rl[e], ul);
+        dl = fma(dth1[e], rl[e], dl);
+        uh = fma(th0[e], rh[e], uh);
+        dh = fma(dth0[e], rh[e], dh);
+    }
+    if (gm & 1u) { ul = rl[0]; dl = rl[1]; }
+    if (gm & 2u) { uh = rh[0]; dh = rh[1]; }
+}
+
+// Normal-direction-first contraction of the loaded neighbour lines into the face arrays.
 template <int N, int P, class FL = FLay<N>>
 __device__ __forceinline__ void nb_contract(const Tab<N>& T, double* NT, int q, unsigned nbmask, const int (&pa)[P],
                                            const int (&pb)[P], const bool (&act)[P], const double (&rl)[P][N],
-                                           const double (&rh)[P][N])
+                                           const double (&rh)[P][N], unsigned gm)
 {
     const bool hl = (nbmask >> (2 * q)) & 1u, hh = (nbmask >> (2 * q + 1)) & 1u;
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-        double ul = 0.0, dl = 0.0, uh = 0.0, dh = 0.0;
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-            ul = fma(T.th1[e], rl[k][e], ul);
-            dl = fma(T.dth1[e], rl[k][e], dl);
-            uh = fma(T.th0[e], rh[k][e], uh);
-            dh = fma(T.dth0[e], rh[k][e], dh);
-        }
+        double ul, dl, uh, dh;
+        nb_traces<N>(T.th0, T.th1, T.dth0, T.dth1, rl[k], rh[k], gm, ul, dl, uh, dh);
         if (act[k]) {
             if (hl) {
                 NT[FL::at(4 * q, pa[k], pb[k])] = ul;
@@ -773,6 +808,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
     }
     {
         double rl[P][N], rh[P][N];
+        unsigned gm0 = 0;   // ghost x-neighbours (never TMA-staged)
         // ---- phase 1: x-pencils (y = a, z = bb) from global, V along x -> A0;
         //      x-neighbour lines loaded alongside and contracted (normal first)
         if (tma_x) {
@@ -790,7 +826,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 }
             }
         } else {
-        nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
+        gm0 = nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
             if (STG) {
@@ -822,11 +858,11 @@ dg_cell_kernel(const __grid_constant__ KParams p)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) A0[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
-        nb_contract<N, P>(T, NT, 0, nbi, pa, pb, act, rl, rh);
+        nb_contract<N, P>(T, NT, 0, nbi, pa, pb, act, rl, rh, gm0);
         csync();
 
         // ---- phase 2: y-pencils (x = a, z = bb): V along y -> A1; y-neighbours; x-arrays step B
-        nb_load<N, P>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
+        const unsigned gm1 = nb_load<N, P>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -838,12 +874,12 @@ dg_cell_kernel(const __grid_constant__ KParams p)
 #pragma unroll
                 for (int e = 0; e < N; ++e) A1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
         nb_tangential<N, TPC>(T.Vs[2], NT, 0, 0, nbi, (lane + TPC / 2) % TPC);
-        nb_contract<N, P>(T, NT, 1, nbi, pa, pb, act, rl, rh);
+        nb_contract<N, P>(T, NT, 1, nbi, pa, pb, act, rl, rh, gm1);
         csync();
 
         // ---- phase 3: z-pencils (x = a, y = bb): u at the Gauss points -> A0; z-neighbours;
         //      y-arrays step B, x-arrays step C
-        nb_load<N, P>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
+        const unsigned gm2 = nb_load<N, P>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -856,7 +892,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
         nb_tangential<N, TPC>(T.Vs[4], NT, 1, 0, nbi, lane);
         nb_tangential<N, TPC>(T.Vs[5], NT, 0, 1, nbi, (lane + TPC / 2) % TPC);
-        nb_contract<N, P>(T, NT, 2, nbi, pa, pb, act, rl, rh);
+        nb_contract<N, P>(T, NT, 2, nbi, pa, pb, act, rl, rh, gm2);
         csync();
     }
 

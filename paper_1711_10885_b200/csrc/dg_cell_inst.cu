@@ -191,7 +191,10 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
     int dev = 0;
     cudaGetDevice(&dev);
 #if DG_N == 8
-    if (use_mma() && !(p.per[0] | p.per[1] | p.per[2]) && p.epi != 2) {   // DMMA variant: no wrap, no SSP epilogue
+    bool ghosts = false;
+    for (int f = 0; f < 6; ++f) ghosts = ghosts || p.ghost[f] != nullptr;
+    // DMMA variant: no wrap, no SSP epilogue, single rank (it reads neighbours as blocks, not traces)
+    if (use_mma() && !(p.per[0] | p.per[1] | p.per[2]) && p.epi != 2 && !ghosts) {
         static int done[64];
         constexpr int BYTES = m8::C * m8::PER_CELL * 8;
         if (dev >= 0 && dev < 64 && !done[dev]) {

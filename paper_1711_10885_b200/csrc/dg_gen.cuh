@@ -259,6 +259,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     // ---------------------------------------------------------------- P1-P3: u at the Gauss points
     {
         double rl[P][N], rh[P][N];
+        unsigned gm = 0;   // ghost neighbours (traces from the halo; x-ghosts are never TMA-staged)
         if (tma_x) {
 #pragma unroll
             for (int k = 0; k < P; ++k) {
@@ -272,7 +273,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 }
             }
         } else {
-            nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
+            gm = nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
             for (int k = 0; k < P; ++k) {
                 if (STG) {
@@ -295,10 +296,10 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) X0[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
-        nb_contract<N, P, GFLay<N>>(T, NT, 0, nbi, pa, pb, act, rl, rh);
+        nb_contract<N, P, GFLay<N>>(T, NT, 0, nbi, pa, pb, act, rl, rh, gm);
         csync();
 
-        nb_load<N, P>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
+        gm = nb_load<N, P>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -309,15 +310,15 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             if (act[k])
 #pragma unroll
                 for (int e = 0; e < N; ++e) X1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
-        nb_contract<N, P, GFLay<N>>(T, NT, 1, nbi, pa, pb, act, rl, rh);
+        nb_contract<N, P, GFLay<N>>(T, NT, 1, nbi, pa, pb, act, rl, rh, gm);
         csync();
 
-        nb_load<N, P>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
+        gm = nb_load<N, P>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
             for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X1[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
-        nb_contract<N, P, GFLay<N>>(T, NT, 2, nbi, pa, pb, act, rl, rh);
+        nb_contract<N, P, GFLay<N>>(T, NT, 2, nbi, pa, pb, act, rl, rh, gm);
     }
     v_fwd_sd<N, P>(T.Vs[2], r, t);                               // t = u on this thread's z-pencils
     {

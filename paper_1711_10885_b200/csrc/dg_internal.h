@@ -19,6 +19,27 @@ namespace dg {
 constexpr int KMAX = 10;
 constexpr int NMAX = KMAX + 1;
 
+// Symmetric positive SEMI-definite test of a row-major 3x3 tensor (the diffusion tensor of
+// eq:modelproblem; D = 0 is admitted): finite, exactly
+// symmetric, and all seven principal minors of D / max|D_ij| >= -1e-13 (a symmetric matrix is
+// PSD iff every principal minor is >= 0; the tolerance admits rounding in semi-definite inputs).
+__host__ __device__ inline bool psd3(const double* d)
+{
+    double s = 0.0;
+    for (int i = 0; i < 9; ++i) {
+        if (!(d[i] - d[i] == 0.0)) return false;              // NaN / inf
+        s = fmax(s, fabs(d[i]));
+    }
+    if (d[1] != d[3] || d[2] != d[6] || d[5] != d[7]) return false;
+    if (s == 0.0) return true;
+    const double a = d[0] / s, b = d[4] / s, c = d[8] / s, x = d[1] / s, y = d[2] / s, z = d[5] / s;
+    const double tol = -1e-13;
+    if (a < tol || b < tol || c < tol) return false;
+    if (a * b - x * x < tol || a * c - y * y < tol || b * c - z * z < tol) return false;
+    const double det = a * (b * c - z * z) - x * (x * c - z * y) + y * (x * z - b * y);
+    return det >= tol;
+}
+
 // 1D tables for one degree (host side, double). Built by tables.cpp.
 struct HostTables {
     int n, m;                // basis size n = k+1, Gauss points per direction m (>= n)
@@ -42,7 +63,7 @@ struct KParams {
     const double* w;          // epi 2: the a w term (nullptr = 0)
     double ea, eb, es;        // epi 2: y = ea w + eb (z + es (f - A z)), es = dt / Delta_T
     int epi;                  // store epilogue: 0 y = A z, 1 residual, 2 SSP-RK stage
-    const double* ghost[6];   // neighbour-rank boundary layers per face 2q+s (nullptr: none)
+    const double* ghost[6];   // neighbour-rank face traces per face 2q+s: [layer cell][u | d][n^2] (nullptr: none)
     const int64_t* task_list; // local linear cell ids (nullptr -> task box)
     int64_t ntasks;
     int64_t task_lo[3], task_cnt[3];
@@ -97,6 +118,12 @@ bool make_row_map(CUtensorMap* map, const double* ptr, int64_t rows);
 int gen_launch_info(int k, LaunchInfo* info);
 
 // Halo / inputs kernels (dg_aux.cu).
+struct TraceArgs {              // face-trace halo of the partition faces (trace_pack_kernel)
+    double* dst[6];             // send buffer of face f (nullptr: no neighbour rank)
+    int64_t start[7];           // prefix sums of the work items (layer cells x n^2) per face
+    double th[2][NMAX], dth[2][NMAX];   // theta_j(s), theta'_j(s), s = 0, 1
+};
+cudaError_t launch_trace_pack(const double* z, const TraceArgs& a, int n, const int64_t nloc[3], cudaStream_t s);
 cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc[3], int face, cudaStream_t s);
 cudaError_t launch_dfield_pack(const double* D9, double* D6, int* bad, int64_t ncell, const double* Jinv,
                                double det, cudaStream_t s);

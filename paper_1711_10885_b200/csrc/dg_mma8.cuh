@@ -126,7 +126,7 @@ __device__ __forceinline__ void nb_face(const KParams& p, const Tab<8>& T, doubl
     } else {
         const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
                                                                             : (lc[0] + p.nloc[0] * lc[1]);
-        zn = p.ghost[f] + gi * n3;
+        zn = p.ghost[f] + gi * n3;   // unreachable: launch_cell runs this variant on single-rank boxes only
     }
     const int se = (q == 0) ? 1 : (q == 1) ? 8 : 64;
     const double* thv = SIDE ? T.th0 : T.th1;      // neighbour face at x_q = 1 - SIDE

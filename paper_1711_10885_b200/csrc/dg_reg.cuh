@@ -82,30 +82,37 @@ __device__ __forceinline__ void rcontract_t(const double (&M)[N][N], const doubl
             }
 }
 
-// the neighbour block across face f = 2q + s (nullptr: none), as nb_load resolves it
+// the neighbour block across face f = 2q + s inside this rank's z (local or periodic wrap), as
+// nb_load resolves it; a neighbour on another rank is read from the trace halo (reg_ghost)
 template <int N>
 __device__ __forceinline__ const double* reg_nb(const KParams& p, const double* zc, int64_t n3, const int (&lc)[3],
-                                                int q, int s, unsigned nbmask)
+                                                int q, int s)
 {
-    if (!((nbmask >> (2 * q + s)) & 1u)) return nullptr;
     const int lq = lc[q];
     const int nq = (int)p.nloc[q];
     const int64_t st = (q == 0) ? 1 : (q == 1) ? p.nloc[0] : p.nloc[0] * p.nloc[1];
-    const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
-                                                                        : (lc[0] + p.nloc[0] * lc[1]);
     const int64_t wst = (int64_t)(nq - 1) * st * n3;
-    const bool local = s == 0 ? (lq > 0 || p.wrap[q]) : (lq + 1 < nq || p.wrap[q]);
-    const double* zn = s == 0 ? ((lq > 0) ? zc - st * n3 : (p.wrap[q] ? zc + wst : p.ghost[2 * q] + gi * n3))
-                              : ((lq + 1 < nq) ? zc + st * n3 : (p.wrap[q] ? zc - wst : p.ghost[2 * q + 1] + gi * n3));
+    const double* zn = s == 0 ? ((lq > 0) ? zc - st * n3 : zc + wst) : ((lq + 1 < nq) ? zc + st * n3 : zc - wst);
 #ifdef DG_CHECK
     {
         const int64_t nall = p.nloc[0] * p.nloc[1] * p.nloc[2] * n3;
-        if (local) DG_ASSERT(zn >= p.z && zn + n3 <= p.z + nall);
-        else DG_ASSERT(p.ghost[2 * q + s] != nullptr);
+        DG_ASSERT(zn >= p.z && zn + n3 <= p.z + nall);
     }
 #endif
-    (void)local;
     return zn;
+}
+// the normal-first contraction [u | d] (2 n^2) of the other-rank neighbour across face 2q + s
+// (dg_trace_pack), or nullptr when that neighbour is in this rank's z
+template <int N>
+__device__ __forceinline__ const double* reg_ghost(const KParams& p, const int (&lc)[3], int q, int s)
+{
+    const int lq = lc[q];
+    const int nq = (int)p.nloc[q];
+    if (p.wrap[q] || (s == 0 ? lq > 0 : lq + 1 < nq)) return nullptr;
+    const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
+                                                                        : (lc[0] + p.nloc[0] * lc[1]);
+    DG_ASSERT(p.ghost[2 * q + s] != nullptr);
+    return p.ghost[2 * q + s] + gi * 2 * N * N;
 }
 
 template <int N>
@@ -161,24 +168,34 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
         double un[N][N], sn[N][N];                 // neighbour u+ and nu.D+ grad u+ (physical)
         double dnb = 0.0;                          // neighbour D_qq (GEN)
         if (interior) {
-            double zn[N * N * N];
-            reg_load<N>(reg_nb<N>(p, zc, n3, lc, Q, s, nbmask), zn);
             // normal first: the neighbour is seen at its x_q = 1 (s = 0) or 0 (s = 1)
             double cu[N][N], cd[N][N];
+            if (const double* tr = reg_ghost<N>(p, lc, Q, s)) {   // contracted by its rank
 #pragma unroll
-            for (int a = 0; a < N; ++a)
+                for (int a = 0; a < N; ++a)
 #pragma unroll
-                for (int b = 0; b < N; ++b) {
-                    double su = 0.0, sd = 0.0;
-#pragma unroll
-                    for (int e = 0; e < N; ++e) {
-                        const double v = zn[rat<N, Q>(e, a, b)];
-                        su = fma(s ? R.th0[e] : R.th1[e], v, su);
-                        sd = fma(s ? R.dth0[e] : R.dth1[e], v, sd);
+                    for (int b = 0; b < N; ++b) {
+                        cu[a][b] = __ldg(tr + a + N * b);
+                        cd[a][b] = __ldg(tr + N * N + a + N * b);
                     }
-                    cu[a][b] = su;
-                    cd[a][b] = sd;
-                }
+            } else {
+                double zn[N * N * N];
+                reg_load<N>(reg_nb<N>(p, zc, n3, lc, Q, s), zn);
+#pragma unroll
+                for (int a = 0; a < N; ++a)
+#pragma unroll
+                    for (int b = 0; b < N; ++b) {
+                        double su = 0.0, sd = 0.0;
+#pragma unroll
+                        for (int e = 0; e < N; ++e) {
+                            const double v = zn[rat<N, Q>(e, a, b)];
+                            su = fma(s ? R.th0[e] : R.th1[e], v, su);
+                            sd = fma(s ? R.dth0[e] : R.dth1[e], v, sd);
+                        }
+                        cu[a][b] = su;
+                        cd[a][b] = sd;
+                    }
+            }
             // tangential stages: V along the first, then the second tangential axis
             double t0[N][N], t1[N][N], dn[N][N];
             fstage<N, 0, false>(R.V, cu, t0);

@@ -251,18 +251,12 @@ dg_vb_kernel(const KParams p)
         int pa[1] = {ya}, pb[1] = {zb};
         bool act[1] = {true};
         double RL[1][N], RH[1][N];
-        nb_load<N, 1>(p, zc, n3, 0, lc, nbi, pa, pb, act, RL, RH);
+        const unsigned gm = nb_load<N, 1>(p, zc, n3, 0, lc, nbi, pa, pb, act, RL, RH);
 #pragma unroll
         for (int e = 0; e < N; ++e) { rl[e] = RL[0][e]; rh[e] = RH[0][e]; }
         const bool hl = (nbi >> 0) & 1u, hh = (nbi >> 1) & 1u;
-        double ul = 0.0, dl = 0.0, uh = 0.0, dh = 0.0;
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-            ul = fma(T.th1[e], rl[e], ul);
-            dl = fma(T.dth1[e], rl[e], dl);
-            uh = fma(T.th0[e], rh[e], uh);
-            dh = fma(T.dth0[e], rh[e], dh);
-        }
+        double ul, dl, uh, dh;
+        nb_traces<N>(T.th0, T.th1, T.dth0, T.dth1, rl, rh, gm, ul, dl, uh, dh);
         if (hl) { NT[FL::at(0, ya, zb)] = ul; NT[FL::at(1, ya, zb)] = dl; }
         if (hh) { NT[FL::at(2, ya, zb)] = uh; NT[FL::at(3, ya, zb)] = dh; }
     }
@@ -289,16 +283,10 @@ dg_vb_kernel(const KParams p)
         int pa[1] = {pa0}, pb[1] = {pb0};
         bool act[1] = {true};
         double RL[1][N], RH[1][N];
-        nb_load<N, 1>(p, zc, n3, q, lc, nbi, pa, pb, act, RL, RH);
+        const unsigned gm = nb_load<N, 1>(p, zc, n3, q, lc, nbi, pa, pb, act, RL, RH);
         const bool hl = (nbi >> (2 * q)) & 1u, hh = (nbi >> (2 * q + 1)) & 1u;
-        double ul = 0.0, dl = 0.0, uh = 0.0, dh = 0.0;
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-            ul = fma(T.th1[e], RL[0][e], ul);
-            dl = fma(T.dth1[e], RL[0][e], dl);
-            uh = fma(T.th0[e], RH[0][e], uh);
-            dh = fma(T.dth0[e], RH[0][e], dh);
-        }
+        double ul, dl, uh, dh;
+        nb_traces<N>(T.th0, T.th1, T.dth0, T.dth1, RL[0], RH[0], gm, ul, dl, uh, dh);
         if (hl) { NT[FL::at(4 * q, pa0, pb0)] = ul; NT[FL::at(4 * q + 1, pa0, pb0)] = dl; }
         if (hh) { NT[FL::at(4 * q + 2, pa0, pb0)] = uh; NT[FL::at(4 * q + 3, pa0, pb0)] = dh; }
     };

@@ -23,7 +23,7 @@ EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residu
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
             "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage", "dg_set_velocity", "dg_set_quadrature",
-            "dg_set_affine", "dg_matrix_size", "dg_assemble", "dg_matrix_apply"]
+            "dg_set_affine", "dg_matrix_size", "dg_assemble", "dg_matrix_apply", "dg_fabric_id"]
 
 
 class DGError(RuntimeError):
@@ -73,6 +73,7 @@ def lib():
         L.dg_fill_uniform.argtypes = [vp, i64, u64, i64, vp]
         L.dg_fill_uniform_local.argtypes = [vp, vp, u64, vp]
         L.dg_nccl_unique_id.argtypes = [vp]
+        L.dg_fabric_id.argtypes = [vp]
         L.dg_get_kernel_info.argtypes = [vp, ctypes.POINTER(KernelInfo)]
         L.dg_partition.argtypes = [ctypes.POINTER(MeshDesc), ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.dg_set_diffusion.argtypes = [vp, vp, ctypes.c_uint, vp]
@@ -115,11 +116,21 @@ def _dev_vec(t, n, name):
         raise TypeError("%s must be a contiguous CUDA float64 tensor" % name)
     if t.numel() != n:
         raise ValueError("%s has %d entries, expected %d" % (name, t.numel(), n))
+    if t.data_ptr() % 16:
+        raise ValueError("%s must be 16-byte aligned (the kernels use 16-byte vector accesses)" % name)
 
 
 def nccl_unique_id():
     buf = (ctypes.c_ubyte * 128)()
     _check(lib().dg_nccl_unique_id(buf), "dg_nccl_unique_id")
+    return bytes(buf)
+
+
+def fabric_id():
+    """Id of an in-process fabric group (dg_fabric_id): the ranks of a partitioned operator as
+    threads of this process, e.g. P ranks on one GPU for a test of the partitioned path."""
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib().dg_fabric_id(buf), "dg_fabric_id")
     return bytes(buf)
 
 
@@ -185,9 +196,13 @@ class Operator:
 
     # -- compute ------------------------------------------------------------------------------------
     def apply(self, z, y, terms=ALL, stream=None):
+        """y = A z (dg_apply), or the parts of A in `terms` (dg_apply_ex)."""
         _dev_vec(z, self.ndofs, "z")
         _dev_vec(y, self.ndofs, "y")
-        _check(lib().dg_apply_ex(self._h, _ptr(z), _ptr(y), terms, _stream(stream)), "dg_apply_ex")
+        if terms == ALL:
+            _check(lib().dg_apply(self._h, _ptr(z), _ptr(y), _stream(stream)), "dg_apply")
+        else:
+            _check(lib().dg_apply_ex(self._h, _ptr(z), _ptr(y), terms, _stream(stream)), "dg_apply_ex")
         return y
 
     def residual(self, z, f, r, stream=None):

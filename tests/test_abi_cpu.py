@@ -52,6 +52,9 @@ def setup_rc(k=2, ncells=(2, 2, 2), lo=(0, 0, 0), hi=(1, 1, 1), D=(1, 0, 0, 0, 1
     (dict(ncells=(0, 2, 2)), dg.DG_EINVAL), (dict(hi=(1, 0, 1)), dg.DG_EINVAL),
     (dict(D=(1, 0.5, 0, 0, 1, 0, 0, 0, 1)), dg.DG_EINVAL),          # not symmetric
     (dict(D=(-1, 0, 0, 0, 1, 0, 0, 0, 1)), dg.DG_EINVAL),           # not PSD
+    (dict(D=(1, 2, 0, 2, 1, 0, 0, 0, 1)), dg.DG_EINVAL),            # indefinite, positive diagonal
+    (dict(D=(1, .9, .9, .9, 1, -.9, .9, -.9, 1)), dg.DG_EINVAL),    # 2x2 minors >= 0, det < 0
+    (dict(D=(1, 0, 0, 0, 0, 0, 0, 0, -1e-3)), dg.DG_EINVAL),        # semi-definite part, one negative
     (dict(sigma=-1.0), dg.DG_EINVAL), (dict(c=float("nan")), dg.DG_EINVAL),
     (dict(parts=(2, 1, 1)), dg.DG_EINVAL),                          # product != nranks
     (dict(parts=(3, 1, 1), nranks=3), dg.DG_EINVAL),                # does not divide ncells
@@ -71,3 +74,19 @@ def test_null_arguments():
     assert L.dg_sync(None) == dg.DG_EINVAL
     assert L.dg_fill_uniform(None, 5, 0, 0, None) == dg.DG_EINVAL
     assert L.dg_nccl_unique_id(None) == dg.DG_EINVAL
+
+
+@pytest.mark.parametrize("D", [
+    (0, 0, 0, 0, 0, 0, 0, 0, 0),            # D = 0: the mass-matrix invariant
+    (1, 0, 0, 0, 0, 0, 0, 0, 0),            # semi-definite diagonal
+    (1, 1, 0, 1, 1, 0, 0, 0, 0),            # rank one, full
+    (2, -1, 0, -1, 2, -1, 0, -1, 2),        # SPD tridiagonal
+])
+def test_setup_accepts_psd(D):
+    # validation passes; without a GPU the call then fails at the device (not DG_EINVAL)
+    assert setup_rc(D=D) != dg.DG_EINVAL
+
+
+def test_fabric_id_distinct():
+    a, b = dg.fabric_id(), dg.fabric_id()
+    assert len(a) == 128 and a[:8] == b"DGFABRIC" and a != b

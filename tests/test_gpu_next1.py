@@ -202,6 +202,50 @@ def test_set_diffusion_rejects_bad_tensors():
     Dc[0, 2, 2] = -1.0                       # negative diagonal
     with pytest.raises(dg.DGError):
         op.set_diffusion(torch.from_numpy(Dc.reshape(-1)).cuda())
+    Dc = spd_field(cfg.ncell, 1)
+    Dc[5] = [[1.0, 2.0, 0.0], [2.0, 1.0, 0.0], [0.0, 0.0, 1.0]]   # indefinite, positive diagonal
+    with pytest.raises(dg.DGError) as ei:
+        op.set_diffusion(torch.from_numpy(Dc.reshape(-1)).cuda())
+    assert ei.value.code == dg.DG_EINVAL
+    op.close()
+
+
+def test_rejected_set_diffusion_keeps_previous_field():
+    """A rejected field leaves the operator as it was (validated before it is committed)."""
+    from paper_1711_10885_b200 import dg
+    cfg = configs.small(3, ncells=(3, 3, 2))
+    op = dg.from_config(cfg)
+    z = torch.empty(op.ndofs, dtype=torch.float64, device="cuda")
+    op.fill_uniform_local(z, 5)
+    y0, y1 = torch.empty_like(z), torch.empty_like(z)
+    good = spd_field(cfg.ncell, 2)
+    op.set_diffusion(torch.from_numpy(good.reshape(-1)).cuda())
+    op.apply(z, y0)
+    bad = spd_field(cfg.ncell, 9)
+    bad[4, 0, 1] += 0.5                      # not symmetric: rejected
+    with pytest.raises(dg.DGError):
+        op.set_diffusion(torch.from_numpy(bad.reshape(-1)).cuda())
+    op.apply(z, y1)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+    yo, _ = o1.apply(*cfg.args(), z.cpu().numpy(), Dcell=good)
+    assert rel(y1.cpu().numpy(), yo) < TOL
+    op.close()
+
+
+def test_misaligned_vectors_rejected():
+    """16-byte alignment is checked at the boundary (include/dg.h), not left to fault."""
+    from paper_1711_10885_b200 import dg
+    cfg = configs.small(7, ncells=(2, 2, 2))
+    op = dg.from_config(cfg)
+    buf = torch.zeros(op.ndofs + 2, dtype=torch.float64, device="cuda")
+    y = torch.empty(op.ndofs, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        op.apply(buf[1:1 + op.ndofs], y)
+    L = dg.lib()
+    assert L.dg_apply(op._h, dg._ptr(buf[1:]), dg._ptr(y), None) == dg.DG_EINVAL
+    assert L.dg_apply(op._h, dg._ptr(buf[2:]), dg._ptr(y), None) == dg.DG_OK
+    torch.cuda.synchronize()
     op.close()
 
 

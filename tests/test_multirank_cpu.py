@@ -1,13 +1,17 @@
 """Multi-rank host logic on CPU (no GPU): world_size 2 (and 4) over torch.distributed gloo.
 
-What runs on the GPU box with NCCL (bench.py --gpus N, dg_apply with nranks > 1) has three
+What runs on the GPU box with NCCL (bench.py --gpus N, dg_apply with nranks > 1) has
 host-side ingredients that can be exercised here:
-  * the block partition (dg_partition in the C ABI, the same rule dg_setup uses),
-  * the halo layout: the face layer of a rank's box, ordered by the two tangential local
-    coordinates (t1 fastest) as documented in include/dg.h and packed by pack_kernel,
-  * the exchange: one send/recv pair per partition face.
+  * the block partition (dg_partition in the C ABI, the same rule dg_setup uses), including
+    periodic wrap ranks,
+  * the exchange pattern: one send/recv pair per partition face, the face layer ordered by the
+    two tangential local coordinates (t1 fastest) as in include/dg.h.
 Each rank computes its own cells with the ORACLE (O-1, sampled mode) from its own z plus the
-received ghost layers; the gathered result must equal the single-process oracle bit for bit.
+neighbour ranks' face layers. The oracle evaluates neighbour traces itself, so what travels
+here is the layer's z blocks; the library ships the face traces of those blocks (2 n^2 per
+cell, include/dg.h), whose layout is pinned on the GPU against the oracle's own tables
+(tests/test_gpu_loopback.py::test_trace_pack_layout_vs_oracle_tables). The gathered result
+must equal the single-process oracle bit for bit.
 """
 import os
 import socket
@@ -33,7 +37,7 @@ def tangential(q):
 
 
 def pack_layer(zloc, nloc, n3, face):
-    """Numpy statement of the halo layout (include/dg.h: layer cells, t1 fastest)."""
+    """The face layer's z blocks, layer cells t1 fastest (the order of include/dg.h)."""
     q, s = face >> 1, face & 1
     t1, t2 = tangential(q)
     Z = zloc.reshape(nloc[2], nloc[1], nloc[0], n3)      # [z][y][x][j]

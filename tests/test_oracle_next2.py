@@ -87,3 +87,56 @@ def test_consistency_linear_velocity(k):
     # control: the same data with the field dropped (constant b = 0) is not consistent
     y0, _ = o1.apply(*args, zs)
     assert rel(y0, F) > 1e-6
+
+
+# ---- the Taylor-Green field itself (eq:2), pinned independently of the
+# operator: hand values at points where every factor is 0 or +-1, div b = 0 by central
+# differences (the field of a transport step must be divergence free, PAPER.md:334-341 relies
+# on it), and 2 pi periodicity on the paper's box (-pi, pi)^3.
+TG_HAND = [  # x -> b, each factor of each component 0 or +-1 (a sign slip on any factor shows)
+    ((0.0, -np.pi / 2, -np.pi / 2), (1.0, 0.0, 0.0)),     # cos 0 sin(pi/2) sin(pi/2)
+    ((np.pi / 2, 0.0, -np.pi / 2), (0.0, 0.5, 0.0)),      # 1/2 sin(pi/2) cos 0 sin(pi/2)
+    ((np.pi / 2, -np.pi / 2, 0.0), (0.0, 0.0, 0.5)),      # 1/2 sin(pi/2) sin(pi/2) cos 0
+    ((np.pi, np.pi / 2, np.pi / 2), (-1.0, 0.0, 0.0)),    # cos pi sin(-pi/2) sin(-pi/2)
+    ((-np.pi / 2, 0.0, np.pi / 2), (0.0, 0.5, 0.0)),      # 1/2 sin(-pi/2) cos 0 sin(-pi/2)
+]
+
+
+def _tg_fields():
+    return {"O-1 (C)": lambda x: o1.velocity(1, x),
+            "O-2 (numpy)": lambda x: o2.taylor_green(np.asarray(x).T).T}
+
+
+@pytest.mark.parametrize("which", ["O-1 (C)", "O-2 (numpy)"])
+def test_taylor_green_hand_values(which):
+    f = _tg_fields()[which]
+    for x, b in TG_HAND:
+        got = f(np.array([x]))[0]
+        assert np.allclose(got, b, rtol=0, atol=1e-15), (which, x, got, b)
+
+
+@pytest.mark.parametrize("which", ["O-1 (C)", "O-2 (numpy)"])
+def test_taylor_green_divergence_free_and_periodic(which):
+    f = _tg_fields()[which]
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-np.pi, np.pi, (64, 3))
+    h = 1e-5
+    div = np.zeros(x.shape[0])
+    for q in range(3):
+        e = np.zeros(3)
+        e[q] = h
+        div += (f(x + e)[:, q] - f(x - e)[:, q]) / (2 * h)
+    assert np.abs(div).max() < 1e-9
+    # not trivially zero: each partial derivative is O(1) somewhere
+    dq = (f(x + [h, 0, 0])[:, 0] - f(x - [h, 0, 0])[:, 0]) / (2 * h)
+    assert np.abs(dq).max() > 0.3
+    for q in range(3):
+        e = np.zeros(3)
+        e[q] = 2 * np.pi
+        assert np.abs(f(x + e) - f(x)).max() < 1e-14
+
+
+def test_o1_linear_field_and_amplitudes():
+    x = np.array([[0.5, -2.0, 3.0]])
+    assert np.array_equal(o1.velocity(2, x), [[-2.0, 3.0, 0.5]])          # b = (x2, x3, x1)
+    assert np.array_equal(o1.velocity(2, x, (2.0, 0.5, -1.0)), [[-4.0, 1.5, -0.5]])
