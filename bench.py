@@ -4,19 +4,23 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
 
 One step = one dg_apply (the whole hot path: volume, interior-face and
-boundary-face terms, plus the halo exchange when N > 1) over the workload's
-synthetic seeded input already resident in HBM. At N = 1 the workload is
-BASELINE.json configs[2] ("C3": 128x64x64 cells, k = 7, 268M DOFs). For N > 1
-(launched by torchrun, one rank per GPU, NCCL) each GPU keeps C3's block
-(weak scaling, reading C-12'), block-partitioned 2x1x1 / 2x2x1 / 2x2x2.
+boundary-face terms, plus the face-trace halo exchange when N > 1) over the
+workload's synthetic seeded input already resident in HBM. At N = 1 the workload
+is BASELINE.json configs[2] ("C3": 128x64x64 cells, k = 7, 268M DOFs). For N > 1
+(one rank per GPU, NCCL; `python bench.py --gpus N` launches the ranks itself
+through torch.distributed.run when WORLD_SIZE is unset) the default is
+BASELINE configs[4]'s weak scaling, 128x128x64 cells per GPU (C5 weak), block-
+partitioned 2x1x1 / 2x2x1 / 2x2x2; `--workload c5strong` is its strong scaling
+(256x128x128 cells in total).
 
 Rank 0 prints ONE JSON line. `value` is whole-job DOFs/s (max-over-ranks device
 time of K steps, CUDA events, barrier + synchronize on both sides); `e2e` is the
 same metric through the C ABI with pinned HOST buffers (dg_apply_host: H2D of z,
-apply, D2H of y inside the timed region); `roofline` is the cell kernel's
-model-flop rate against the derived B200 FP64 peak; `cpu_baseline` is the oracle
-O-1 timed on the host cores on a bounded sample of cells (N = 1, rank 0).
-`--impl reference` times that oracle as the reference arm.
+apply, D2H of y inside the timed region); `roofline` is the operator kernel's
+EXECUTED FP64 rate (ncu flop count of this build x DOFs / kernel time) against
+the derived B200 FP64 peak (the paper-model rate is `model_tflops`);
+`cpu_baseline` is the oracle O-1 timed on the host cores on a bounded sample of
+cells (N = 1, rank 0). `--impl reference` times that oracle as the reference arm.
 """
 import argparse
 import json
@@ -46,7 +50,7 @@ def env_int(name, default):
 
 def workload(name, world):
     if name in (None, "", "default"):
-        return configs.c3() if world == 1 else configs.c3_weak(world)
+        return configs.c3() if world == 1 else configs.c5_weak(world)
     name = name.lower()
     if name == "c3weak":
         return configs.c3_weak(world)
@@ -183,18 +187,28 @@ def cpu_model():
     return "unknown CPU"
 
 
-def load_ncu(cfg):
-    """The committed ncu --set full summary of the cell kernel for this workload (or {})."""
+def load_ncu(cfg, kname):
+    """The committed ncu --set full summary of this workload's operator kernel, or ({}, why).
+    Only a capture of THIS build (paper_1711_10885_b200.build.kernel_hash) and of the same kernel
+    and per-rank DOF count is used; at N > 1 the N = 1 capture of the same per-GPU block."""
+    from paper_1711_10885_b200.build import kernel_hash
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        ent = d.get(cfg.name)
-        if ent and ent.get("ndofs") == cfg.ndofs // max(1, cfg.parts[0] * cfg.parts[1] * cfg.parts[2]):
-            return ent
-    except Exception:
-        pass
-    return {}
+    except Exception as e:  # noqa: BLE001
+        return {}, "no ncu summary (%s)" % e
+    name = cfg.name.replace("-P%d" % (cfg.parts[0] * cfg.parts[1] * cfg.parts[2]), "-P1") \
+        if cfg.name.startswith("C5-weak") else cfg.name
+    ent = d.get(name)
+    if not ent:
+        return {}, "no ncu capture of %s" % name
+    if ent.get("build_hash") != kernel_hash():
+        return {}, "ncu capture of %s belongs to build %s, not %s" % (name, ent.get("build_hash"), kernel_hash())
+    if kname.split("<")[0] not in ent.get("kernel", ""):
+        return {}, "ncu capture of %s is of %s" % (name, ent.get("kernel"))
+    return ent, "profiles/ncu_full_summary.json[%s] (ncu --set full, --clock-control none, build %s)" % (
+        name, ent["build_hash"])
 
 
 def measured_peaks():
@@ -203,6 +217,75 @@ def measured_peaks():
             return json.load(f)
     except Exception:
         return {}
+
+
+def fp64_measured():
+    """The builder's FP64 microbenchmarks on this pool's B200 (profiles/r01_fp64_peaks.json)."""
+    out = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")) as f:
+            for line in f:
+                line = line.strip()
+                if not line:
+                    continue
+                d = json.loads(line)
+                if d.get("kernel") == "dfma":
+                    out["dfma"] = d["tflops"]
+                elif "DGEMM" in d.get("kernel", ""):
+                    out["dgemm"] = d["tflops_best"]
+    except Exception:
+        pass
+    return out
+
+
+def submesh_parity(cfg, op, y, rank, dev, count=6):
+    """Partition invariance on this run's own output (SURVEY 8(e) evidence 4), with the product
+    path only: for sampled cells of this rank -- one next to every partition face, the rest
+    random -- a SINGLE-rank operator on the (up to) 3x3x3-cell sub-box around the cell (same h,
+    coefficients and sigma; a clipped side is the global Dirichlet boundary) applied to the same
+    seeded z (inputs.uniform_cells by global cell index) must reproduce the cell's y block.
+    Returns (cells checked, max |dy| / max |y_sub|, bitwise)."""
+    import torch
+    from paper_1711_10885_b200 import dg
+    if any(cfg.periodic) or cfg.dfield_seed >= 0 or cfg.bkind:
+        return 0, None, None
+    G, n3 = cfg.ncells, cfg.n3
+    h = [(cfg.hi[q] - cfg.lo[q]) / G[q] for q in range(3)]
+    lo, cnt = op.cell_lo, op.cell_cnt
+    rng = np.random.default_rng(1000 + rank)
+    picks = []
+    for f in range(6):
+        if op.halo_info(f)[0] < 0:
+            continue
+        q, sd = f >> 1, f & 1
+        l = [int(rng.integers(0, cnt[r])) for r in range(3)]
+        l[q] = cnt[q] - 1 if sd else 0
+        picks.append(l)
+    while len(picks) < count:
+        picks.append([int(rng.integers(0, cnt[r])) for r in range(3)])
+    worst, bitwise = 0.0, True
+    yv = y.view(-1, n3)
+    for l in picks:
+        g = [lo[r] + l[r] for r in range(3)]
+        slo = [max(0, g[r] - 1) for r in range(3)]
+        shi = [min(G[r], g[r] + 2) for r in range(3)]
+        sc = [shi[r] - slo[r] for r in range(3)]
+        sub = dg.Operator(sc, [cfg.lo[r] + slo[r] * h[r] for r in range(3)],
+                          [cfg.lo[r] + shi[r] * h[r] for r in range(3)], cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma,
+                          device=dev.index)
+        gz, gy, gx = np.meshgrid(np.arange(slo[2], shi[2]), np.arange(slo[1], shi[1]), np.arange(slo[0], shi[0]),
+                                 indexing="ij")
+        cells = (gx + G[0] * (gy + G[1] * gz)).reshape(-1)
+        zs = torch.from_numpy(inputs.uniform_cells(cells, n3, cfg.seed).reshape(-1)).to(dev)
+        ys = torch.empty_like(zs)
+        sub.apply(zs, ys)
+        mid = (g[0] - slo[0]) + sc[0] * ((g[1] - slo[1]) + sc[1] * (g[2] - slo[2]))
+        a = ys.view(-1, n3)[mid]
+        b = yv[l[0] + cnt[0] * (l[1] + cnt[1] * l[2])]
+        worst = max(worst, float((a - b).abs().max() / ys.abs().max()))
+        bitwise = bitwise and bool(torch.equal(a, b))
+        sub.close()
+    return len(picks), worst, bitwise
 
 
 def vs_baseline(cfg, value):
@@ -282,6 +365,10 @@ def run_ours(args, rank, world, local_rank):
     kname = ("dg_vb_kernel<%d,%d>" % (cfg.k + 1, cfg.m or cfg.k + 1) if (cfg.bkind or (cfg.m and cfg.m != cfg.k + 1))
              else ("dg_gen_kernel<%d>" % (cfg.k + 1) if general else "dg_cell_kernel<%d>" % (cfg.k + 1)))
     info = op.kernel_info()
+    transport, comm_ranks = op.comm_info()
+    if world > 1 and rank == 0:
+        print("[bench] halo transport %s: communicator of %d ranks (torch.distributed world %d)"
+              % (transport, comm_ranks, world), file=sys.stderr, flush=True)
     z = torch.empty(op.ndofs, dtype=torch.float64, device=dev)
     y = torch.empty_like(z)
     op.fill_uniform_local(z, cfg.seed)
@@ -303,10 +390,12 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed region: %d x dg_apply" % args.steps)
     e0.record(stream)
     for _ in range(args.steps):
         op.apply(z, y)
     e1.record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     barrier()
     t_local = e0.elapsed_time(e1) * 1e-3
@@ -345,38 +434,41 @@ def run_ours(args, rank, world, local_rank):
     value = total_dofs * args.steps / t
     ms_per_step = t / args.steps * 1e3
 
-    # ---- roofline of the dominant kernel (the fused cell kernel)
+    # ---- roofline of the dominant kernel (the fused operator kernel): EXECUTED FP64 flops of this
+    # build (ncu) per launch / the kernel's time per apply, against the FP64 peak derived from the
+    # unit counts and clock (B200_PROFILING.md: 148 SMs; 64 FP64 FMA/clk/SM; clocks.max.sm)
     per_dof = perfmodel.flopdof(3, cfg.k)
-    flops_launch_rank = per_dof * op.ndofs
-    kern_t = tk / args.steps   # one cell-kernel pass over all local cells per apply (2 launches at N > 1)
-    achieved = flops_launch_rank / kern_t / 1e12
-    peak = perfmodel.fp64_peak_tflops(clk["sm_max_mhz"] or 1965.0)
-    ncu = load_ncu(cfg)
-    hbm_peak = None
-    try:
-        mp = measured_peaks()
-        hbm_peak = float(mp.get("hbm_copy_gbs") or mp.get("hbm_gbs") or mp.get("hbm", {}).get("copy_gbs"))
-    except Exception:
-        hbm_peak = None
-    traffic = ncu.get("dram_bytes_per_launch")
+    kern_t = tk / args.steps   # one operator pass over all local cells per apply (inner + shell at N > 1)
+    smax = clk["sm_max_mhz"] or 1965.0
+    peak = perfmodel.fp64_peak_tflops(smax)
+    meas = fp64_measured()
+    ncu, ncu_src = load_ncu(cfg, kname)
     exec_per_dof = ncu.get("executed_flops_per_dof")
-    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+    traffic = ncu.get("dram_bytes_per_launch")
+    achieved = exec_per_dof * op.ndofs / kern_t / 1e12 if exec_per_dof else None
+    model_tf = per_dof * op.ndofs / kern_t / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if achieved else None,
             "traffic": traffic,
+            "flops_basis": ("executed FP64 flops of this build: ncu 2 DFMA + DADD + DMUL = %.1f flop/DOF x %d DOFs "
+                            "per apply" % (exec_per_dof, op.ndofs)) if exec_per_dof else
+                           ("unavailable: %s" % ncu_src),
+            "peak_basis": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x %.0f MHz (MEASURED_PEAKS.json has no FP64 "
+                          "entry; B200_PROFILING.md unit counts)" % smax,
+            "frac_of_measured_dfma": achieved / meas["dfma"] if (achieved and "dfma" in meas) else None,
+            "frac_of_measured_dgemm": achieved / meas["dgemm"] if (achieved and "dgemm" in meas) else None,
+            "measured_fp64_tflops": dict(meas, source="profiles/r01_fp64_peaks.json (tools/fp64_peaks.cu, "
+                                                       "torch float64 matmul)"),
+            "model_tflops": model_tf, "model_frac": model_tf / peak,
+            "model_basis": "paper model FLOPDOF_vol + FLOPDOF_face(3,%d) = %.1f flop/DOF (PAPER.md:675-676); the "
+                           "kernel executes fewer (collocation derivatives, even-odd stages), so model_frac can "
+                           "exceed 1" % (cfg.k, per_dof),
             "traffic_algorithmic_bytes": 16.0 * op.ndofs,
             "hbm_gbs_at_traffic": (traffic / kern_t / 1e9) if traffic else None,
-            "hbm_frac_of_measured_copy": ((traffic / kern_t / 1e9) / hbm_peak) if (traffic and hbm_peak) else None,
             "ncu_fp64_pipe_pct": ncu.get("fp64_pipe_pct"), "ncu_smem_wavefront_pct": ncu.get("smem_wavefront_pct"),
             "ncu_issue_active_pct": ncu.get("issue_active_pct"),
-            "executed_flops_per_dof": exec_per_dof,
-            "executed_achieved": (exec_per_dof * op.ndofs / kern_t / 1e12) if exec_per_dof else None,
-            "executed_frac": (exec_per_dof * op.ndofs / kern_t / 1e12 / peak) if exec_per_dof else None,
-            "ncu_source": "profiles/ncu_full_summary.json (ncu --set full, --clock-control none)" if ncu else None,
+            "ncu_source": ncu_src,
             "kernel": "%s (FP64 DFMA pipe)" % kname,
-            "flops_basis": "paper model FLOPDOF_vol+FLOPDOF_face(3,%d) = %.1f flop/DOF x %d DOFs per launch "
-                           "(PAPER.md:675-676); the kernel executes fewer (collocation variant, DESIGN.md)"
-                           % (cfg.k, per_dof, op.ndofs),
-            "peak_basis": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x %.0f MHz (B200_PROFILING.md SM count/clock; "
-                          "MEASURED_PEAKS.json has no FP64 entry)" % (clk["sm_max_mhz"] or 1965.0),
             "kernel_ms": kern_t * 1e3}
 
     # ---- end to end through the C ABI with pinned host buffers
@@ -405,16 +497,33 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         zn = z.cpu().numpy()
         rate, cores, text, _, cells, yo = cpu_oracle_rate(cfg, zn, args.cpu_seconds)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": text}
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": "extrapolated: DOF/s measured on a sample -- " + text}
         # the same oracle blocks double as a parity check of this run's y (reading C-14)
         yg = y.view(-1, cfg.n3)[torch.from_numpy(cells).to(dev)].cpu().numpy()
         ymax = float(y.abs().max())
         parity = {"vs": "O-1 on the cpu_baseline sample (%d cells)" % cells.size,
                   "max_abs_err_over_max_abs_y": float(np.abs(yg - yo).max() / ymax), "tolerance": 1e-12}
 
+    if world > 1 or args.submesh_check:
+        nchk, worst, bitw = submesh_parity(cfg, op, y, rank, dev)
+        if nchk:
+            tt = torch.tensor([worst, 0.0 if bitw else 1.0, float(nchk)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            sub = {"vs": "single-rank GPU operator on the 3x3x3-cell sub-box around sampled cells (one next to "
+                         "every partition face per rank; partition invariance, SURVEY 8(e))",
+                   "cells_per_rank": nchk, "max_abs_err_over_max_abs_y": float(tt[0]),
+                   "bitwise": bool(tt[1] == 0.0), "tolerance": 1e-12}
+            if parity is None:
+                parity = sub
+            else:
+                parity["partition_invariance"] = sub
+
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+               "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+               "scaling": "strong" if cfg.name.startswith("C5-strong") else "weak",
                "vs_baseline": vs_baseline(cfg, value), "dtype": "f64",
                "data": "synthetic (seeded counter-based uniform[-1,1] z, C-13)",
                "config": workload_desc(cfg, world),
@@ -422,18 +531,34 @@ def run_ours(args, rank, world, local_rank):
                "roofline": roof, "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "clocks": clk,
                "step_ms": {"mean": ms_per_step, "min": min(step_ms) if step_ms else None,
                            "median": float(np.median(step_ms)) if step_ms else None},
-               "gpu_launches": args.steps * (info["launches_per_apply"] if world == 1 else
-                                             (2 + sum(1 for f in range(6) if op.halo_info(f)[0] >= 0))),
-               "kernel_info": info}
+               "gpu_launches": args.steps * info["launches_per_apply"],
+               "kernel_info": info,
+               "comm": {"transport": transport, "nranks": comm_ranks,
+                        "halo": "face traces, 2 n^2 doubles per partition-face cell (%d B per cell at k=%d)"
+                                % (16 * (cfg.k + 1) ** 2, cfg.k) if world > 1 else None}}
         if world > 1:   # the exchange's cost = t(apply) - t(apply with the halo exchange skipped)
             out["halo_ablation"] = {"ms_per_apply": t / args.steps * 1e3,
                                     "ms_per_apply_no_exchange": tk / args.steps * 1e3,
-                                    "what": "same applies with DG_HALO_EXTERNAL (stale receive buffers, timing only)"}
+                                    "what": "same applies with DG_HALO_EXTERNAL (no trace pack, no exchange; "
+                                            "stale receive buffers, timing only)"}
         print(json.dumps(out), flush=True)
     op.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def spawn_ranks(n):
+    """`python bench.py --gpus N` without torchrun: launch the N ranks (one process per GPU)
+    through torch.distributed.run on this node, exactly as the driver does, and return its code."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -451,12 +576,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline sample budget")
     ap.add_argument("--ref-seconds", type=float, default=120.0, help="reference arm total budget")
+    ap.add_argument("--submesh-check", action="store_true", help="partition-invariance check also at N = 1")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
-    if world != args.gpus and world == 1 and args.gpus > 1:
-        raise SystemExit("--gpus %d needs torchrun (one process per GPU)" % args.gpus)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

@@ -240,6 +240,11 @@ int dg_nccl_unique_id(void* out128);
    timeout -> DG_ENCCL). */
 int dg_fabric_id(void* out128);
 
+/* The halo transport of this context: transport 0 = none (single rank or DG_HALO_EXTERNAL only),
+   1 = NCCL, 2 = in-process fabric; nranks = the communicator's rank count as NCCL reports it
+   (ncclCommCount), else the dg_setup nranks. */
+int dg_comm_info(const dg_ctx* ctx, int* transport, int* nranks);
+
 /* Library / kernel facts for the harness: kernel launches per dg_apply, threads and
    cells per CTA, dynamic shared memory per CTA, registers per thread, of the kernel the
    next apply launches (the general-coefficient kernel after dg_set_diffusion / full D). */

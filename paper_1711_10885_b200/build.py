@@ -7,6 +7,7 @@ tables, dispatch, NCCL loader and auxiliary kernels; objects compile in parallel
 """
 import argparse
 import concurrent.futures as cf
+import hashlib
 import os
 import subprocess
 import sys
@@ -39,6 +40,21 @@ def _sources():
         extra = ["-x", "cu"] if name.endswith(".cpp") else []
         jobs.append((os.path.join(CSRC, name), os.path.join(OBJ, base + ".o"), extra))
     return jobs
+
+
+def kernel_hash():
+    """Hash of everything that determines the compiled operator kernels (kernel headers, their
+    translation units, the shared declarations, the tables, the flags): the key under which
+    profiles/ncu_full_summary.json stores executed-flop counts, so bench.py never pairs a timing
+    with the counts of another build. Host-only files (the ABI, dispatch, transport) are not in it."""
+    h = hashlib.sha256()
+    h.update(" ".join(ARCH + FLAGS[:3]).encode())
+    for f in sorted(os.listdir(CSRC)):
+        if f.endswith(".cuh") or f.endswith("_inst.cu") or f in ("dg_internal.h", "tables.cpp"):
+            h.update(f.encode())
+            with open(os.path.join(CSRC, f), "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()[:16]
 
 
 def _deps():

@@ -12,6 +12,8 @@
 #include <vector>
 
 #include "dg_internal.h"
+#include <nvtx3/nvToolsExt.h>   // header-only; ranges are no-ops unless a profiler (nsys) injects
+
 #include "dg_fabric.h"
 #include "dg_nccl.h"
 
@@ -24,7 +26,8 @@ struct dg_ctx {
     int64_t nloc[3] = {0, 0, 0}, gofs[3] = {0, 0, 0}, gcells[3] = {0, 0, 0};
     int64_t ndofs = 0;
     int nbr[6] = {-1, -1, -1, -1, -1, -1};
-    int64_t halo_count[6] = {0, 0, 0, 0, 0, 0};
+    int64_t halo_count[6] = {0, 0, 0, 0, 0, 0};   // doubles of face f's traces (layer cells x 2 n^2)
+    int64_t layer_cells[6] = {0, 0, 0, 0, 0, 0};  // cells of face f's layer
     double* sendbuf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     double* recvbuf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     bool partitioned = false;        // some face has a neighbour rank
@@ -325,7 +328,8 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
                 ctx->partitioned = true;
             }
             const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
-            ctx->halo_count[f] = ctx->nloc[t1] * ctx->nloc[t2] * 2 * ctx->n * ctx->n;   // face traces
+            ctx->layer_cells[f] = ctx->nloc[t1] * ctx->nloc[t2];
+            ctx->halo_count[f] = ctx->layer_cells[f] * 2 * ctx->n * ctx->n;   // face traces
         }
 
     // kernel constants (eq:gauss_points; penalty reading C-4)
@@ -450,7 +454,7 @@ static int alloc_dfield(dg_ctx* ctx)
     if (!ctx->dbad && cudaMalloc(&ctx->dbad, sizeof(int)) != cudaSuccess) return DG_ENOMEM;
     for (int f = 0; f < 6; ++f) {
         if (ctx->nbr[f] < 0 || ctx->dsend[f]) continue;
-        const size_t bytes = (size_t)(ctx->halo_count[f] / ctx->n3) * 6 * sizeof(double);
+        const size_t bytes = (size_t)ctx->layer_cells[f] * 6 * sizeof(double);
         if (cudaMalloc(&ctx->dsend[f], bytes) != cudaSuccess || cudaMalloc(&ctx->drecv[f], bytes) != cudaSuccess ||
             cudaMalloc(&ctx->drecv_next[f], bytes) != cudaSuccess)
             return DG_ENOMEM;
@@ -575,7 +579,7 @@ extern "C" int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags
         DG_CUDA(launch_dfield_const(ctx->dfield_next, ctx->Dconst, ncell, s));
         for (int f = 0; f < 6; ++f)
             if (ctx->drecv_next[f])
-                DG_CUDA(launch_dfield_const(ctx->drecv_next[f], ctx->Dconst, ctx->halo_count[f] / ctx->n3, s));
+                DG_CUDA(launch_dfield_const(ctx->drecv_next[f], ctx->Dconst, ctx->layer_cells[f], s));
     } else {
         DG_CUDA(cudaMemsetAsync(ctx->dbad, 0, sizeof(int), s));
         // physical tensors; on an affine mesh each is mapped to |J| J^-1 D J^-T on the fly
@@ -595,7 +599,7 @@ extern "C" int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags
                 if (ctx->nbr[f] >= 0) DG_CUDA(launch_pack(ctx->dfield_next, ctx->dsend[f], 6, ctx->nloc, f, s));
             if (!(flags & DG_HALO_EXTERNAL)) {
                 size_t cnt[6];
-                for (int f = 0; f < 6; ++f) cnt[f] = (size_t)(ctx->halo_count[f] / ctx->n3) * 6;
+                for (int f = 0; f < 6; ++f) cnt[f] = (size_t)ctx->layer_cells[f] * 6;
                 rc = exchange(ctx, ctx->dsend, ctx->drecv_next, cnt, s);
                 if (rc != DG_OK) return rc;
             }
@@ -702,6 +706,12 @@ struct Epi {             // store epilogue (KParams::epi)
     double a = 0.0, b = 1.0, s = 0.0;
 };
 
+// NVTX range of the enclosing scope (nsys timelines of the halo overlap)
+struct NvtxRange {
+    explicit NvtxRange(const char* s) { nvtxRangePushA(s); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, unsigned terms, cudaStream_t s,
                       const Epi* epi = nullptr, const int64_t* tasks = nullptr, int64_t ntasks = 0)
 {
@@ -737,12 +747,14 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         }
         return cuda_rc(launch_any(ctx, p, s));
     }
+    NvtxRange r_apply("dg_apply (partitioned)");
     // (iv) of SURVEY.md 3 / 8(e): the partition faces' traces are packed and exchanged on the comm
     // stream while the inner-box cells (no remote data) run on s; the shell cells follow the
     // receive. The pack is off s: it is launched first, so its few CTAs start ahead of the
     // inner kernel's wave, and nothing on s waits for it.
     const bool need_comm = !external && (p.mask & DG_INTERIOR_FACES);
     if (need_comm) {
+        NvtxRange r_comm("trace pack + exchange (comm stream)");
         DG_CUDA(cudaEventRecord(ctx->ev_z, s));
         DG_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_z, 0));
         int rc = exchange_prepare(ctx, ctx->comm_stream);
@@ -757,7 +769,11 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
     // inner cells: no remote data
     set_box(p, ctx->inner_lo, ctx->inner_cnt);
     auto launch = [&](const KParams& kp) { return launch_any(ctx, kp, s); };
-    DG_CUDA(launch(p));
+    {
+        NvtxRange r_inner("inner-box cells");
+        DG_CUDA(launch(p));
+    }
+    NvtxRange r_shell("shell cells (after the receive)");
     if (need_comm) DG_CUDA(cudaStreamWaitEvent(s, ctx->ev_recv, 0));
     p.task_list = ctx->shell;
     p.ntasks = ctx->nshell;
@@ -1070,6 +1086,26 @@ extern "C" int dg_fill_uniform_cells(dg_ctx* ctx, double* dst, int per_cell, uin
     return cuda_rc(launch_fill_uniform_local(dst, per_cell, ctx->nloc, ctx->gofs, ctx->gcells, seed, (cudaStream_t)stream));
 }
 
+extern "C" int dg_comm_info(const dg_ctx* ctx, int* transport, int* nranks)
+{
+    if (!ctx) return DG_EINVAL;
+    int t = 0, n = ctx->nranks;
+    if (ctx->fabric) {
+        t = 2;
+    } else if (ctx->comm) {
+        t = 1;
+        const NcclApi* api = nccl_api();
+        int c = 0;
+        if (api && api->ncclCommCount) {
+            if (api->ncclCommCount(ctx->comm, &c) != 0) return DG_ENCCL;
+            n = c;
+        }
+    }
+    if (transport) *transport = t;
+    if (nranks) *nranks = n;
+    return DG_OK;
+}
+
 extern "C" int dg_get_kernel_info(const dg_ctx* ctx, dg_kernel_info* info)
 {
     if (!ctx || !info) return DG_EINVAL;
@@ -1078,7 +1114,7 @@ extern "C" int dg_get_kernel_info(const dg_ctx* ctx, dg_kernel_info* info)
     const int rc = ctx->vb ? vb_launch_info(ctx->k, ctx->m, &li)
                            : (ctx->general ? gen_launch_info(ctx->k, &li) : cell_launch_info(ctx->k, &li));
     if (rc != 0) return DG_ECUDA;
-    info->launches_per_apply = ctx->partitioned ? 2 : 1;
+    info->launches_per_apply = ctx->partitioned ? 3 : 1;   // trace pack, inner box, shell
     info->cells_per_cta = li.cells_per_cta;
     info->threads_per_cta = li.threads;
     info->smem_bytes = li.smem;

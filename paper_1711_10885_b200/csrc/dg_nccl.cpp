@@ -30,6 +30,7 @@ const NcclApi* nccl_api()
     DG_SYM(ncclRecv);
     DG_SYM(ncclGroupStart);
     DG_SYM(ncclGroupEnd);
+    DG_SYM(ncclCommCount);
 #undef DG_SYM
     if (!g_api.ncclGetUniqueId || !g_api.ncclCommInitRank || !g_api.ncclSend || !g_api.ncclRecv ||
         !g_api.ncclGroupStart || !g_api.ncclGroupEnd || !g_api.ncclCommDestroy) {

@@ -21,6 +21,7 @@ struct NcclApi {
     ncclResult_t (*ncclRecv)(void*, size_t, int, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*ncclGroupStart)();
     ncclResult_t (*ncclGroupEnd)();
+    ncclResult_t (*ncclCommCount)(const ncclComm_t, int*);   // optional
 };
 
 const NcclApi* nccl_api();   // nullptr if NCCL cannot be loaded

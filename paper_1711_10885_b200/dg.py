@@ -23,7 +23,7 @@ EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residu
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
             "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage", "dg_set_velocity", "dg_set_quadrature",
-            "dg_set_affine", "dg_matrix_size", "dg_assemble", "dg_matrix_apply", "dg_fabric_id"]
+            "dg_set_affine", "dg_matrix_size", "dg_assemble", "dg_matrix_apply", "dg_fabric_id", "dg_comm_info"]
 
 
 class DGError(RuntimeError):
@@ -74,6 +74,7 @@ def lib():
         L.dg_fill_uniform_local.argtypes = [vp, vp, u64, vp]
         L.dg_nccl_unique_id.argtypes = [vp]
         L.dg_fabric_id.argtypes = [vp]
+        L.dg_comm_info.argtypes = [vp, vp, vp]
         L.dg_get_kernel_info.argtypes = [vp, ctypes.POINTER(KernelInfo)]
         L.dg_partition.argtypes = [ctypes.POINTER(MeshDesc), ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.dg_set_diffusion.argtypes = [vp, vp, ctypes.c_uint, vp]
@@ -311,6 +312,12 @@ class Operator:
 
     def halo_pack(self, z, stream=None):
         _check(lib().dg_halo_pack(self._h, _ptr(z), _stream(stream)), "dg_halo_pack")
+
+    def comm_info(self):
+        """(transport, nranks): transport 'none' | 'nccl' | 'fabric', nranks as the communicator reports."""
+        t, n = ctypes.c_int(), ctypes.c_int()
+        _check(lib().dg_comm_info(self._h, ctypes.byref(t), ctypes.byref(n)), "dg_comm_info")
+        return ("none", "nccl", "fabric")[t.value], n.value
 
     # -- info / lifetime ----------------------------------------------------------------------------
     def kernel_info(self):

@@ -11,7 +11,7 @@ GLOBAL cell-major DOF index g (reading C-13), all arithmetic mod 2^64:
     z = (x >> 11) * 2^-53 * 2 - 1
 
 The same generator exists as a CUDA kernel in the library (dg_fill_uniform,
-paper_1711_10885_b200/csrc/dg_inputs.cu) so multi-GB inputs can be produced in
+paper_1711_10885_b200/csrc/dg_aux.cu) so multi-GB inputs can be produced in
 HBM; tests check the two bit for bit. It is exact in FP64 and independent of
 the partition, so a rank can generate its own block from global indices.
 """

@@ -353,8 +353,8 @@ def test_general_kernel_symmetry_and_energy():
     yw = run(cfg, w, (1, 1, 1), Dcell=Dc)
     assert abs(w @ yz - z @ yw) < 1e-13 * abs(w @ yz)
     cfg2 = configs.small(3, ncells=(4, 3, 2), hi=(1.0, 0.75, 0.5), D=(0,) * 9, b=(1.0, -0.5, 0.25), c=0.0)
-    op = dg.Operator(cfg2.ncells, cfg2.lo, cfg2.hi, cfg2.k, (0, 0.1, 0, 0.1, 0, 0, 0, 0, 0), cfg2.b, 0.0,
-                     cfg2.sigma, bc=dg.bc_from_periodic((1, 1, 1)))   # off-diagonal D: the general kernel
+    op = dg.Operator(cfg2.ncells, cfg2.lo, cfg2.hi, cfg2.k, (0.1, 0.1, 0, 0.1, 0.1, 0, 0, 0, 0), cfg2.b, 0.0,
+                     cfg2.sigma, bc=dg.bc_from_periodic((1, 1, 1)))   # off-diagonal (PSD) D: the general kernel
     op.set_diffusion(torch.zeros(cfg2.ncell * 9, dtype=torch.float64, device="cuda"))
     zz = inputs.uniform(cfg2.ndofs, 3)
     zt = torch.from_numpy(zz).cuda()

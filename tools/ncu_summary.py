@@ -21,6 +21,9 @@ KEYS = {
     "dfma_per_cycle": "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed",
     "dadd_per_cycle": "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed",
     "dmul_per_cycle": "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed",
+    "dfma_sum": "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+    "dadd_sum": "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+    "dmul_sum": "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
     "cycles": "sm__cycles_elapsed.avg",
     "clock_hz": "sm__cycles_elapsed.avg.per_second",
     "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
@@ -73,7 +76,9 @@ def summarize(d):
     if s["dram_read"] is not None and s["dram_write"] is not None:
         s["dram_bytes_per_launch"] = s["dram_read"] + s["dram_write"]
     cyc = s.get("cycles")
-    if cyc and s.get("dfma_per_cycle") is not None:
+    if s.get("dfma_sum") is not None:       # thread-level FP64 instruction counts (flops = 2 DFMA + DADD + DMUL)
+        s["executed_fp64_flops"] = 2 * s["dfma_sum"] + (s.get("dadd_sum") or 0) + (s.get("dmul_sum") or 0)
+    elif cyc and s.get("dfma_per_cycle") is not None:
         s["executed_fp64_flops"] = cyc * (2 * s["dfma_per_cycle"] + (s.get("dadd_per_cycle") or 0)
                                           + (s.get("dmul_per_cycle") or 0))
     stalls = []
@@ -93,10 +98,15 @@ def main():
     ap.add_argument("--name", default=None)
     ap.add_argument("--ndofs", type=int, default=None)
     ap.add_argument("--json", default=None, help="merge {name: summary} into this JSON file")
+    ap.add_argument("--kernel", default=None, help="substring of the kernel name to summarise")
     args = ap.parse_args()
     launches = raw(args.rep)
-    cell = [d for d in launches if any(k in d.get("Kernel Name", ("", ""))[0] for k in ("dg_cell", "dg_reg", "dg_gen", "dg_vb"))] or launches
+    keys = (args.kernel,) if args.kernel else ("dg_cell", "dg_reg", "dg_gen", "dg_vb", "dg_geo")
+    cell = [d for d in launches if any(k in d.get("Kernel Name", ("", ""))[0] for k in keys)] or launches
     s = summarize(cell[0])
+    sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+    from paper_1711_10885_b200.build import kernel_hash
+    s["build_hash"] = kernel_hash()     # the build this capture belongs to (bench.py checks it)
     if args.ndofs:
         s["ndofs"] = args.ndofs
         if s.get("executed_fp64_flops"):
