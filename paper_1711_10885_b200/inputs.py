@@ -69,3 +69,48 @@ def tensor_field_from_uniforms(u6):
 def tensor_field_cells(cells, seed):
     """Host tensors [len(cells), 9] of the Problem A field for explicit global cell indices."""
     return tensor_field_from_uniforms(uniform_cells(cells, 6, seed))
+
+
+# ---- multilinear meshes (NEXT-3: Problem C's "multilinear geometries", PAPER.md:957-961) -------
+# The paper does not print its meshes. The stand-in: the box's regular vertex grid with every
+# vertex moved by amp * h_q * U(seed, 3 g + q) in each direction q (g = the GLOBAL vertex index
+# ix + (Nx+1)(iy + (Ny+1) iz)); vertices on a Dirichlet side of the box keep their normal
+# coordinate (the domain stays the box); along a periodic direction the perturbation of vertex
+# N_q is that of vertex 0 (the grid stays periodic). amp <= 0.25 keeps every cell's Jacobian
+# determinant positive (each corner moves less than h/4 per direction).
+def vertex_grid(ncells, lo, hi, amp, seed, periodic=(0, 0, 0), box=None):
+    """Vertex coordinates [iz][iy][ix][3] of the global grid (or of the sub-box
+    box = ((i0, j0, k0), (i1, j1, k1)) of vertex indices, i1 exclusive; indices outside
+    0..N are wrapped on periodic directions, clamped otherwise)."""
+    N = [int(v) for v in ncells]
+    h = [(hi[q] - lo[q]) / N[q] for q in range(3)]
+    if box is None:
+        box = ((0, 0, 0), (N[0] + 1, N[1] + 1, N[2] + 1))
+    (i0, j0, k0), (i1, j1, k1) = box
+    ks, js, is_ = np.arange(k0, k1), np.arange(j0, j1), np.arange(i0, i1)
+    K, Jg, I = np.meshgrid(ks, js, is_, indexing="ij")
+    idx = [I, Jg, K]
+    out = np.empty(K.shape + (3,))
+    for q in range(3):
+        v = idx[q]
+        if periodic[q]:
+            shift = np.floor_divide(v, N[q])            # whole periods (a vertex index beyond the box)
+            base = np.mod(v, N[q])
+        else:
+            shift = np.zeros_like(v)
+            base = np.clip(v, 0, N[q])
+        out[..., q] = lo[q] + (base + shift * N[q]) * h[q]
+        if not periodic[q] and np.any((v < 0) | (v > N[q])):
+            out[..., q] += (v - base) * h[q]             # regular continuation outside a Dirichlet box
+    # perturbation by the wrapped vertex index
+    wr = []
+    for q in range(3):
+        v = idx[q]
+        wr.append(np.mod(v, N[q]) if periodic[q] else np.clip(v, 0, N[q]))
+    g = (wr[0] + (N[0] + 1) * (wr[1] + (N[1] + 1) * wr[2])).astype(np.uint64)
+    for q in range(3):
+        d = amp * h[q] * uniform_from_index(3 * g + np.uint64(q), seed)
+        if not periodic[q]:
+            d = np.where((wr[q] == 0) | (wr[q] == N[q]), 0.0, d)   # the box sides stay planar
+        out[..., q] += d
+    return out

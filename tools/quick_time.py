@@ -1,8 +1,12 @@
 """Quick device timing of dg_apply for one config (development aid; bench.py is the contract)."""
+import os
 import sys
 import time
 
 import torch
+
+if os.environ.get("PYTHONPATH"):
+    sys.path.insert(0, os.environ["PYTHONPATH"].split(":")[0])   # tools/ab_time.py: the tree under test first
 
 from paper_1711_10885_b200 import configs, dg
 
