@@ -159,6 +159,32 @@ int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags, void* str
  * set, or per-cell tensors already set). */
 int dg_set_affine(dg_ctx* ctx, const double J[9]);
 
+/* Multilinear (Q1) geometry (NEXT-3: the paper's Problem C has "multilinear geometries",
+ * PAPER.md:957-961; "the transformation x = mu_T(xhat) ... is a d-valued Q_1 finite element
+ * function and sum-factorization can be used to evaluate its values and derivatives at quadrature
+ * points"). Cell (i, j, k) of this rank's box is the image of [0,1]^3 under the
+ * trilinear map of its 8 vertices; every integral of eq:blf is evaluated with the map's Jacobian
+ * at each of the m^3 volume / m^2 face Gauss points (gradients J^-T grad_hat, dx = det J dxi,
+ * face normal cof(J) e_q / |cof(J) e_q|, dS = |cof(J) e_q| dxi; each side of a face with its own
+ * Jacobian; penalty <delta-, delta+> sigma with delta = nu^T D nu, sigma as given).
+ *   vert  caller-owned array (device or host) of the PADDED vertex grid of this rank's box:
+ *         (nloc[0]+3) x (nloc[1]+3) x (nloc[2]+3) vertices x 3 doubles (x, y, z), x fastest;
+ *         local vertex (i, j, k), -1 <= i <= nloc[0] + 1, at index
+ *         ((k+1) (nloc[1]+3) + (j+1)) (nloc[0]+3) + (i+1). The outer layer holds the vertices of
+ *         the neighbour cells across the box faces: on a partition face the neighbour rank's, on
+ *         a periodic side the periodic continuation (the far side's vertices shifted by the
+ *         period); unused on Dirichlet sides. The library copies it (not timed). NULL reverts to
+ *         the axis-aligned box mesh of dg_setup.
+ *   m     Gauss points per direction: k+1 (q = 2p), k+3 (q = 2p+4) or ceil((3k+5)/2) (Problem
+ *         C's q = 3p+4) while m <= 16.
+ * D (full symmetric PSD), b and c are the constants of dg_setup. Not combined with per-cell
+ * tensors, velocity fields, dg_set_affine or dg_ssp_stage (the mass of a multilinear cell is not
+ * Delta_T I).
+ * Errors: DG_EINVAL (m < k+1; a cell with det J <= 0 at a quadrature point or corner: the
+ * operator is then unchanged), DG_EUNSUPPORTED (uncompiled (k, m), the combinations above),
+ * DG_ENOMEM, DG_ECUDA. */
+int dg_set_geometry(dg_ctx* ctx, const double* vert, int m, void* stream);
+
 /* Velocity field b(x) evaluated at every quadrature point (NEXT-2: the paper's Taylor-Green
  * transport run):
  *   kind 0: the constant b of dg_setup (default);

@@ -26,6 +26,9 @@ NS = list(range(2, 12))
 # (n, m) pairs of the variable-velocity / over-integrated kernel: m = n (q = 2p) and m = n + 2
 # (q = 2p + 4, the paper's Taylor-Green run), k <= 8
 VB = [(n, m) for n in range(2, 10) for m in (n, n + 2)]
+# (n, m) pairs of the multilinear-geometry kernel: m = n, n + 2 and ceil((3k + 5) / 2) (q = 3p + 4,
+# PAPER.md:957-961), m <= 16 (the cell's shared memory)
+GEO = sorted({(n, m) for n in range(2, 12) for m in (n, n + 2, -(-(3 * n + 2) // 2)) if m <= 16})
 
 
 def _sources():
@@ -34,6 +37,9 @@ def _sources():
         jobs.append((os.path.join(CSRC, "dg_cell_inst.cu"), os.path.join(OBJ, "dg_cell_n%d.o" % n), ["-DDG_N=%d" % n]))
     for n, m in VB:
         jobs.append((os.path.join(CSRC, "dg_vb_inst.cu"), os.path.join(OBJ, "dg_vb_n%d_m%d.o" % (n, m)),
+                     ["-DDG_N=%d" % n, "-DDG_M=%d" % m]))
+    for n, m in GEO:
+        jobs.append((os.path.join(CSRC, "dg_geo_inst.cu"), os.path.join(OBJ, "dg_geo_n%d_m%d.o" % (n, m)),
                      ["-DDG_N=%d" % n, "-DDG_M=%d" % m]))
     for name in ("dg_aux.cu", "dg_matrix.cu", "dg_abi.cpp", "dg_dispatch.cpp", "dg_nccl.cpp", "dg_fabric.cpp", "tables.cpp"):
         base = os.path.splitext(name)[0]

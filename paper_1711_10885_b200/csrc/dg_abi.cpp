@@ -67,6 +67,9 @@ struct dg_ctx {
     const double* tma_y = nullptr;
     bool tma_z_ok = false, tma_y_ok = false;
     CUtensorMap tmz, tmy;
+    // multilinear geometry (dg_set_geometry; NEXT-3): library copy of the padded vertex grid
+    bool geo = false;
+    double* vert = nullptr;
     double* mscratch = nullptr;      // dg_matrix_apply slot-split partial sums
     int64_t mscratch_n = 0;
     KParams base;
@@ -74,6 +77,7 @@ struct dg_ctx {
 
 static cudaError_t launch_any(const dg_ctx* ctx, const KParams& p, cudaStream_t s)
 {
+    if (ctx->geo) return launch_geo(ctx->k, ctx->m, p, s);
     if (ctx->vb) return launch_vb(ctx->k, ctx->m, p, s);
     return ctx->general ? launch_gen(ctx->k, p, s) : launch_cell(ctx->k, p, s);
 }
@@ -128,6 +132,7 @@ static void free_ctx(dg_ctx* c)
     if (c->hz) cudaFree(c->hz);
     if (c->hy) cudaFree(c->hy);
     if (c->mscratch) cudaFree(c->mscratch);
+    if (c->vert) cudaFree(c->vert);
     if (c->comm) {
         const NcclApi* api = nccl_api();
         if (api) api->ncclCommDestroy(c->comm);
@@ -470,7 +475,7 @@ static void bind_dfield(dg_ctx* ctx)
 }
 
 static std::mutex g_vb_mu;
-static bool g_vb_done[64][KMAX + 1][NMAX + 1];
+static bool g_vb_done[64][KMAX + 1][MMAX + 1];
 
 // switch between the fast kernels and the variable-velocity / over-integrated kernel
 static int update_vb(dg_ctx* ctx)
@@ -498,7 +503,7 @@ extern "C" int dg_set_affine(dg_ctx* ctx, const double J[9])
     const double det = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
                        J[2] * (J[3] * J[7] - J[4] * J[6]);
     if (!(det > 0.0)) return DG_EINVAL;                   // orientation preserving, non-degenerate
-    if (ctx->vb) return DG_EUNSUPPORTED;                  // b(x) / over-integration: axis-aligned only
+    if (ctx->vb || ctx->geo) return DG_EUNSUPPORTED;                  // b(x) / over-integration: axis-aligned only
     if (ctx->general && !ctx->dfield_const) return DG_EUNSUPPORTED;   // set the map before per-cell tensors
     DG_CUDA(cudaSetDevice(ctx->device));
     for (int i = 0; i < 9; ++i) ctx->J[i] = J[i];
@@ -522,9 +527,65 @@ extern "C" int dg_set_affine(dg_ctx* ctx, const double J[9])
     return dg_set_diffusion(ctx, nullptr, 0, nullptr) == DG_OK ? cuda_rc(cudaStreamSynchronize(nullptr)) : DG_ECUDA;
 }
 
+static std::mutex g_geo_mu;
+static bool g_geo_done[64][KMAX + 1][MMAX + 1];
+
+extern "C" int dg_set_geometry(dg_ctx* ctx, const double* vert, int m, void* stream)
+{
+    if (!ctx) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!vert) {                                        // back to the axis-aligned box mesh
+        ctx->geo = false;
+        ctx->m = ctx->k + 1;
+        return DG_OK;
+    }
+    if (m < ctx->k + 1 || m > MMAX) return DG_EINVAL;
+    if (!geo_available(ctx->k, m)) return DG_EUNSUPPORTED;
+    if (ctx->vb || ctx->affine || (ctx->general && !ctx->dfield_const)) return DG_EUNSUPPORTED;
+    {
+        std::lock_guard<std::mutex> lk(g_geo_mu);
+        if (!g_geo_done[ctx->device][ctx->k][m]) {
+            HostTables t;
+            if (build_tables_m(ctx->k, m, &t) != 0) return DG_EINVAL;
+            if (upload_tables_geo(ctx->k, m, t) != 0) return DG_ECUDA;
+            g_geo_done[ctx->device][ctx->k][m] = true;
+        }
+    }
+    const int64_t nv = (ctx->nloc[0] + 3) * (ctx->nloc[1] + 3) * (ctx->nloc[2] + 3) * 3;
+    double* buf = nullptr;
+    if (cudaMalloc(&buf, (size_t)nv * sizeof(double)) != cudaSuccess) return DG_ENOMEM;
+    if (!ctx->dbad && cudaMalloc(&ctx->dbad, sizeof(int)) != cudaSuccess) { cudaFree(buf); return DG_ENOMEM; }
+    int bad = 0;
+    HostTables t;
+    build_tables_m(ctx->k, m, &t);
+    GeoPts g;
+    g.m = m;
+    for (int i = 0; i < m; ++i) g.xi[i] = t.xi[i];
+    if (cudaMemcpyAsync(buf, vert, (size_t)nv * sizeof(double), cudaMemcpyDefault, s) != cudaSuccess ||
+        cudaMemsetAsync(ctx->dbad, 0, sizeof(int), s) != cudaSuccess ||
+        launch_geo_check(buf, ctx->nloc, g, ctx->dbad, s) != cudaSuccess ||
+        cudaMemcpyAsync(&bad, ctx->dbad, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaFree(buf);
+        return DG_ECUDA;
+    }
+    if (bad) { cudaFree(buf); return DG_EINVAL; }      // an inverted or degenerate cell: nothing changes
+    if (ctx->vert) cudaFree(ctx->vert);
+    ctx->vert = buf;
+    KParams& p = ctx->base;
+    p.vert = buf;
+    for (int i = 0; i < 9; ++i) p.Dp[i] = ctx->Dphys[i];
+    for (int r = 0; r < 3; ++r) p.bp[r] = ctx->bphys[r];
+    ctx->m = m;
+    ctx->geo = true;
+    return DG_OK;
+}
+
 extern "C" int dg_set_velocity(dg_ctx* ctx, int kind, const double amp[3])
 {
     if (!ctx || kind < 0 || kind > 2 || (kind != 0 && !amp)) return DG_EINVAL;
+    if (ctx->geo && kind != 0) return DG_EUNSUPPORTED;
     for (int r = 0; r < 3 && kind; ++r)
         if (!std::isfinite(amp[r])) return DG_EINVAL;
     DG_CUDA(cudaSetDevice(ctx->device));
@@ -543,7 +604,8 @@ extern "C" int dg_set_velocity(dg_ctx* ctx, int kind, const double amp[3])
 
 extern "C" int dg_set_quadrature(dg_ctx* ctx, int m)
 {
-    if (!ctx || m < ctx->k + 1 || m > NMAX) return DG_EINVAL;
+    if (!ctx || m < ctx->k + 1 || m > MMAX) return DG_EINVAL;
+    if (ctx->geo) return DG_EUNSUPPORTED;                 // the geometry kernel's m is dg_set_geometry's
     DG_CUDA(cudaSetDevice(ctx->device));
     const int old = ctx->m;
     ctx->m = m;
@@ -570,6 +632,7 @@ extern "C" int dg_set_diffusion(dg_ctx* ctx, const double* Dcell, unsigned flags
         return DG_OK;
     }
     if (ctx->vb) return DG_EUNSUPPORTED;   // b(x) / over-integration run on constant diagonal D only
+    if (ctx->geo && Dcell) return DG_EUNSUPPORTED;   // multilinear meshes: one constant tensor
     int rc = alloc_dfield(ctx);
     if (rc != DG_OK) return rc;
     // Everything is built in the *_next buffers and committed (pointer swap) only when it is
@@ -658,7 +721,7 @@ extern "C" int dg_local_layout(const dg_ctx* ctx, int64_t cell_lo[3], int64_t ce
 static void set_tma(dg_ctx* ctx, KParams& p, const double* z, double* y)
 {
     p.tma = 0;
-    if (ctx->k != 7 || ctx->vb || ctx->no_tma) return;
+    if (ctx->k != 7 || ctx->vb || ctx->geo || ctx->no_tma) return;
     const int64_t rows = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2] * 64;
     if (z != ctx->tma_z) {
         ctx->tma_z_ok = make_row_map(&ctx->tmz, z, rows);
@@ -777,6 +840,7 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
     if (need_comm) DG_CUDA(cudaStreamWaitEvent(s, ctx->ev_recv, 0));
     p.task_list = ctx->shell;
     p.ntasks = ctx->nshell;
+    p.ghosts = 1;
     return cuda_rc(launch(p));
 }
 
@@ -847,6 +911,7 @@ extern "C" int dg_ssp_stage(dg_ctx* ctx, const double* z, const double* f, const
 {
     if (!ctx || !z || !out || out == z || (f && f == out)) return DG_EINVAL;
     if (!std::isfinite(a) || !std::isfinite(b) || !std::isfinite(dt)) return DG_EINVAL;
+    if (ctx->geo) return DG_EUNSUPPORTED;   // the mass matrix of a multilinear cell is not Delta_T I
     Epi e;
     e.mode = 2;
     e.f = f;
@@ -1111,7 +1176,7 @@ extern "C" int dg_get_kernel_info(const dg_ctx* ctx, dg_kernel_info* info)
     if (!ctx || !info) return DG_EINVAL;
     DG_CUDA(cudaSetDevice(ctx->device));
     LaunchInfo li;
-    const int rc = ctx->vb ? vb_launch_info(ctx->k, ctx->m, &li)
+    const int rc = ctx->geo ? geo_launch_info(ctx->k, ctx->m, &li) : ctx->vb ? vb_launch_info(ctx->k, ctx->m, &li)
                            : (ctx->general ? gen_launch_info(ctx->k, &li) : cell_launch_info(ctx->k, &li));
     if (rc != 0) return DG_ECUDA;
     info->launches_per_apply = ctx->partitioned ? 3 : 1;   // trace pack, inner box, shell

@@ -87,6 +87,61 @@ cudaError_t launch_trace_pack(const double* z, const TraceArgs& a, int n, const 
     return cudaGetLastError();
 }
 
+// Multilinear mesh check (dg_set_geometry): every local cell's Q1 map must be orientation
+// preserving at all m^3 quadrature points and its 8 corners (det J > 0); *bad != 0 otherwise.
+__global__ void geo_check_kernel(const double* __restrict__ vert, int64_t n0, int64_t n1, int64_t n2, GeoPts g,
+                                 int* bad)
+{
+    const int64_t ncell = n0 * n1 * n2, PX = n0 + 3, PY = n1 + 3;
+    const int npts = g.m * g.m * g.m + 8;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncell * npts;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = i / npts;
+        const int t = (int)(i - e * npts);
+        const int64_t ix = e % n0, iy = (e / n0) % n1, iz = e / (n0 * n1);
+        double xi[3];
+        if (t < g.m * g.m * g.m) {
+            xi[0] = g.xi[t % g.m];
+            xi[1] = g.xi[(t / g.m) % g.m];
+            xi[2] = g.xi[t / (g.m * g.m)];
+        } else {
+            const int c = t - g.m * g.m * g.m;
+            xi[0] = c & 1; xi[1] = (c >> 1) & 1; xi[2] = c >> 2;
+        }
+        // vertex (i, j, k) of the cell's corner cube: padded index (ix + 1 + i, ...)
+        auto X = [&](int a, int b, int c, int r) {
+            return vert[(((iz + 1 + c) * PY + (iy + 1 + b)) * PX + (ix + 1 + a)) * 3 + r];
+        };
+        double J[3][3];
+        for (int r = 0; r < 3; ++r) {
+            double j0 = 0.0, j1 = 0.0, j2 = 0.0;
+            for (int u = 0; u < 2; ++u)
+                for (int v = 0; v < 2; ++v) {
+                    const double bu1 = u ? xi[1] : 1.0 - xi[1], bv2 = v ? xi[2] : 1.0 - xi[2];
+                    const double bu0 = u ? xi[0] : 1.0 - xi[0], bv1 = v ? xi[1] : 1.0 - xi[1];
+                    j0 += bu1 * bv2 * (X(1, u, v, r) - X(0, u, v, r));
+                    j1 += bu0 * bv2 * (X(u, 1, v, r) - X(u, 0, v, r));
+                    j2 += bu0 * bv1 * (X(u, v, 1, r) - X(u, v, 0, r));
+                }
+            J[r][0] = j0; J[r][1] = j1; J[r][2] = j2;
+        }
+        const double det = J[0][0] * (J[1][1] * J[2][2] - J[2][1] * J[1][2]) -
+                           J[0][1] * (J[1][0] * J[2][2] - J[2][0] * J[1][2]) +
+                           J[0][2] * (J[1][0] * J[2][1] - J[2][0] * J[1][1]);
+        if (!(det > 0.0)) atomicOr(bad, 1);
+    }
+}
+
+cudaError_t launch_geo_check(const double* vert, const int64_t nloc[3], const GeoPts& g, int* bad, cudaStream_t s)
+{
+    const int64_t total = nloc[0] * nloc[1] * nloc[2] * (int64_t)(g.m * g.m * g.m + 8);
+    if (total == 0) return cudaSuccess;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    geo_check_kernel<<<(unsigned)blocks, 256, 0, s>>>(vert, nloc[0], nloc[1], nloc[2], g, bad);
+    return cudaGetLastError();
+}
+
 __device__ __forceinline__ double splitmix_uniform(uint64_t g, uint64_t seed)
 {
     uint64_t x = (seed << 40) + g + 0x9E3779B97F4A7C15ull;

@@ -418,6 +418,52 @@ __device__ __forceinline__ void c_apply_s(const EO<N>& A2, const double (&r)[P][
     }
 }
 
+// ---------------------------------------------------------------------------------- rectangular stages
+// (m >= n Gauss points: the over-integrated kernels dg_vb.cuh, dg_geo.cuh)
+// r (n modal values) -> t (m points): t_i = sum_j V_ij r_j, even-odd over the symmetric rule
+template <int N, int M>
+__device__ __forceinline__ void vr_fwd(const double (&Vh)[(M + 1) / 2][N], const double (&r)[N], double (&t)[M])
+{
+    constexpr int H = M / 2;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        double E = 0.0, O = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (j & 1) O = fma(Vh[i][j], r[j], O);
+            else E = fma(Vh[i][j], r[j], E);
+        }
+        t[i] = E + O;
+        t[M - 1 - i] = E - O;
+    }
+    if (M & 1) {
+        double E = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; j += 2) E = fma(Vh[H][j], r[j], E);
+        t[H] = E;
+    }
+}
+
+// t (m points) -> r (n modal values): r_j = sum_i V_ij t_i
+template <int N, int M>
+__device__ __forceinline__ void vr_bwd(const double (&Vh)[(M + 1) / 2][N], const double (&t)[M], double (&r)[N])
+{
+    constexpr int H = M / 2;
+    double s[H > 0 ? H : 1], d[H > 0 ? H : 1];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        s[i] = t[i] + t[M - 1 - i];
+        d[i] = t[i] - t[M - 1 - i];
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        double acc = ((M & 1) && !(j & 1)) ? Vh[H][j] * t[H] : 0.0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) acc = fma(Vh[i][j], (j & 1) ? d[i] : s[i], acc);
+        r[j] = acc;
+    }
+}
+
 // ---------------------------------------------------------------------------------- face terms
 // Contribution cv * phi_i + cg_phys * d_q phi_i of one face point, returned as
 // (cv, cg = cg_phys / h_q, the coefficient of the REFERENCE normal derivative).
@@ -460,7 +506,7 @@ __device__ __forceinline__ FaceOut flux_boundary(const KParams& p, int q, int s,
 // 8(e), dg_trace_pack in dg_aux.cu: 2 n^2 doubles per face cell, [u | d] at a + n bb). For such
 // a "ghost" side the two values land in rl/rh[k][0..1] and bit 0 (low) / 1 (high) of the
 // returned mask tells nb_traces to take them as they are.
-template <int N, int P>
+template <int N, int P, bool GH = true>
 __device__ __forceinline__ unsigned nb_load(const KParams& p, const double* zc, const int64_t n3, int q, const int lc[3],
                                             unsigned nbmask, const int (&pa)[P], const int (&pb)[P], const bool (&act)[P],
                                             double (&rl)[P][N], double (&rh)[P][N])
@@ -472,8 +518,10 @@ __device__ __forceinline__ unsigned nb_load(const KParams& p, const double* zc, 
     const int64_t gi = (q == 0) ? (lc[1] + p.nloc[1] * lc[2]) : (q == 1) ? (lc[0] + p.nloc[0] * lc[2])
                                                                         : (lc[0] + p.nloc[0] * lc[1]);
     const bool hl = (nbmask >> (2 * q)) & 1u, hh = (nbmask >> (2 * q + 1)) & 1u;
-    const bool gl = hl && lq == 0 && !p.wrap[q];           // the low neighbour lives on another rank
-    const bool gh = hh && lq + 1 == nq && !p.wrap[q];
+    // (GH = false: a launch over cells with no neighbour on another rank -- the inner box or a
+    // single-rank operator -- compiles this away)
+    const bool gl = GH && hl && lq == 0 && !p.wrap[q];     // the low neighbour lives on another rank
+    const bool gh = GH && hh && lq + 1 == nq && !p.wrap[q];
     const int64_t wst = (int64_t)(nq - 1) * st * n3;   // periodic wrap inside this rank's box
     const double* zl = (lq > 0) ? zc - st * n3 : (p.wrap[q] ? zc + wst : zc);
     const double* zh = (lq + 1 < nq) ? zc + st * n3 : (p.wrap[q] ? zc - wst : zc);
@@ -731,7 +779,7 @@ __device__ __forceinline__ void epilogue(const KParams& p, int64_t off, double (
 }
 
 // ---------------------------------------------------------------------------------- kernel
-template <int N>
+template <int N, bool GH>
 __global__ void __launch_bounds__(Cfg<N>::C * Cfg<N>::TPC, Cfg<N>::MINB)
 dg_cell_kernel(const __grid_constant__ KParams p)
 {
@@ -826,7 +874,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 }
             }
         } else {
-        gm0 = nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
+        gm0 = nb_load<N, P, GH>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
             if (STG) {
@@ -862,7 +910,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         csync();
 
         // ---- phase 2: y-pencils (x = a, z = bb): V along y -> A1; y-neighbours; x-arrays step B
-        const unsigned gm1 = nb_load<N, P>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
+        const unsigned gm1 = nb_load<N, P, GH>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -879,7 +927,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
 
         // ---- phase 3: z-pencils (x = a, y = bb): u at the Gauss points -> A0; z-neighbours;
         //      y-arrays step B, x-arrays step C
-        const unsigned gm2 = nb_load<N, P>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
+        const unsigned gm2 = nb_load<N, P, GH>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll

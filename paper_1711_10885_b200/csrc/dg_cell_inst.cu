@@ -16,7 +16,7 @@
 namespace dg {
 
 template <int N>
-static void fill_eo(EO<N>& o, const double (&A)[NMAX][NMAX], bool transpose)
+static void fill_eo(EO<N>& o, const double (&A)[MMAX][MMAX], bool transpose)
 {
     constexpr int H = N / 2;
     auto a = [&](int i, int j) { return transpose ? A[j][i] : A[i][j]; };
@@ -40,7 +40,7 @@ int DG_CAT(upload_tables_n, DG_N)(const HostTables& t)
         for (int i = 0; i < Tab<N>::HC; ++i)
             for (int j = 0; j < N; ++j) h.Vh[c][i][j] = t.V[i][j];
     {   // sigma/delta form (dg_cell.cuh): doubled forward V, doubled Dc and Dc^T diag(w)
-        static double D2[NMAX][NMAX], A2[NMAX][NMAX];
+        static double D2[MMAX][MMAX], A2[MMAX][MMAX];
         for (int i = 0; i < N; ++i)
             for (int j = 0; j < N; ++j) {
                 D2[i][j] = 2.0 * t.Dc[i][j];
@@ -208,13 +208,16 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
     }
 #endif
     if (dev >= 0 && dev < 64 && !g_attr_done[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(dg_cell_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(dg_cell_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Smem<N>::BYTES);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(dg_cell_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<N>::BYTES);
         if (e != cudaSuccess) return e;
         g_attr_done[dev] = 1;
     }
     const int64_t grid = (p.ntasks + C - 1) / C;
-    dg_cell_kernel<N><<<(unsigned)grid, THREADS, Smem<N>::BYTES, s>>>(p);
+    if (p.ghosts) dg_cell_kernel<N, true><<<(unsigned)grid, THREADS, Smem<N>::BYTES, s>>>(p);
+    else dg_cell_kernel<N, false><<<(unsigned)grid, THREADS, Smem<N>::BYTES, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -236,13 +239,16 @@ cudaError_t DG_CAT(launch_gen_n, DG_N)(const KParams& p, cudaStream_t s)
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !g_gen_attr_done[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(dg_gen_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(dg_gen_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              GSmem<N>::BYTES);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(dg_gen_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GSmem<N>::BYTES);
         if (e != cudaSuccess) return e;
         g_gen_attr_done[dev] = 1;
     }
     const int64_t grid = (p.ntasks + C - 1) / C;
-    dg_gen_kernel<N><<<(unsigned)grid, C * GCfg<N>::TPC, GSmem<N>::BYTES, s>>>(p);
+    if (p.ghosts) dg_gen_kernel<N, true><<<(unsigned)grid, C * GCfg<N>::TPC, GSmem<N>::BYTES, s>>>(p);
+    else dg_gen_kernel<N, false><<<(unsigned)grid, C * GCfg<N>::TPC, GSmem<N>::BYTES, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -267,13 +273,13 @@ int DG_CAT(gen_info_n, DG_N)(LaunchInfo* info)
     info->threads = GCfg<N>::C * GCfg<N>::TPC;
     info->smem = GSmem<N>::BYTES;
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, dg_gen_kernel<N>) != cudaSuccess) return -3;
+    if (cudaFuncGetAttributes(&fa, dg_gen_kernel<N, false>) != cudaSuccess) return -3;
     info->regs = fa.numRegs;
-    if (cudaFuncSetAttribute(dg_gen_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, GSmem<N>::BYTES) !=
+    if (cudaFuncSetAttribute(dg_gen_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GSmem<N>::BYTES) !=
         cudaSuccess)
         return -3;
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_gen_kernel<N>, info->threads, GSmem<N>::BYTES) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_gen_kernel<N, false>, info->threads, GSmem<N>::BYTES) !=
         cudaSuccess)
         return -3;
     info->ctas_per_sm = blocks;
@@ -318,18 +324,18 @@ int DG_CAT(cell_info_n, DG_N)(LaunchInfo* info)
     info->threads = Cfg<N>::C * Cfg<N>::TPC;
     info->smem = Smem<N>::BYTES;
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, dg_cell_kernel<N>) != cudaSuccess) return -3;
+    if (cudaFuncGetAttributes(&fa, dg_cell_kernel<N, false>) != cudaSuccess) return -3;
     info->regs = fa.numRegs;
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !g_attr_done[dev]) {
-        if (cudaFuncSetAttribute(dg_cell_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<N>::BYTES) !=
+        if (cudaFuncSetAttribute(dg_cell_kernel<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<N>::BYTES) !=
             cudaSuccess)
             return -3;
         g_attr_done[dev] = 1;
     }
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_cell_kernel<N>, info->threads, Smem<N>::BYTES) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_cell_kernel<N, false>, info->threads, Smem<N>::BYTES) !=
         cudaSuccess)
         return -3;
     info->ctas_per_sm = blocks;

@@ -174,7 +174,7 @@ struct GSmem {
     static constexpr int BYTES = GCfg<N>::C * PER_CELL * 8 + STAGE * 8;
 };
 
-template <int N>
+template <int N, bool GH>
 #ifndef DG_GMB
 #define DG_GMB ((DG_N) == 4 ? 12 : (DG_N) == 10 ? 5 : 1)   // min CTAs per SM (n = 4: A-k3 30.5 -> 31.0; n = 10: A-k9 29.7 -> 31.0)
 #endif
@@ -273,7 +273,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 }
             }
         } else {
-            gm = nb_load<N, P>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
+            gm = nb_load<N, P, GH>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
             for (int k = 0; k < P; ++k) {
                 if (STG) {
@@ -299,7 +299,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         nb_contract<N, P, GFLay<N>>(T, NT, 0, nbi, pa, pb, act, rl, rh, gm);
         csync();
 
-        gm = nb_load<N, P>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
+        gm = nb_load<N, P, GH>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -313,7 +313,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         nb_contract<N, P, GFLay<N>>(T, NT, 1, nbi, pa, pb, act, rl, rh, gm);
         csync();
 
-        gm = nb_load<N, P>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
+        gm = nb_load<N, P, GH>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll

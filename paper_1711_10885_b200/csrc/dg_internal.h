@@ -18,6 +18,7 @@ namespace dg {
 
 constexpr int KMAX = 10;
 constexpr int NMAX = KMAX + 1;
+constexpr int MMAX = 18;          // Gauss points per direction: up to q = 3p + 4 at p = 10
 
 // Symmetric positive SEMI-definite test of a row-major 3x3 tensor (the diffusion tensor of
 // eq:modelproblem; D = 0 is admitted): finite, exactly
@@ -43,14 +44,14 @@ __host__ __device__ inline bool psd3(const double* d)
 // 1D tables for one degree (host side, double). Built by tables.cpp.
 struct HostTables {
     int n, m;                // basis size n = k+1, Gauss points per direction m (>= n)
-    double xi[NMAX], w[NMAX];
-    double V[NMAX][NMAX];    // V[i][j]  = theta_j(xi_i)                    (A^(q) of eq:evalfe)
-    double Dc[NMAX][NMAX];   // Dc[i][l] = L'_l(xi_i): collocation derivative at the Gauss points
-    double L0[NMAX], L1[NMAX];    // L_l(0), L_l(1): Lagrange basis at the Gauss points, at the endpoints
-    double LD0[NMAX], LD1[NMAX];  // L'_l(0), L'_l(1)
+    double xi[MMAX], w[MMAX];
+    double V[MMAX][NMAX];    // V[i][j]  = theta_j(xi_i)                    (A^(q) of eq:evalfe)
+    double Dc[MMAX][MMAX];   // Dc[i][l] = L'_l(xi_i): collocation derivative at the Gauss points
+    double L0[MMAX], L1[MMAX];    // L_l(0), L_l(1): Lagrange basis at the Gauss points, at the endpoints
+    double LD0[MMAX], LD1[MMAX];  // L'_l(0), L'_l(1)
     double th0[NMAX], th1[NMAX];  // theta_j(0), theta_j(1)       (B^(d) of PAPER.md:528-545)
     double dth0[NMAX], dth1[NMAX];// theta'_j(0), theta'_j(1)
-    double G[NMAX][NMAX];    // G[i][j]  = theta'_j(xi_i)   (reference derivative, modal -> Gauss points)
+    double G[MMAX][NMAX];    // G[i][j]  = theta'_j(xi_i)   (reference derivative, modal -> Gauss points)
 };
 int build_tables(int k, HostTables* t);
 int build_tables_m(int k, int m, HostTables* t);
@@ -64,6 +65,7 @@ struct KParams {
     double ea, eb, es;        // epi 2: y = ea w + eb (z + es (f - A z)), es = dt / Delta_T
     int epi;                  // store epilogue: 0 y = A z, 1 residual, 2 SSP-RK stage
     const double* ghost[6];   // neighbour-rank face traces per face 2q+s: [layer cell][u | d][n^2] (nullptr: none)
+    int ghosts;               // this launch covers cells with a neighbour on another rank (the shell launch)
     const int64_t* task_list; // local linear cell ids (nullptr -> task box)
     int64_t ntasks;
     int64_t task_lo[3], task_cnt[3];
@@ -97,6 +99,11 @@ struct KParams {
     // [cells * 64 rows][8 doubles] with the 64-byte swizzle
     int tma;                  // 1: tmz (loads) valid; 2: tmy (store) valid too
     CUtensorMap tmz, tmy;
+    // multilinear-geometry kernel (NEXT-3, dg_geo.cuh): the padded vertex grid of this rank's box
+    // ((nloc+3)^3 x 3 doubles, local vertex -1 .. nloc+1) and the physical D, b
+    const double* vert;
+    double Dp[9];
+    double bp[3];
 };
 
 struct LaunchInfo {
@@ -116,6 +123,11 @@ int cell_launch_info(int k, LaunchInfo* info);
 // 2D tensor map [rows][8 doubles] (64-byte rows, box 64 x 8, 64-byte swizzle) over ptr; false if unavailable
 bool make_row_map(CUtensorMap* map, const double* ptr, int64_t rows);
 int gen_launch_info(int k, LaunchInfo* info);
+// multilinear-geometry kernel for (k, m) (dg_geo.cuh; pairs in dg_dispatch.cpp)
+bool geo_available(int k, int m);
+int upload_tables_geo(int k, int m, const HostTables& t);
+cudaError_t launch_geo(int k, int m, const KParams& p, cudaStream_t s);
+int geo_launch_info(int k, int m, LaunchInfo* info);
 
 // Halo / inputs kernels (dg_aux.cu).
 struct TraceArgs {              // face-trace halo of the partition faces (trace_pack_kernel)
@@ -123,6 +135,8 @@ struct TraceArgs {              // face-trace halo of the partition faces (trace
     int64_t start[7];           // prefix sums of the work items (layer cells x n^2) per face
     double th[2][NMAX], dth[2][NMAX];   // theta_j(s), theta'_j(s), s = 0, 1
 };
+struct GeoPts { int m; double xi[MMAX]; };   // the m-point Gauss rule of dg_set_geometry's check
+cudaError_t launch_geo_check(const double* vert, const int64_t nloc[3], const GeoPts& g, int* bad, cudaStream_t s);
 cudaError_t launch_trace_pack(const double* z, const TraceArgs& a, int n, const int64_t nloc[3], cudaStream_t s);
 cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc[3], int face, cudaStream_t s);
 cudaError_t launch_dfield_pack(const double* D9, double* D6, int* bad, int64_t ncell, const double* Jinv,

@@ -73,50 +73,6 @@ template <int N, int M> struct VSmem {
     static constexpr int BYTES = VCfg<M>::C * PER_CELL * 8;
 };
 
-// r (n modal values) -> t (m points): t_i = sum_j V_ij r_j, even-odd over the symmetric rule
-template <int N, int M>
-__device__ __forceinline__ void vr_fwd(const double (&Vh)[(M + 1) / 2][N], const double (&r)[N], double (&t)[M])
-{
-    constexpr int H = M / 2;
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-        double E = 0.0, O = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-            if (j & 1) O = fma(Vh[i][j], r[j], O);
-            else E = fma(Vh[i][j], r[j], E);
-        }
-        t[i] = E + O;
-        t[M - 1 - i] = E - O;
-    }
-    if (M & 1) {
-        double E = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; j += 2) E = fma(Vh[H][j], r[j], E);
-        t[H] = E;
-    }
-}
-
-// t (m points) -> r (n modal values): r_j = sum_i V_ij t_i
-template <int N, int M>
-__device__ __forceinline__ void vr_bwd(const double (&Vh)[(M + 1) / 2][N], const double (&t)[M], double (&r)[N])
-{
-    constexpr int H = M / 2;
-    double s[H > 0 ? H : 1], d[H > 0 ? H : 1];
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-        s[i] = t[i] + t[M - 1 - i];
-        d[i] = t[i] - t[M - 1 - i];
-    }
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-        double acc = ((M & 1) && !(j & 1)) ? Vh[H][j] * t[H] : 0.0;
-#pragma unroll
-        for (int i = 0; i < H; ++i) acc = fma(Vh[i][j], (j & 1) ? d[i] : s[i], acc);
-        r[j] = acc;
-    }
-}
-
 // separable velocity field: function id per (kind, component r, direction d) and sign per (kind, r)
 // fn: 0 = x, 1 = sin x, 2 = cos x, 3 = 1
 __device__ __forceinline__ int bfn(int kind, int r, int d)

@@ -8,7 +8,7 @@
 namespace dg {
 
 template <int N, int M>
-static void fill_eo_m(EO<M>& o, const double (&A)[NMAX][NMAX], bool transpose)
+static void fill_eo_m(EO<M>& o, const double (&A)[MMAX][MMAX], bool transpose)
 {
     constexpr int H = M / 2;
     auto a = [&](int i, int j) { return transpose ? A[j][i] : A[i][j]; };

@@ -42,12 +42,12 @@ int build_tables(int k, HostTables* t) { return build_tables_m(k, k + 1, t); }
 // first m basis functions, exact for the degree-k traces and lines).
 int build_tables_m(int k, int m, HostTables* t)
 {
-    if (k < 1 || k > KMAX || m < k + 1 || m > NMAX) return -1;
+    if (k < 1 || k > KMAX || m < k + 1 || m > MMAX) return -1;
     const int n = k + 1;
     t->n = n;
     t->m = m;
-    ld xi[NMAX], w[NMAX];
-    ld P[NMAX + 2], dP[NMAX + 2];
+    ld xi[MMAX], w[MMAX];
+    ld P[MMAX + 2], dP[MMAX + 2];
     for (int i = 0; i < m; ++i) {
         // initial guess (ascending): roots of P_m near cos(pi (m - i - 0.25)/(m + 0.5)) mapped to [0,1]
         ld x = 0.5L * (1.0L + cosl(3.14159265358979323846264338327950288L * ((ld)(m - i) - 0.25L) / ((ld)m + 0.5L)));
@@ -62,7 +62,7 @@ int build_tables_m(int k, int m, HostTables* t)
         // weight on [0,1]: 1 / (x(1-x) Pt'_m(x)^2)
         w[i] = 1.0L / (x * (1.0L - x) * dP[m] * dP[m]);
     }
-    ld th[NMAX][NMAX], dth[NMAX][NMAX];      // theta_j, theta'_j at the m points, j < m
+    ld th[MMAX][MMAX], dth[MMAX][MMAX];      // theta_j, theta'_j at the m points, j < m
     for (int i = 0; i < m; ++i) {
         shifted_legendre(m, xi[i], P, dP);
         for (int j = 0; j < m; ++j) {
@@ -71,7 +71,7 @@ int build_tables_m(int k, int m, HostTables* t)
             dth[i][j] = s * dP[j];
         }
     }
-    ld e0[NMAX], e1[NMAX], de0[NMAX], de1[NMAX];
+    ld e0[MMAX], e1[MMAX], de0[MMAX], de1[MMAX];
     shifted_legendre(m, 0.0L, P, dP);
     for (int j = 0; j < m; ++j) { ld s = sqrtl(2.0L * j + 1.0L); e0[j] = s * P[j]; de0[j] = s * dP[j]; }
     shifted_legendre(m, 1.0L, P, dP);

@@ -23,7 +23,8 @@ EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residu
             "dg_sync", "dg_destroy", "dg_strerror", "dg_halo_info", "dg_halo_buffer", "dg_halo_pack",
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
             "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage", "dg_set_velocity", "dg_set_quadrature",
-            "dg_set_affine", "dg_matrix_size", "dg_assemble", "dg_matrix_apply", "dg_fabric_id", "dg_comm_info"]
+            "dg_set_affine", "dg_matrix_size", "dg_assemble", "dg_matrix_apply", "dg_fabric_id", "dg_comm_info",
+            "dg_set_geometry"]
 
 
 class DGError(RuntimeError):
@@ -75,6 +76,7 @@ def lib():
         L.dg_nccl_unique_id.argtypes = [vp]
         L.dg_fabric_id.argtypes = [vp]
         L.dg_comm_info.argtypes = [vp, vp, vp]
+        L.dg_set_geometry.argtypes = [vp, vp, ctypes.c_int, vp]
         L.dg_get_kernel_info.argtypes = [vp, ctypes.POINTER(KernelInfo)]
         L.dg_partition.argtypes = [ctypes.POINTER(MeshDesc), ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.dg_set_diffusion.argtypes = [vp, vp, ctypes.c_uint, vp]
@@ -267,6 +269,25 @@ class Operator:
         """Physical mesh x = lo + J (xhat - lo) of the axis-aligned box (dg_set_affine; NEXT-3)."""
         a = (ctypes.c_double * 9)(*[float(v) for v in np.asarray(J, dtype=np.float64).ravel()])
         _check(lib().dg_set_affine(self._h, a), "dg_set_affine")
+
+    def set_geometry(self, vert, m=None, stream=None):
+        """Multilinear mesh (dg_set_geometry; NEXT-3): vert = the padded vertex grid of this rank's
+        box, (nloc+3)^3 x 3 doubles (CUDA float64 tensor or numpy array), or None to revert;
+        m Gauss points per direction (default k+1)."""
+        if vert is None:
+            _check(lib().dg_set_geometry(self._h, None, 0, _stream(stream)), "dg_set_geometry")
+            return
+        cnt = (self.cell_cnt[0] + 3) * (self.cell_cnt[1] + 3) * (self.cell_cnt[2] + 3) * 3
+        if isinstance(vert, np.ndarray):
+            vert = np.ascontiguousarray(vert, dtype=np.float64)
+            if vert.size != cnt:
+                raise ValueError("vert has %d entries, expected %d" % (vert.size, cnt))
+            ptr = a_ptr(vert)
+        else:
+            _dev_vec(vert, cnt, "vert")
+            ptr = _ptr(vert)
+        _check(lib().dg_set_geometry(self._h, ptr, int(m if m else self.k + 1), _stream(stream)),
+               "dg_set_geometry")
 
     def set_velocity(self, kind, amp=(1.0, 1.0, 1.0)):
         """Velocity field b(x) at every quadrature point: 0 constant, 1 Taylor-Green, 2 linear (dg_set_velocity)."""
