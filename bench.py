@@ -63,6 +63,8 @@ def workload(name, world):
         return configs.problem_a(int(name[3:]), world)
     if name.startswith("tg-k") and world == 1:
         return configs.taylor_green(int(name[4:]))
+    if name.startswith("c-k"):
+        return configs.problem_c(int(name[3:]), world)
     cfg = configs.by_name(name)
     if world != 1:
         raise SystemExit("workload %s is single-GPU" % name)
@@ -75,6 +77,9 @@ def workload_desc(cfg, world):
     bc = "periodic" if all(cfg.periodic) else ("Dirichlet" if not any(cfg.periodic) else "periodic %s" % (cfg.periodic,))
     if cfg.bkind:
         bc += ", b(x) = Taylor-Green field at every quadrature point" if cfg.bkind == 1 else ", b(x) linear field"
+    if cfg.geo_amp > 0:
+        bc += (", multilinear mesh: vertices moved by <= %g h per direction (inputs.vertex_grid, seed %d)"
+               % (cfg.geo_amp, cfg.geo_seed))
     if cfg.m and cfg.m != cfg.k + 1:
         bc += ", m = %d Gauss points per direction (q = %d)" % (cfg.m, 2 * cfg.m - 1)
     return {"workload": "%s: %dx%dx%d cells, k=%d, %d DOFs, box %s-%s, D=%s, b=%s, c=%g, sigma=%g, %s, seed %d"
@@ -359,11 +364,17 @@ def run_ours(args, rank, world, local_rank):
         op.set_tensor_field(cfg.dfield_seed)
     if cfg.bkind:
         op.set_velocity(cfg.bkind)
-    if cfg.m and cfg.m != cfg.k + 1:
+    if cfg.geo_amp > 0:
+        op.set_geometry(dg.padded_vertex_grid(cfg, op.cell_lo, op.cell_cnt), cfg.m or cfg.k + 1)
+    elif cfg.m and cfg.m != cfg.k + 1:
         op.set_quadrature(cfg.m)
     general = cfg.dfield_seed >= 0 or any(cfg.D[i] != 0 for i in (1, 2, 3, 5, 6, 7))
-    kname = ("dg_vb_kernel<%d,%d>" % (cfg.k + 1, cfg.m or cfg.k + 1) if (cfg.bkind or (cfg.m and cfg.m != cfg.k + 1))
-             else ("dg_gen_kernel<%d>" % (cfg.k + 1) if general else "dg_cell_kernel<%d>" % (cfg.k + 1)))
+    if cfg.geo_amp > 0:
+        kname = "dg_geo_kernel<%d,%d>" % (cfg.k + 1, cfg.m or cfg.k + 1)
+    elif cfg.bkind or (cfg.m and cfg.m != cfg.k + 1):
+        kname = "dg_vb_kernel<%d,%d>" % (cfg.k + 1, cfg.m or cfg.k + 1)
+    else:
+        kname = "dg_gen_kernel<%d>" % (cfg.k + 1) if general else "dg_cell_kernel<%d>" % (cfg.k + 1)
     info = op.kernel_info()
     transport, comm_ranks = op.comm_info()
     if world > 1 and rank == 0:
@@ -494,7 +505,11 @@ def run_ours(args, rank, world, local_rank):
     # ---- CPU baseline: the oracle on the host cores (rank 0, N = 1 only)
     cpu = None
     parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.geo_amp > 0:
+        cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle",
+               "sample": "not timed: the multilinear-geometry oracle (oracle/o2_geometry.py) assembles dense "
+                         "matrices on tiny meshes only"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         zn = z.cpu().numpy()
         rate, cores, text, _, cells, yo = cpu_oracle_rate(cfg, zn, args.cpu_seconds)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",

@@ -193,13 +193,16 @@ int dg_set_geometry(dg_ctx* ctx, const double* vert, int m, void* stream);
  *   kind 2: the linear divergence-free test field b = (x2, x3, x1);
  * each component times amp[r]. b is continuous, so b.nu is evaluated once per face point
  * (reading N-4); a periodic box needs a box-periodic field (Taylor-Green on (-pi, pi)^3).
- * Runs on the variable-velocity kernel (constant diagonal D; k <= 8).
- * Errors: DG_EINVAL (kind, non-finite amp), DG_EUNSUPPORTED (per-cell / full D set, k > 8). */
+ * Runs on the variable-velocity kernel (constant diagonal D).
+ * Errors: DG_EINVAL (kind, non-finite amp), DG_EUNSUPPORTED (per-cell / full D set, multilinear
+ * geometry set, an uncompiled (k, m)). */
 int dg_set_velocity(dg_ctx* ctx, int kind, const double amp[3]);
 
 /* Gauss points per direction m (NEXT-3 over-integration; q = 2p + 4 is m = k + 3, PAPER.md:950-956,
- * :1102-1104). m = k + 1 (default) or k + 3 with k <= 8. Errors: DG_EINVAL (m < k + 1),
- * DG_EUNSUPPORTED (other m, per-cell / full D set). */
+ * :1102-1104; Problem C's q = 3p + 4 is m = ceil((3k + 5) / 2)) on the
+ * variable-velocity kernel: m = k + 1 (default), k + 3 or ceil((3k + 5) / 2), each while m <= 16.
+ * Errors: DG_EINVAL (m < k + 1), DG_EUNSUPPORTED (other m, per-cell / full D set, multilinear
+ * geometry set: its m is dg_set_geometry's). */
 int dg_set_quadrature(dg_ctx* ctx, int m);
 
 /* ---- matrix-based comparison (the paper's "matrix-based" columns of

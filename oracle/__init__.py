@@ -16,6 +16,9 @@ o2_assembled.py      O-2: dense matrix assembled entry by entry from the weak
                      form (numpy), tiny meshes only.
 o3_kron.py           O-3: Kronecker closed form for diagonal D (numpy/scipy),
                      full-size vectors.
+o2_geometry.py       O-2 on multilinear (Q1-mapped) meshes: the weak form with the
+                     map's Jacobian at every quadrature point (NEXT-3, Problem C's
+                     geometry), tiny meshes only.
 rhs.py               l_h, L2 projection and the upwind
                      energy functional used by the invariant tests.
 tables.py            1D Gauss rule and orthonormal Legendre basis (numpy).

@@ -76,6 +76,11 @@ def _phys_grad(J, gref):
     return np.einsum("prs,spj->rpj", JinvT, gref)
 
 
+def _bil(W, a, b):
+    """sum_p W_p a_pi b_pj (a quadrature-weighted bilinear form; numpy matmul)."""
+    return (a * W[:, None]).T @ b
+
+
 def face_normal(J, q):
     """N = t_{q+1} x t_{q+2} (cyclic) at each point: the area-weighted normal towards +xi_q."""
     a, b = (q + 1) % 3, (q + 2) % 3
@@ -117,7 +122,7 @@ def assemble(ncells, X, k, D, b, c, sigma, m=0, periodic=(0, 0, 0), mask=ALL):
                     flux = np.einsum("rs,spj->rpj", D, grad) - b[:, None, None] * phi[None]
                     e = cid(ic)
                     A[e * n3:(e + 1) * n3, e * n3:(e + 1) * n3] += (
-                        np.einsum("p,rpi,rpj->ij", W, grad, flux) + c * np.einsum("p,pi,pj->ij", W, phi, phi))
+                        sum(_bil(W, grad[r], flux[r]) for r in range(3)) + c * _bil(W, phi, phi))
 
     # ---- faces
     for q in range(3):
@@ -162,9 +167,8 @@ def assemble(ncells, X, k, D, b, c, sigma, m=0, periodic=(0, 0, 0), mask=ALL):
                         Phi = np.where(bnu >= 0, bnu * um, bnu * up)
                         nDg = wm * np.einsum("pr,rs,spj->pj", nu, D, gm) + wp * np.einsum("pr,rs,spj->pj", nu, D, gp)
                         jump = um - up
-                        B = (np.einsum("p,pi,pj->ij", Wf, jump, Phi) - np.einsum("p,pi,pj->ij", Wf, jump, nDg)
-                             - np.einsum("p,pi,pj->ij", Wf, nDg, jump)
-                             + np.einsum("p,pi,pj->ij", Wf * gam, jump, jump))
+                        B = (_bil(Wf, jump, Phi) - _bil(Wf, jump, nDg) - _bil(Wf, nDg, jump)
+                             + _bil(Wf * gam, jump, jump))
                         for bi, ci in ((0, e), (1, f)):
                             for bj, cj in ((0, e), (1, f)):
                                 A[ci * n3:(ci + 1) * n3, cj * n3:(cj + 1) * n3] += \
@@ -186,9 +190,8 @@ def assemble(ncells, X, k, D, b, c, sigma, m=0, periodic=(0, 0, 0), mask=ALL):
                             Phi = np.where(bnu >= 0, bnu * phs, 0.0)
                             sn = np.einsum("pr,rs,spj->pj", nuo, D, grs)
                             gam = np.einsum("pr,rs,ps->p", nuo, D, nuo) * sigma
-                            B = (np.einsum("p,pi,pj->ij", Wf, phs, Phi) - np.einsum("p,pi,pj->ij", Wf, phs, sn)
-                                 - np.einsum("p,pi,pj->ij", Wf, sn, phs)
-                                 + np.einsum("p,pi,pj->ij", Wf * gam, phs, phs))
+                            B = (_bil(Wf, phs, Phi) - _bil(Wf, phs, sn) - _bil(Wf, sn, phs)
+                                 + _bil(Wf * gam, phs, phs))
                             A[e * n3:(e + 1) * n3, e * n3:(e + 1) * n3] += B
     return A
 

@@ -23,9 +23,9 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.
 NS = list(range(2, 12))
 
 
-# (n, m) pairs of the variable-velocity / over-integrated kernel: m = n (q = 2p) and m = n + 2
-# (q = 2p + 4, the paper's Taylor-Green run), k <= 8
-VB = [(n, m) for n in range(2, 10) for m in (n, n + 2)]
+# (n, m) pairs of the variable-velocity / over-integrated kernel: m = n (q = 2p), m = n + 2
+# (q = 2p + 4, the paper's Taylor-Green run) and ceil((3k + 5) / 2) (q = 3p + 4), m <= 16
+VB = sorted({(n, m) for n in range(2, 12) for m in (n, n + 2, -(-(3 * n + 2) // 2)) if m <= 16})
 # (n, m) pairs of the multilinear-geometry kernel: m = n, n + 2 and ceil((3k + 5) / 2) (q = 3p + 4,
 # PAPER.md:957-961), m <= 16 (the cell's shared memory)
 GEO = sorted({(n, m) for n in range(2, 12) for m in (n, n + 2, -(-(3 * n + 2) // 2)) if m <= 16})

@@ -25,6 +25,8 @@ class Config:
     dfield_seed: int = -1          # >= 0: per-cell tensor field inputs.tensor_field_* (Problem A)
     bkind: int = 0                 # velocity field: 0 constant b, 1 Taylor-Green (NEXT-2)
     m: int = 0                     # Gauss points per direction (0: k+1)
+    geo_amp: float = 0.0           # > 0: multilinear mesh, inputs.vertex_grid(..., geo_amp, geo_seed) (NEXT-3)
+    geo_seed: int = 0
 
     @property
     def n3(self):
@@ -137,6 +139,27 @@ def taylor_green(k, N=None):
                   0.0, sigma_for(k, h), 8, (1, 1, 1), (1, 1, 1), -1, 1, k + 3)
 
 
+D_C = (1.0, 0.25, 0.125, 0.25, 1.5, -0.25, 0.125, -0.25, 0.75)   # a fixed full SPD tensor
+
+
+def problem_c(k, P=1, m=None):
+    """The paper's Problem C as a synthetic stand-in: "multilinear geometries" --
+    the periodic unit box's N^3 grid with every vertex moved by up to 0.2 h per direction
+    (inputs.vertex_grid, seed 9), N = round(736.8/(k+1)) (~4e8 DOFs, the Table 1 protocol
+    PAPER.md:933-936) -- and q = 3p + 4, i.e. m = ceil((3k+5)/2) Gauss points per direction (m <= 16;
+    k = 10 falls back to m = 13). The paper's polynomial coefficients are not printed: a constant
+    full SPD tensor D_C, b = (1, 1/2, 1/4), c = 1, sigma = 3k(k+2)N. P > 1: the same block per GPU."""
+    N = int(round(736.8 / (k + 1)))
+    if m is None:
+        m = -(-(3 * k + 5) // 2)
+        if m > 16:
+            m = k + 3
+    px, py, pz = _WEAK_GRID[P]
+    nc = (N * px, N * py, N * pz)
+    return Config("C-k%d" % k if P == 1 else "C-k%d-P%d" % (k, P), nc, (0, 0, 0), (float(px), float(py), float(pz)),
+                  k, D_C, B_A, 1.0, sigma_for(k, 1.0 / N), 10, (px, py, pz), (1, 1, 1), -1, 0, m, 0.2, 9)
+
+
 def by_name(name):
     name = name.lower()
     table = {"c1": c1, "c2": c2, "c3": c3, "c5strong": c5_strong, "c5weak": c5_weak}
@@ -148,6 +171,8 @@ def by_name(name):
         return taylor_green(int(name[4:]))
     if name.startswith("mb-k"):
         return problem_a_matrix(int(name[4:]))
+    if name.startswith("c-k"):
+        return problem_c(int(name[3:]))
     return table[name]()
 
 

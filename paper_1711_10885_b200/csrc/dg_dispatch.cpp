@@ -62,21 +62,50 @@ namespace dg {
     int upload_tables_vb_n##n##_m##m(const HostTables&);                  \
     cudaError_t launch_vb_n##n##_m##m(const KParams&, cudaStream_t);      \
     int vb_info_n##n##_m##m(LaunchInfo*);
-#define DG_VPAIR(n, m2) DG_VDECL(n, n) DG_VDECL(n, m2)
-DG_VPAIR(2, 4) DG_VPAIR(3, 5) DG_VPAIR(4, 6) DG_VPAIR(5, 7) DG_VPAIR(6, 8) DG_VPAIR(7, 9) DG_VPAIR(8, 10) DG_VPAIR(9, 11)
+// (n, m) pairs of the variable-velocity kernel: m = n (q = 2p), n + 2 (q = 2p + 4, the paper's
+// Taylor-Green run) and ceil((3k + 5) / 2) (q = 3p + 4) while m <= 16
+DG_VDECL(2, 2)
+DG_VDECL(2, 4)
+DG_VDECL(3, 3)
+DG_VDECL(3, 5)
+DG_VDECL(3, 6)
+DG_VDECL(4, 4)
+DG_VDECL(4, 6)
+DG_VDECL(4, 7)
+DG_VDECL(5, 5)
+DG_VDECL(5, 7)
+DG_VDECL(5, 9)
+DG_VDECL(6, 6)
+DG_VDECL(6, 8)
+DG_VDECL(6, 10)
+DG_VDECL(7, 7)
+DG_VDECL(7, 9)
+DG_VDECL(7, 12)
+DG_VDECL(8, 8)
+DG_VDECL(8, 10)
+DG_VDECL(8, 13)
+DG_VDECL(9, 9)
+DG_VDECL(9, 11)
+DG_VDECL(9, 15)
+DG_VDECL(10, 10)
+DG_VDECL(10, 12)
+DG_VDECL(10, 16)
+DG_VDECL(11, 11)
+DG_VDECL(11, 13)
 
-#define DG_VCASES(call)                                                                            \
-    switch ((k + 1) * 100 + m) {                                                                   \
-    case 202: return call(2, 2); case 204: return call(2, 4); case 303: return call(3, 3);         \
-    case 305: return call(3, 5); case 404: return call(4, 4); case 406: return call(4, 6);         \
-    case 505: return call(5, 5); case 507: return call(5, 7); case 606: return call(6, 6);         \
-    case 608: return call(6, 8); case 707: return call(7, 7); case 709: return call(7, 9);         \
-    case 808: return call(8, 8); case 810: return call(8, 10); case 909: return call(9, 9);        \
-    case 911: return call(9, 11);                                                                  \
-    default: break;                                                                                \
+#define DG_VCASES(call)                 \
+    switch ((k + 1) * 100 + m) {        \
+    case 202: return call(2, 2); case 204: return call(2, 4); case 303: return call(3, 3); case 305: return call(3, 5); case 306: return call(3, 6); case 404: return call(4, 4); case 406: return call(4, 6); case 407: return call(4, 7); case 505: return call(5, 5); case 507: return call(5, 7); case 509: return call(5, 9); case 606: return call(6, 6); case 608: return call(6, 8); case 610: return call(6, 10); case 707: return call(7, 7); case 709: return call(7, 9); case 712: return call(7, 12); case 808: return call(8, 8); case 810: return call(8, 10); case 813: return call(8, 13); case 909: return call(9, 9); case 911: return call(9, 11); case 915: return call(9, 15); case 1010: return call(10, 10); case 1012: return call(10, 12); case 1016: return call(10, 16); case 1111: return call(11, 11); case 1113: return call(11, 13); \
+    default: break;                     \
     }
 
-bool vb_available(int k, int m) { return k >= 1 && k <= 8 && (m == k + 1 || m == k + 3); }
+bool vb_available(int k, int m)
+{
+    switch ((k + 1) * 100 + m) {
+    case 202: case 204: case 303: case 305: case 306: case 404: case 406: case 407: case 505: case 507: case 509: case 606: case 608: case 610: case 707: case 709: case 712: case 808: case 810: case 813: case 909: case 911: case 915: case 1010: case 1012: case 1016: case 1111: case 1113: return true;
+    default: return false;
+    }
+}
 
 int upload_tables_vb(int k, int m, const HostTables& t)
 {

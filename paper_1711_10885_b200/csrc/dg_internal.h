@@ -65,7 +65,6 @@ struct KParams {
     double ea, eb, es;        // epi 2: y = ea w + eb (z + es (f - A z)), es = dt / Delta_T
     int epi;                  // store epilogue: 0 y = A z, 1 residual, 2 SSP-RK stage
     const double* ghost[6];   // neighbour-rank face traces per face 2q+s: [layer cell][u | d][n^2] (nullptr: none)
-    int ghosts;               // this launch covers cells with a neighbour on another rank (the shell launch)
     const int64_t* task_list; // local linear cell ids (nullptr -> task box)
     int64_t ntasks;
     int64_t task_lo[3], task_cnt[3];
@@ -104,6 +103,7 @@ struct KParams {
     const double* vert;
     double Dp[9];
     double bp[3];
+    int ghosts;               // this launch covers cells with a neighbour on another rank (the shell launch)
 };
 
 struct LaunchInfo {

@@ -380,6 +380,16 @@ def from_config(cfg, **kw):
     op = Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, **kw)
     if getattr(cfg, "bkind", 0):
         op.set_velocity(cfg.bkind)
-    if getattr(cfg, "m", 0) and cfg.m != cfg.k + 1:
+    if getattr(cfg, "geo_amp", 0.0) > 0.0:
+        op.set_geometry(padded_vertex_grid(cfg, op.cell_lo, op.cell_cnt), cfg.m or cfg.k + 1)
+    elif getattr(cfg, "m", 0) and cfg.m != cfg.k + 1:
         op.set_quadrature(cfg.m)
     return op
+
+
+def padded_vertex_grid(cfg, cell_lo, cell_cnt):
+    """The padded vertex grid dg_set_geometry takes for a rank's box (include/dg.h), from the
+    seeded multilinear mesh of a config (inputs.vertex_grid)."""
+    from . import inputs
+    box = (tuple(cell_lo[q] - 1 for q in range(3)), tuple(cell_lo[q] + cell_cnt[q] + 2 for q in range(3)))
+    return inputs.vertex_grid(cfg.ncells, cfg.lo, cfg.hi, cfg.geo_amp, cfg.geo_seed, cfg.periodic, box=box)

@@ -73,14 +73,16 @@ def test_geometry_term_masks(mask):
     assert rel(y, A @ z) < 1e-12
 
 
-@pytest.mark.parametrize("k,m", [(6, 7), (6, 12), (7, 8), (7, 13), (8, 15), (9, 16), (10, 13)])
+@pytest.mark.parametrize("k,m", [(6, 7), (6, 12), (7, 8), (7, 10), (7, 13), (8, 15), (9, 16), (10, 11), (10, 13)])
 def test_geometry_high_degree_vs_o2(k, m):
-    nc, lo, hi = (2, 2, 1), (0.0, 0.0, 0.0), (1.0, 1.0, 0.5)
+    """Two cells: an interior and two Dirichlet x-faces, self-periodic y and z (wrap onto itself)."""
+    nc, lo, hi = (2, 1, 1), (0.0, 0.0, 0.0), (1.0, 0.5, 0.5)
+    per = (0, 1, 1)
     sigma = 3.0 * k * (k + 2) / 0.5
-    z = inputs.uniform(4 * (k + 1) ** 3, 21)
-    X = inputs.vertex_grid(nc, lo, hi, 0.2, 8, (0, 0, 1))
-    A = o2g.assemble(nc, X, k, DFULL, B, 0.3, sigma, m=m, periodic=(0, 0, 1))
-    y = gpu_apply(nc, lo, hi, k, DFULL, B, 0.3, sigma, z, m, 0.2, 8, (0, 0, 1))
+    z = inputs.uniform(2 * (k + 1) ** 3, 21)
+    X = inputs.vertex_grid(nc, lo, hi, 0.2, 8, per)
+    A = o2g.assemble(nc, X, k, DFULL, B, 0.3, sigma, m=m, periodic=per)
+    y = gpu_apply(nc, lo, hi, k, DFULL, B, 0.3, sigma, z, m, 0.2, 8, per)
     assert rel(y, A @ z) < 1e-12
 
 

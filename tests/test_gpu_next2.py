@@ -46,15 +46,20 @@ def run(cfg, z_np, kind, m, amp=(1.0, 1.0, 1.0), terms=7, periodic=None):
     return y.cpu().numpy(), info
 
 
-@pytest.mark.parametrize("k", list(range(1, 9)))
-@pytest.mark.parametrize("extra", [0, 2])
-def test_taylor_green_vs_o1(k, extra):
+@pytest.mark.parametrize("k", list(range(1, 11)))
+@pytest.mark.parametrize("rule", ["2p", "2p+4", "3p+4"])
+def test_taylor_green_vs_o1(k, rule):
+    """q = 2p (m = k+1), 2p + 4 (m = k+3, the paper's Taylor-Green run) and Problem C's 3p + 4
+    (m = ceil((3k+5)/2), PAPER.md:957-961) while m <= 16."""
+    m = {"2p": k + 1, "2p+4": k + 3, "3p+4": -(-(3 * k + 5) // 2)}[rule]
+    if m > 16:
+        pytest.skip("m > 16 is not compiled (shared memory of one cell)")
     cfg = tg_cfg(k, D=0.05)
     z = inputs.uniform(cfg.ndofs, 40 + k)
-    y, info = run(cfg, z, 1, k + 1 + extra)
-    yref, _ = o1.apply(*cfg.args(), z, m=k + 1 + extra, bkind=1, periodic=(1, 1, 1))
+    y, info = run(cfg, z, 1, m)
+    yref, _ = o1.apply(*cfg.args(), z, m=m, bkind=1, periodic=(1, 1, 1))
     assert rel(y, yref) < TOL
-    assert info["threads_per_cta"] >= (k + 1 + extra) ** 2
+    assert info["threads_per_cta"] >= m ** 2
 
 
 @pytest.mark.parametrize("k", [1, 3, 6])
@@ -187,5 +192,7 @@ def test_mode_switching_and_errors():
     op.close()
     op9 = dg.Operator((2, 2, 2), (0, 0, 0), (1, 1, 1), 9, cfg.D, cfg.b, cfg.c, 100.0)
     with pytest.raises(dg.DGError):
-        op9.set_quadrature(12)                    # k = 9: m = k + 3 > 11 points
+        op9.set_quadrature(13)                    # k = 9: only m = 10, 12, 16 are compiled
+    with pytest.raises(dg.DGError):
+        op9.set_quadrature(19)                    # beyond the tables
     op9.close()

@@ -2,7 +2,8 @@
 
     python tools/ab_time.py --trees . variants/r1 --workloads c3 a-k7 [--rounds 3]
 
-Each tree is a directory holding a built paper_1711_10885_b200 package (binding + .so; e.g. an
+Each tree is a directory holding a built paper_1711_10885_b200 package (or a variant .so of
+tools/variant.py, loaded through DG_LIB with this tree's binding) (binding + .so; e.g. an
 older commit's package copied under variants/, git-ignored). Runs tools/quick_time.py once per
 (round, workload, tree) in a fresh process with PYTHONPATH at the tree, alternating the order so
 clock drift hits all alike, and prints the median GDOF/s per (workload, tree)."""
@@ -27,8 +28,11 @@ def main():
     for r in range(a.rounds):
         for w in a.workloads:
             for lib in (a.trees if r % 2 == 0 else a.trees[::-1]):
-                env = dict(os.environ, PYTHONPATH=os.path.abspath(lib))
-                env.pop("DG_LIB", None)
+                if lib.endswith(".so"):       # a variant library (tools/variant.py) with this tree's binding
+                    env = dict(os.environ, PYTHONPATH=ROOT, DG_LIB=os.path.abspath(lib))
+                else:
+                    env = dict(os.environ, PYTHONPATH=os.path.abspath(lib))
+                    env.pop("DG_LIB", None)
                 out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "quick_time.py"), w, str(a.reps)],
                                      capture_output=True, text=True, env=env).stdout
                 m = re.search(r"GDOF/s ([0-9.]+)", out)
