@@ -102,8 +102,12 @@ __device__ __forceinline__ double adjugate(const double (&J)[3][3], double (&A)[
     return J[0][0] * A[0][0] + J[1][0] * A[0][1] + J[2][0] * A[0][2];
 }
 
+// minimum CTAs per SM (one cell each for m >= 6)
+#ifndef DG_GEO_MINB
+#define DG_GEO_MINB ((DG_M) <= 13 ? 2 : 1)   // c-k7 (m = 13): 2.8 -> 4.3 GDOF/s; m = 15 spills at 2 (c-k9 2.5 -> 2.2)
+#endif
 template <int N, int M>
-__global__ void __launch_bounds__(GCfg<M>::TPC)
+__global__ void __launch_bounds__(GCfg<M>::TPC, DG_GEO_MINB)
 dg_geo_kernel(const __grid_constant__ KParams p)
 {
     constexpr int CW = GCfg<M>::CW, CC = GCfg<M>::C;
@@ -278,8 +282,10 @@ dg_geo_kernel(const __grid_constant__ KParams p)
     //      the face slots are overwritten with the lift coefficients:
     //      c = 0: c_v, 1: c_g w_q (normal), 2: c_g w_t1, 3: c_g w_t2, w = adj(J) D nu / det J
     const double* Dp = p.Dp;
-    for (int t = lane; t < 3 * MM; t += CW) {
-        const int q = t / MM, a = (t % MM) % M, b = (t % MM) / M;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)                      // (q static: no runtime-indexed local arrays)
+    for (int t = lane; t < MM; t += CW) {
+        const int a = t % M, b = t / M;
         const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
         const double* Dq[4] = {U, DX, DY, DZ};
 #pragma unroll 1
@@ -294,7 +300,7 @@ dg_geo_kernel(const __grid_constant__ KParams p)
             // own traces: u and the reference gradient extrapolated along the normal pencil
             double tr[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 4; ++c) {   // (unrolled: Dq[c] static)
                 double acc = 0.0;
 #pragma unroll
                 for (int l = 0; l < M; ++l) {

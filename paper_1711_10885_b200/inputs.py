@@ -76,8 +76,11 @@ def tensor_field_cells(cells, seed):
 # vertex moved by amp * h_q * U(seed, 3 g + q) in each direction q (g = the GLOBAL vertex index
 # ix + (Nx+1)(iy + (Ny+1) iz)); vertices on a Dirichlet side of the box keep their normal
 # coordinate (the domain stays the box); along a periodic direction the perturbation of vertex
-# N_q is that of vertex 0 (the grid stays periodic). amp <= 0.25 keeps every cell's Jacobian
-# determinant positive (each corner moves less than h/4 per direction).
+# N_q is that of vertex 0 (the grid stays periodic). With amp < 1/6 every edge vector of a cell
+# has its own-direction component >= (1 - 2 amp) h and the other two <= 2 amp h, so every
+# Jacobian (a convex combination of edge vectors per column) is column diagonally dominant with
+# a positive diagonal: det J > 0 everywhere. Larger amp is allowed but not guaranteed valid
+# (dg_set_geometry checks det J > 0 at every quadrature point and corner).
 def vertex_grid(ncells, lo, hi, amp, seed, periodic=(0, 0, 0), box=None):
     """Vertex coordinates [iz][iy][ix][3] of the global grid (or of the sub-box
     box = ((i0, j0, k0), (i1, j1, k1)) of vertex indices, i1 exclusive; indices outside

@@ -7,6 +7,8 @@ import torch
 
 if os.environ.get("PYTHONPATH"):
     sys.path.insert(0, os.environ["PYTHONPATH"].split(":")[0])   # tools/ab_time.py: the tree under test first
+else:
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_1711_10885_b200 import configs, dg
 
