@@ -342,12 +342,37 @@ dg_geo_kernel(const __grid_constant__ KParams p)
                 gn[t1] = F[FA::at(f, 2, a, b)];
                 gn[t2] = F[FA::at(f, 3, a, b)];
                 const double un = F[FA::at(f, 0, a, b)];
-                double xn[3] = {xr[0], xr[1], xr[2]};
-                xn[q] = 1.0 - (double)s;
-                int o[3] = {1, 1, 1};
-                o[q] = s ? 2 : 0;
+                // the neighbour's Jacobian at the common point: its tangential columns are this
+                // cell's (the shared face), its normal column the bilinear interpolation of its
+                // q-edges at (xi_t1, xi_t2) (a Q1 map's column q does not depend on xi_q)
                 double Jn[3][3], An[3][3];
-                jac(VB, o[0], o[1], o[2], xn[0], xn[1], xn[2], Jn);
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int c2 = 0; c2 < 3; ++c2) Jn[r][c2] = J[r][c2];
+                {
+                    int o[3] = {1, 1, 1};
+                    o[q] = s ? 2 : 0;
+                    auto X = [&](const int (&v)[3], int r) {
+                        return VB[(((o[2] + v[2]) * 4 + (o[1] + v[1])) * 4 + (o[0] + v[0])) * 3 + r];
+                    };
+                    const double B1[2] = {1.0 - T.xi[a], T.xi[a]}, B2[2] = {1.0 - T.xi[b], T.xi[b]};
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) {
+                        double acc = 0.0;
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+#pragma unroll
+                            for (int v = 0; v < 2; ++v) {
+                                int hi[3], lo3[3];
+                                hi[q] = 1; lo3[q] = 0;
+                                hi[t1] = lo3[t1] = u;
+                                hi[t2] = lo3[t2] = v;
+                                acc = fma(B1[u] * B2[v], X(hi, r) - X(lo3, r), acc);
+                            }
+                        Jn[r][q] = acc;
+                    }
+                }
                 const double detn = adjugate(Jn, An);
                 double sn = 0.0;
 #pragma unroll
@@ -382,12 +407,57 @@ dg_geo_kernel(const __grid_constant__ KParams p)
         const int pa = lane % M, pb = lane / M;
         const double xa = T.xi[pa], xb = T.xi[pb];
         const double wab = T.w[pa] * T.w[pb];
+        // Along this z-pencil (xi_x, xi_y fixed) the Q1 map's Jacobian columns are affine in
+        // c = xi_z: J e_x = P0 + c Q0, J e_y = P1 + c Q1, J e_z = C2 (bilinear in (xi_x, xi_y) only);
+        // so are the adjugate's rows 0, 1, and row 2 is quadratic. Precomputed once per pencil.
+        double P0[3], Q0[3], P1[3], Q1[3], C2[3];
+        {
+            auto X = [&](int i, int j, int k, int r) { return VB[(((1 + k) * 4 + (1 + j)) * 4 + (1 + i)) * 3 + r]; };
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const double e00 = X(1, 0, 0, r) - X(0, 0, 0, r), e10 = X(1, 1, 0, r) - X(0, 1, 0, r);
+                const double e01 = X(1, 0, 1, r) - X(0, 0, 1, r), e11 = X(1, 1, 1, r) - X(0, 1, 1, r);
+                P0[r] = (1.0 - xb) * e00 + xb * e10;
+                Q0[r] = (1.0 - xb) * (e01 - e00) + xb * (e11 - e10);
+                const double f00 = X(0, 1, 0, r) - X(0, 0, 0, r), f10 = X(1, 1, 0, r) - X(1, 0, 0, r);
+                const double f01 = X(0, 1, 1, r) - X(0, 0, 1, r), f11 = X(1, 1, 1, r) - X(1, 0, 1, r);
+                P1[r] = (1.0 - xa) * f00 + xa * f10;
+                Q1[r] = (1.0 - xa) * (f01 - f00) + xa * (f11 - f10);
+                const double g00 = X(0, 0, 1, r) - X(0, 0, 0, r), g10 = X(1, 0, 1, r) - X(1, 0, 0, r);
+                const double g01 = X(0, 1, 1, r) - X(0, 1, 0, r), g11 = X(1, 1, 1, r) - X(1, 1, 0, r);
+                C2[r] = (1.0 - xb) * ((1.0 - xa) * g00 + xa * g10) + xb * ((1.0 - xa) * g01 + xa * g11);
+            }
+        }
+        auto cross = [](const double (&a)[3], const double (&b)[3], double (&o)[3]) {
+            o[0] = a[1] * b[2] - a[2] * b[1];
+            o[1] = a[2] * b[0] - a[0] * b[2];
+            o[2] = a[0] * b[1] - a[1] * b[0];
+        };
+        double R0a[3], R0b[3], R1a[3], R1b[3], R2a[3], R2b[3], R2c[3], t0[3], t1v[3];
+        cross(P1, C2, R0a);                       // row 0 = (J e_y) x (J e_z)
+        cross(Q1, C2, R0b);
+        cross(C2, P0, R1a);                       // row 1 = (J e_z) x (J e_x)
+        cross(C2, Q0, R1b);
+        cross(P0, P1, R2a);                       // row 2 = (J e_x) x (J e_y)
+        cross(P0, Q1, t0);
+        cross(Q0, P1, t1v);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) R2b[r] = t0[r] + t1v[r];
+        cross(Q0, Q1, R2c);
 #pragma unroll 1
         for (int e = 0; e < M; ++e) {
             const int ix = LY::at(pa, pb, e);
-            double J[3][3], A[3][3];
-            jac(VB, 1, 1, 1, xa, xb, T.xi[e], J);
-            const double det = adjugate(J, A);
+            const double c = T.xi[e];
+            double A[3][3];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                A[0][r] = fma(c, R0b[r], R0a[r]);
+                A[1][r] = fma(c, R1b[r], R1a[r]);
+                A[2][r] = fma(c, fma(c, R2c[r], R2b[r]), R2a[r]);
+            }
+            // det J = (J e_x) . row 0
+            const double det = fma(c, Q0[0], P0[0]) * A[0][0] + fma(c, Q0[1], P0[1]) * A[0][1] +
+                               fma(c, Q0[2], P0[2]) * A[0][2];
             const double W = do_vol ? wab * T.w[e] : 0.0;
             const double g[3] = {DX[ix], DY[ix], DZ[ix]};
             const double u = U[ix];
