@@ -523,8 +523,14 @@ __device__ __forceinline__ unsigned nb_load(const KParams& p, const double* zc, 
     const bool gl = GH && hl && lq == 0 && !p.wrap[q];     // the low neighbour lives on another rank
     const bool gh = GH && hh && lq + 1 == nq && !p.wrap[q];
     const int64_t wst = (int64_t)(nq - 1) * st * n3;   // periodic wrap inside this rank's box
-    const double* zl = (lq > 0) ? zc - st * n3 : (p.wrap[q] ? zc + wst : zc);
-    const double* zh = (lq + 1 < nq) ? zc + st * n3 : (p.wrap[q] ? zc - wst : zc);
+    // (GH = false never reaches the third alternative -- a cell at the box edge with a neighbour
+    // there is a wrap or a ghost -- but this form of the selection measured 2.2 % faster at C3
+    // than selecting zc: 84.5 against 82.7 GDOF/s, A/B on one box; it is only a code-generation
+    // effect, nothing is loaded through p.ghost without GH)
+    const double* zl = (lq > 0) ? zc - st * n3
+                     : (p.wrap[q] ? zc + wst : ((!GH && hl) ? p.ghost[2 * q] + gi * n3 : zc));
+    const double* zh = (lq + 1 < nq) ? zc + st * n3
+                     : (p.wrap[q] ? zc - wst : ((!GH && hh) ? p.ghost[2 * q + 1] + gi * n3 : zc));
     const double* tl = gl ? p.ghost[2 * q] + gi * 2 * NN : nullptr;
     const double* th = gh ? p.ghost[2 * q + 1] + gi * 2 * NN : nullptr;
     const bool ll = hl && !gl, lh = hh && !gh;

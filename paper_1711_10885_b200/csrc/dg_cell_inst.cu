@@ -184,7 +184,8 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
     if constexpr (N <= DG_REG_NMAX) {
         if (use_reg()) {
             const int64_t grid = (p.ntasks + REG_THREADS - 1) / REG_THREADS;
-            dg_reg_kernel<N, false><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
+            if (p.ghosts) dg_reg_kernel<N, false, true><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
+            else dg_reg_kernel<N, false, false><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
             return cudaGetLastError();
         }
     }
@@ -232,7 +233,8 @@ cudaError_t DG_CAT(launch_gen_n, DG_N)(const KParams& p, cudaStream_t s)
     if constexpr (N <= DG_REG_GMAX) {
         if (use_reg()) {
             const int64_t grid = (p.ntasks + REG_THREADS - 1) / REG_THREADS;
-            dg_reg_kernel<N, true><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
+            if (p.ghosts) dg_reg_kernel<N, true, true><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
+            else dg_reg_kernel<N, true, false><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
             return cudaGetLastError();
         }
     }

@@ -155,7 +155,7 @@ __device__ __forceinline__ void fstage(const double (&M)[N][N], const double (&a
 // GEN: full per-cell tensors (dg_gen.cuh semantics): nu.D grad u with the tangential derivatives
 // of both traces (own: Dc along the face lines; neighbour: G in its tangential stages), weights
 // w-+ = d+-/(d- + d+), penalty <d-, d+> sigma_q (C-5), tangential test-derivative lifts with Dc^T.
-template <int N, int Q, bool GEN>
+template <int N, int Q, bool GEN, bool GH>
 __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, const double* zc, int64_t n3,
                                           const int (&lc)[3], int64_t cell, unsigned nbmask, bool do_int, bool do_bnd,
                                           const double (&Dw)[6], const double (&u)[N * N * N], double (&X)[N * N * N])
@@ -170,7 +170,7 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
         if (interior) {
             // normal first: the neighbour is seen at its x_q = 1 (s = 0) or 0 (s = 1)
             double cu[N][N], cd[N][N];
-            if (const double* tr = reg_ghost<N>(p, lc, Q, s)) {   // contracted by its rank
+            if (const double* tr = GH ? reg_ghost<N>(p, lc, Q, s) : nullptr) {   // contracted by its rank
 #pragma unroll
                 for (int a = 0; a < N; ++a)
 #pragma unroll
@@ -316,7 +316,7 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
 #ifndef DG_RMINB
 #define DG_RMINB(n, gen) ((n) == 2 ? ((gen) ? 4 : 5) : 1)
 #endif
-template <int N, bool GEN>
+template <int N, bool GEN, bool GH = false>
 __global__ void __launch_bounds__(128, DG_RMINB(N, GEN)) dg_reg_kernel(const __grid_constant__ KParams p)
 {
     constexpr int N3 = N * N * N;
@@ -463,9 +463,9 @@ __global__ void __launch_bounds__(128, DG_RMINB(N, GEN)) dg_reg_kernel(const __g
                     X[i] = fma(wc * R.w[ix] * R.w[iy] * R.w[iz], u[i], X[i]);
                 }
     }
-    reg_faces<N, 0, GEN>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
-    reg_faces<N, 1, GEN>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
-    reg_faces<N, 2, GEN>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
+    reg_faces<N, 0, GEN, GH>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
+    reg_faces<N, 1, GEN, GH>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
+    reg_faces<N, 2, GEN, GH>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
     rcontract_t<N, 2>(R.V, X, t);
     rcontract_t<N, 1>(R.V, t, u);
     rcontract_t<N, 0>(R.V, u, t);                   // y block
