@@ -233,6 +233,21 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     double Dw[6];                                                // this cell's tensor
 #pragma unroll
     for (int i = 0; i < 6; ++i) Dw[i] = __ldg(p.Dfield + 6 * cell + i);
+    // The face passes give work item tk = lane (one pass over 6 n face lines when TPC >= 6 n) the
+    // lines of face f = lane / n: that face's neighbour tensor is loaded here, long before its use
+    // (the dependent L2 loads in the passes were long-scoreboard stalls)
+    constexpr bool PREF = TPC >= 6 * N;
+    double pf_qq = 0.0, pf_q1 = 0.0, pf_q2 = 0.0;
+    if (PREF && lane < 6 * N) {
+        const int f = lane / N, q = f >> 1;
+        const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
+        if ((nbmask >> f) & 1u) {
+            const double* Dn = nb_dfield(p, lc, cell, f, nbmask);
+            pf_qq = __ldg(Dn + q);
+            pf_q1 = __ldg(Dn + dsym(q, t1));
+            pf_q2 = __ldg(Dn + dsym(q, t2));
+        }
+    }
 
     int pa[P], pb[P];
     bool act[P];
@@ -374,8 +389,15 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         const int f = tk / N, line = tk - f * N, q = f >> 1;
         if (!((nbi >> f) & 1u)) continue;
         const int t1 = (q == 0) ? 1 : 0;
-        const double* Dn = nb_dfield(p, lc, cell, f, nbmask);
-        const double cqq = __ldg(Dn + q) * p.hinv[q], cq1 = __ldg(Dn + dsym(q, t1)) * p.hinv[t1];
+        double cqq, cq1;
+        if (PREF) {
+            cqq = pf_qq * p.hinv[q];
+            cq1 = pf_q1 * p.hinv[t1];
+        } else {
+            const double* Dn = nb_dfield(p, lc, cell, f, nbmask);
+            cqq = __ldg(Dn + q) * p.hinv[q];
+            cq1 = __ldg(Dn + dsym(q, t1)) * p.hinv[t1];
+        }
         double rr[1][N], tt[1][N], ga[N];
 #pragma unroll
         for (int e = 0; e < N; ++e) rr[0][e] = NT[GFLay<N>::at(2 * f, e, line)];
@@ -401,8 +423,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         if (tk < 6 * N) {
             // neighbour stage 2 (lines along i2): u+ = V Va, s+ = V E + D+_qt2/h_t2 G Va
             if (!((nbi >> f) & 1u)) continue;
-            const double* Dn = nb_dfield(p, lc, cell, f, nbmask);
-            const double cq2 = __ldg(Dn + dsym(q, t2)) * p.hinv[t2];
+            const double cq2 = (PREF ? pf_q2 : __ldg(nb_dfield(p, lc, cell, f, nbmask) + dsym(q, t2))) * p.hinv[t2];
             double rr[1][N], tt[1][N], va[N], gv[N];
 #pragma unroll
             for (int e = 0; e < N; ++e) va[e] = NT[GFLay<N>::at(2 * f, line, e)];
@@ -479,7 +500,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
             for (int e = 0; e < N; ++e) so[e] = fma(cq2, tt[0][e], OT[GFLay<N>::at(2 * f + 1, line, e)]);
         }
         double dnb = 0.0;
-        if (interior) dnb = __ldg(nb_dfield(p, lc, cell, f, nbmask) + q);
+        if (interior) dnb = PREF ? pf_qq : __ldg(nb_dfield(p, lc, cell, f, nbmask) + q);
         const double dm = sd ? dme : dnb, dp = sd ? dnb : dme;     // delta of T-, T+
         const double dsum = dm + dp;
         const double rsum = dsum == 0.0 ? 0.0 : 1.0 / dsum;
