@@ -196,7 +196,7 @@ def load_ncu(cfg, kname):
     """The committed ncu --set full summary of this workload's operator kernel, or ({}, why).
     Only a capture of THIS build (paper_1711_10885_b200.build.kernel_hash) and of the same kernel
     and per-rank DOF count is used; at N > 1 the N = 1 capture of the same per-GPU block."""
-    from paper_1711_10885_b200.build import kernel_hash
+    from paper_1711_10885_b200.build import kernel_family, kernel_hash
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as f:
@@ -208,8 +208,9 @@ def load_ncu(cfg, kname):
     ent = d.get(name)
     if not ent:
         return {}, "no ncu capture of %s" % name
-    if ent.get("build_hash") != kernel_hash():
-        return {}, "ncu capture of %s belongs to build %s, not %s" % (name, ent.get("build_hash"), kernel_hash())
+    want = kernel_hash(kernel_family(kname))
+    if ent.get("build_hash") != want:
+        return {}, "ncu capture of %s belongs to build %s, not %s" % (name, ent.get("build_hash"), want)
     if kname.split("<")[0] not in ent.get("kernel", ""):
         return {}, "ncu capture of %s is of %s" % (name, ent.get("kernel"))
     return ent, "profiles/ncu_full_summary.json[%s] (ncu --set full, --clock-control none, build %s)" % (

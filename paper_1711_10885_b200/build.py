@@ -48,18 +48,31 @@ def _sources():
     return jobs
 
 
-def kernel_hash():
-    """Hash of everything that determines the compiled operator kernels (kernel headers, their
-    translation units, the shared declarations, the tables, the flags): the key under which
+# the sources each kernel family's translation unit compiles (its .cu, the headers it includes, the
+# shared declarations and the tables it is given)
+KERNEL_SOURCES = {
+    "cell": ["dg_cell_inst.cu", "dg_cell.cuh", "dg_gen.cuh", "dg_reg.cuh", "dg_mma8.cuh", "dg_internal.h", "tables.cpp"],
+    "vb": ["dg_vb_inst.cu", "dg_vb.cuh", "dg_cell.cuh", "dg_internal.h", "tables.cpp"],
+    "geo": ["dg_geo_inst.cu", "dg_geo.cuh", "dg_cell.cuh", "dg_internal.h", "tables.cpp"],
+}
+
+
+def kernel_family(kernel_name):
+    """'cell' | 'vb' | 'geo' for a kernel name such as 'dg_gen_kernel<8>'."""
+    return "vb" if "dg_vb" in kernel_name else ("geo" if "dg_geo" in kernel_name else "cell")
+
+
+def kernel_hash(family="cell"):
+    """Hash of everything that determines one kernel family's compiled code (its translation unit
+    and the headers it includes, the tables, the flags): the key under which
     profiles/ncu_full_summary.json stores executed-flop counts, so bench.py never pairs a timing
     with the counts of another build. Host-only files (the ABI, dispatch, transport) are not in it."""
     h = hashlib.sha256()
     h.update(" ".join(ARCH + FLAGS[:3]).encode())
-    for f in sorted(os.listdir(CSRC)):
-        if f.endswith(".cuh") or f.endswith("_inst.cu") or f in ("dg_internal.h", "tables.cpp"):
-            h.update(f.encode())
-            with open(os.path.join(CSRC, f), "rb") as fh:
-                h.update(fh.read())
+    for f in KERNEL_SOURCES[family]:
+        h.update(f.encode())
+        with open(os.path.join(CSRC, f), "rb") as fh:
+            h.update(fh.read())
     return h.hexdigest()[:16]
 
 

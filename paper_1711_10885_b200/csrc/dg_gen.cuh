@@ -236,7 +236,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     // The face passes give work item tk = lane (one pass over 6 n face lines when TPC >= 6 n) the
     // lines of face f = lane / n: that face's neighbour tensor is loaded here, long before its use
     // (the dependent L2 loads in the passes were long-scoreboard stalls)
-    constexpr bool PREF = TPC >= 6 * N;
+    constexpr bool PREF = TPC >= 6 * N && N != 10;   // (n = 10: A-k9 -3.6 %; A-k7 +6.4 %, A-k5 +3.5 %)
     double pf_qq = 0.0, pf_q1 = 0.0, pf_q2 = 0.0;
     if (PREF && lane < 6 * N) {
         const int f = lane / N, q = f >> 1;

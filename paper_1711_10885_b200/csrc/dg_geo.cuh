@@ -288,6 +288,19 @@ dg_geo_kernel(const __grid_constant__ KParams p)
         const int a = t % M, b = t / M;
         const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
         const double* Dq[4] = {U, DX, DY, DZ};
+        double tr0[4], tr1[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {   // (unrolled: Dq[c] static)
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int l = 0; l < M; ++l) {
+                const double v = Dq[c][q == 0 ? LY::at(l, a, b) : (q == 1 ? LY::at(a, l, b) : LY::at(a, b, l))];
+                a0 = fma(T.L[0][l], v, a0);
+                a1 = fma(T.L[1][l], v, a1);
+            }
+            tr0[c] = a0;
+            tr1[c] = a1;
+        }
 #pragma unroll 1
         for (int s = 0; s < 2; ++s) {
             const int f = 2 * q + s;
@@ -297,18 +310,11 @@ dg_geo_kernel(const __grid_constant__ KParams p)
                 for (int c = 0; c < 4; ++c) F[FA::at(f, c, a, b)] = 0.0;
                 continue;
             }
-            // own traces: u and the reference gradient extrapolated along the normal pencil
+            // own traces: u and the reference gradient extrapolated along the normal pencil (both
+            // faces' in the first pass: each pencil value is read once)
             double tr[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {   // (unrolled: Dq[c] static)
-                double acc = 0.0;
-#pragma unroll
-                for (int l = 0; l < M; ++l) {
-                    const int ix = q == 0 ? LY::at(l, a, b) : (q == 1 ? LY::at(a, l, b) : LY::at(a, b, l));
-                    acc = fma(T.L[s][l], Dq[c][ix], acc);
-                }
-                tr[c] = acc;
-            }
+            for (int c = 0; c < 4; ++c) tr[c] = s ? tr1[c] : tr0[c];
             double xr[3];
             xr[q] = (double)s;
             xr[t1] = T.xi[a];

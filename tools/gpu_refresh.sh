@@ -1,15 +1,28 @@
-# Round-end refresh on one B200 (run under gpurun): GPU suite, bench line, launch list,
-# ncu --set full captures of the operator kernels, degree / workload sweeps.
+# Refresh of the committed evidence on one B200 (run under gpurun): GPU suite, bench lines,
+# launch list, ncu --set full captures of the operator kernels, degree / workload sweeps.
 # Every ncu command follows a plain run of the same command that exited 0 (B200_PROFILING.md).
+# Summarise here afterwards: python tools/ncu_summary.py gpurun_out/<rep> --name <cfg> --ndofs <n> --json profiles/ncu_full_summary.json
 export PYTHONPATH=$PWD
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
-python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log | cut -c1-300
-python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain_c3.log 2>&1 &&
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain_c3b.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:dg_cell_kernel -s 3 -c 1 -o gpurun_out/cell_full python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo "ncu C3 rc=$?"
+# captures first (fresh clocks), each after its plain run
+python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain_c3.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:dg_cell_kernel -s 3 -c 1 -o gpurun_out/c3_full python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_c3.log 2>&1; echo "ncu C3 rc=$?"
+python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain_c3l.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 for w in a-k7 c-k7 tg-k5; do
   python tools/quick_time.py $w 2 > gpurun_out/plain_$w.log 2>&1 &&
   ncu --set full --clock-control none --import-source on -k regex:"dg_(gen|geo|vb)_kernel" -s 2 -c 1 -o gpurun_out/${w}_full python tools/quick_time.py $w 2 > gpurun_out/ncu_$w.log 2>&1; echo "ncu $w rc=$?"
 done
+# bench lines
+python bench.py --steps 20 --warmup 5 --submesh-check > gpurun_out/bench_c3.log 2>&1; echo "bench C3 rc=$?"; tail -1 gpurun_out/bench_c3.log | cut -c1-200
+for w in c5weak c5strong a-k7 c-k7 tg-k5; do
+  python bench.py --workload $w --steps 10 --warmup 3 --no-e2e --submesh-check > gpurun_out/bench_$w.log 2>&1; echo "bench $w rc=$?"
+done
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "reference rc=$?"
+# sweeps
+python tools/sweep.py --out gpurun_out/sweep.json > gpurun_out/sweep.log 2>&1; echo "sweep rc=$?"
+for k in 1 2 3 4 5 6 7 8 9 10; do echo "a-k$k $(python tools/quick_time.py a-k$k 5 | tail -1)"; done > gpurun_out/problemA.log
+for k in 1 2 3 4 5 6 7 8 9 10; do echo "tg-k$k $(python tools/quick_time.py tg-k$k 3 | tail -1)"; done > gpurun_out/tg.log
+bash tools/geo_sweep.sh > gpurun_out/geo.log 2>&1
+echo done

@@ -105,8 +105,8 @@ def main():
     cell = [d for d in launches if any(k in d.get("Kernel Name", ("", ""))[0] for k in keys)] or launches
     s = summarize(cell[0])
     sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
-    from paper_1711_10885_b200.build import kernel_hash
-    s["build_hash"] = kernel_hash()     # the build this capture belongs to (bench.py checks it)
+    from paper_1711_10885_b200.build import kernel_family, kernel_hash
+    s["build_hash"] = kernel_hash(kernel_family(s["kernel"]))   # the build this capture belongs to (bench.py checks it)
     if args.ndofs:
         s["ndofs"] = args.ndofs
         if s.get("executed_fp64_flops"):
