@@ -51,15 +51,19 @@ def _sources():
 # the sources each kernel family's translation unit compiles (its .cu, the headers it includes, the
 # shared declarations and the tables it is given)
 KERNEL_SOURCES = {
-    "cell": ["dg_cell_inst.cu", "dg_cell.cuh", "dg_gen.cuh", "dg_reg.cuh", "dg_mma8.cuh", "dg_internal.h", "tables.cpp"],
+    "cell": ["dg_cell_inst.cu", "dg_cell.cuh", "dg_reg.cuh", "dg_mma8.cuh", "dg_internal.h", "tables.cpp"],
+    "gen": ["dg_cell_inst.cu", "dg_gen.cuh", "dg_cell.cuh", "dg_reg.cuh", "dg_internal.h", "tables.cpp"],
     "vb": ["dg_vb_inst.cu", "dg_vb.cuh", "dg_cell.cuh", "dg_internal.h", "tables.cpp"],
     "geo": ["dg_geo_inst.cu", "dg_geo.cuh", "dg_cell.cuh", "dg_internal.h", "tables.cpp"],
 }
 
 
 def kernel_family(kernel_name):
-    """'cell' | 'vb' | 'geo' for a kernel name such as 'dg_gen_kernel<8>'."""
-    return "vb" if "dg_vb" in kernel_name else ("geo" if "dg_geo" in kernel_name else "cell")
+    """'cell' | 'gen' | 'vb' | 'geo' for a kernel name such as 'dg_gen_kernel<8>'."""
+    for fam in ("gen", "vb", "geo"):
+        if "dg_%s" % fam in kernel_name:
+            return fam
+    return "cell"
 
 
 def kernel_hash(family="cell"):

@@ -133,21 +133,6 @@ template <int N, int ARR, int CR> struct GFLayRot {
     }
 };
 template <> struct GFLay<7> : GFLayRot<7, 49, 6> {};
-// n = 8: the fast kernel's XOR swizzle with the face parity (arr >> 1) & 1 flipping both the row
-// half (bit 3 of the bank) and bit 2 of the column swizzle. The face passes put faces f and f + 1
-// in one half-warp (8 lanes each: lines along i1 or along i2); with FLay<8> their lines landed on
-// the same 8 banks (2-way conflicts on every face-pass access: ncu A-k7, 25 % of the shared
-// wavefronts), here on complementary ones; per-point accesses (fixed array) stay conflict free
-#ifndef DG_GEN8_FLAY_OLD
-template <> struct GFLay<8> {
-    static constexpr int SLOT = 12 * 64;
-    __device__ __forceinline__ static int at(int arr, int i1, int i2)
-    {
-        const int fp = (arr >> 1) & 1;
-        return 64 * arr + 8 * (i2 ^ (arr & 1) ^ fp) + (i1 ^ ((i2 >> 1) | ((arr & 1) << 2)) ^ (fp << 2));
-    }
-};
-#endif
 template <> struct GFLay<5> : GFLayPad<5> {};
 template <> struct GFLay<11> : GFLayPad<11> {};
 // n = 4: the face passes give one lane per line of faces f .. f + 3 on arrays 2f (+1): swizzle by
