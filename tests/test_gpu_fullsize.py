@@ -129,3 +129,43 @@ def test_c4_full_vector_vs_o3(k):
     torch.cuda.empty_cache()
     y3 = o3.apply(*cfg.args(), zn)
     assert np.abs(yn - y3).max() <= TOL * np.abs(y3).max()
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_problem_c_full_size_sampled_vs_geometry_oracle(k):
+    """The Problem C stand-in at its full size (~4e8 DOFs: multilinear periodic mesh, q = 3p+4;
+    the bench's workload c-kK, through dg.from_config as bench.py runs it) against the geometry
+    oracle O-2g on the 3 x 3 x 3-cell sub-mesh around sampled cells: the sub-mesh's vertices are
+    the full mesh's (inputs.vertex_grid over that vertex box), its middle cell has all six
+    neighbours inside it, so O-2g's y there is the full mesh's."""
+    from oracle import o2_geometry as o2g
+    from paper_1711_10885_b200 import dg
+    cfg = configs.problem_c(k)
+    op = dg.from_config(cfg)
+    z = torch.empty(op.ndofs, dtype=torch.float64, device="cuda")
+    op.fill_uniform_local(z, cfg.seed)
+    y = torch.empty_like(z)
+    op.apply(z, y)
+    torch.cuda.synchronize()
+    N = cfg.ncells
+    n3 = cfg.n3
+    ymax = float(y.abs().max())
+    rng = np.random.default_rng(7 + k)
+    picks = [(0, 0, 0), (N[0] - 1, N[1] // 2, N[2] - 1)] + [tuple(int(v) for v in rng.integers(0, N[0], 3))
+                                                          for _ in range(3)]
+    worst = 0.0
+    for c in picks:
+        # the sub-mesh's cells (periodic wrap of the global indices) and vertex box
+        idx = [[(c[q] + d) % N[q] for d in (-1, 0, 1)] for q in range(3)]
+        cells = np.array([idx[0][a] + N[0] * (idx[1][b] + N[1] * idx[2][cc])
+                          for cc in range(3) for b in range(3) for a in range(3)])
+        box = (tuple(c[q] - 1 for q in range(3)), tuple(c[q] + 3 for q in range(3)))
+        X = inputs.vertex_grid(cfg.ncells, cfg.lo, cfg.hi, cfg.geo_amp, cfg.geo_seed, cfg.periodic, box=box)
+        zsub = inputs.uniform_cells(cells, n3, cfg.seed).reshape(-1)
+        A = o2g.assemble((3, 3, 3), X, k, cfg.D, cfg.b, cfg.c, cfg.sigma, m=cfg.m)
+        ysub = (A @ zsub).reshape(27, n3)[13]
+        mid = cells[13]
+        yg = y[mid * n3:(mid + 1) * n3].cpu().numpy()
+        worst = max(worst, float(np.abs(yg - ysub).max()))
+    op.close()
+    assert worst <= TOL * ymax, (worst, ymax)
