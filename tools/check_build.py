@@ -1,5 +1,7 @@
 """Build the bounds-checked library (-DDG_CHECK: device-side index asserts that trap) into
-checkbuild/libdg_b200.so; run the GPU tests against it with DG_LIB=$PWD/checkbuild/libdg_b200.so."""
+variants/checked/libdg_b200.so (travels with gpurun); run the GPU tests against it with
+DG_LIB=$PWD/variants/checked/libdg_b200.so."""
+import concurrent.futures as cf
 import os
 import subprocess
 import sys
@@ -10,14 +12,17 @@ from paper_1711_10885_b200 import build as B  # noqa: E402
 
 
 def main():
-    out = os.path.join(ROOT, "checkbuild")
+    out = os.path.join(ROOT, "variants", "checked")
     os.makedirs(out, exist_ok=True)
-    objs = []
-    for src, obj, extra in B._sources():
+
+    def one(job):
+        src, obj, extra = job
         o = os.path.join(out, os.path.basename(obj))
-        cmd = [B.NVCC] + B.ARCH + B.FLAGS + ["-DDG_CHECK"] + extra + ["-c", src, "-o", o]
-        subprocess.check_call(cmd)
-        objs.append(o)
+        subprocess.check_call([B.NVCC] + B.ARCH + B.FLAGS + ["-DDG_CHECK"] + extra + ["-c", src, "-o", o])
+        return o
+
+    with cf.ThreadPoolExecutor(max_workers=max(2, os.cpu_count() or 2)) as ex:
+        objs = list(ex.map(one, B._sources()))
     subprocess.check_call([B.NVCC] + B.ARCH + ["-shared", "-o", os.path.join(out, "libdg_b200.so")] + objs +
                           ["-ldl", "-lpthread"])
     print(os.path.join(out, "libdg_b200.so"))
