@@ -144,6 +144,26 @@ def test_assembled_affine_vs_o2():
     assert rel(M, Aref) < TOL
 
 
+@pytest.mark.parametrize("periodic", [(0, 0, 0), (1, 0, 1)])
+def test_assembled_multilinear_vs_o2g(periodic):
+    """The assembled operator of a multilinear mesh (NEXT-3, q = 3p + 4) is the geometry oracle's
+    matrix entry by entry (probing runs the geometry kernel)."""
+    from oracle import o2_geometry as o2g
+    from paper_1711_10885_b200 import dg, inputs
+    k, nc, lo, hi = 2, (3, 3, 2), (0.0, 0.0, 0.0), (1.5, 1.5, 1.0)
+    m = -(-(3 * k + 5) // 2)
+    D = (1.0, 0.2, 0.1, 0.2, 2.0, -0.3, 0.1, -0.3, 0.5)
+    op = dg.Operator(nc, lo, hi, k, D, (1.0, -0.5, 0.25), 0.3, 40.0, bc=dg.bc_from_periodic(periodic))
+    box = ((-1, -1, -1), (nc[0] + 2, nc[1] + 2, nc[2] + 2))
+    op.set_geometry(inputs.vertex_grid(nc, lo, hi, 0.2, 3, periodic, box=box), m)
+    A = assembled(op).cpu().numpy()
+    op.close()
+    M = dense_from_blocks(A, nc, (k + 1) ** 3, periodic)
+    Aref = o2g.assemble(nc, inputs.vertex_grid(nc, lo, hi, 0.2, 3, periodic), k, D, (1.0, -0.5, 0.25), 0.3, 40.0,
+                        m=m, periodic=periodic)
+    assert rel(M, Aref) < TOL
+
+
 @pytest.mark.parametrize("k", [1, 3, 5, 7, 10])
 @pytest.mark.parametrize("periodic", [(0, 0, 0), (1, 1, 1)])
 def test_matrix_apply_vs_o1(k, periodic):
