@@ -36,6 +36,7 @@
 #ifndef DG_B200_H
 #define DG_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -268,10 +269,33 @@ int dg_nccl_unique_id(void* out128);
    A rank's exchange blocks its thread until its neighbours reach the same exchange (120 s
    timeout -> DG_ENCCL). */
 int dg_fabric_id(void* out128);
+/* The same, but the group's applies use the DIRECT (fused) halo: each rank's trace pack kernel
+   stores the partition faces' traces straight into the neighbour's receive buffer (no send buffer,
+   no copy), ordered by events (see dg_p2p_import). Setup-time exchanges still copy. */
+int dg_fabric_id_direct(void* out128);
+
+/* ---- direct (fused) halo between PROCESSES (one per GPU): the trace pack kernel stores every
+ * partition face's traces straight into the neighbour rank's receive buffer over NVLink, through a
+ * CUDA IPC mapping of that buffer: the compute step and the transfer are one kernel, with no send
+ * buffer and no collective (SURVEY 8(e) "fused collective"). Per apply: the pack waits on the
+ * neighbours' "consumed" events of the previous apply (write-after-read), records "packed"; the
+ * shell cells wait on the neighbours' "packed" events and record "consumed"; counters in a POSIX
+ * shared-memory segment order every record before the peers' waits (no kernel waits on another).
+ * Setup-time exchanges (dg_set_diffusion) keep NCCL. Usage, after dg_setup on every rank (with an
+ * ncclUniqueId): blob = dg_p2p_blob_bytes() bytes from dg_p2p_export; all-gather the blobs in rank
+ * order; dg_p2p_import(ctx, all_blobs, shm_name) with a name common to the ranks ("/..."; rank 0
+ * creates the segment). Collective; synchronous.
+ * Errors: DG_EINVAL (not partitioned, in-process fabric, import before export or twice),
+ * DG_ECUDA (IPC handles / events), DG_ENCCL (shared memory, timeout). */
+size_t dg_p2p_blob_bytes(void);
+int dg_p2p_export(dg_ctx* ctx, void* blob);
+int dg_p2p_import(dg_ctx* ctx, const void* blobs, const char* shm_name);
 
 /* The halo transport of this context: transport 0 = none (single rank or DG_HALO_EXTERNAL only),
-   1 = NCCL, 2 = in-process fabric; nranks = the communicator's rank count as NCCL reports it
-   (ncclCommCount), else the dg_setup nranks. */
+   1 = NCCL, 2 = in-process fabric (copies), 3 = in-process fabric, direct (fused pack into the
+   peers' buffers), 4 = direct over CUDA IPC (fused pack storing over NVLink; NCCL for setup-time
+   exchanges); nranks = the communicator's rank count as NCCL reports it (ncclCommCount), else the
+   dg_setup nranks. */
 int dg_comm_info(const dg_ctx* ctx, int* transport, int* nranks);
 
 /* Library / kernel facts for the harness: kernel launches per dg_apply, threads and

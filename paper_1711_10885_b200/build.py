@@ -41,7 +41,7 @@ def _sources():
     for n, m in GEO:
         jobs.append((os.path.join(CSRC, "dg_geo_inst.cu"), os.path.join(OBJ, "dg_geo_n%d_m%d.o" % (n, m)),
                      ["-DDG_N=%d" % n, "-DDG_M=%d" % m]))
-    for name in ("dg_aux.cu", "dg_matrix.cu", "dg_abi.cpp", "dg_dispatch.cpp", "dg_nccl.cpp", "dg_fabric.cpp", "tables.cpp"):
+    for name in ("dg_aux.cu", "dg_matrix.cu", "dg_abi.cpp", "dg_dispatch.cpp", "dg_nccl.cpp", "dg_fabric.cpp", "dg_p2p.cpp", "tables.cpp"):
         base = os.path.splitext(name)[0]
         extra = ["-x", "cu"] if name.endswith(".cpp") else []
         jobs.append((os.path.join(CSRC, name), os.path.join(OBJ, base + ".o"), extra))

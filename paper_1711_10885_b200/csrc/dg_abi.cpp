@@ -15,6 +15,7 @@
 #include <nvtx3/nvToolsExt.h>   // header-only; ranges are no-ops unless a profiler (nsys) injects
 
 #include "dg_fabric.h"
+#include "dg_p2p.h"
 #include "dg_nccl.h"
 
 using namespace dg;
@@ -40,6 +41,8 @@ struct dg_ctx {
     ncclComm_t comm = nullptr;       // the halo transport: NCCL (one process per GPU) ...
     Fabric* fabric = nullptr;        // ... or the in-process fabric (ranks as threads; dg_fabric.h)
     TraceArgs targs;                 // trace pack of the partition faces (dg_aux.cu)
+    P2P* p2p = nullptr;              // direct (fused) halo: the pack stores into the peers' receive buffers
+    bool p2p_active = false;         // ... and applies use it (fabric-direct at setup, IPC after dg_p2p_import)
     double* hz = nullptr;            // device staging for dg_apply_host
     double* hy = nullptr;
     // general-coefficient path (full / per-cell D, dg_gen.cuh)
@@ -138,6 +141,7 @@ static void free_ctx(dg_ctx* c)
         if (api) api->ncclCommDestroy(c->comm);
     }
     if (c->fabric) fabric_leave(c->fabric, c->rank);
+    if (c->p2p) p2p_destroy(c->p2p);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->host_stream) cudaStreamDestroy(c->host_stream);
     if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
@@ -165,6 +169,39 @@ extern "C" int dg_fabric_id(void* out128)
 {
     if (!out128) return DG_EINVAL;
     fabric_make_id(out128);
+    return DG_OK;
+}
+
+extern "C" int dg_fabric_id_direct(void* out128)
+{
+    if (!out128) return DG_EINVAL;
+    fabric_make_id(out128);
+    static_cast<unsigned char*>(out128)[16] = 1;   // applies use the direct (fused) halo
+    return DG_OK;
+}
+
+extern "C" size_t dg_p2p_blob_bytes(void) { return p2p_blob_bytes(); }
+
+extern "C" int dg_p2p_export(dg_ctx* ctx, void* blob)
+{
+    if (!ctx || !blob || !ctx->partitioned || ctx->fabric) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    if (!ctx->p2p && p2p_ipc_create(ctx->rank, ctx->nranks, ctx->nbr, ctx->recvbuf, &ctx->p2p) != 0) {
+        ctx->p2p = nullptr;
+        return DG_ECUDA;
+    }
+    const int r = p2p_ipc_export(ctx->p2p, blob);
+    return r == 0 ? DG_OK : DG_ECUDA;
+}
+
+extern "C" int dg_p2p_import(dg_ctx* ctx, const void* blobs, const char* shm_name)
+{
+    if (!ctx || !blobs || !shm_name || !ctx->p2p || ctx->p2p_active) return DG_EINVAL;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    DG_CUDA(cudaDeviceSynchronize());                // no apply in flight across the switch
+    const int r = p2p_ipc_import(ctx->p2p, blobs, shm_name);
+    if (r != 0) return r == -2 ? DG_ECUDA : DG_ENCCL;
+    ctx->p2p_active = true;
     return DG_OK;
 }
 
@@ -424,6 +461,16 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
         }
         if (nccl_unique_id && fabric_id_is(nccl_unique_id)) {
             if (fabric_join(nccl_unique_id, rank, nranks, &ctx->fabric) != 0) { ctx->fabric = nullptr; free_ctx(ctx); return DG_ENCCL; }
+            if (static_cast<const unsigned char*>(nccl_unique_id)[16] == 1) {   // fabric-direct (dg_fabric_id_direct)
+                uint64_t key;
+                std::memcpy(&key, static_cast<const unsigned char*>(nccl_unique_id) + 8, sizeof(key));
+                if (p2p_local_join(key, rank, nranks, ctx->nbr, ctx->recvbuf, &ctx->p2p) != 0) {
+                    ctx->p2p = nullptr;
+                    free_ctx(ctx);
+                    return DG_ENCCL;
+                }
+                ctx->p2p_active = true;
+            }
         } else if (nccl_unique_id) {
             const NcclApi* api = nccl_api();
             if (!api) { free_ctx(ctx); return DG_ENCCL; }
@@ -820,14 +867,27 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         NvtxRange r_comm("trace pack + exchange (comm stream)");
         DG_CUDA(cudaEventRecord(ctx->ev_z, s));
         DG_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_z, 0));
-        int rc = exchange_prepare(ctx, ctx->comm_stream);
-        if (rc != DG_OK) return rc;
-        DG_CUDA(launch_trace_pack(z, ctx->targs, ctx->n, ctx->nloc, ctx->comm_stream));
-        size_t cnt[6];
-        for (int f = 0; f < 6; ++f) cnt[f] = (size_t)ctx->halo_count[f];
-        rc = exchange(ctx, ctx->sendbuf, ctx->recvbuf, cnt, ctx->comm_stream);
-        if (rc != DG_OK) return rc;
-        DG_CUDA(cudaEventRecord(ctx->ev_recv, ctx->comm_stream));
+        if (ctx->p2p_active) {
+            // fused: the pack kernel stores the traces straight into the neighbours' receive
+            // buffers (NVLink peer stores through the IPC mapping, or the same device's memory
+            // for ranks as threads); no send buffer, no collective (dg_p2p.h)
+            int r = p2p_before_pack(ctx->p2p, ctx->comm_stream);
+            if (r != 0) return r == -2 ? DG_ECUDA : DG_ENCCL;
+            TraceArgs a = ctx->targs;
+            for (int f = 0; f < 6; ++f) a.dst[f] = ctx->nbr[f] >= 0 ? p2p_remote(ctx->p2p, f) : nullptr;
+            DG_CUDA(launch_trace_pack(z, a, ctx->n, ctx->nloc, ctx->comm_stream));
+            r = p2p_after_pack(ctx->p2p, ctx->comm_stream);
+            if (r != 0) return r == -2 ? DG_ECUDA : DG_ENCCL;
+        } else {
+            int rc = exchange_prepare(ctx, ctx->comm_stream);
+            if (rc != DG_OK) return rc;
+            DG_CUDA(launch_trace_pack(z, ctx->targs, ctx->n, ctx->nloc, ctx->comm_stream));
+            size_t cnt[6];
+            for (int f = 0; f < 6; ++f) cnt[f] = (size_t)ctx->halo_count[f];
+            rc = exchange(ctx, ctx->sendbuf, ctx->recvbuf, cnt, ctx->comm_stream);
+            if (rc != DG_OK) return rc;
+            DG_CUDA(cudaEventRecord(ctx->ev_recv, ctx->comm_stream));
+        }
     }
     // inner cells: no remote data
     set_box(p, ctx->inner_lo, ctx->inner_cnt);
@@ -837,11 +897,23 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         DG_CUDA(launch(p));
     }
     NvtxRange r_shell("shell cells (after the receive)");
-    if (need_comm) DG_CUDA(cudaStreamWaitEvent(s, ctx->ev_recv, 0));
+    if (need_comm) {
+        if (ctx->p2p_active) {
+            const int r = p2p_before_shell(ctx->p2p, s);
+            if (r != 0) return r == -2 ? DG_ECUDA : DG_ENCCL;
+        } else {
+            DG_CUDA(cudaStreamWaitEvent(s, ctx->ev_recv, 0));
+        }
+    }
     p.task_list = ctx->shell;
     p.ntasks = ctx->nshell;
     p.ghosts = 1;
-    return cuda_rc(launch(p));
+    DG_CUDA(launch(p));
+    if (need_comm && ctx->p2p_active) {
+        const int r = p2p_after_shell(ctx->p2p, s);
+        if (r != 0) return r == -2 ? DG_ECUDA : DG_ENCCL;
+    }
+    return DG_OK;
 }
 
 extern "C" int dg_apply(dg_ctx* ctx, const double* z, double* y, void* stream)
@@ -1156,7 +1228,7 @@ extern "C" int dg_comm_info(const dg_ctx* ctx, int* transport, int* nranks)
     if (!ctx) return DG_EINVAL;
     int t = 0, n = ctx->nranks;
     if (ctx->fabric) {
-        t = 2;
+        t = ctx->p2p_active ? 3 : 2;
     } else if (ctx->comm) {
         t = 1;
         const NcclApi* api = nccl_api();
@@ -1166,6 +1238,7 @@ extern "C" int dg_comm_info(const dg_ctx* ctx, int* transport, int* nranks)
             n = c;
         }
     }
+    if (ctx->p2p_active && !ctx->fabric) t = 4;
     if (transport) *transport = t;
     if (nranks) *nranks = n;
     return DG_OK;

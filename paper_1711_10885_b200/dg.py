@@ -24,7 +24,7 @@ EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residu
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
             "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage", "dg_set_velocity", "dg_set_quadrature",
             "dg_set_affine", "dg_matrix_size", "dg_assemble", "dg_matrix_apply", "dg_fabric_id", "dg_comm_info",
-            "dg_set_geometry"]
+            "dg_set_geometry", "dg_fabric_id_direct", "dg_p2p_blob_bytes", "dg_p2p_export", "dg_p2p_import"]
 
 
 class DGError(RuntimeError):
@@ -77,6 +77,10 @@ def lib():
         L.dg_fabric_id.argtypes = [vp]
         L.dg_comm_info.argtypes = [vp, vp, vp]
         L.dg_set_geometry.argtypes = [vp, vp, ctypes.c_int, vp]
+        L.dg_fabric_id_direct.argtypes = [vp]
+        L.dg_p2p_blob_bytes.argtypes = []
+        L.dg_p2p_export.argtypes = [vp, vp]
+        L.dg_p2p_import.argtypes = [vp, vp, ctypes.c_char_p]
         L.dg_get_kernel_info.argtypes = [vp, ctypes.POINTER(KernelInfo)]
         L.dg_partition.argtypes = [ctypes.POINTER(MeshDesc), ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.dg_set_diffusion.argtypes = [vp, vp, ctypes.c_uint, vp]
@@ -91,6 +95,7 @@ def lib():
         for name in EXPORTED:
             if name != "dg_strerror":
                 getattr(L, name).restype = ctypes.c_int
+        L.dg_p2p_blob_bytes.restype = ctypes.c_size_t
         _lib = L
     return _lib
 
@@ -135,6 +140,35 @@ def fabric_id():
     buf = (ctypes.c_ubyte * 128)()
     _check(lib().dg_fabric_id(buf), "dg_fabric_id")
     return bytes(buf)
+
+
+def fabric_id_direct():
+    """Id of an in-process fabric group whose applies use the direct (fused) halo: each rank's trace
+    pack stores into the neighbours' receive buffers (dg_fabric_id_direct)."""
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib().dg_fabric_id_direct(buf), "dg_fabric_id_direct")
+    return bytes(buf)
+
+
+def p2p_attach(op, shm_name=None, group=None):
+    """Switch a partitioned NCCL operator (one process per GPU) to the direct (fused) halo over CUDA
+    IPC: export this rank's blob, all-gather the blobs through torch.distributed, import them
+    (dg_p2p_export / dg_p2p_import). Collective."""
+    import os as _os
+    import torch.distributed as dist
+    n = lib().dg_p2p_blob_bytes()
+    blob = (ctypes.c_ubyte * n)()
+    _check(lib().dg_p2p_export(op._h, blob), "dg_p2p_export")
+    world = dist.get_world_size(group)
+    if shm_name is None:
+        name = ["/dg_p2p_%d_%d" % (_os.getpid(), id(op))] if dist.get_rank(group) == 0 else [None]
+        dist.broadcast_object_list(name, src=0, group=group)
+        shm_name = name[0]
+    blobs = [None] * world
+    dist.all_gather_object(blobs, bytes(blob), group=group)
+    allb = (ctypes.c_ubyte * (n * world)).from_buffer_copy(b"".join(blobs))
+    _check(lib().dg_p2p_import(op._h, allb, shm_name.encode()), "dg_p2p_import")
+    return shm_name
 
 
 def mesh_desc(ncells, lo, hi, parts=(1, 1, 1), bc=(BC_DIRICHLET,) * 6):
@@ -335,10 +369,11 @@ class Operator:
         _check(lib().dg_halo_pack(self._h, _ptr(z), _stream(stream)), "dg_halo_pack")
 
     def comm_info(self):
-        """(transport, nranks): transport 'none' | 'nccl' | 'fabric', nranks as the communicator reports."""
+        """(transport, nranks): transport 'none' | 'nccl' | 'fabric' | 'fabric-direct' | 'p2p-ipc', nranks as
+        the communicator reports."""
         t, n = ctypes.c_int(), ctypes.c_int()
         _check(lib().dg_comm_info(self._h, ctypes.byref(t), ctypes.byref(n)), "dg_comm_info")
-        return ("none", "nccl", "fabric")[t.value], n.value
+        return ("none", "nccl", "fabric", "fabric-direct", "p2p-ipc")[t.value], n.value
 
     # -- info / lifetime ----------------------------------------------------------------------------
     def kernel_info(self):

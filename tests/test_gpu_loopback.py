@@ -180,16 +180,19 @@ def gather(cfg, ops, per_rank):
     return yg
 
 
-def run_fabric(cfg, parts, periodic=(0, 0, 0), Dcell=None, seeds=(0,), mode="apply"):
+def run_fabric(cfg, parts, periodic=(0, 0, 0), Dcell=None, seeds=(0,), mode="apply", direct=False):
     """Every rank on its own thread and stream; per seed one collective call. Returns the
-    gathered result per seed."""
+    gathered result per seed. direct: the fused halo (the pack stores into the neighbours' receive
+    buffers, dg_fabric_id_direct) instead of send buffers + copies."""
     from paper_1711_10885_b200 import dg
     world = parts[0] * parts[1] * parts[2]
-    fid = dg.fabric_id()
+    fid = dg.fabric_id_direct() if direct else dg.fabric_id()
     ops = [dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, rank=r, nranks=world,
                        parts=parts, nccl_id=fid, bc=dg.bc_from_periodic(periodic)) for r in range(world)]
     out = [None] * world
     errors = []
+    for op in ops:
+        assert op.comm_info() == ("fabric-direct" if direct else "fabric", world)
 
     def work(r):
         try:
@@ -264,12 +267,13 @@ def single_fn(cfg, periodic, Dcell, mode):
     (3, (4, 4, 4), (2, 2, 2), (1, 1, 1)), (1, (4, 6, 8), (1, 2, 4), (0, 1, 1)), (10, (2, 2, 4), (1, 1, 2), (0, 0, 1)),
     (5, (2, 2, 2), (2, 2, 2), (1, 1, 1)),          # one cell per rank: every cell is a shell cell
 ])
-def test_fabric_apply_equals_single_and_oracle(k, ncells, parts, periodic):
+@pytest.mark.parametrize("direct", [False, True])
+def test_fabric_apply_equals_single_and_oracle(k, ncells, parts, periodic, direct):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     cfg = configs.small(k, ncells=ncells, hi=(1.5, 1.0, 0.75), b=(1.0, -0.5, 0.25), c=0.3)
     seeds = (0, 1, 2)
-    yps = run_fabric(cfg, parts, periodic, seeds=seeds)
+    yps = run_fabric(cfg, parts, periodic, seeds=seeds, direct=direct)
     op, run = single_fn(cfg, periodic, None, "apply")
     for sd, yp in zip(seeds, yps):
         assert np.array_equal(yp, run(sd)), sd
@@ -279,11 +283,12 @@ def test_fabric_apply_equals_single_and_oracle(k, ncells, parts, periodic):
 
 
 @pytest.mark.parametrize("mode", ["residual", "ssp"])
-def test_fabric_epilogues(mode):
+@pytest.mark.parametrize("direct", [False, True])
+def test_fabric_epilogues(mode, direct):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     cfg = configs.small(4, ncells=(4, 4, 2), hi=(1.5, 1.0, 0.75), b=(1.0, -0.5, 0.25), c=0.3)
-    yps = run_fabric(cfg, (2, 2, 1), (1, 0, 0), seeds=(0, 1), mode=mode)
+    yps = run_fabric(cfg, (2, 2, 1), (1, 0, 0), seeds=(0, 1), mode=mode, direct=direct)
     op, run = single_fn(cfg, (1, 0, 0), None, mode)
     for sd, yp in zip((0, 1), yps):
         assert np.array_equal(yp, run(sd))
@@ -292,9 +297,10 @@ def test_fabric_epilogues(mode):
 
 @pytest.mark.parametrize("k,parts,periodic", [(2, (2, 2, 1), (1, 1, 0)), (7, (2, 1, 1), (1, 1, 1)),
                                               (3, (2, 2, 2), (0, 0, 0))])
-def test_fabric_percell_tensors(k, parts, periodic):
+@pytest.mark.parametrize("direct", [False, True])
+def test_fabric_percell_tensors(k, parts, periodic, direct):
     """dg_set_diffusion exchanges the partition layers of the tensor field through the fabric
-    (NEXT-1), then applies exchange the traces."""
+    (NEXT-1), then applies exchange the traces (copied, or stored directly by the pack)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     cfg = configs.small(k, ncells=(4, 2, 2) if k == 7 else (4, 4, 4), hi=(1.5, 1.0, 0.75), b=(1.0, -0.5, 0.25),
@@ -302,7 +308,7 @@ def test_fabric_percell_tensors(k, parts, periodic):
     rng = np.random.default_rng(k)
     M = rng.normal(size=(cfg.ncell, 3, 3))
     Dc = (np.einsum("eij,ekj->eik", M, M) + 0.5 * np.eye(3)).reshape(cfg.ncell, 9)
-    yps = run_fabric(cfg, parts, periodic, Dcell=Dc, seeds=(0, 1))
+    yps = run_fabric(cfg, parts, periodic, Dcell=Dc, seeds=(0, 1), direct=direct)
     op, run = single_fn(cfg, periodic, Dc, "apply")
     for sd, yp in zip((0, 1), yps):
         assert np.array_equal(yp, run(sd))
