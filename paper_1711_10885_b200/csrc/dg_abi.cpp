@@ -73,6 +73,8 @@ struct dg_ctx {
     // multilinear geometry (dg_set_geometry; NEXT-3): library copy of the padded vertex grid
     bool geo = false;
     double* vert = nullptr;
+    double* vtab = nullptr;          // velocity tables of the variable-velocity kernel (update_vb)
+    int vtab_m = 0;
     double* mscratch = nullptr;      // dg_matrix_apply slot-split partial sums
     int64_t mscratch_n = 0;
     KParams base;
@@ -136,6 +138,7 @@ static void free_ctx(dg_ctx* c)
     if (c->hy) cudaFree(c->hy);
     if (c->mscratch) cudaFree(c->mscratch);
     if (c->vert) cudaFree(c->vert);
+    if (c->vtab) cudaFree(c->vtab);
     if (c->comm) {
         const NcclApi* api = nccl_api();
         if (api) api->ncclCommDestroy(c->comm);
@@ -537,6 +540,27 @@ static int update_vb(dg_ctx* ctx)
         if (build_tables_m(ctx->k, ctx->m, &t) != 0) return DG_EINVAL;
         if (upload_tables_vb(ctx->k, ctx->m, t) != 0) return DG_ECUDA;
         g_vb_done[ctx->device][ctx->k][ctx->m] = true;
+    }
+    if (ctx->base.bkind != 0 && ctx->vtab_m != ctx->m) {   // the 1D velocity tables of this rank's cells
+        if (ctx->vtab) cudaFree(ctx->vtab);
+        ctx->vtab = nullptr;
+        ctx->vtab_m = 0;
+        const int64_t cnt = (ctx->nloc[0] + ctx->nloc[1] + ctx->nloc[2]) * 4 * (ctx->m + 2);
+        if (cudaMalloc(&ctx->vtab, (size_t)cnt * sizeof(double)) != cudaSuccess) { ctx->vtab = nullptr; return DG_ENOMEM; }
+        HostTables t;
+        if (build_tables_m(ctx->k, ctx->m, &t) != 0) return DG_EINVAL;
+        GeoPts g;
+        g.m = ctx->m;
+        for (int i = 0; i < ctx->m; ++i) g.xi[i] = t.xi[i];
+        KParams& p = ctx->base;
+        if (launch_vel_tables(ctx->vtab, ctx->nloc, ctx->gofs, p.lo, p.h, g, nullptr) != cudaSuccess ||
+            cudaStreamSynchronize(nullptr) != cudaSuccess)
+            return DG_ECUDA;
+        p.vtab = ctx->vtab;
+        p.vtoff[0] = 0;
+        p.vtoff[1] = ctx->nloc[0] * 4 * (ctx->m + 2);
+        p.vtoff[2] = p.vtoff[1] + ctx->nloc[1] * 4 * (ctx->m + 2);
+        ctx->vtab_m = ctx->m;
     }
     ctx->vb = true;
     return DG_OK;

@@ -87,6 +87,41 @@ cudaError_t launch_trace_pack(const double* z, const TraceArgs& a, int n, const 
     return cudaGetLastError();
 }
 
+__global__ void vel_table_kernel(double* __restrict__ out, int64_t n0, int64_t n1, int64_t n2, int64_t g0, int64_t g1,
+                                 int64_t g2, double l0, double l1, double l2, double h0, double h1, double h2, GeoPts g)
+{
+    const int M2 = g.m + 2;
+    const int64_t nl[3] = {n0, n1, n2}, go[3] = {g0, g1, g2};
+    const double lo[3] = {l0, l1, l2}, h[3] = {h0, h1, h2};
+    const int64_t total = (n0 + n1 + n2) * M2;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int d = 0;
+        int64_t r = t, off = 0;
+        while (r >= nl[d] * M2) { r -= nl[d] * M2; off += nl[d] * 4 * M2; ++d; }
+        const int64_t i = r / M2;
+        const int e = (int)(r - i * M2);
+        const double xr = (e < g.m) ? g.xi[e] : (double)(e - g.m);   // reference coordinate
+        const double x = lo[d] + ((double)(go[d] + i) + xr) * h[d];
+        double sn, cs;
+        sincos(x, &sn, &cs);
+        double* o = out + off + i * 4 * M2;
+        o[0 * M2 + e] = x;
+        o[1 * M2 + e] = sn;
+        o[2 * M2 + e] = cs;
+        o[3 * M2 + e] = 1.0;
+    }
+}
+
+cudaError_t launch_vel_tables(double* out, const int64_t nloc[3], const int64_t gofs[3], const double lo[3],
+                              const double h[3], const GeoPts& g, cudaStream_t s)
+{
+    const int64_t total = (nloc[0] + nloc[1] + nloc[2]) * (g.m + 2);
+    if (total == 0) return cudaSuccess;
+    vel_table_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(out, nloc[0], nloc[1], nloc[2], gofs[0], gofs[1],
+                                                                     gofs[2], lo[0], lo[1], lo[2], h[0], h[1], h[2], g);
+    return cudaGetLastError();
+}
+
 // Multilinear mesh check (dg_set_geometry): every local cell's Q1 map must be orientation
 // preserving at all m^3 quadrature points and its 8 corners (det J > 0); *bad != 0 otherwise.
 __global__ void geo_check_kernel(const double* __restrict__ vert, int64_t n0, int64_t n1, int64_t n2, GeoPts g,

@@ -106,7 +106,7 @@ __device__ __forceinline__ double adjugate(const double (&J)[3][3], double (&A)[
 #ifndef DG_GEO_MINB
 #define DG_GEO_MINB ((DG_M) <= 13 ? 2 : 1)   // c-k7 (m = 13): 2.8 -> 4.3 GDOF/s; m = 15 spills at 2 (c-k9 2.5 -> 2.2)
 #endif
-template <int N, int M>
+template <int N, int M, bool GH>
 __global__ void __launch_bounds__(GCfg<M>::TPC, DG_GEO_MINB)
 dg_geo_kernel(const __grid_constant__ KParams p)
 {
@@ -176,7 +176,7 @@ dg_geo_kernel(const __grid_constant__ KParams p)
         for (int q = 0; q < 3; ++q) {
             if (!((nbi >> (2 * q)) & 3u)) continue;
             double RL[1][N], RH[1][N];
-            const unsigned gm = nb_load<N, 1>(p, zc, n3, q, lc, nbi, pa, pb, act, RL, RH);
+            const unsigned gm = nb_load<N, 1, GH>(p, zc, n3, q, lc, nbi, pa, pb, act, RL, RH);
             double ul, dl, uh, dh;
             nb_traces<N>(T.th0, T.th1, T.dth0, T.dth1, RL[0], RH[0], gm, ul, dl, uh, dh);
             if ((nbi >> (2 * q)) & 1u) { F[FA::at(2 * q, 0, ya, zb)] = ul; F[FA::at(2 * q, 1, ya, zb)] = dl; }

@@ -60,13 +60,18 @@ cudaError_t DG_CAT3(launch_geo_n, DG_N, m, DG_M)(const KParams& p, cudaStream_t 
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !g_attr[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(geo::dg_geo_kernel<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(geo::dg_geo_kernel<N, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              geo::GSmem<N, M>::BYTES);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(geo::dg_geo_kernel<N, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     geo::GSmem<N, M>::BYTES);
         if (e != cudaSuccess) return e;
         g_attr[dev] = 1;
     }
     constexpr int C = geo::GCfg<M>::C;
-    geo::dg_geo_kernel<N, M><<<(unsigned)((p.ntasks + C - 1) / C), geo::GCfg<M>::TPC, geo::GSmem<N, M>::BYTES, s>>>(p);
+    const unsigned grid = (unsigned)((p.ntasks + C - 1) / C);
+    if (p.ghosts) geo::dg_geo_kernel<N, M, true><<<grid, geo::GCfg<M>::TPC, geo::GSmem<N, M>::BYTES, s>>>(p);
+    else geo::dg_geo_kernel<N, M, false><<<grid, geo::GCfg<M>::TPC, geo::GSmem<N, M>::BYTES, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -77,13 +82,13 @@ int DG_CAT3(geo_info_n, DG_N, m, DG_M)(LaunchInfo* info)
     info->threads = geo::GCfg<M>::TPC;
     info->smem = geo::GSmem<N, M>::BYTES;
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, geo::dg_geo_kernel<N, M>) != cudaSuccess) return -3;
+    if (cudaFuncGetAttributes(&fa, geo::dg_geo_kernel<N, M, false>) != cudaSuccess) return -3;
     info->regs = fa.numRegs;
-    if (cudaFuncSetAttribute(geo::dg_geo_kernel<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(geo::dg_geo_kernel<N, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              geo::GSmem<N, M>::BYTES) != cudaSuccess)
         return -3;
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, geo::dg_geo_kernel<N, M>, info->threads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, geo::dg_geo_kernel<N, M, false>, info->threads,
                                                       geo::GSmem<N, M>::BYTES) != cudaSuccess)
         return -3;
     info->ctas_per_sm = blocks;

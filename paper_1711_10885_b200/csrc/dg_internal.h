@@ -104,6 +104,9 @@ struct KParams {
     double Dp[9];
     double bp[3];
     int ghosts;               // this launch covers cells with a neighbour on another rank (the shell launch)
+    // variable-velocity kernel: the 1D velocity tables (fields at the end keep the offsets above)
+    const double* vtab;       // per direction d, local cell i: [x | sin x | cos x | 1][m + 2 points] (vel_table_kernel)
+    int64_t vtoff[3];         // offset of direction d's tables in vtab
 };
 
 struct LaunchInfo {
@@ -135,7 +138,11 @@ struct TraceArgs {              // face-trace halo of the partition faces (trace
     int64_t start[7];           // prefix sums of the work items (layer cells x n^2) per face
     double th[2][NMAX], dth[2][NMAX];   // theta_j(s), theta'_j(s), s = 0, 1
 };
-struct GeoPts { int m; double xi[MMAX]; };   // the m-point Gauss rule of dg_set_geometry's check
+struct GeoPts { int m; double xi[MMAX]; };
+// 1D velocity tables of the variable-velocity kernel: for every direction d and local cell index i,
+// x, sin x, cos x, 1 at the m Gauss coordinates and the two endpoints (x = lo + (gofs + i + xr) h)
+cudaError_t launch_vel_tables(double* out, const int64_t nloc[3], const int64_t gofs[3], const double lo[3],
+                              const double h[3], const GeoPts& g, cudaStream_t s);   // the m-point Gauss rule of dg_set_geometry's check
 cudaError_t launch_geo_check(const double* vert, const int64_t nloc[3], const GeoPts& g, int* bad, cudaStream_t s);
 cudaError_t launch_trace_pack(const double* z, const TraceArgs& a, int n, const int64_t nloc[3], cudaStream_t s);
 cudaError_t launch_pack(const double* z, double* dst, int n3, const int64_t nloc[3], int face, cudaStream_t s);

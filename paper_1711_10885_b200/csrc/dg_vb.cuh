@@ -117,7 +117,7 @@ __device__ __forceinline__ Flux vflux_boundary(const KParams& p, int q, int s, d
     return o;
 }
 
-template <int N, int M>
+template <int N, int M, bool GH>
 // minimum CTAs per SM, measured per (n, m) of the Taylor-Green runs (q = 2p + 4): (3, 5) 8
 // (TG-k2 13.3 -> 13.6 GDOF/s), (4, 6) 8 (k3 17.5 -> 18.4), (5, 7) 6 (k4 19.2 -> 19.5), (7, 9) 6
 // (k6 25.8 -> 27.3); elsewhere the compiler's choice (an explicit minimum of 1 already changed
@@ -178,18 +178,13 @@ dg_vb_kernel(const KParams p)
     const int kind = p.bkind;
 
     // ---- 1D velocity tables of this cell: x, sin x, cos x, 1 at the m Gauss coordinates and x = 0, 1
+    //      per direction, copied from the per-rank tables dg_set_velocity computed once
+    //      (vel_table_kernel in dg_aux.cu: the same sincos of the same coordinates, so the values
+    //      are those the cell would compute; no trigonometric code in this kernel)
     if (kind != 0) {
-        for (int i = lane; i < 3 * (M + 2); i += TPC) {
-            const int d = i / (M + 2), e = i - d * (M + 2);
-            const double xr = (e < M) ? T.xi[e] : (double)(e - M);   // reference coordinate
-            const double x = p.lo[d] + ((double)(p.gofs[d] + lc[d]) + xr) * p.h[d];
-            double sn, cs;
-            sincos(x, &sn, &cs);
-            double* bt = BT + d * 4 * (M + 2);
-            bt[0 * (M + 2) + e] = x;
-            bt[1 * (M + 2) + e] = sn;
-            bt[2 * (M + 2) + e] = cs;
-            bt[3 * (M + 2) + e] = 1.0;
+        for (int i = lane; i < 3 * 4 * (M + 2); i += TPC) {
+            const int d = i / (4 * (M + 2)), r = i - d * 4 * (M + 2);
+            BT[i] = __ldg(p.vtab + p.vtoff[d] + (int64_t)lc[d] * 4 * (M + 2) + r);
         }
     }
     auto btab = [&](int d, int fn, int e) { return BT[(d * 4 + fn) * (M + 2) + e]; };
@@ -207,7 +202,7 @@ dg_vb_kernel(const KParams p)
         int pa[1] = {ya}, pb[1] = {zb};
         bool act[1] = {true};
         double RL[1][N], RH[1][N];
-        const unsigned gm = nb_load<N, 1>(p, zc, n3, 0, lc, nbi, pa, pb, act, RL, RH);
+        const unsigned gm = nb_load<N, 1, GH>(p, zc, n3, 0, lc, nbi, pa, pb, act, RL, RH);
 #pragma unroll
         for (int e = 0; e < N; ++e) { rl[e] = RL[0][e]; rh[e] = RH[0][e]; }
         const bool hl = (nbi >> 0) & 1u, hh = (nbi >> 1) & 1u;
@@ -239,7 +234,7 @@ dg_vb_kernel(const KParams p)
         int pa[1] = {pa0}, pb[1] = {pb0};
         bool act[1] = {true};
         double RL[1][N], RH[1][N];
-        const unsigned gm = nb_load<N, 1>(p, zc, n3, q, lc, nbi, pa, pb, act, RL, RH);
+        const unsigned gm = nb_load<N, 1, GH>(p, zc, n3, q, lc, nbi, pa, pb, act, RL, RH);
         const bool hl = (nbi >> (2 * q)) & 1u, hh = (nbi >> (2 * q + 1)) & 1u;
         double ul, dl, uh, dh;
         nb_traces<N>(T.th0, T.th1, T.dth0, T.dth1, RL[0], RH[0], gm, ul, dl, uh, dh);

@@ -63,13 +63,18 @@ cudaError_t DG_CAT3(launch_vb_n, DG_N, m, DG_M)(const KParams& p, cudaStream_t s
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !g_attr[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(vb::dg_vb_kernel<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(vb::dg_vb_kernel<N, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              vb::VSmem<N, M>::BYTES);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(vb::dg_vb_kernel<N, M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     vb::VSmem<N, M>::BYTES);
         if (e != cudaSuccess) return e;
         g_attr[dev] = 1;
     }
     constexpr int C = vb::VCfg<M>::C;
-    vb::dg_vb_kernel<N, M><<<(unsigned)((p.ntasks + C - 1) / C), vb::VCfg<M>::TPC, vb::VSmem<N, M>::BYTES, s>>>(p);
+    const unsigned grid = (unsigned)((p.ntasks + C - 1) / C);
+    if (p.ghosts) vb::dg_vb_kernel<N, M, true><<<grid, vb::VCfg<M>::TPC, vb::VSmem<N, M>::BYTES, s>>>(p);
+    else vb::dg_vb_kernel<N, M, false><<<grid, vb::VCfg<M>::TPC, vb::VSmem<N, M>::BYTES, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -80,13 +85,13 @@ int DG_CAT3(vb_info_n, DG_N, m, DG_M)(LaunchInfo* info)
     info->threads = vb::VCfg<M>::TPC;
     info->smem = vb::VSmem<N, M>::BYTES;
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, vb::dg_vb_kernel<N, M>) != cudaSuccess) return -3;
+    if (cudaFuncGetAttributes(&fa, vb::dg_vb_kernel<N, M, false>) != cudaSuccess) return -3;
     info->regs = fa.numRegs;
-    if (cudaFuncSetAttribute(vb::dg_vb_kernel<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(vb::dg_vb_kernel<N, M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              vb::VSmem<N, M>::BYTES) != cudaSuccess)
         return -3;
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, vb::dg_vb_kernel<N, M>, info->threads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, vb::dg_vb_kernel<N, M, false>, info->threads,
                                                       vb::VSmem<N, M>::BYTES) != cudaSuccess)
         return -3;
     info->ctas_per_sm = blocks;
