@@ -313,8 +313,11 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
 
 // minimum CTAs per SM: n = 2 at 5 with constant D (96 registers: C4-k1 83.3 -> 84.7 GDOF/s) and
 // at 4 with tensors (128 registers, a few spills instead of 150: Problem A k = 1 47.2 -> 50.9)
+#ifndef DG_RMINB3
+#define DG_RMINB3 1
+#endif
 #ifndef DG_RMINB
-#define DG_RMINB(n, gen) ((n) == 2 ? ((gen) ? 4 : 5) : 1)
+#define DG_RMINB(n, gen) ((n) == 2 ? ((gen) ? 4 : 5) : DG_RMINB3)
 #endif
 template <int N, bool GEN, bool GH = false>
 __global__ void __launch_bounds__(128, DG_RMINB(N, GEN)) dg_reg_kernel(const __grid_constant__ KParams p)
