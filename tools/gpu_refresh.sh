@@ -10,6 +10,8 @@ python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/pla
 ncu --set full --clock-control none --import-source on -k regex:dg_cell_kernel -s 3 -c 1 -o gpurun_out/c3_full python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_c3.log 2>&1; echo "ncu C3 rc=$?"
 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain_c3l.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+python bench.py --workload c5weak --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain_c5w.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:dg_cell_kernel -s 3 -c 1 -o gpurun_out/c5w_full python bench.py --workload c5weak --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_c5w.log 2>&1; echo "ncu C5 weak rc=$?"
 for w in a-k7 c-k7 tg-k5; do
   python tools/quick_time.py $w 2 > gpurun_out/plain_$w.log 2>&1 &&
   ncu --set full --clock-control none --import-source on -k regex:"dg_(gen|geo|vb)_kernel" -s 2 -c 1 -o gpurun_out/${w}_full python tools/quick_time.py $w 2 > gpurun_out/ncu_$w.log 2>&1; echo "ncu $w rc=$?"
@@ -21,6 +23,7 @@ for w in c5weak c5strong a-k7 c-k7 tg-k5; do
 done
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "reference rc=$?"
 # sweeps
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 python tools/sweep.py --out gpurun_out/sweep.json > gpurun_out/sweep.log 2>&1; echo "sweep rc=$?"
 for k in 1 2 3 4 5 6 7 8 9 10; do echo "a-k$k $(python tools/quick_time.py a-k$k 5 | tail -1)"; done > gpurun_out/problemA.log
 for k in 1 2 3 4 5 6 7 8 9 10; do echo "tg-k$k $(python tools/quick_time.py tg-k$k 3 | tail -1)"; done > gpurun_out/tg.log
