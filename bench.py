@@ -463,6 +463,10 @@ def run_ours(args, rank, world, local_rank):
     peak = perfmodel.fp64_peak_tflops(smax)
     meas = fp64_measured()
     ncu, ncu_src = load_ncu(cfg, kname)
+    try:
+        hbm_peak = float(measured_peaks().get("hbm_gbs"))      # MEASURED_PEAKS.json copy bandwidth
+    except (TypeError, ValueError):
+        hbm_peak = None
     exec_per_dof = ncu.get("executed_flops_per_dof")
     traffic = ncu.get("dram_bytes_per_launch")
     achieved = exec_per_dof * op.ndofs / kern_t / 1e12 if exec_per_dof else None
@@ -485,6 +489,7 @@ def run_ours(args, rank, world, local_rank):
                            "exceed 1" % (cfg.k, per_dof),
             "traffic_algorithmic_bytes": 16.0 * op.ndofs,
             "hbm_gbs_at_traffic": (traffic / kern_t / 1e9) if traffic else None,
+            "hbm_frac_of_measured_copy": (traffic / kern_t / 1e9 / hbm_peak) if (traffic and hbm_peak) else None,
             "ncu_fp64_pipe_pct": ncu.get("fp64_pipe_pct"), "ncu_smem_wavefront_pct": ncu.get("smem_wavefront_pct"),
             "ncu_issue_active_pct": ncu.get("issue_active_pct"),
             "ncu_source": ncu_src,
