@@ -219,9 +219,9 @@ __device__ __forceinline__ int at(const double* S, int L, int e)
 // (into XL, XH) and wait for them; returns whether both x-neighbours are TMA-staged (a ghost
 // neighbour on another rank is read by per-thread loads instead). One cell per CTA.
 __device__ __forceinline__ bool stage_x(const KParams& p, double* STG, double* XL, double* XH, int tid,
-                                       const int (&lc)[3], int64_t cell, unsigned nbi)
+                                       const int (&lc)[3], int64_t cell, unsigned nbi, uint64_t* mbar = nullptr)
 {
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(STG + 512);
+    if (!mbar) mbar = reinterpret_cast<uint64_t*>(STG + 512);   // (default: right after the staging block)
     const int nq = (int)p.nloc[0];
     const bool hl = (nbi & 1u) != 0, hh = (nbi & 2u) != 0;
     const bool ll = hl && (lc[0] > 0 || p.wrap[0]), lh = hh && (lc[0] + 1 < nq || p.wrap[0]);

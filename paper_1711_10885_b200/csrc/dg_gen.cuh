@@ -167,10 +167,15 @@ template <int N> struct GCfg {
                          C = DG_GOVR(DG_GC, GCfgD<N>::C);
 };
 
+// Per cell: three volume arrays (A0, X0, X1) and two face slots (NT, OT). d_z u is not stored:
+// the pointwise step forms it on the thread's own z-pencil and applies the z role's Dc^T there
+// (a fourth array cost 4 KB per cell at n = 8: 6 -> 8 CTAs per SM without it). n = 8 stages its
+// TMA loads in OT (own block), X1 and A0 (x-neighbours), all free in phase 1, and its store in
+// X0; only the mbarrier (16 B) is extra.
 template <int N>
 struct GSmem {
-    static constexpr int PER_CELL = 4 * Lay<N>::SLOT + 2 * GFLay<N>::SLOT;
-    static constexpr int STAGE = (N == 8) ? 512 + 16 + 16 : 0;   // TMA staging of the own block (n = 8)
+    static constexpr int PER_CELL = 3 * Lay<N>::SLOT + 2 * GFLay<N>::SLOT;
+    static constexpr int STAGE = (N == 8) ? 2 : 0;
     static constexpr int BYTES = GCfg<N>::C * PER_CELL * 8 + STAGE * 8;
 };
 
@@ -193,8 +198,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     double* A0 = smem + slot * GSmem<N>::PER_CELL;   // u, then the quadrature-space accumulator
     double* X0 = A0 + Lay<N>::SLOT;                  // d_x u -> x^(1)   (also a stage temporary)
     double* X1 = X0 + Lay<N>::SLOT;                  // d_y u -> x^(2)
-    double* X2 = X1 + Lay<N>::SLOT;                  // d_z u -> x^(3)
-    double* NT = X2 + Lay<N>::SLOT;                  // neighbour face arrays (2 per face)
+    double* NT = X1 + Lay<N>::SLOT;                  // neighbour face arrays (2 per face)
     double* OT = NT + GFLay<N>::SLOT;                 // own face arrays (2 per face)
     auto csync = [&]() {
         if (32 % TPC == 0) __syncwarp(); else __syncthreads();   // a cell within one warp, else CTA-wide
@@ -261,14 +265,16 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     }
 
     double r[P][N], t[P][N];
-    // TMA staging (n = 8): own block (STG) and the local x-neighbours' blocks (X1, X2: free in P1)
+    // TMA staging (n = 8): own block (STG = OT) and the local x-neighbours' blocks (X1, A0), all
+    // free in P1; the mbarrier after the cell's arrays
     double* STG = nullptr;
+    double* XH = A0;
     bool tma_x = false;
     if constexpr (N == 8 && C == 1) {
         if (p.tma) {
-            STG = reinterpret_cast<double*>(
-                (reinterpret_cast<uintptr_t>(smem + GSmem<N>::PER_CELL) + 127) & ~(uintptr_t)127);
-            tma_x = tma::stage_x(p, STG, X1, X2, tid, lc, cell, nbi);
+            STG = OT;
+            tma_x = tma::stage_x(p, STG, X1, XH, tid, lc, cell, nbi,
+                                 reinterpret_cast<uint64_t*>(smem + GSmem<N>::PER_CELL));
         }
     }
     // ---------------------------------------------------------------- P1-P3: u at the Gauss points
@@ -281,7 +287,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 const int L = pa[k] + N * pb[k];
 #pragma unroll
                 for (int e = 0; e < N; e += 2) {
-                    const double2 a = tma::line2(STG, L, e), lo = tma::line2(X1, L, e), hi = tma::line2(X2, L, e);
+                    const double2 a = tma::line2(STG, L, e), lo = tma::line2(X1, L, e), hi = tma::line2(XH, L, e);
                     r[k][e] = a.x; r[k][e + 1] = a.y;
                     rl[k][e] = lo.x; rl[k][e + 1] = lo.y;
                     rh[k][e] = hi.x; rh[k][e + 1] = hi.y;
@@ -337,16 +343,11 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     }
     v_fwd_sd<N, P>(T.Vs[2], r, t);                               // t = u on this thread's z-pencils
     {
-        double g[P][N], z0[P][(N / 2) > 0 ? N / 2 : 1], zm[P];
-        c_apply_s<N, P, false>(T.Dcs[0], t, g, z0, z0, zm);
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (act[k]) {
 #pragma unroll
-                for (int e = 0; e < N; ++e) {
-                    A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
-                    X2[Lay<N>::at(pa[k], pb[k], e)] = g[k][e];
-                }
+                for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = t[k][e];
                 // own z-face traces: u and the reference normal derivative at z = 0, 1
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
@@ -456,27 +457,49 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         }
     }
     {
-        // x^(r) = W (sum_s D_rs/(h_r h_s) d_s u - b_r/h_r u), accumulator A0 = W c u   (eq:gauss_points)
+        // x^(r) = W (sum_s D_rs/(h_r h_s) d_s u - b_r/h_r u)   (eq:gauss_points) on the thread's
+        // z-pencils; d_z u = Dc u along the pencil here; the z role's Dc^T x^(3) is applied in
+        // registers and A0 = W c u + Dc_z^T x^(3) (the x, y roles and the z lifts add later)
         double Dh[3][3];
 #pragma unroll
         for (int rr = 0; rr < 3; ++rr)
 #pragma unroll
             for (int ss = 0; ss < 3; ++ss) Dh[rr][ss] = Dw[dsym(rr, ss)] * (p.hinv[rr] * p.hinv[ss]);
+        double u[P][N], g[P][N];
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int e = 0; e < N; ++e) u[k][e] = act[k] ? A0[Lay<N>::at(pa[k], pb[k], e)] : 0.0;
+        {
+            double z0[P][(N / 2) > 0 ? N / 2 : 1], zm[P];
+            c_apply_s<N, P, false>(T.Dcs[0], u, g, z0, z0, zm);   // d_z u
+        }
+        double cu[P][(N / 2) > 0 ? N / 2 : 1], cl[P][(N / 2) > 0 ? N / 2 : 1], cm[P];
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-            if (!act[k]) continue;
             const double wab = do_vol ? p.dT * T.w[pa[k]] * T.w[pb[k]] : 0.0;
 #pragma unroll
             for (int e = 0; e < N; ++e) {
                 const int ix = Lay<N>::at(pa[k], pb[k], e);
                 const double W = wab * T.w[e];
-                const double u = A0[ix], g0 = X0[ix], g1 = X1[ix], g2 = X2[ix];
-                X0[ix] = W * (Dh[0][0] * g0 + Dh[0][1] * g1 + Dh[0][2] * g2 - p.kb[0] * u);
-                X1[ix] = W * (Dh[1][0] * g0 + Dh[1][1] * g1 + Dh[1][2] * g2 - p.kb[1] * u);
-                X2[ix] = W * (Dh[2][0] * g0 + Dh[2][1] * g1 + Dh[2][2] * g2 - p.kb[2] * u);
-                A0[ix] = W * p.c * u;
+                const double uu = u[k][e], g0 = act[k] ? X0[ix] : 0.0, g1 = act[k] ? X1[ix] : 0.0, g2 = g[k][e];
+                if (act[k]) {
+                    X0[ix] = W * (Dh[0][0] * g0 + Dh[0][1] * g1 + Dh[0][2] * g2 - p.kb[0] * uu);
+                    X1[ix] = W * (Dh[1][0] * g0 + Dh[1][1] * g1 + Dh[1][2] * g2 - p.kb[1] * uu);
+                }
+                g[k][e] = W * (Dh[2][0] * g0 + Dh[2][1] * g1 + Dh[2][2] * g2 - p.kb[2] * uu);   // x^(3)
+                const double wcu = W * p.c * uu;
+                if (e < N / 2) cu[k][e] = wcu;                  // added to output e (< n/2)
+                else if (2 * e + 1 == N) cm[k] = wcu;           // the middle (odd n)
+                else cl[k][N - 1 - e] = wcu;                    // output e = n-1-i
             }
         }
+        c_apply_s<N, P, true>(T.DcTs[4], g, u, cu, cl, cm);      // u <- W c u + Dc_z^T x^(3)
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (act[k])
+#pragma unroll
+                for (int e = 0; e < N; ++e) A0[Lay<N>::at(pa[k], pb[k], e)] = u[k][e];
     }
     csync();
 
@@ -560,19 +583,25 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     csync();
 
     // ---------------------------------------------------------------- P8-P10: roles, A0 += Dc_q^T x^(q) + lifts
+    // (the z role's Dc^T x^(3) is already in A0: that role adds the z-face lifts only)
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        double* X = q == 0 ? X0 : (q == 1 ? X1 : X2);
+        double* X = q == 0 ? X0 : X1;
         auto at = [&](int k, int e) {
             return q == 0 ? Lay<N>::at(e, pa[k], pb[k]) : (q == 1 ? Lay<N>::at(pa[k], e, pb[k]) : Lay<N>::at(pa[k], pb[k], e));
         };
+        if (q < 2) {
 #pragma unroll
-        for (int k = 0; k < P; ++k)
+            for (int k = 0; k < P; ++k)
 #pragma unroll
-            for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X[at(k, e)] : 0.0;
-        {
+                for (int e = 0; e < N; ++e) r[k][e] = act[k] ? X[at(k, e)] : 0.0;
             double z0[P][(N / 2) > 0 ? N / 2 : 1], zm[P];
             c_apply_s<N, P, false>(T.DcTs[2 + q], r, t, z0, z0, zm);
+        } else {
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+#pragma unroll
+                for (int e = 0; e < N; ++e) t[k][e] = act[k] ? A0[at(k, e)] : 0.0;
         }
 #pragma unroll
         for (int k = 0; k < P; ++k) {
@@ -594,11 +623,6 @@ dg_gen_kernel(const __grid_constant__ KParams p)
 #pragma unroll
                     for (int e = 0; e < N; ++e) A0[at(k, e)] += t[k][e];
             csync();
-        } else {
-#pragma unroll
-            for (int k = 0; k < P; ++k)
-#pragma unroll
-                for (int e = 0; e < N; ++e) t[k][e] += act[k] ? A0[at(k, e)] : 0.0;
         }
     }
     // ---------------------------------------------------------------- P10-P12: V^T along z, y, x; store
@@ -626,14 +650,14 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         for (int e = 0; e < N; ++e) r[k][e] = act[k] ? A0[Lay<N>::at(e, pa[k], pb[k])] : 0.0;
     v_bwd_sd<N, P>(T.Vh[11], r, t);
     if constexpr (N == 8 && C == 1) {
-        if (STG && p.tma == 2 && p.epi == 0) {   // y through the staging block and one TMA store
+        if (STG && p.tma == 2 && p.epi == 0) {   // y through a staging block (X0, free) and one TMA store
 #pragma unroll
             for (int k = 0; k < P; ++k) {
                 const int L = pa[k] + N * pb[k];
 #pragma unroll
-                for (int e = 0; e < N; e += 2) tma::put2(STG, L, e, t[k][e], t[k][e + 1]);
+                for (int e = 0; e < N; e += 2) tma::put2(X0, L, e, t[k][e], t[k][e + 1]);
             }
-            tma::store_block(p, STG, tid, cell);
+            tma::store_block(p, X0, tid, cell);
             return;
         }
     }
