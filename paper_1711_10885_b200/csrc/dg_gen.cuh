@@ -181,7 +181,7 @@ struct GSmem {
 
 template <int N, bool GH>
 #ifndef DG_GMB
-#define DG_GMB ((DG_N) == 4 ? 12 : (DG_N) == 10 ? 5 : 1)   // min CTAs per SM (n = 4: A-k3 30.5 -> 31.0; n = 10: A-k9 29.7 -> 31.0)
+#define DG_GMB ((DG_N) == 4 ? 12 : (DG_N) == 8 ? 8 : (DG_N) == 10 ? 5 : 1)   // min CTAs per SM (n = 4: A-k3 30.5 -> 31.0; n = 8: the 8 CTAs its shared memory allows; n = 10: A-k9 29.7 -> 31.0)
 #endif
 __global__ void __launch_bounds__(GCfg<N>::C * GCfg<N>::TPC, DG_GMB)
 dg_gen_kernel(const __grid_constant__ KParams p)
@@ -529,29 +529,31 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         const double rsum = dsum == 0.0 ? 0.0 : 1.0 / dsum;
         const double wm = dsum == 0.0 ? 0.5 : dp * rsum, wp = dsum == 0.0 ? 0.5 : dm * rsum;   // C-5
         const double gam = (interior ? 2.0 * dm * dp * rsum : dme) * p.sigq[q];
-        const double wself = sd ? wm : wp;
         const double bq = p.bq[q];
+        // The face terms as one branch-free expression in the own (o) and neighbour (n) traces,
+        // with per-line scalars (sg = +-1: the own side is T- for sd = 1):
+        //   interior: J = u- - u+ = sg (uo - un), {nu.D grad u}_w = ws so + wn sn,
+        //             upwind Phi = bq u_up, cv = sg Wf (Phi - {.}_w + gam J),
+        //             coef = -Wf w_self J;
+        //   boundary (weak Dirichlet, outward normal sg): cv = Wf (Phi - sg so + gam uo) with
+        //             Phi = max(sg bq, 0) uo, coef = -Wf sg uo  (un = sn = 0, ws = 1, wn = 0).
+        const double sg = sd ? 1.0 : -1.0;
+        const bool own_up = interior ? ((bq >= 0.0) == (sd != 0)) : (sg * bq >= 0.0);
+        const double ws = interior ? (sd ? wm : wp) : 1.0, wn = interior ? (sd ? wp : wm) : 0.0;
+        // com = cv / (sg Wf) = ko uo + kn un - (ws so + wn sn)   (sg^2 = 1 folds the boundary case)
+        const double ko = (own_up ? bq : 0.0) + sg * gam;
+        const double kn = interior ? ((own_up ? 0.0 : bq) - sg * gam) : 0.0;
+        const double cw = ws;                                // coef = -Wf sg cw (uo - un)
+        const double Wl = p.dF[q] * T.w[line] * sg;
         double c2[N];
 #pragma unroll
         for (int e = 0; e < N; ++e) {
-            const double Wf = p.dF[q] * T.w[line] * T.w[e];        // face point (i1 = line, i2 = e)
-            double coef;
-            if (interior) {
-                const double un = NT[GFLay<N>::at(2 * f, line, e)], sn = NT[GFLay<N>::at(2 * f + 1, line, e)];
-                const double um = sd ? uo[e] : un, up = sd ? un : uo[e];
-                const double sm = sd ? so[e] : sn, sp = sd ? sn : so[e];
-                const double Phi = (bq >= 0.0) ? bq * um : bq * up;   // upwind flux
-                const double J = um - up;
-                const double com = Phi - (wm * sm + wp * sp) + gam * J;
-                cv[e] = sd ? Wf * com : -Wf * com;
-                coef = -Wf * wself * J;                                // coefficient of e_q.D grad(phi)
-            } else {
-                const double nu = sd ? 1.0 : -1.0;                     // outward normal
-                const double bn = nu * bq;
-                const double Phi = (bn >= 0.0) ? bn * uo[e] : 0.0;
-                cv[e] = Wf * (Phi - nu * so[e] + gam * uo[e]);
-                coef = -Wf * uo[e] * nu;
-            }
+            const double Wf = Wl * T.w[e];                         // face point (i1 = line, i2 = e), times sg
+            const double un = interior ? NT[GFLay<N>::at(2 * f, line, e)] : 0.0;
+            const double sn = interior ? NT[GFLay<N>::at(2 * f + 1, line, e)] : 0.0;
+            const double com = fma(ko, uo[e], fma(kn, un, -fma(ws, so[e], wn * sn)));
+            cv[e] = Wf * com;
+            const double coef = -Wf * cw * (uo[e] - un);       // coefficient of e_q.D grad(phi)
             OT[GFLay<N>::at(2 * f + 1, line, e)] = coef * cn;         // normal part (lifted with L')
             NT[GFLay<N>::at(2 * f, line, e)] = coef * c1;             // t1 part (Dc^T along i1 in P7)
             c2[e] = coef * cq2;                                      // t2 part (Dc^T along i2 below)
