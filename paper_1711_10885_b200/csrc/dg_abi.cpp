@@ -792,7 +792,11 @@ extern "C" int dg_local_layout(const dg_ctx* ctx, int64_t cell_lo[3], int64_t ce
 static void set_tma(dg_ctx* ctx, KParams& p, const double* z, double* y)
 {
     p.tma = 0;
-    if (ctx->k != 7 || ctx->vb || ctx->geo || ctx->no_tma) return;
+    if (ctx->vb || ctx->geo || ctx->no_tma) return;
+    if (ctx->k != 7) {   // other degrees: bulk copies of whole cell blocks (dg_cell.cuh, namespace bulk)
+        p.tma = 2;
+        return;
+    }
     const int64_t rows = ctx->nloc[0] * ctx->nloc[1] * ctx->nloc[2] * 64;
     if (z != ctx->tma_z) {
         ctx->tma_z_ok = make_row_map(&ctx->tmz, z, rows);

@@ -169,7 +169,9 @@ struct Smem {
     static constexpr int PER_CELL = 2 * Lay<N>::SLOT + FLay<N>::SLOT;
     // n = 8: TMA staging of the own block (4 KB, 128-byte aligned) plus the mbarrier; the two
     // x-neighbour blocks are staged in A1 and face slots 4..11, free during phase 1
-    static constexpr int STAGE = (N == 8) ? 512 + 16 + 16 : 0;
+    // n = 7, 9, 10, 11: the own block is staged by a bulk copy in A1 (free in phase 1) and y
+    // leaves from A1 by a bulk copy (namespace bulk); only the mbarrier is extra
+    static constexpr int STAGE = (N == 8) ? 512 + 16 + 16 : (N >= 7 ? 2 : 0);
     static constexpr int BYTES = Cfg<N>::C * PER_CELL * 8 + STAGE * 8;
 };
 
@@ -242,6 +244,11 @@ __device__ __forceinline__ bool stage_x(const KParams& p, double* STG, double* X
     wait(mbar, 0);
     return tma_x;
 }
+__device__ __forceinline__ void mbar_init_n(uint64_t* b, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
 // x-line L (elements e, e+1) of a staged block
 __device__ __forceinline__ double2 line2(const double* S, int L, int e)
 {
@@ -259,6 +266,48 @@ __device__ __forceinline__ void store_block(const KParams& p, const double* S, i
     if (tid == 0) store_rows(&p.tmy, (int)(cell * 64), S);
 }
 }  // namespace tma
+
+// ---------------------------------------------------------------------------------- bulk copies (n != 8)
+// A cell block (n^3 doubles, x-lines of n) moves between HBM and a LINEAR shared-memory image by
+// one non-tensor bulk copy (cp.async.bulk, 16-byte granules): the image S is placed so that
+// S == the block start (mod 16 bytes); the 16-byte-aligned interior is copied, a leading and / or
+// trailing odd double (a block start 8 mod 16, an odd remainder) goes by plain loads / stores.
+// Each thread reads / writes its x-lines at N L + e of the image: bank-conflict free (odd n: N L
+// mod 16 is a bijection on 16 lanes; even n: 16-byte accesses, N L / 2 mod 8 a bijection on 8).
+// It replaces the per-thread line loads (a lane's n doubles at an n-double lane stride, n sectors
+// per warp instruction) and the per-thread stores that held the CTA until they drained.
+namespace bulk {
+struct Span {
+    int sh;          // image offset in doubles (0, 1): S = base + sh
+    int hd, tl;      // leading / trailing plain doubles
+    uint32_t bytes;  // bulk-copied bytes
+};
+template <int N>
+__device__ __forceinline__ Span span(const double* g, const double* base)
+{
+    constexpr int n3 = N * N * N;
+    Span o;
+    const uint32_t gp = (uint32_t)(reinterpret_cast<uintptr_t>(g) >> 3) & 1u;
+    o.sh = (int)((gp ^ (tma::saddr(base) >> 3)) & 1u);
+    o.hd = (int)gp;
+    o.tl = (n3 - o.hd) & 1;
+    o.bytes = (uint32_t)(n3 - o.hd - o.tl) * 8u;
+    return o;
+}
+__device__ __forceinline__ void load(double* s, const double* g, uint32_t bytes, uint64_t* mbar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(tma::saddr(s)), "l"(reinterpret_cast<uint64_t>(g)), "r"(bytes), "r"(tma::saddr(mbar))
+                 : "memory");
+}
+__device__ __forceinline__ void store(double* g, const double* s, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                 ::"l"(reinterpret_cast<uint64_t>(g)), "r"(tma::saddr(s)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+}  // namespace bulk
 
 // ---------------------------------------------------------------------------------- 1D stages
 // t[k][i] = sum_j V_ij r[k][j]  (even-odd: V_{n-1-i,j} = (-1)^j V_ij)
@@ -860,6 +909,26 @@ dg_cell_kernel(const __grid_constant__ KParams p)
             tma_x = tma::stage_x(p, STG, A1, NT + 4 * 64, tid, lc, cell, nbi);
         }
     }
+    // bulk staging of the own block (n = 7, 9, 10, 11) in A1, free in phase 1 (C4 k = 6 / 8 / 9 / 10:
+    // 58.6 -> 60.0, 51.9 -> 54.5, 51.6 -> 53.7, 50.3 -> 53.4 GDOF/s; n = 6 measured 62.8 -> 60.9: off)
+    constexpr bool BULK = (N >= 7 && N != 8);
+    static_assert(!BULK || Lay<N>::SLOT >= NN * N + 1, "A1 holds the shifted block image");
+    double* SB = nullptr;
+    bulk::Span bs{};
+    if constexpr (BULK) {
+        if (p.tma) {
+            uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + C * Smem<N>::PER_CELL);
+            bs = bulk::span<N>(zc, A1);
+            SB = A1 + bs.sh;
+            if (tid == 0) tma::mbar_init_n(mbar, C);
+            __syncthreads();
+            if (lane == 0) {
+                tma::expect_tx(mbar, bs.bytes);
+                bulk::load(SB + bs.hd, zc + bs.hd, bs.bytes, mbar);
+            }
+            tma::wait(mbar, 0);
+        }
+    }
     {
         double rl[P][N], rh[P][N];
         unsigned gm0 = 0;   // ghost x-neighbours (never TMA-staged)
@@ -892,6 +961,21 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 }
                 continue;
             }
+            if (BULK && SB) {
+                const double* src = SB + N * (pa[k] + N * pb[k]);
+                if (N % 2 == 0) {
+#pragma unroll
+                    for (int e = 0; e < N; e += 2) {
+                        const double2 v = act[k] ? *reinterpret_cast<const double2*>(src + e) : make_double2(0.0, 0.0);
+                        r[k][e] = v.x;
+                        r[k][e + 1] = v.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < N; ++e) r[k][e] = act[k] ? src[e] : 0.0;
+                }
+                continue;
+            }
             const double* src = zc + N * (pa[k] + N * pb[k]);
             if (N % 2 == 0) {
 #pragma unroll
@@ -904,6 +988,10 @@ dg_cell_kernel(const __grid_constant__ KParams p)
 #pragma unroll
                 for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
             }
+        }
+        if (BULK && SB) {   // the plain leading / trailing doubles of the block
+            if (bs.hd && lane == 0) r[0][0] = __ldg(zc);
+            if (bs.tl && lane == (NN - 1) % TPC) r[(NN - 1) / TPC][N - 1] = __ldg(zc + NN * N - 1);
         }
         }
         v_fwd_sd<N, P>(T.Vs[0], r, t);
@@ -1028,6 +1116,33 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 for (int e = 0; e < N; e += 2) tma::put2(STG, L, e, t[k][e], t[k][e + 1]);
             }
             tma::store_block(p, STG, tid, cell);
+            return;
+        }
+    }
+    if constexpr (BULK) {
+        if (p.tma == 2 && p.epi == 0) {   // y through the linear image in A1 (free) and one bulk store
+            double* yc = p.y + cell * n3;
+            const bulk::Span ys = bulk::span<N>(yc, A1);
+            double* S = A1 + ys.sh;
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                if (!act[k]) continue;
+                double* dst = S + N * (pa[k] + N * pb[k]);
+                if (N % 2 == 0) {
+#pragma unroll
+                    for (int e = 0; e < N; e += 2) *reinterpret_cast<double2*>(dst + e) = make_double2(t[k][e], t[k][e + 1]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < N; ++e) dst[e] = t[k][e];
+                }
+            }
+            if (valid) {
+                if (ys.hd && lane == 0) __stcs(yc, t[0][0]);
+                if (ys.tl && lane == (NN - 1) % TPC) __stcs(yc + NN * N - 1, t[(NN - 1) / TPC][N - 1]);
+            }
+            tma::fence_async();
+            __syncthreads();
+            if (valid && lane == 0) bulk::store(yc + ys.hd, S + ys.hd, ys.bytes);
             return;
         }
     }

@@ -96,7 +96,7 @@ struct KParams {
     double lo[3];             // physical coordinates of the global box's low corner
     // TMA staging of the x-direction cell blocks (n = 8 fast kernel): z and y viewed as
     // [cells * 64 rows][8 doubles] with the 64-byte swizzle
-    int tma;                  // 1: tmz (loads) valid; 2: tmy (store) valid too
+    int tma;                  // n = 8: 1 tmz (loads) valid, 2 tmy (store) valid too; other n: 2 = bulk copies
     CUtensorMap tmz, tmy;
     // multilinear-geometry kernel (NEXT-3, dg_geo.cuh): the padded vertex grid of this rank's box
     // ((nloc+3)^3 x 3 doubles, local vertex -1 .. nloc+1) and the physical D, b
