@@ -175,7 +175,7 @@ template <int N> struct GCfg {
 template <int N>
 struct GSmem {
     static constexpr int PER_CELL = 3 * Lay<N>::SLOT + 2 * GFLay<N>::SLOT;
-    static constexpr int STAGE = (N == 8) ? 2 : 0;
+    static constexpr int STAGE = (N >= 7) ? 2 : 0;   // the mbarrier (n = 8: TMA; n = 7, 9, 11: bulk copies)
     static constexpr int BYTES = GCfg<N>::C * PER_CELL * 8 + STAGE * 8;
 };
 
@@ -277,6 +277,27 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                                  reinterpret_cast<uint64_t*>(smem + GSmem<N>::PER_CELL));
         }
     }
+    // n = 7, 9, 11: the own block by one bulk copy into a linear image in OT (free in P1), y out of
+    // X0 by one bulk copy (dg_cell.cuh, namespace bulk): A-k6 / k8 / k10 29.8 -> 30.7, 33.5 -> 35.0,
+    // 30.6 -> 34.1 GDOF/s; n = 10 measured 34.9 -> 33.7: off
+    constexpr bool BULK = (N == 7 || N == 9 || N == 11) && C == 1;
+    static_assert(!BULK || (GFLay<N>::SLOT >= NN * N + 1 && Lay<N>::SLOT >= NN * N + 1), "block images");
+    double* SB = nullptr;
+    bulk::Span bs{};
+    if constexpr (BULK) {
+        if (p.tma) {
+            uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + GSmem<N>::PER_CELL);
+            bs = bulk::span<N>(zc, OT);
+            SB = OT + bs.sh;
+            if (tid == 0) tma::mbar_init_n(mbar, 1);
+            __syncthreads();
+            if (tid == 0) {
+                tma::expect_tx(mbar, bs.bytes);
+                bulk::load(SB + bs.hd, zc + bs.hd, bs.bytes, mbar);
+            }
+            tma::wait(mbar, 0);
+        }
+    }
     // ---------------------------------------------------------------- P1-P3: u at the Gauss points
     {
         double rl[P][N], rh[P][N];
@@ -306,9 +327,28 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                     }
                     continue;
                 }
+                if (BULK && SB) {
+                    const double* src = SB + N * (pa[k] + N * pb[k]);
+                    if (N % 2 == 0) {
+#pragma unroll
+                        for (int e = 0; e < N; e += 2) {
+                            const double2 v = act[k] ? *reinterpret_cast<const double2*>(src + e) : make_double2(0.0, 0.0);
+                            r[k][e] = v.x;
+                            r[k][e + 1] = v.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < N; ++e) r[k][e] = act[k] ? src[e] : 0.0;
+                    }
+                    continue;
+                }
                 const double* src = zc + N * (pa[k] + N * pb[k]);
 #pragma unroll
                 for (int e = 0; e < N; ++e) r[k][e] = act[k] ? __ldg(src + e) : 0.0;
+            }
+            if (BULK && SB) {   // the plain leading / trailing doubles of the block
+                if (bs.hd && lane == 0) r[0][0] = __ldg(zc);
+                if (bs.tl && lane == (NN - 1) % TPC) r[(NN - 1) / TPC][N - 1] = __ldg(zc + NN * N - 1);
             }
         }
         v_fwd_sd<N, P>(T.Vs[0], r, t);
@@ -660,6 +700,33 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 for (int e = 0; e < N; e += 2) tma::put2(X0, L, e, t[k][e], t[k][e + 1]);
             }
             tma::store_block(p, X0, tid, cell);
+            return;
+        }
+    }
+    if constexpr (BULK) {
+        if (p.tma == 2 && p.epi == 0) {   // y through a linear image in X0 (free) and one bulk store
+            double* yc = p.y + cell * n3;
+            const bulk::Span ys = bulk::span<N>(yc, X0);
+            double* S = X0 + ys.sh;
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                if (!act[k]) continue;
+                double* dst = S + N * (pa[k] + N * pb[k]);
+                if (N % 2 == 0) {
+#pragma unroll
+                    for (int e = 0; e < N; e += 2) *reinterpret_cast<double2*>(dst + e) = make_double2(t[k][e], t[k][e + 1]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < N; ++e) dst[e] = t[k][e];
+                }
+            }
+            if (valid) {
+                if (ys.hd && lane == 0) __stcs(yc, t[0][0]);
+                if (ys.tl && lane == (NN - 1) % TPC) __stcs(yc + NN * N - 1, t[(NN - 1) / TPC][N - 1]);
+            }
+            tma::fence_async();
+            __syncthreads();
+            if (valid && tid == 0) bulk::store(yc + ys.hd, S + ys.hd, ys.bytes);
             return;
         }
     }
