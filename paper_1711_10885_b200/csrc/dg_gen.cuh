@@ -283,19 +283,45 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     constexpr bool BULK = (N == 7 || N == 9 || N == 11) && C == 1;
     static_assert(!BULK || (GFLay<N>::SLOT >= NN * N + 1 && Lay<N>::SLOT >= NN * N + 1), "block images");
     double* SB = nullptr;
-    bulk::Span bs{};
+    double *SL = nullptr, *SH = nullptr;   // the local x-neighbours' images (X1, A0: free in P1)
+    bulk::Span bs{}, bl{}, bh{};
+    bool bulk_x = false;
     if constexpr (BULK) {
         if (p.tma) {
             uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + GSmem<N>::PER_CELL);
+            const int nq = (int)p.nloc[0];
+            const bool hl = (nbi & 1u) != 0, hh = (nbi & 2u) != 0;
+            const bool ll = hl && (lc[0] > 0 || p.wrap[0]), lh = hh && (lc[0] + 1 < nq || p.wrap[0]);
+            // x-neighbours staged too (n = 11 only: A-k10 34.1 -> 35.6 GDOF/s; n = 7, 9 -0.5 / -0.9 %)
+            // when every x-neighbour is on this rank (ghosts: per-thread loads)
+            bulk_x = N == 11 && (ll || !hl) && (lh || !hh);
+            const double* zlo = p.z + ((lc[0] > 0) ? cell - 1 : cell + (nq - 1)) * n3;
+            const double* zhi = p.z + ((lc[0] + 1 < nq) ? cell + 1 : cell - (nq - 1)) * n3;
             bs = bulk::span<N>(zc, OT);
             SB = OT + bs.sh;
+            if (bulk_x) {
+                bl = bulk::span<N>(zlo, X1);
+                bh = bulk::span<N>(zhi, A0);
+                SL = X1 + bl.sh;
+                SH = A0 + bh.sh;
+            }
             if (tid == 0) tma::mbar_init_n(mbar, 1);
             __syncthreads();
             if (tid == 0) {
-                tma::expect_tx(mbar, bs.bytes);
+                const bool xl = bulk_x && hl, xh = bulk_x && hh;
+                tma::expect_tx(mbar, bs.bytes + (xl ? bl.bytes : 0u) + (xh ? bh.bytes : 0u));
                 bulk::load(SB + bs.hd, zc + bs.hd, bs.bytes, mbar);
+                if (xl) bulk::load(SL + bl.hd, zlo + bl.hd, bl.bytes, mbar);
+                if (xh) bulk::load(SH + bh.hd, zhi + bh.hd, bh.bytes, mbar);
             }
             tma::wait(mbar, 0);
+            if (bulk_x) {   // the plain leading / trailing doubles of the neighbour images
+                if (bl.hd && tid == 0) SL[0] = __ldg(zlo);
+                if (bh.hd && tid == 0) SH[0] = __ldg(zhi);
+                if (bl.tl && tid == 0) SL[n3 - 1] = __ldg(zlo + n3 - 1);
+                if (bh.tl && tid == 0) SH[n3 - 1] = __ldg(zhi + n3 - 1);
+                if ((bl.hd | bh.hd | bl.tl | bh.tl) && hl | hh) __syncthreads();
+            }
         }
     }
     // ---------------------------------------------------------------- P1-P3: u at the Gauss points
@@ -315,7 +341,29 @@ dg_gen_kernel(const __grid_constant__ KParams p)
                 }
             }
         } else {
-            gm = nb_load<N, P, GH>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
+            if (bulk_x) {
+#pragma unroll
+                for (int k = 0; k < P; ++k) {
+                    const int o = N * (pa[k] + N * pb[k]);
+                    if (N % 2 == 0) {
+#pragma unroll
+                        for (int e = 0; e < N; e += 2) {
+                            const double2 lo = *reinterpret_cast<const double2*>(SL + o + e);
+                            const double2 hi = *reinterpret_cast<const double2*>(SH + o + e);
+                            rl[k][e] = lo.x; rl[k][e + 1] = lo.y;
+                            rh[k][e] = hi.x; rh[k][e + 1] = hi.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < N; ++e) {
+                            rl[k][e] = SL[o + e];
+                            rh[k][e] = SH[o + e];
+                        }
+                    }
+                }
+            } else {
+                gm = nb_load<N, P, GH>(p, zc, n3, 0, lc, nbi, pa, pb, act, rl, rh);
+            }
 #pragma unroll
             for (int k = 0; k < P; ++k) {
                 if (STG) {
