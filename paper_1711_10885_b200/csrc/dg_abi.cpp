@@ -792,8 +792,8 @@ extern "C" int dg_local_layout(const dg_ctx* ctx, int64_t cell_lo[3], int64_t ce
 static void set_tma(dg_ctx* ctx, KParams& p, const double* z, double* y)
 {
     p.tma = 0;
-    if (ctx->vb || ctx->geo || ctx->no_tma) return;
-    if (ctx->k != 7) {   // other degrees: bulk copies of whole cell blocks (dg_cell.cuh, namespace bulk)
+    if (ctx->geo || ctx->no_tma) return;
+    if (ctx->k != 7 || ctx->vb) {   // bulk copies of whole cell blocks (dg_cell.cuh, namespace bulk)
         p.tma = 2;
         return;
     }

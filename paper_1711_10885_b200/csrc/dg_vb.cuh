@@ -67,10 +67,16 @@ template <int M> struct VFL {                               // 12 face arrays of
 };
 template <> struct VFL<8> : FLay<8> {};
 template <> struct VFL<4> : FLay<4> {};
+#ifndef DG_VB_BULK_NMIN
+#define DG_VB_BULK_NMIN 6   // TG k = 5..10 +2.4 / 4.3 / 5.6 / 3.6 / 5.6 / 0.9 %; n = 5 (k = 4) -2.3 %: off
+#endif
 template <int N, int M> struct VSmem {
     static constexpr int BT = 3 * 4 * (M + 2);               // 1D velocity tables: [dir][fn][point]
     static constexpr int PER_CELL = 2 * VLay<N, M>::SLOT + VFL<M>::SLOT + BT;
-    static constexpr int BYTES = VCfg<M>::C * PER_CELL * 8;
+    // bulk copies of the own block in (image in B) and of y out (image in A), dg_cell.cuh namespace
+    // bulk, where an array holds the shifted n^3 image; + the mbarrier
+    static constexpr bool BULK = N >= DG_VB_BULK_NMIN && VLay<N, M>::SLOT >= N * N * N + 1;
+    static constexpr int BYTES = VCfg<M>::C * PER_CELL * 8 + (BULK ? 16 : 0);
 };
 
 // separable velocity field: function id per (kind, component r, direction d) and sign per (kind, r)
@@ -189,13 +195,47 @@ dg_vb_kernel(const KParams p)
     }
     auto btab = [&](int d, int fn, int e) { return BT[(d * 4 + fn) * (M + 2) + e]; };
 
+    constexpr bool BULK = VSmem<N, M>::BULK;
+    double* SB = nullptr;
+    bulk::Span bs{};
+    if constexpr (BULK) {
+        if (p.tma) {
+            uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + CC * VSmem<N, M>::PER_CELL);
+            bs = bulk::span<N>(zc, B);
+            SB = B + bs.sh;
+            if (threadIdx.x == 0) tma::mbar_init_n(mbar, CC);
+            __syncthreads();
+            if (lane == 0) {
+                tma::expect_tx(mbar, bs.bytes);
+                bulk::load(SB + bs.hd, zc + bs.hd, bs.bytes, mbar);
+            }
+            tma::wait(mbar, 0);
+        }
+    }
     double rl[N], rh[N];
     // ---- phase 1: modal x-lines (y, z < n): V along x -> A(x < m, y, z); x-neighbours (normal first)
     if (lane < NN) {
         const int ya = lane % N, zb = lane / N;
         double r[N], t[M];
+        if (BULK && SB) {
+            const double* src = SB + N * (ya + N * zb);
+            if (N % 2 == 0) {
 #pragma unroll
-        for (int e = 0; e < N; ++e) r[e] = __ldg(zc + N * (ya + N * zb) + e);
+                for (int e = 0; e < N; e += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(src + e);
+                    r[e] = v.x;
+                    r[e + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < N; ++e) r[e] = src[e];
+            }
+            if (bs.hd && lane == 0) r[0] = __ldg(zc);
+            if (bs.tl && lane == NN - 1) r[N - 1] = __ldg(zc + NN * N - 1);
+        } else {
+#pragma unroll
+            for (int e = 0; e < N; ++e) r[e] = __ldg(zc + N * (ya + N * zb) + e);
+        }
         vr_fwd<N, M>(T.Vh[0], r, t);
 #pragma unroll
         for (int e = 0; e < M; ++e) A[LY::at(e, ya, zb)] = t[e];
@@ -380,6 +420,34 @@ dg_vb_kernel(const KParams p)
     }
     __syncthreads();
     // phase 8: V^T along x on modal pencils (y, z < n); the single store of y (+ epilogue)
+    if constexpr (BULK) {
+        if (p.tma == 2 && p.epi == 0) {   // through a linear image in A (free) and one bulk store
+            double* yc = p.y + cell * n3;
+            const bulk::Span ys = bulk::span<N>(yc, A);
+            double* S = A + ys.sh;
+            if (lane < NN) {
+                const int ya = lane % N, zb = lane / N;
+                double t[M], r[N];
+#pragma unroll
+                for (int e = 0; e < M; ++e) t[e] = B[LY::at(e, ya, zb)];
+                vr_bwd<N, M>(T.Vh[5], t, r);
+                double* dst = S + N * (ya + N * zb);
+                if (N % 2 == 0) {
+#pragma unroll
+                    for (int e = 0; e < N; e += 2) *reinterpret_cast<double2*>(dst + e) = make_double2(r[e], r[e + 1]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < N; ++e) dst[e] = r[e];
+                }
+                if (valid && ys.hd && lane == 0) __stcs(yc, r[0]);
+                if (valid && ys.tl && lane == NN - 1) __stcs(yc + NN * N - 1, r[N - 1]);
+            }
+            tma::fence_async();
+            __syncthreads();
+            if (valid && lane == 0) bulk::store(yc + ys.hd, S + ys.hd, ys.bytes);
+            return;
+        }
+    }
     if (lane < NN && valid) {
         const int ya = lane % N, zb = lane / N;
         double t[M], r[N];
