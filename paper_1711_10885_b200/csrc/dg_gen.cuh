@@ -134,6 +134,18 @@ template <int N, int ARR, int CR> struct GFLayRot {
 };
 template <> struct GFLay<7> : GFLayRot<7, 49, 6> {};
 template <> struct GFLay<5> : GFLayPad<5> {};
+// n = 8: a half-warp of the face passes (tk = lane: face f = tk / 8, line = tk % 8) covers the lines
+// of two faces f, f + 1 (arrays 2f + c, 2f + 2 + c). Within an array the low three bits of the word
+// index are i1 ^ i2 (a Latin square: a bijection along i1 and along i2) and bit 3 is i2 & 1, so one
+// face's 8 lines along i1 or along i2, and 16 points (a, b) with b in {2h, 2h + 1}, take 8 (16)
+// distinct banks; the array stride 68 = 4 mod 8 moves face f + 1 to the complementary 8 banks.
+// Conflict free for every face-array access of this kernel (FLay<8> left 27 % of the shared-memory
+// wavefronts as conflicts here, ncu A-k7), and cheaper index arithmetic than FLay<8>'s swizzle.
+template <> struct GFLay<8> {
+    static constexpr int ARR = 68;
+    static constexpr int SLOT = 12 * ARR;
+    __device__ __forceinline__ static int at(int arr, int i1, int i2) { return ARR * arr + 8 * i2 + (i1 ^ i2); }
+};
 template <> struct GFLay<11> : GFLayPad<11> {};
 // n = 4: the face passes give one lane per line of faces f .. f + 3 on arrays 2f (+1): swizzle by
 // the face index (arr >> 1) instead of the array index, so those 4 arrays take 4 different
