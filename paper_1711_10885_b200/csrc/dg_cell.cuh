@@ -154,15 +154,35 @@ template <> struct FLay<4> {
         return 16 * arr + (i1 ^ s) + 4 * (i2 ^ s);
     }
 };
-// n = 8: 64 doubles per array, XOR swizzle conflict free for the three access patterns
-// (point (a, b) per lane; lines along i1 and along i2 over 4 consecutive arrays per warp).
-template <> struct FLay<8> {
+// n = 8 (round 1; kept for the variable-velocity kernel): 64 doubles per array, XOR swizzle.
+struct FLaySwz8 {
     static constexpr int SLOT = 12 * 64;
     __device__ __forceinline__ static int at(int arr, int i1, int i2)
     {
         return 64 * arr + 8 * (i2 ^ (arr & 1)) + (i1 ^ ((i2 >> 1) | ((arr & 1) << 2)));
     }
 };
+// n = 8: the low three bits of the word index are i1 ^ i2 (a Latin square: a bijection along i1 and
+// along i2), bit 3 is i2 & 1, and the array stride 72 = 8 mod 16 puts arrays a and a + 1 on
+// complementary banks: conflict free for points (a, b) per lane and for the tangential stages'
+// lines along i1 or i2 of two consecutive arrays per half-warp, with less index arithmetic than
+// the XOR swizzle (DG_FLAY_SWZ=1 restores it).
+#ifndef DG_FLAY_SWZ
+#define DG_FLAY_SWZ 0
+#endif
+#if DG_FLAY_SWZ
+template <> struct FLay<8> : FLaySwz8 {};
+#else
+template <> struct FLay<8> {
+    static constexpr int ARR = 72;
+    static constexpr int SLOT = 12 * ARR;
+    __device__ __forceinline__ static int at(int arr, int i1, int i2) { return ARR * arr + 8 * i2 + (i1 ^ i2); }
+};
+#endif
+// n = 8: the high x-neighbour block is TMA-staged in the face slots 4.. (free in phase 1) at a
+// 512-byte aligned offset past arrays 0..3 (written in phase 1)
+constexpr int XH8 = DG_FLAY_SWZ ? 256 : 320;
+static_assert(XH8 >= 4 * (FLay<8>::SLOT / 12) && XH8 + 512 <= FLay<8>::SLOT, "x-neighbour staging inside face slots 4..11");
 
 template <int N>
 struct Smem {
@@ -906,7 +926,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
         if (p.tma) {
             STG = reinterpret_cast<double*>(
                 (reinterpret_cast<uintptr_t>(smem + Smem<N>::PER_CELL) + 127) & ~(uintptr_t)127);
-            tma_x = tma::stage_x(p, STG, A1, NT + 4 * 64, tid, lc, cell, nbi);
+            tma_x = tma::stage_x(p, STG, A1, NT + XH8, tid, lc, cell, nbi);
         }
     }
     // bulk staging of the own block (n = 7, 9, 10, 11) in A1, free in phase 1 (C4 k = 6 / 8 / 9 / 10:
@@ -942,7 +962,7 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 for (int e = 0; e < N; e += 2) {
                     const double2 a = tma::line2(STG, L, e);
                     const double2 lo = tma::line2(A1, L, e);
-                    const double2 hi = tma::line2(NT + 4 * 64, L, e);
+                    const double2 hi = tma::line2(NT + XH8, L, e);
                     r[k][e] = a.x; r[k][e + 1] = a.y;
                     rl[k][e] = lo.x; rl[k][e + 1] = lo.y;
                     rh[k][e] = hi.x; rh[k][e + 1] = hi.y;

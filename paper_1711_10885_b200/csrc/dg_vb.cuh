@@ -65,7 +65,7 @@ template <int M> struct VFL {                               // 12 face arrays of
     static constexpr int SLOT = 12 * FS;
     __device__ __forceinline__ static int at(int arr, int i1, int i2) { return arr * FS + i1 + M * i2; }
 };
-template <> struct VFL<8> : FLay<8> {};
+template <> struct VFL<8> : FLaySwz8 {};
 template <> struct VFL<4> : FLay<4> {};
 #ifndef DG_VB_BULK_NMIN
 #define DG_VB_BULK_NMIN 6   // TG k = 5..10 +2.4 / 4.3 / 5.6 / 3.6 / 5.6 / 0.9 %; n = 5 (k = 4) -2.3 %: off
