@@ -1,7 +1,8 @@
 # Refresh of the committed evidence on one B200 (run under gpurun): GPU suite, bench lines,
 # launch list, ncu --set full captures of the operator kernels, degree / workload sweeps.
 # Every ncu command follows a plain run of the same command that exited 0 (B200_PROFILING.md).
-# Summarise here afterwards: python tools/ncu_summary.py gpurun_out/<rep> --name <cfg> --ndofs <n> --json profiles/ncu_full_summary.json
+# The captures are summarised on the box (tools/ncu_summary.py) before the bench lines run; copy
+# gpurun_out/ncu_full_summary.json to profiles/ afterwards.
 export PYTHONPATH=$PWD
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
@@ -16,6 +17,11 @@ for w in a-k7 c-k7 tg-k5; do
   python tools/quick_time.py $w 2 > gpurun_out/plain_$w.log 2>&1 &&
   ncu --set full --clock-control none --import-source on -k regex:"dg_(gen|geo|vb)_kernel" -s 2 -c 1 -o gpurun_out/${w}_full python tools/quick_time.py $w 2 > gpurun_out/ncu_$w.log 2>&1; echo "ncu $w rc=$?"
 done
+# summaries of the captures (this build's kernel hashes), so the bench lines below carry the roofline
+for a in "c3_full C3 268435456" "c5w_full C5-weak-P1 536870912" "a-k7_full A-k7 398688256" "c-k7_full C-k7 398688256" "tg-k5_full TG-k5 401947272"; do
+  set -- $a; [ -f gpurun_out/$1.ncu-rep ] && python tools/ncu_summary.py gpurun_out/$1.ncu-rep --name $2 --ndofs $3 --json profiles/ncu_full_summary.json > /dev/null
+done
+cp profiles/ncu_full_summary.json gpurun_out/ncu_full_summary.json
 # bench lines
 python bench.py --steps 20 --warmup 5 --submesh-check > gpurun_out/bench_c3.log 2>&1; echo "bench C3 rc=$?"; tail -1 gpurun_out/bench_c3.log | cut -c1-200
 for w in c5weak c5strong a-k7 c-k7 tg-k5; do
