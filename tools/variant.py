@@ -31,8 +31,9 @@ def main():
         sys.exit("compile failed:\n" + r.stderr[-2000:])
     lines = r.stderr.splitlines()
     for i, l in enumerate(lines):
-        if "dg_cell_kernel" in l and "Compiling" in l:
-            print(name, " | ".join(x.strip() for x in lines[i + 1:i + 4] if "Used" in x or "spill" in x))
+        if "Compiling" in l and ("_kernel" in l):
+            kn = l.split("'")[1] if "'" in l else l
+            print(name, kn[:48], " | ".join(x.strip()[-70:] for x in lines[i + 1:i + 4] if "Used" in x or "spill" in x))
     objs = [os.path.join(B.OBJ, f) for f in sorted(os.listdir(B.OBJ)) if f.endswith(".o") and f != replaced]
     out = os.path.join(ROOT, "variants", name + ".so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
