@@ -347,19 +347,32 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     from paper_1711_10885_b200 import dg
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # --share-gpu (development / CI on a one-GPU box): all ranks on the visible GPUs round-robin,
+    # torch.distributed over gloo, no NCCL communicator (ncclCommInitRank refuses two ranks on one
+    # device), the direct IPC halo; every cross-rank dependency is a stream wait on a recorded event,
+    # no kernel waits on another rank (B200_PROFILING.md). Exercises the whole N-rank path; its
+    # timing is N ranks time-sharing one GPU, not a scaling number.
+    shared = bool(args.share_gpu) and world > 1
+    gpu = local_rank % max(1, torch.cuda.device_count()) if shared else local_rank
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if shared else dev   # device of the reduction tensors (gloo: host)
     cfg = workload(args.workload, world)
+    if shared and args.halo != "p2p":
+        raise SystemExit("--share-gpu runs the direct IPC halo only (no NCCL communicator)")
     nccl_id = None
-    if world > 1:
+    if world > 1 and not shared:
         idt = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             idt.copy_(torch.tensor(list(dg.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().tolist())
-    op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, device=local_rank, rank=rank,
+    op = dg.Operator(cfg.ncells, cfg.lo, cfg.hi, cfg.k, cfg.D, cfg.b, cfg.c, cfg.sigma, device=gpu, rank=rank,
                      nranks=world, parts=cfg.parts, nccl_id=nccl_id, bc=dg.bc_from_periodic(cfg.periodic))
     if cfg.dfield_seed >= 0:
         op.set_tensor_field(cfg.dfield_seed)
@@ -383,7 +396,12 @@ def run_ours(args, rank, world, local_rank):
         try:
             dg.p2p_attach(op)
         except Exception as e:  # noqa: BLE001 -- reported in the JSON line, NCCL carries on
+            if shared:
+                raise
             halo_note = "direct halo unavailable (%s): NCCL send/recv" % e
+        if shared:
+            halo_note = ("--share-gpu: %d ranks time-share %d GPU(s); the timing is not a scaling number"
+                         % (world, torch.cuda.device_count()))
     info = op.kernel_info()
     transport, comm_ranks = op.comm_info()
     if world > 1 and rank == 0:
@@ -402,7 +420,7 @@ def run_ours(args, rank, world, local_rank):
         op.apply(z, y)
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(gpu)
     clocks.start()
     time.sleep(0.2)
     # ---- timed region: K steps, device time by CUDA events on the launching stream
@@ -447,7 +465,7 @@ def run_ours(args, rank, world, local_rank):
     t = t_local
     tk = tk_local
     if world > 1:
-        tt = torch.tensor([t_local, tk_local], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_local, tk_local], dtype=torch.float64, device=red_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t, tk = float(tt[0]), float(tt[1])
     total_dofs = cfg.ndofs   # whole job (all ranks)
@@ -509,7 +527,7 @@ def run_ours(args, rank, world, local_rank):
             op.apply_host(zh, yh)
         te = time.perf_counter() - t0
         if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            tt = torch.tensor([te], dtype=torch.float64, device=red_dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt[0])
         e2e = {"value": total_dofs * ke / te, "unit": UNIT, "h2d_bytes_per_step": op.ndofs * 8 * world,
@@ -537,7 +555,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1 or args.submesh_check:
         nchk, worst, bitw = submesh_parity(cfg, op, y, rank, dev)
         if nchk:
-            tt = torch.tensor([worst, 0.0 if bitw else 1.0, float(nchk)], dtype=torch.float64, device=dev)
+            tt = torch.tensor([worst, 0.0 if bitw else 1.0, float(nchk)], dtype=torch.float64, device=red_dev)
             if world > 1:
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             sub = {"vs": "single-rank GPU operator on the 3x3x3-cell sub-box around sampled cells (one next to "
@@ -562,6 +580,7 @@ def run_ours(args, rank, world, local_rank):
                            "median": float(np.median(step_ms)) if step_ms else None},
                "gpu_launches": args.steps * info["launches_per_apply"],
                "kernel_info": info,
+               "shared_gpu": shared or None,
                "comm": {"transport": transport, "nranks": comm_ranks, "note": halo_note,
                         "halo": "face traces, 2 n^2 doubles per partition-face cell (%d B per cell at k=%d)"
                                 % (16 * (cfg.k + 1) ** 2, cfg.k) if world > 1 else None}}
@@ -609,6 +628,9 @@ def main():
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1: the fused halo (the trace pack stores into the neighbours' buffers over "
                          "NVLink through CUDA IPC; default) or NCCL send/recv from send buffers")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="development: N ranks on the visible GPU(s) (gloo + the IPC halo, no NCCL), to "
+                         "exercise the N-rank path on a one-GPU box; not a scaling measurement")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return spawn_ranks(args.gpus)
