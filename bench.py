@@ -451,6 +451,19 @@ def run_ours(args, rank, world, local_rank):
     else:
         tk_local = t_local
     clk = clocks.stop()
+    # overlap evidence: one armed apply's launch timeline per rank (dg_timeline)
+    timeline = None
+    if world > 1:
+        op.timeline_arm()
+        op.apply(z, y)
+        tl = op.timeline()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, tl)
+        timeline = {"ms_since_apply_start": gathered,
+                    "pack_hidden_in_inner": [g["pack_end"] <= g["inner_end"] for g in gathered],
+                    "what": "one apply after the timed region: the trace pack (+ exchange) on the comm stream "
+                            "against the inner-box kernel on the compute stream, and the shell kernel after "
+                            "the received traces (CUDA events, dg_timeline)"}
     # per-step distribution (separate, after the timed region): median / min of single applies
     step_ms = []
     if world == 1:
@@ -584,6 +597,8 @@ def run_ours(args, rank, world, local_rank):
                "comm": {"transport": transport, "nranks": comm_ranks, "note": halo_note,
                         "halo": "face traces, 2 n^2 doubles per partition-face cell (%d B per cell at k=%d)"
                                 % (16 * (cfg.k + 1) ** 2, cfg.k) if world > 1 else None}}
+        if timeline is not None:
+            out["overlap_timeline"] = timeline
         if world > 1:   # the exchange's cost = t(apply) - t(apply with the halo exchange skipped)
             out["halo_ablation"] = {"ms_per_apply": t / args.steps * 1e3,
                                     "ms_per_apply_no_exchange": tk / args.steps * 1e3,

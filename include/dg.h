@@ -298,6 +298,16 @@ int dg_p2p_import(dg_ctx* ctx, const void* blobs, const char* shm_name);
    dg_setup nranks. */
 int dg_comm_info(const dg_ctx* ctx, int* transport, int* nranks);
 
+/* Overlap evidence for the partitioned apply (the face-trace exchange concurrent with
+   the inner-box cells). arm = 1: the next dg_apply / dg_residual of this
+   (partitioned) context records timing events around its launches. arm = 0: waits for that apply
+   and writes n >= 6 times in ms, relative to the apply's start on the caller's stream:
+   ms[0] / ms[1] the trace pack (+ exchange) begin / end on the comm stream (begin before the waits
+   on the neighbours' buffers), ms[2] / ms[3] the inner-box kernel begin / end, ms[4] the shell
+   kernel's start (after its wait for the received traces), ms[5] its end. DG_EUNSUPPORTED for a
+   single-rank context, DG_EINVAL when no armed apply has run or n < 6. */
+int dg_timeline(dg_ctx* ctx, int arm, double* ms, int n);
+
 /* Library / kernel facts for the harness: kernel launches per dg_apply, threads and
    cells per CTA, dynamic shared memory per CTA, registers per thread, of the kernel the
    next apply launches (the general-coefficient kernel after dg_set_diffusion / full D). */

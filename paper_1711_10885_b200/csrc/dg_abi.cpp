@@ -38,6 +38,9 @@ struct dg_ctx {
     cudaStream_t comm_stream = nullptr, host_stream = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t ev_slab[2] = {nullptr, nullptr}, ev_done = nullptr;   // dg_apply_host pipeline
     cudaEvent_t ev_z = nullptr, ev_recv = nullptr;   // z ready on the caller's stream; halo received
+    // dg_timeline: timing events around the launches of the next partitioned apply (armed once)
+    bool tl_armed = false, tl_done = false;
+    cudaEvent_t tl_ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     ncclComm_t comm = nullptr;       // the halo transport: NCCL (one process per GPU) ...
     Fabric* fabric = nullptr;        // ... or the in-process fabric (ranks as threads; dg_fabric.h)
     TraceArgs targs;                 // trace pack of the partition faces (dg_aux.cu)
@@ -152,6 +155,8 @@ static void free_ctx(dg_ctx* c)
     for (int i = 0; i < 2; ++i)
         if (c->ev_slab[i]) cudaEventDestroy(c->ev_slab[i]);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
+    for (cudaEvent_t e : c->tl_ev)
+        if (e) cudaEventDestroy(e);
     if (c->ev_z) cudaEventDestroy(c->ev_z);
     if (c->ev_recv) cudaEventDestroy(c->ev_recv);
     delete c;
@@ -441,7 +446,12 @@ extern "C" int dg_setup(dg_ctx** out, const dg_mesh_desc* mesh, int k, const dou
             if (cudaMemcpy(ctx->shell, shell.data(), shell.size() * sizeof(int64_t), cudaMemcpyHostToDevice) !=
                 cudaSuccess) { free_ctx(ctx); return DG_ECUDA; }
         }
-        if (cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        // the comm stream at the highest priority: the trace pack's few CTAs are dispatched ahead of
+        // the inner-box kernel's pending CTAs (launched right after it on the caller's stream), so
+        // the pack and the transfer run under the inner kernel instead of after its last wave
+        int prio_lo = 0, prio_hi = 0;
+        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+        if (cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->ev_z, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->ev_recv, cudaEventDisableTiming) != cudaSuccess) {
             free_ctx(ctx);
@@ -886,6 +896,12 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         return cuda_rc(launch_any(ctx, p, s));
     }
     NvtxRange r_apply("dg_apply (partitioned)");
+    // dg_timeline (armed): 0 start on s, 1 / 2 pack (+ exchange) begin / end on the comm stream,
+    // 3 / 4 inner kernel begin / end, 5 shell launch (after its wait), 6 shell end, on s
+    const bool tl = ctx->tl_armed;
+    ctx->tl_armed = false;
+    auto mark = [&](int i, cudaStream_t st) { return tl ? cudaEventRecord(ctx->tl_ev[i], st) : cudaSuccess; };
+    DG_CUDA(mark(0, s));
     // (iv) of SURVEY.md 3 / 8(e): the partition faces' traces are packed and exchanged on the comm
     // stream while the inner-box cells (no remote data) run on s; the shell cells follow the
     // receive. The pack is off s: it is launched first, so its few CTAs start ahead of the
@@ -896,6 +912,7 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
         DG_CUDA(cudaEventRecord(ctx->ev_z, s));
         DG_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_z, 0));
         if (ctx->p2p_active) {
+            DG_CUDA(mark(1, ctx->comm_stream));   // (before the waits on the neighbours' consumed events)
             // fused: the pack kernel stores the traces straight into the neighbours' receive
             // buffers (NVLink peer stores through the IPC mapping, or the same device's memory
             // for ranks as threads); no send buffer, no collective (dg_p2p.h)
@@ -904,9 +921,11 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
             TraceArgs a = ctx->targs;
             for (int f = 0; f < 6; ++f) a.dst[f] = ctx->nbr[f] >= 0 ? p2p_remote(ctx->p2p, f) : nullptr;
             DG_CUDA(launch_trace_pack(z, a, ctx->n, ctx->nloc, ctx->comm_stream));
+            DG_CUDA(mark(2, ctx->comm_stream));
             r = p2p_after_pack(ctx->p2p, ctx->comm_stream);
             if (r != 0) return r == -2 ? DG_ECUDA : DG_ENCCL;
         } else {
+            DG_CUDA(mark(1, ctx->comm_stream));
             int rc = exchange_prepare(ctx, ctx->comm_stream);
             if (rc != DG_OK) return rc;
             DG_CUDA(launch_trace_pack(z, ctx->targs, ctx->n, ctx->nloc, ctx->comm_stream));
@@ -914,15 +933,21 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
             for (int f = 0; f < 6; ++f) cnt[f] = (size_t)ctx->halo_count[f];
             rc = exchange(ctx, ctx->sendbuf, ctx->recvbuf, cnt, ctx->comm_stream);
             if (rc != DG_OK) return rc;
+            DG_CUDA(mark(2, ctx->comm_stream));
             DG_CUDA(cudaEventRecord(ctx->ev_recv, ctx->comm_stream));
         }
+    } else if (tl) {
+        DG_CUDA(mark(1, s));
+        DG_CUDA(mark(2, s));
     }
     // inner cells: no remote data
     set_box(p, ctx->inner_lo, ctx->inner_cnt);
     auto launch = [&](const KParams& kp) { return launch_any(ctx, kp, s); };
     {
         NvtxRange r_inner("inner-box cells");
+        DG_CUDA(mark(3, s));
         DG_CUDA(launch(p));
+        DG_CUDA(mark(4, s));
     }
     NvtxRange r_shell("shell cells (after the receive)");
     if (need_comm) {
@@ -936,10 +961,35 @@ static int apply_impl(dg_ctx* ctx, const double* z, const double* f, double* y, 
     p.task_list = ctx->shell;
     p.ntasks = ctx->nshell;
     p.ghosts = 1;
+    DG_CUDA(mark(5, s));
     DG_CUDA(launch(p));
+    DG_CUDA(mark(6, s));
+    if (tl) ctx->tl_done = true;
     if (need_comm && ctx->p2p_active) {
         const int r = p2p_after_shell(ctx->p2p, s);
         if (r != 0) return r == -2 ? DG_ECUDA : DG_ENCCL;
+    }
+    return DG_OK;
+}
+
+extern "C" int dg_timeline(dg_ctx* ctx, int arm, double* ms, int n)
+{
+    if (!ctx) return DG_EINVAL;
+    if (!ctx->partitioned) return DG_EUNSUPPORTED;
+    DG_CUDA(cudaSetDevice(ctx->device));
+    if (arm) {
+        for (cudaEvent_t& e : ctx->tl_ev)
+            if (!e && cudaEventCreate(&e) != cudaSuccess) return DG_ECUDA;
+        ctx->tl_armed = true;
+        ctx->tl_done = false;
+        return DG_OK;
+    }
+    if (!ms || n < 6 || !ctx->tl_done) return DG_EINVAL;
+    DG_CUDA(cudaEventSynchronize(ctx->tl_ev[6]));
+    for (int i = 1; i <= 6; ++i) {
+        float t = 0.0f;
+        DG_CUDA(cudaEventElapsedTime(&t, ctx->tl_ev[0], ctx->tl_ev[i]));
+        ms[i - 1] = (double)t;
     }
     return DG_OK;
 }

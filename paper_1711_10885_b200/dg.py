@@ -24,7 +24,8 @@ EXPORTED = ["dg_setup", "dg_local_layout", "dg_apply", "dg_apply_ex", "dg_residu
             "dg_fill_uniform", "dg_fill_uniform_local", "dg_nccl_unique_id", "dg_get_kernel_info", "dg_partition",
             "dg_set_diffusion", "dg_fill_uniform_cells", "dg_ssp_stage", "dg_set_velocity", "dg_set_quadrature",
             "dg_set_affine", "dg_matrix_size", "dg_assemble", "dg_matrix_apply", "dg_fabric_id", "dg_comm_info",
-            "dg_set_geometry", "dg_fabric_id_direct", "dg_p2p_blob_bytes", "dg_p2p_export", "dg_p2p_import"]
+            "dg_set_geometry", "dg_fabric_id_direct", "dg_p2p_blob_bytes", "dg_p2p_export", "dg_p2p_import",
+            "dg_timeline"]
 
 
 class DGError(RuntimeError):
@@ -76,6 +77,7 @@ def lib():
         L.dg_nccl_unique_id.argtypes = [vp]
         L.dg_fabric_id.argtypes = [vp]
         L.dg_comm_info.argtypes = [vp, vp, vp]
+        L.dg_timeline.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int]
         L.dg_set_geometry.argtypes = [vp, vp, ctypes.c_int, vp]
         L.dg_fabric_id_direct.argtypes = [vp]
         L.dg_p2p_blob_bytes.argtypes = []
@@ -374,6 +376,18 @@ class Operator:
         t, n = ctypes.c_int(), ctypes.c_int()
         _check(lib().dg_comm_info(self._h, ctypes.byref(t), ctypes.byref(n)), "dg_comm_info")
         return ("none", "nccl", "fabric", "fabric-direct", "p2p-ipc")[t.value], n.value
+
+    def timeline_arm(self):
+        """Record timing events around the launches of the next (partitioned) apply (dg_timeline)."""
+        _check(lib().dg_timeline(self._h, 1, None, 0), "dg_timeline")
+
+    def timeline(self):
+        """ms since the armed apply's start: pack (+ exchange) begin / end on the comm stream, inner
+        kernel begin / end, shell kernel start / end (waits for that apply)."""
+        t = (ctypes.c_double * 6)()
+        _check(lib().dg_timeline(self._h, 0, t, 6), "dg_timeline")
+        keys = ("pack_begin", "pack_end", "inner_begin", "inner_end", "shell_begin", "shell_end")
+        return dict(zip(keys, list(t)))
 
     # -- info / lifetime ----------------------------------------------------------------------------
     def kernel_info(self):

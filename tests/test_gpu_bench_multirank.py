@@ -33,3 +33,10 @@ def test_bench_n_ranks_on_one_gpu(n, workload):
     assert par["cells_per_rank"] > 0 and par["bitwise"] and par["max_abs_err_over_max_abs_y"] == 0.0
     assert d["halo_ablation"]["ms_per_apply"] > 0 and d["value"] > 0
     assert d["config"]["parts"][0] * d["config"]["parts"][1] * d["config"]["parts"][2] == n
+    # the overlap evidence: per rank, the pack (comm stream) and the inner / shell kernels (dg_timeline)
+    tl = d["overlap_timeline"]["ms_since_apply_start"]
+    assert len(tl) == n
+    for t in tl:
+        assert 0.0 <= t["pack_begin"] <= t["pack_end"]
+        assert 0.0 <= t["inner_begin"] <= t["inner_end"] <= t["shell_begin"] <= t["shell_end"]
+        assert t["pack_end"] <= t["shell_end"]
