@@ -304,7 +304,9 @@ int dg_comm_info(const dg_ctx* ctx, int* transport, int* nranks);
    and writes n >= 6 times in ms, relative to the apply's start on the caller's stream:
    ms[0] / ms[1] the trace pack (+ exchange) begin / end on the comm stream (begin before the waits
    on the neighbours' buffers), ms[2] / ms[3] the inner-box kernel begin / end, ms[4] the shell
-   kernel's start (after its wait for the received traces), ms[5] its end. DG_EUNSUPPORTED for a
+   kernel's start (after its wait for the received traces; after the inner box on the caller's
+   stream, or concurrent with it on the comm stream with DG_SHELL_STREAM=1), ms[5] its end.
+   DG_EUNSUPPORTED for a
    single-rank context, DG_EINVAL when no armed apply has run or n < 6. */
 int dg_timeline(dg_ctx* ctx, int arm, double* ms, int n);
 

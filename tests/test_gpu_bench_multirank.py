@@ -38,5 +38,5 @@ def test_bench_n_ranks_on_one_gpu(n, workload):
     assert len(tl) == n
     for t in tl:
         assert 0.0 <= t["pack_begin"] <= t["pack_end"]
-        assert 0.0 <= t["inner_begin"] <= t["inner_end"] <= t["shell_begin"] <= t["shell_end"]
-        assert t["pack_end"] <= t["shell_end"]
+        assert 0.0 <= t["inner_begin"] <= t["inner_end"]
+        assert t["pack_end"] <= t["shell_begin"] <= t["shell_end"]   # the shell after its traces arrived
