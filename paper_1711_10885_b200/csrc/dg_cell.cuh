@@ -99,11 +99,11 @@ template <> struct Cfg<3> { static constexpr int TPC = DG_OVR(3, DG_TPC, 16), P 
 template <> struct Cfg<4> { static constexpr int TPC = DG_OVR(4, DG_TPC, 16), P = DG_OVR(4, DG_P, 1), C = DG_OVR(4, DG_C, 4), MINB = DG_OVR(4, DG_MINB, 12); };
 template <> struct Cfg<5> { static constexpr int TPC = DG_OVR(5, DG_TPC, 32), P = DG_OVR(5, DG_P, 1), C = DG_OVR(5, DG_C, 1), MINB = DG_OVR(5, DG_MINB, 16); };
 template <> struct Cfg<6> { static constexpr int TPC = DG_OVR(6, DG_TPC, 36), P = DG_OVR(6, DG_P, 1), C = DG_OVR(6, DG_C, 4), MINB = DG_OVR(6, DG_MINB, 5); };
-template <> struct Cfg<7> { static constexpr int TPC = DG_OVR(7, DG_TPC, 64), P = DG_OVR(7, DG_P, 1), C = DG_OVR(7, DG_C, 1), MINB = DG_OVR(7, DG_MINB, 10); };
+template <> struct Cfg<7> { static constexpr int TPC = DG_OVR(7, DG_TPC, 64), P = DG_OVR(7, DG_P, 1), C = DG_OVR(7, DG_C, 1), MINB = DG_OVR(7, DG_MINB, 12); };
 template <> struct Cfg<8> { static constexpr int TPC = DG_OVR(8, DG_TPC, 64), P = DG_OVR(8, DG_P, 1), C = DG_OVR(8, DG_C, 1), MINB = DG_OVR(8, DG_MINB, 10); };
-template <> struct Cfg<9> { static constexpr int TPC = DG_OVR(9, DG_TPC, 48), P = DG_OVR(9, DG_P, 2), C = DG_OVR(9, DG_C, 2), MINB = DG_OVR(9, DG_MINB, 3); };
+template <> struct Cfg<9> { static constexpr int TPC = DG_OVR(9, DG_TPC, 96), P = DG_OVR(9, DG_P, 1), C = DG_OVR(9, DG_C, 1), MINB = DG_OVR(9, DG_MINB, 8); };
 template <> struct Cfg<10> { static constexpr int TPC = DG_OVR(10, DG_TPC, 64), P = DG_OVR(10, DG_P, 2), C = DG_OVR(10, DG_C, 1), MINB = DG_OVR(10, DG_MINB, 8); };
-template <> struct Cfg<11> { static constexpr int TPC = DG_OVR(11, DG_TPC, 128), P = DG_OVR(11, DG_P, 1), C = DG_OVR(11, DG_C, 1), MINB = DG_OVR(11, DG_MINB, 5); };
+template <> struct Cfg<11> { static constexpr int TPC = DG_OVR(11, DG_TPC, 128), P = DG_OVR(11, DG_P, 1), C = DG_OVR(11, DG_C, 1), MINB = DG_OVR(11, DG_MINB, 6); };
 
 // Shared-memory layout of one n^3 cell array: x-, y- and z-pencil accesses of a warp are
 // (nearly) bank-conflict free (searched offline; n = 8 uses an XOR swizzle that is conflict

@@ -193,7 +193,7 @@ struct GSmem {
 
 template <int N, bool GH>
 #ifndef DG_GMB
-#define DG_GMB ((DG_N) == 4 ? 12 : (DG_N) == 8 ? 8 : (DG_N) == 10 ? 5 : 1)   // min CTAs per SM (n = 4: A-k3 30.5 -> 31.0; n = 8: the 8 CTAs its shared memory allows; n = 10: A-k9 29.7 -> 31.0)
+#define DG_GMB ((DG_N) == 4 ? 12 : (DG_N) == 8 ? 8 : (DG_N) == 10 ? 5 : (DG_N) == 11 ? 3 : 1)   // min CTAs per SM (n = 4: A-k3 30.5 -> 31.0; n = 8: the 8 CTAs its shared memory allows; n = 10: A-k9 29.7 -> 31.0; n = 11: the 3 its shared memory allows, A-k10 35.4 -> 36.1)
 #endif
 __global__ void __launch_bounds__(GCfg<N>::C * GCfg<N>::TPC, DG_GMB)
 dg_gen_kernel(const __grid_constant__ KParams p)
