@@ -631,7 +631,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default=None,
-                    help="default: C3 (N=1) / C3-per-GPU weak (N>1); also c1, c2, c4-kK, c5weak, c5strong, "
+                    help="default: C3 (N=1) / C5 weak, 128x128x64 cells per GPU (N>1); also c1, c2, c3weak, c4-kK, c5weak, c5strong, "
                          "a-kK (the paper's Problem A: periodic, per-cell tensor D, ~4e8 DOFs), "
                          "tg-kK (the Taylor-Green transport operator: b(x) at every point, q = 2p+4)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -17,7 +17,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("n,workload", [(2, "c3weak"), (4, "c3weak"), (2, "c5strong")])
+# (8, c5weak): the driver's default N = 8 line (2 x 2 x 2 blocks of 128 x 128 x 64 cells, every rank with
+# neighbours across all three partition directions)
+@pytest.mark.parametrize("n,workload", [(2, "c3weak"), (4, "c3weak"), (2, "c5strong"), (8, "c5weak")])
 def test_bench_n_ranks_on_one_gpu(n, workload):
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--share-gpu", "--workload", workload,
            "--steps", "3", "--warmup", "3", "--no-e2e"]
