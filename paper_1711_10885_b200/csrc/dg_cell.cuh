@@ -1021,10 +1021,18 @@ dg_cell_kernel(const __grid_constant__ KParams p)
 #pragma unroll
                 for (int e = 0; e < N; ++e) A0[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
         nb_contract<N, P>(T, NT, 0, nbi, pa, pb, act, rl, rh, gm0);
+#ifndef DG_EARLYNB
+#define DG_EARLYNB 1
+#endif
+        // each phase's neighbour loads issued before the previous phase's barrier, so they fly during
+        // the wait (A/B on one box: C3 +0.2 %, A-k7 +0.5 %, A-k10 +0.7 %; the fast n = 11 -0.5 %: off)
+        constexpr bool ENB = DG_EARLYNB && N != 11;
+        unsigned gm1 = 0;
+        if (ENB) gm1 = nb_load<N, P, GH>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
         csync();
 
         // ---- phase 2: y-pencils (x = a, z = bb): V along y -> A1; y-neighbours; x-arrays step B
-        const unsigned gm1 = nb_load<N, P, GH>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
+        if (!ENB) gm1 = nb_load<N, P, GH>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -1037,11 +1045,13 @@ dg_cell_kernel(const __grid_constant__ KParams p)
                 for (int e = 0; e < N; ++e) A1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
         nb_tangential<N, TPC>(T.Vs[2], NT, 0, 0, nbi, (lane + TPC / 2) % TPC);
         nb_contract<N, P>(T, NT, 1, nbi, pa, pb, act, rl, rh, gm1);
+        unsigned gm2 = 0;
+        if (ENB) gm2 = nb_load<N, P, GH>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
         csync();
 
         // ---- phase 3: z-pencils (x = a, y = bb): u at the Gauss points -> A0; z-neighbours;
         //      y-arrays step B, x-arrays step C
-        const unsigned gm2 = nb_load<N, P, GH>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
+        if (!ENB) gm2 = nb_load<N, P, GH>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll

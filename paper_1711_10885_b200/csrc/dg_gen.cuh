@@ -418,9 +418,10 @@ dg_gen_kernel(const __grid_constant__ KParams p)
 #pragma unroll
                 for (int e = 0; e < N; ++e) X0[Lay<N>::at(e, pa[k], pb[k])] = t[k][e];
         nb_contract<N, P, GFLay<N>>(T, NT, 0, nbi, pa, pb, act, rl, rh, gm);
+        if (DG_EARLYNB) gm = nb_load<N, P, GH>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
         csync();
 
-        gm = nb_load<N, P, GH>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
+        if (!DG_EARLYNB) gm = nb_load<N, P, GH>(p, zc, n3, 1, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
@@ -432,9 +433,10 @@ dg_gen_kernel(const __grid_constant__ KParams p)
 #pragma unroll
                 for (int e = 0; e < N; ++e) X1[Lay<N>::at(pa[k], e, pb[k])] = t[k][e];
         nb_contract<N, P, GFLay<N>>(T, NT, 1, nbi, pa, pb, act, rl, rh, gm);
+        if (DG_EARLYNB) gm = nb_load<N, P, GH>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
         csync();
 
-        gm = nb_load<N, P, GH>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
+        if (!DG_EARLYNB) gm = nb_load<N, P, GH>(p, zc, n3, 2, lc, nbi, pa, pb, act, rl, rh);
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
