@@ -2,6 +2,8 @@
 
     python tools/variant.py NAME N [-DFLAG[=V] ...]
     python tools/variant.py NAME matrix [-DFLAG[=V] ...]
+    python tools/variant.py NAME geo:N:M [-DFLAG[=V] ...]     (multilinear-geometry kernel (n, m))
+    python tools/variant.py NAME vb:N:M [-DFLAG[=V] ...]      (variable-velocity kernel (n, m))
 
 Recompiles dg_cell_inst.cu for n = N (or dg_matrix.cu) with the extra flags, links it with the standard
 objects into variants/NAME.so (select at run time with DG_LIB=$PWD/variants/NAME.so).
@@ -17,15 +19,19 @@ from paper_1711_10885_b200 import build as B  # noqa: E402
 
 def main():
     name, flags = sys.argv[1], sys.argv[3:]
-    matrix = sys.argv[2] == "matrix"
-    n = 0 if matrix else int(sys.argv[2])
+    what = sys.argv[2]
     B.build()
     obj = os.path.join(ROOT, "build", "var", name + ".o")
     os.makedirs(os.path.dirname(obj), exist_ok=True)
-    src = os.path.join(B.CSRC, "dg_matrix.cu" if matrix else "dg_cell_inst.cu")
-    replaced = "dg_matrix.o" if matrix else "dg_cell_n%d.o" % n
-    cmd = [B.NVCC] + B.ARCH + B.FLAGS + ([] if matrix else ["-DDG_N=%d" % n]) + flags + ["-Xptxas", "-v", "-c", src,
-                                                                                       "-o", obj]
+    if what == "matrix":
+        src, replaced, defs = os.path.join(B.CSRC, "dg_matrix.cu"), "dg_matrix.o", []
+    elif what.startswith(("geo:", "vb:")):
+        fam, n, m = what.split(":")
+        src = os.path.join(B.CSRC, "dg_%s_inst.cu" % fam)
+        replaced, defs = "dg_%s_n%s_m%s.o" % (fam, n, m), ["-DDG_N=%s" % n, "-DDG_M=%s" % m]
+    else:
+        src, replaced, defs = os.path.join(B.CSRC, "dg_cell_inst.cu"), "dg_cell_n%d.o" % int(what), ["-DDG_N=%s" % what]
+    cmd = [B.NVCC] + B.ARCH + B.FLAGS + defs + flags + ["-Xptxas", "-v", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         sys.exit("compile failed:\n" + r.stderr[-2000:])
