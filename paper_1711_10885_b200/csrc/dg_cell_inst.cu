@@ -173,7 +173,20 @@ static bool use_reg()
     }
     return v == 1;
 }
-constexpr int REG_THREADS = 128;
+constexpr int REG_THREADS = REG_CTA;
+// dynamic shared memory of the register kernel (the staged images, RStage; 0 when not staged)
+template <int N, bool GEN, bool GH>
+static cudaError_t reg_attr()
+{
+    static int done[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (RStage<N, GEN>::BYTES == 0 || dev < 0 || dev >= 64 || done[dev]) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(dg_reg_kernel<N, GEN, GH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         RStage<N, GEN>::BYTES);
+    if (e == cudaSuccess) done[dev] = 1;
+    return e;
+}
 
 cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
 {
@@ -184,8 +197,8 @@ cudaError_t DG_CAT(launch_cell_n, DG_N)(const KParams& p, cudaStream_t s)
     if constexpr (N <= DG_REG_NMAX) {
         if (use_reg()) {
             const int64_t grid = (p.ntasks + REG_THREADS - 1) / REG_THREADS;
-            if (p.ghosts) dg_reg_kernel<N, false, true><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
-            else dg_reg_kernel<N, false, false><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
+            if (p.ghosts) { cudaError_t e = reg_attr<N, false, true>(); if (e != cudaSuccess) return e; dg_reg_kernel<N, false, true><<<(unsigned)grid, REG_THREADS, RStage<N, false>::BYTES, s>>>(p); }
+            else { cudaError_t e = reg_attr<N, false, false>(); if (e != cudaSuccess) return e; dg_reg_kernel<N, false, false><<<(unsigned)grid, REG_THREADS, RStage<N, false>::BYTES, s>>>(p); }
             return cudaGetLastError();
         }
     }
@@ -233,8 +246,8 @@ cudaError_t DG_CAT(launch_gen_n, DG_N)(const KParams& p, cudaStream_t s)
     if constexpr (N <= DG_REG_GMAX) {
         if (use_reg()) {
             const int64_t grid = (p.ntasks + REG_THREADS - 1) / REG_THREADS;
-            if (p.ghosts) dg_reg_kernel<N, true, true><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
-            else dg_reg_kernel<N, true, false><<<(unsigned)grid, REG_THREADS, 0, s>>>(p);
+            if (p.ghosts) { cudaError_t e = reg_attr<N, true, true>(); if (e != cudaSuccess) return e; dg_reg_kernel<N, true, true><<<(unsigned)grid, REG_THREADS, RStage<N, true>::BYTES, s>>>(p); }
+            else { cudaError_t e = reg_attr<N, true, false>(); if (e != cudaSuccess) return e; dg_reg_kernel<N, true, false><<<(unsigned)grid, REG_THREADS, RStage<N, true>::BYTES, s>>>(p); }
             return cudaGetLastError();
         }
     }
@@ -260,12 +273,13 @@ int DG_CAT(gen_info_n, DG_N)(LaunchInfo* info)
     if constexpr (N <= DG_REG_GMAX) if (use_reg()) {
         info->cells_per_cta = REG_THREADS;
         info->threads = REG_THREADS;
-        info->smem = 0;
+        info->smem = RStage<N, true>::BYTES;
         cudaFuncAttributes fa;
         if (cudaFuncGetAttributes(&fa, dg_reg_kernel<N, true>) != cudaSuccess) return -3;
         info->regs = fa.numRegs;
         int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_reg_kernel<N, true>, REG_THREADS, 0) !=
+        if (reg_attr<N, true, false>() != cudaSuccess) return -3;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_reg_kernel<N, true>, REG_THREADS, RStage<N, true>::BYTES) !=
             cudaSuccess)
             return -3;
         info->ctas_per_sm = blocks;
@@ -294,12 +308,13 @@ int DG_CAT(cell_info_n, DG_N)(LaunchInfo* info)
     if constexpr (N <= DG_REG_NMAX) if (use_reg()) {
         info->cells_per_cta = REG_THREADS;
         info->threads = REG_THREADS;
-        info->smem = 0;
+        info->smem = RStage<N, false>::BYTES;
         cudaFuncAttributes fa;
         if (cudaFuncGetAttributes(&fa, dg_reg_kernel<N, false>) != cudaSuccess) return -3;
         info->regs = fa.numRegs;
         int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_reg_kernel<N, false>, REG_THREADS, 0) != cudaSuccess)
+        if (reg_attr<N, false, false>() != cudaSuccess) return -3;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dg_reg_kernel<N, false>, REG_THREADS, RStage<N, false>::BYTES) != cudaSuccess)
             return -3;
         info->ctas_per_sm = blocks;
         return 0;

@@ -132,6 +132,63 @@ __device__ __forceinline__ void reg_load(const double* src, double (&a)[N * N * 
     }
 }
 
+// ---------------------------------------------------------------------------------- staged blocks (n = 3)
+// One thread per cell and 128 consecutive cells per CTA: the CTA's own blocks (with the x-neighbours
+// at both ends of the range) and the rows of y-neighbour blocks below and above are contiguous
+// ranges of z, so they arrive by three bulk copies (cp.async.bulk) into linear shared-memory images
+// and y leaves by one, instead of 27 strided 8-byte loads / stores per block and thread (ncu C4-k2:
+// long_scoreboard and lg_throttle were the top stalls at 26 % issue). A neighbour outside the images
+// (periodic wrap, another rank, the z direction) is read from global memory as before.
+#ifndef DG_REG_STAGE
+#define DG_REG_STAGE 4     // bit 2 (n - 2) + GEN: staged instantiations (bit 2: n = 3, constant diagonal D)
+#endif
+constexpr int REG_CTA = 128;                       // threads = cells per CTA of dg_reg_kernel
+template <int N, bool GEN> struct RStage {
+    static constexpr bool ON = N >= 2 && N <= 3 && ((DG_REG_STAGE >> (2 * (N - 2) + (GEN ? 1 : 0))) & 1);
+    static constexpr int N3 = N * N * N;
+    static constexpr int IMG0 = (REG_CTA + 2) * N3 + 2;   // own blocks + one x-neighbour each side (+ shift pad)
+    static constexpr int IMG = REG_CTA * N3 + 2;          // one row of y-neighbour blocks
+    static constexpr int BYTES = ON ? (IMG0 + 2 * IMG) * 8 + 16 : 0;
+};
+struct RImg {
+    const double* S;   // smem: global double d of the range sits at S[d - d0]
+    int64_t d0, d1;    // global double range [d0, d1) of z held (empty: d0 == d1)
+};
+// tid 0: bulk-copy the 16-byte-aligned interior of z[d0, d1) to base + (d0 & 1) + ..., plain loads for an
+// odd leading / trailing double (stored after the wait by the caller's thread 0, see rimg_fix)
+__device__ __forceinline__ RImg rimg_make(double* base, int64_t d0, int64_t d1)
+{
+    RImg im;
+    im.d0 = d0;
+    im.d1 = d1 > d0 ? d1 : d0;
+    im.S = base + (d0 & 1);                        // S + (d - d0) == z + d (mod 16 bytes)
+    return im;
+}
+__device__ __forceinline__ uint32_t rimg_bytes(const RImg& im)
+{
+    const int64_t a0 = im.d0 + (im.d0 & 1), a1 = im.d1 - (im.d1 & 1);
+    return a1 > a0 ? (uint32_t)((a1 - a0) * 8) : 0u;
+}
+__device__ __forceinline__ void rimg_issue(const double* z, const RImg& im, uint64_t* mbar)
+{
+    const int64_t a0 = im.d0 + (im.d0 & 1);
+    const uint32_t b = rimg_bytes(im);
+    if (b) bulk::load(const_cast<double*>(im.S) + (a0 - im.d0), z + a0, b, mbar);
+}
+__device__ __forceinline__ void rimg_fix(const double* z, const RImg& im)
+{
+    double* S = const_cast<double*>(im.S);
+    if (im.d1 <= im.d0) return;
+    if (im.d0 & 1) S[0] = __ldg(z + im.d0);                                  // odd leading double
+    if (im.d1 & 1) S[im.d1 - 1 - im.d0] = __ldg(z + im.d1 - 1);              // odd trailing double
+}
+template <int N>
+__device__ __forceinline__ void reg_load_smem(const double* src, double (&a)[N * N * N])
+{
+#pragma unroll
+    for (int e = 0; e < N * N * N; ++e) a[e] = src[e];
+}
+
 // 2D face-array stages: o(i, b) = sum_j M[i][j] a(j, b) (AX = 0) or o(a, i) = sum_j M[i][j] a(a, j)
 template <int N, int AX, bool TR>
 __device__ __forceinline__ void fstage(const double (&M)[N][N], const double (&a)[N][N], double (&o)[N][N])
@@ -158,7 +215,8 @@ __device__ __forceinline__ void fstage(const double (&M)[N][N], const double (&a
 template <int N, int Q, bool GEN, bool GH>
 __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, const double* zc, int64_t n3,
                                           const int (&lc)[3], int64_t cell, unsigned nbmask, bool do_int, bool do_bnd,
-                                          const double (&Dw)[6], const double (&u)[N * N * N], double (&X)[N * N * N])
+                                          const double (&Dw)[6], const double (&u)[N * N * N], double (&X)[N * N * N],
+                                          const double* slo = nullptr, const double* shi = nullptr)
 {
     constexpr int T1 = (Q == 0) ? 1 : 0, T2 = (Q == 2) ? 1 : 2;
 #pragma unroll
@@ -180,7 +238,8 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
                     }
             } else {
                 double zn[N * N * N];
-                reg_load<N>(reg_nb<N>(p, zc, n3, lc, Q, s), zn);
+                if (const double* sb = s ? shi : slo) reg_load_smem<N>(sb, zn);   // staged image (RStage)
+                else reg_load<N>(reg_nb<N>(p, zc, n3, lc, Q, s), zn);
 #pragma unroll
                 for (int a = 0; a < N; ++a)
 #pragma unroll
@@ -320,12 +379,47 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
 #define DG_RMINB(n, gen) ((n) == 2 ? ((gen) ? 4 : 5) : DG_RMINB3)
 #endif
 template <int N, bool GEN, bool GH = false>
-__global__ void __launch_bounds__(128, DG_RMINB(N, GEN)) dg_reg_kernel(const __grid_constant__ KParams p)
+__global__ void __launch_bounds__(REG_CTA, DG_RMINB(N, GEN)) dg_reg_kernel(const __grid_constant__ KParams p)
 {
     constexpr int N3 = N * N * N;
     const RTab<N>& R = g_rtab;
-    const int64_t task = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (task >= p.ntasks) return;
+    int64_t task = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // staged images (RStage): consecutive tasks are consecutive cells when the task box spans whole
+    // x-rows and y-planes of this rank's box
+    const bool stg = RStage<N, GEN>::ON && p.tma == 2 && !p.task_list && p.task_lo[0] == 0 && p.task_lo[1] == 0 &&
+                     p.task_cnt[0] == p.nloc[0] && p.task_cnt[1] == p.nloc[1];
+    const bool valid = task < p.ntasks;
+    if (!stg && !valid) return;
+    if (!valid) task = p.ntasks - 1;               // (staged: every thread takes part in the barriers)
+    extern __shared__ __align__(16) double rsm[];
+    int64_t soff[3] = {0, 0, 0};                   // first global double of each image
+    if constexpr (RStage<N, GEN>::ON) {
+        if (stg) {
+            const int64_t nxy = p.nloc[0] * p.nloc[1], ncell = nxy * p.nloc[2];
+            const int64_t cb = p.task_lo[2] * nxy + blockIdx.x * (int64_t)REG_CTA;    // first cell of the CTA
+            const int64_t nv = min((int64_t)REG_CTA, p.ntasks - blockIdx.x * (int64_t)REG_CTA);
+            auto clampc = [&](int64_t c) { return c < 0 ? (int64_t)0 : (c > ncell ? ncell : c); };
+            const int64_t lo[3] = {clampc(cb - 1), clampc(cb - p.nloc[0]), clampc(cb + p.nloc[0])};
+            const int64_t hi[3] = {clampc(cb + nv + 1), clampc(cb - p.nloc[0] + nv), clampc(cb + p.nloc[0] + nv)};
+#pragma unroll
+            for (int i = 0; i < 3; ++i) soff[i] = N3 * lo[i];
+            uint64_t* mbar = reinterpret_cast<uint64_t*>(rsm + RStage<N, GEN>::IMG0 + 2 * RStage<N, GEN>::IMG);
+            if (threadIdx.x == 0) {
+                RImg im[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    im[i] = rimg_make(rsm + (i == 0 ? 0 : RStage<N, GEN>::IMG0 + (i - 1) * RStage<N, GEN>::IMG), N3 * lo[i], N3 * hi[i]);
+                tma::mbar_init_n(mbar, 1);
+                tma::expect_tx(mbar, rimg_bytes(im[0]) + rimg_bytes(im[1]) + rimg_bytes(im[2]));
+#pragma unroll
+                for (int i = 0; i < 3; ++i) rimg_issue(p.z, im[i], mbar);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) rimg_fix(p.z, im[i]);
+            }
+            __syncthreads();
+            tma::wait(mbar, 0);
+        }
+    }
     int lc[3];
     if (p.task_list) {
         const int64_t e = p.task_list[task];
@@ -351,8 +445,23 @@ __global__ void __launch_bounds__(128, DG_RMINB(N, GEN)) dg_reg_kernel(const __g
         if (p.per[q] || (g >= 0 && g < p.gcells[q])) nbmask |= 1u << f;
     }
 
+    // this thread's blocks in the staged images: own, x- / y-neighbours inside this rank's box (no wrap)
+    const double *sown = nullptr, *sx0 = nullptr, *sx1 = nullptr, *sy0 = nullptr, *sy1 = nullptr;
+    if constexpr (RStage<N, GEN>::ON) {
+        if (stg) {
+            const double* S0 = rsm + (soff[0] & 1);
+            const double* S1 = rsm + RStage<N, GEN>::IMG0 + (soff[1] & 1);
+            const double* S2 = rsm + RStage<N, GEN>::IMG0 + RStage<N, GEN>::IMG + (soff[2] & 1);
+            sown = S0 + (cell * n3 - soff[0]);
+            if (lc[0] > 0) sx0 = sown - n3;
+            if (lc[0] + 1 < p.nloc[0]) sx1 = sown + n3;
+            if (lc[1] > 0) sy0 = S1 + ((cell - p.nloc[0]) * n3 - soff[1]);
+            if (lc[1] + 1 < p.nloc[1]) sy1 = S2 + ((cell + p.nloc[0]) * n3 - soff[2]);
+        }
+    }
     double u[N3], t[N3], X[N3];
-    reg_load<N>(zc, t);
+    if (sown) reg_load_smem<N>(sown, t);
+    else reg_load<N>(zc, t);
     rcontract<N, 0>(R.V, t, u);
     rcontract<N, 1>(R.V, u, t);
     rcontract<N, 2>(R.V, t, u);                     // u at the Gauss points
@@ -466,13 +575,36 @@ __global__ void __launch_bounds__(128, DG_RMINB(N, GEN)) dg_reg_kernel(const __g
                     X[i] = fma(wc * R.w[ix] * R.w[iy] * R.w[iz], u[i], X[i]);
                 }
     }
-    reg_faces<N, 0, GEN, GH>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
-    reg_faces<N, 1, GEN, GH>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
+    reg_faces<N, 0, GEN, GH>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X, sx0, sx1);
+    reg_faces<N, 1, GEN, GH>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X, sy0, sy1);
     reg_faces<N, 2, GEN, GH>(p, R, zc, n3, lc, cell, nbmask, do_int, do_bnd, Dw, u, X);
     rcontract_t<N, 2>(R.V, X, t);
     rcontract_t<N, 1>(R.V, t, u);
     rcontract_t<N, 0>(R.V, u, t);                   // y block
     double* yc = p.y + cell * n3;
+    if constexpr (RStage<N, GEN>::ON) {
+        if (stg && p.epi == 0) {   // y through a linear image (over the free images) and one bulk store
+            const int64_t nv = min((int64_t)REG_CTA, p.ntasks - blockIdx.x * (int64_t)REG_CTA);
+            const int64_t cb = cell - threadIdx.x;
+            const int64_t d0 = cb * n3, d1 = (cb + nv) * n3;
+            __syncthreads();                           // every image read
+            double* S = rsm + (d0 & 1);                // S + (d - d0) == y + d (mod 16 bytes)
+            if (valid) {
+#pragma unroll
+                for (int e = 0; e < N3; ++e) S[threadIdx.x * N3 + e] = t[e];
+            }
+            tma::fence_async();
+            __syncthreads();
+            const int64_t a0 = d0 + (d0 & 1), a1 = d1 - (d1 & 1);
+            if (threadIdx.x == 0) {
+                if (a1 > a0) bulk::store(p.y + a0, S + (a0 - d0), (uint32_t)((a1 - a0) * 8));
+                if (d0 & 1) __stcs(p.y + d0, S[0]);
+                if (d1 & 1) __stcs(p.y + d1 - 1, S[d1 - 1 - d0]);
+            }
+            return;
+        }
+    }
+    if (!valid) return;
     epilogue<N3>(p, cell * n3, t);
     if constexpr (N3 % 2 == 0) {
 #pragma unroll

@@ -92,7 +92,7 @@ for k in (1, 2):
             yref, _ = o1.apply(*cfg.args(), z, mask=mask, periodic=per, Dcell=Dc)
             den = max(np.abs(yref).max(), 1e-300)
             out.append([k, str(per), tensors, mask, float(np.abs(y.cpu().numpy() - yref).max() / den),
-                        float(np.abs(yref).max()), info["smem_bytes"]])
+                        float(np.abs(yref).max()), info["cells_per_cta"] == info["threads_per_cta"]])
         op.close()
 print(json.dumps({"rows": out}))
 """
@@ -108,10 +108,9 @@ def test_low_degree_kernels_vs_o1(kernel):
     assert r.returncode == 0, r.stderr[-2000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert len(res["rows"]) == 2 * 4 * 4
-    for k, per, tensors, mask, err, scale, smem in res["rows"]:
-        # the register kernels use no shared memory: shows which kernel ran
-        reg_expected = kernel == "reg"
-        assert (smem == 0) == reg_expected, (k, per, tensors, smem)
+    for k, per, tensors, mask, err, scale, one_thread_per_cell in res["rows"]:
+        # the register kernels run one thread per cell (the pencil kernels several): shows which kernel ran
+        assert one_thread_per_cell == (kernel == "reg"), (k, per, tensors)
         if scale == 0.0:
             assert err == 0.0
         else:
