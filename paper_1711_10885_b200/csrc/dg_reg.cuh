@@ -375,8 +375,11 @@ __device__ __forceinline__ void reg_faces(const KParams& p, const RTab<N>& R, co
 #ifndef DG_RMINB3
 #define DG_RMINB3 1
 #endif
+#ifndef DG_RMINB2F
+#define DG_RMINB2F 5
+#endif
 #ifndef DG_RMINB
-#define DG_RMINB(n, gen) ((n) == 2 ? ((gen) ? 4 : 5) : DG_RMINB3)
+#define DG_RMINB(n, gen) ((n) == 2 ? ((gen) ? 4 : DG_RMINB2F) : DG_RMINB3)
 #endif
 template <int N, bool GEN, bool GH = false>
 __global__ void __launch_bounds__(REG_CTA, DG_RMINB(N, GEN)) dg_reg_kernel(const __grid_constant__ KParams p)
