@@ -148,7 +148,12 @@ template <int N, bool GEN> struct RStage {
     static constexpr int N3 = N * N * N;
     static constexpr int IMG0 = (REG_CTA + 2) * N3 + 2;   // own blocks + one x-neighbour each side (+ shift pad)
     static constexpr int IMG = REG_CTA * N3 + 2;          // one row of y-neighbour blocks
-    static constexpr int BYTES = ON ? (IMG0 + 2 * IMG) * 8 + 16 : 0;
+#ifndef DG_REG_NIMG
+#define DG_REG_NIMG 1      // 1: the own / x image only (C4-k2 68.9 against 68.5 GDOF/s with the y rows too)
+#endif
+    static constexpr int NIMG = DG_REG_NIMG;
+    static constexpr int MB = IMG0 + (NIMG > 1 ? 2 * IMG : 0);   // the mbarrier (doubles)
+    static constexpr int BYTES = ON ? MB * 8 + 16 : 0;
 };
 struct RImg {
     const double* S;   // smem: global double d of the range sits at S[d - d0]
@@ -403,10 +408,12 @@ __global__ void __launch_bounds__(REG_CTA, DG_RMINB(N, GEN)) dg_reg_kernel(const
             const int64_t nv = min((int64_t)REG_CTA, p.ntasks - blockIdx.x * (int64_t)REG_CTA);
             auto clampc = [&](int64_t c) { return c < 0 ? (int64_t)0 : (c > ncell ? ncell : c); };
             const int64_t lo[3] = {clampc(cb - 1), clampc(cb - p.nloc[0]), clampc(cb + p.nloc[0])};
-            const int64_t hi[3] = {clampc(cb + nv + 1), clampc(cb - p.nloc[0] + nv), clampc(cb + p.nloc[0] + nv)};
+            // (RStage::NIMG = 1: the own / x image only, the y-neighbour rows from global memory)
+            const int64_t hi[3] = {clampc(cb + nv + 1), RStage<N, GEN>::NIMG > 1 ? clampc(cb - p.nloc[0] + nv) : lo[1],
+                                   RStage<N, GEN>::NIMG > 1 ? clampc(cb + p.nloc[0] + nv) : lo[2]};
 #pragma unroll
             for (int i = 0; i < 3; ++i) soff[i] = N3 * lo[i];
-            uint64_t* mbar = reinterpret_cast<uint64_t*>(rsm + RStage<N, GEN>::IMG0 + 2 * RStage<N, GEN>::IMG);
+            uint64_t* mbar = reinterpret_cast<uint64_t*>(rsm + RStage<N, GEN>::MB);
             if (threadIdx.x == 0) {
                 RImg im[3];
 #pragma unroll
@@ -458,8 +465,8 @@ __global__ void __launch_bounds__(REG_CTA, DG_RMINB(N, GEN)) dg_reg_kernel(const
             sown = S0 + (cell * n3 - soff[0]);
             if (lc[0] > 0) sx0 = sown - n3;
             if (lc[0] + 1 < p.nloc[0]) sx1 = sown + n3;
-            if (lc[1] > 0) sy0 = S1 + ((cell - p.nloc[0]) * n3 - soff[1]);
-            if (lc[1] + 1 < p.nloc[1]) sy1 = S2 + ((cell + p.nloc[0]) * n3 - soff[2]);
+            if (RStage<N, GEN>::NIMG > 1 && lc[1] > 0) sy0 = S1 + ((cell - p.nloc[0]) * n3 - soff[1]);
+            if (RStage<N, GEN>::NIMG > 1 && lc[1] + 1 < p.nloc[1]) sy1 = S2 + ((cell + p.nloc[0]) * n3 - soff[2]);
         }
     }
     double u[N3], t[N3], X[N3];
