@@ -98,7 +98,7 @@ template <> struct Cfg<2> { static constexpr int TPC = DG_OVR(2, DG_TPC, 8), P =
 template <> struct Cfg<3> { static constexpr int TPC = DG_OVR(3, DG_TPC, 16), P = DG_OVR(3, DG_P, 1), C = DG_OVR(3, DG_C, 8), MINB = DG_OVR(3, DG_MINB, 8); };
 template <> struct Cfg<4> { static constexpr int TPC = DG_OVR(4, DG_TPC, 16), P = DG_OVR(4, DG_P, 1), C = DG_OVR(4, DG_C, 4), MINB = DG_OVR(4, DG_MINB, 12); };
 template <> struct Cfg<5> { static constexpr int TPC = DG_OVR(5, DG_TPC, 32), P = DG_OVR(5, DG_P, 1), C = DG_OVR(5, DG_C, 1), MINB = DG_OVR(5, DG_MINB, 16); };
-template <> struct Cfg<6> { static constexpr int TPC = DG_OVR(6, DG_TPC, 36), P = DG_OVR(6, DG_P, 1), C = DG_OVR(6, DG_C, 4), MINB = DG_OVR(6, DG_MINB, 5); };
+template <> struct Cfg<6> { static constexpr int TPC = DG_OVR(6, DG_TPC, 36), P = DG_OVR(6, DG_P, 1), C = DG_OVR(6, DG_C, 3), MINB = DG_OVR(6, DG_MINB, 7); };
 template <> struct Cfg<7> { static constexpr int TPC = DG_OVR(7, DG_TPC, 64), P = DG_OVR(7, DG_P, 1), C = DG_OVR(7, DG_C, 1), MINB = DG_OVR(7, DG_MINB, 12); };
 template <> struct Cfg<8> { static constexpr int TPC = DG_OVR(8, DG_TPC, 64), P = DG_OVR(8, DG_P, 1), C = DG_OVR(8, DG_C, 1), MINB = DG_OVR(8, DG_MINB, 10); };
 template <> struct Cfg<9> { static constexpr int TPC = DG_OVR(9, DG_TPC, 96), P = DG_OVR(9, DG_P, 1), C = DG_OVR(9, DG_C, 1), MINB = DG_OVR(9, DG_MINB, 8); };

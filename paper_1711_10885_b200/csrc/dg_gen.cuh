@@ -167,12 +167,13 @@ template <> struct GFLay<4> {
 #endif
 // (one pencil per thread is better than the fast kernel's 2 for n = 9, 10: A-k8 14.7 -> 31.4,
 // A-k9 19.5 -> 27.5 GDOF/s;
-// n = 6: 36 threads per cell (every thread a pencil), 2 cells per CTA straddling warps: A-k5
-// 26.6 -> 28.5; measured with tools/variant.py)
+// n = 6: 36 threads per cell (every thread a pencil), cells straddling warps: 2 cells per CTA A-k5
+// 26.6 -> 28.5; 3 cells (108 threads) at 4 CTAs/SM 31.1 -> 34.3 (4 cells at 2 / 3 CTAs 29.0 / 32.6,
+// 3 cells at 5 CTAs spills: 30.7); measured with tools/variant.py)
 template <int N> struct GCfgD {
     static constexpr int TPC = (N == 6) ? 36 : (N == 9) ? 96 : (N == 10) ? 128 : Cfg<N>::TPC;
     static constexpr int P = (N == 6 || N == 9 || N == 10) ? 1 : Cfg<N>::P;
-    static constexpr int C = (N == 6) ? 2 : (N == 9 || N == 10) ? 1 : Cfg<N>::C;
+    static constexpr int C = (N == 6) ? 3 : (N == 9 || N == 10) ? 1 : Cfg<N>::C;
 };
 template <int N> struct GCfg {
     static constexpr int TPC = DG_GOVR(DG_GTPC, GCfgD<N>::TPC), P = DG_GOVR(DG_GP, GCfgD<N>::P),
@@ -193,7 +194,7 @@ struct GSmem {
 
 template <int N, bool GH>
 #ifndef DG_GMB
-#define DG_GMB ((DG_N) == 4 ? 12 : (DG_N) == 8 ? 8 : (DG_N) == 10 ? 5 : (DG_N) == 11 ? 3 : 1)   // min CTAs per SM (n = 4: A-k3 30.5 -> 31.0; n = 8: the 8 CTAs its shared memory allows; n = 10: A-k9 29.7 -> 31.0; n = 11: the 3 its shared memory allows, A-k10 35.4 -> 36.1)
+#define DG_GMB ((DG_N) == 4 ? 12 : (DG_N) == 6 ? 4 : (DG_N) == 8 ? 8 : (DG_N) == 10 ? 5 : (DG_N) == 11 ? 3 : 1)   // min CTAs per SM (n = 4: A-k3 30.5 -> 31.0; n = 8: the 8 CTAs its shared memory allows; n = 10: A-k9 29.7 -> 31.0; n = 11: the 3 its shared memory allows, A-k10 35.4 -> 36.1)
 #endif
 __global__ void __launch_bounds__(GCfg<N>::C * GCfg<N>::TPC, DG_GMB)
 dg_gen_kernel(const __grid_constant__ KParams p)
