@@ -467,6 +467,10 @@ __global__ void __launch_bounds__(REG_CTA, DG_RMINB(N, GEN)) dg_reg_kernel(const
             if (lc[0] + 1 < p.nloc[0]) sx1 = sown + n3;
             if (RStage<N, GEN>::NIMG > 1 && lc[1] > 0) sy0 = S1 + ((cell - p.nloc[0]) * n3 - soff[1]);
             if (RStage<N, GEN>::NIMG > 1 && lc[1] + 1 < p.nloc[1]) sy1 = S2 + ((cell + p.nloc[0]) * n3 - soff[2]);
+            constexpr int IMG0 = RStage<N, GEN>::IMG0;   // (the staged blocks lie inside image 0)
+            DG_ASSERT(sown >= rsm && sown + n3 <= rsm + IMG0);
+            DG_ASSERT(!sx0 || (sx0 >= rsm && sx0 + n3 <= rsm + IMG0));
+            DG_ASSERT(!sx1 || (sx1 >= rsm && sx1 + n3 <= rsm + IMG0));
         }
     }
     double u[N3], t[N3], X[N3];
