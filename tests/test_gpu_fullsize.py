@@ -100,7 +100,7 @@ def test_c5_weak_block_slab():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("k", [2, 7])
+@pytest.mark.parametrize("k", [2, 5, 7, 8])   # register (n = 3), 3-cell CTAs (n = 6), TMA (n = 8), bulk (n = 9)
 def test_problem_a_full_size_slab(k):
     """The paper's Problem A at ~4e8 DOFs (periodic, per-cell tensor field) on the general kernel;
     the slab wraps around the periodic z sides."""
