@@ -102,7 +102,7 @@ template <> struct Cfg<6> { static constexpr int TPC = DG_OVR(6, DG_TPC, 36), P 
 template <> struct Cfg<7> { static constexpr int TPC = DG_OVR(7, DG_TPC, 64), P = DG_OVR(7, DG_P, 1), C = DG_OVR(7, DG_C, 1), MINB = DG_OVR(7, DG_MINB, 12); };
 template <> struct Cfg<8> { static constexpr int TPC = DG_OVR(8, DG_TPC, 64), P = DG_OVR(8, DG_P, 1), C = DG_OVR(8, DG_C, 1), MINB = DG_OVR(8, DG_MINB, 10); };
 template <> struct Cfg<9> { static constexpr int TPC = DG_OVR(9, DG_TPC, 96), P = DG_OVR(9, DG_P, 1), C = DG_OVR(9, DG_C, 1), MINB = DG_OVR(9, DG_MINB, 8); };
-template <> struct Cfg<10> { static constexpr int TPC = DG_OVR(10, DG_TPC, 64), P = DG_OVR(10, DG_P, 2), C = DG_OVR(10, DG_C, 1), MINB = DG_OVR(10, DG_MINB, 8); };
+template <> struct Cfg<10> { static constexpr int TPC = DG_OVR(10, DG_TPC, 128), P = DG_OVR(10, DG_P, 1), C = DG_OVR(10, DG_C, 1), MINB = DG_OVR(10, DG_MINB, 6); };
 template <> struct Cfg<11> { static constexpr int TPC = DG_OVR(11, DG_TPC, 128), P = DG_OVR(11, DG_P, 1), C = DG_OVR(11, DG_C, 1), MINB = DG_OVR(11, DG_MINB, 6); };
 
 // Shared-memory layout of one n^3 cell array: x-, y- and z-pencil accesses of a warp are

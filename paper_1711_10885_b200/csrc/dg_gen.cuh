@@ -185,11 +185,19 @@ template <int N> struct GCfg {
 // (a fourth array cost 4 KB per cell at n = 8: 6 -> 8 CTAs per SM without it). n = 8 stages its
 // TMA loads in OT (own block), X1 and A0 (x-neighbours), all free in phase 1, and its store in
 // X0; only the mbarrier (16 B) is extra.
+// How the face passes read this cell's tensor D (indexed by the face's direction, a run-time value):
+// 0 from Dw (then in local memory), 1 a select chain over Dw in registers, 2 a shared-memory copy
+// (A/B, tools/variant.py -DDG_DW_SEL: A-k3 36.8 -> 38.0 (2); A-k4 33.1 -> 34.4 (1), 34.2 (2);
+// A-k6 30.7 -> 31.3 (1), 31.6 (2); A-k7 50.0 -> 45.0 (1), 45.9 (2), A-k8 35.3 -> 33.9 (2), A-k5 34.2 -> 30.8 (1),
+// A-k9 35.2 -> 33.4 (1), A-k10 36.5 -> 33.4 (1), 34.9 (2): spills / registers)
+#ifndef DG_DW_SEL
+#define DG_DW_SEL ((DG_N) == 5 ? 1 : ((DG_N) == 4 || (DG_N) == 7) ? 2 : 0)
+#endif
 template <int N>
 struct GSmem {
     static constexpr int PER_CELL = 3 * Lay<N>::SLOT + 2 * GFLay<N>::SLOT;
     static constexpr int STAGE = (N >= 7) ? 2 : 0;   // the mbarrier (n = 8: TMA; n = 7, 9, 11: bulk copies)
-    static constexpr int BYTES = GCfg<N>::C * PER_CELL * 8 + STAGE * 8;
+    static constexpr int BYTES = GCfg<N>::C * PER_CELL * 8 + STAGE * 8 + (DG_DW_SEL == 2 ? GCfg<N>::C * 64 : 0);
 };
 
 template <int N, bool GH>
@@ -250,6 +258,24 @@ dg_gen_kernel(const __grid_constant__ KParams p)
     double Dw[6];                                                // this cell's tensor
 #pragma unroll
     for (int i = 0; i < 6; ++i) Dw[i] = __ldg(p.Dfield + 6 * cell + i);
+#if DG_DW_SEL == 1
+    // face passes index the tensor by the face's direction: a select chain keeps Dw in registers
+    // (a dynamic index would place it in local memory)
+    auto dwv = [&](int i) {
+        double r = Dw[0];
+#pragma unroll
+        for (int j = 1; j < 6; ++j) r = (i == j) ? Dw[j] : r;
+        return r;
+    };
+#elif DG_DW_SEL == 2
+    // face passes index the tensor by the face's direction: read it from a shared copy (a dynamic
+    // index into Dw would place Dw in local memory); first read after the phase barriers
+    double* Dsm = smem + C * GSmem<N>::PER_CELL + GSmem<N>::STAGE + 8 * slot;
+    if (lane < 6) Dsm[lane] = __ldg(p.Dfield + 6 * cell + lane);
+    auto dwv = [&](int i) { return Dsm[i]; };
+#else
+    auto dwv = [&](int i) { return Dw[i]; };
+#endif
     // The face passes give work item tk = lane (one pass over 6 n face lines when TPC >= 6 n) the
     // lines of face f = lane / n: that face's neighbour tensor is loaded here, long before its use
     // (the dependent L2 loads in the passes were long-scoreboard stalls)
@@ -546,7 +572,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         } else {
             // own pass A (lines along i1): s_part = D_qq/h_q d_n u + D_qt1/h_t1 Dc u-
             if (!((fact >> f) & 1u)) continue;
-            const double cqq = Dw[q] * p.hinv[q], cq1 = Dw[dsym(q, t1)] * p.hinv[t1];
+            const double cqq = dwv(q) * p.hinv[q], cq1 = dwv(dsym(q, t1)) * p.hinv[t1];
             double rr[1][N], tt[1][N];
 #pragma unroll
             for (int e = 0; e < N; ++e) rr[0][e] = OT[GFLay<N>::at(2 * f, e, line)];
@@ -567,7 +593,7 @@ dg_gen_kernel(const __grid_constant__ KParams p)
 #pragma unroll
         for (int rr = 0; rr < 3; ++rr)
 #pragma unroll
-            for (int ss = 0; ss < 3; ++ss) Dh[rr][ss] = Dw[dsym(rr, ss)] * (p.hinv[rr] * p.hinv[ss]);
+            for (int ss = 0; ss < 3; ++ss) Dh[rr][ss] = dwv(dsym(rr, ss)) * (p.hinv[rr] * p.hinv[ss]);
         double u[P][N], g[P][N];
 #pragma unroll
         for (int k = 0; k < P; ++k)
@@ -612,9 +638,9 @@ dg_gen_kernel(const __grid_constant__ KParams p)
         if (!((fact >> f) & 1u)) continue;
         const int t1 = (q == 0) ? 1 : 0, t2 = (q == 2) ? 1 : 2;
         const bool interior = (nbmask >> f) & 1u;
-        const double dme = Dw[q];
-        const double cq2 = Dw[dsym(q, t2)] * p.hinv[t2];
-        const double cn = dme * p.hinv[q], c1 = Dw[dsym(q, t1)] * p.hinv[t1];
+        const double dme = dwv(q);
+        const double cq2 = dwv(dsym(q, t2)) * p.hinv[t2];
+        const double cn = dme * p.hinv[q], c1 = dwv(dsym(q, t1)) * p.hinv[t1];
         double uo[N], so[N], cv[N];
         {
             double rr[1][N], tt[1][N];
