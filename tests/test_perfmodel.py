@@ -44,3 +44,20 @@ def test_matrix_meshes_fit_and_use_27_colour_classes():
         assert N % 3 == 0 and cfg.ncells == (N, N, N)
         assert cfg.ndofs * 7 * (n3 + (n3 & 1)) * 8 <= 24e9
         assert cfg.periodic == (1, 1, 1) and cfg.dfield_seed >= 0
+
+
+def test_committed_ncu_summary_belongs_to_this_build():
+    """bench.py's roofline.frac divides executed flops from profiles/ncu_full_summary.json by the
+    kernel time and refuses a capture of another build (bench.load_ncu). A kernel-source change
+    without a fresh capture (tools/gpu_refresh_captures.sh) would leave the bench line without a
+    fraction: fail here instead."""
+    import json
+    import os
+    from paper_1711_10885_b200.build import kernel_family, kernel_hash
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "profiles", "ncu_full_summary.json")) as f:
+        d = json.load(f)
+    for name in ("C3", "C5-weak-P1", "A-k7", "C-k7", "TG-k5"):
+        ent = d[name]
+        assert ent["build_hash"] == kernel_hash(kernel_family(ent["kernel"])), name
+        assert ent["executed_flops_per_dof"] > 0 and ent["duration_ns"] > 0
